@@ -1,0 +1,536 @@
+/*
+ * orc.c -- plain, slow, obviously-correct complex128 CPU ORACLE for the RAS-PML hot path of
+ * arXiv 2602.00735 ("Massively parallel Schwarz methods for the high frequency Helmholtz equation").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product (paper_2602_00735_b200/, libhelm) never
+ * links, includes or calls it, and this file shares no code, header or table with the product.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section / equation named alongside).
+ * Readings of ambiguous passages are the D-numbers of DESIGN.md section 3 (same IDs as SURVEY.md 8(c)).
+ *
+ * Everything is IEEE fp64 complex (C99 double complex).  No BLAS, no blocking, no reordering beyond the
+ * textbook definition of each step.  OpenMP is used only to run independent subdomains concurrently.
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): grid sizes printed in BASELINE.json; the interior
+ * stencil closed form; PML closed forms / finite differences; A = A^T when sigma0 = 0; interior local
+ * matrix = global matrix of the (int box + kappa PML) problem; band LU vs numpy.linalg.solve;
+ * dense sum_j R~_j^T A_j^-1 R_j vs the apply; single subdomain => B^-1 = A^-1; Hankel far field;
+ * FEM order 2.  No function here is "parity unpinned".
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef double complex zc;
+
+/* ------------------------------------------------------------------------------------------------
+ * Problem description.  Omega_int = (0, nix*h) x (0, niy*h) ("hyper-rectangle"), surrounded by
+ * ng PML cells per side (Omega = prod (a - kappa_g, b + kappa_g)).  The PML profile width
+ * kappa (D3: the same kappa_g = 10 h profile for global and local layers) is separate from the
+ * number of PML cells so that layers thicker than kappa_g use the linear continuation.
+ * ----------------------------------------------------------------------------------------------*/
+typedef struct {
+    double k;       /* wavenumber (c = 1) */
+    double sigma0;  /* PML strength in g (BASELINE.json configs[0]) */
+    double h;       /* mesh size */
+    int nix, niy;   /* cells of Omega_int per axis */
+    int ng;         /* global PML cells per side */
+    double kappa;   /* profile width kappa_g in length units */
+    int px, py;     /* subdomains per axis (Cartesian covering) */
+    int novlp;      /* overlap delta in cells, per side of every interior face (D8) */
+    int npml;       /* local PML kappa in cells on every interior face */
+} orc_params;
+
+typedef struct {
+    /* per axis: node-index ranges (nodes 0..N on that axis) */
+    int own_lo[2], own_hi[2];   /* owned nodes [own_lo, own_hi)  (D10) */
+    int int_lo[2], int_hi[2];   /* int box nodes a_j, b_j */
+    int full_lo[2], full_hi[2]; /* full box nodes */
+    int has_lo[2], has_hi[2];   /* local PML on lower / upper face (kappa_{j,l/u} != 0) */
+    int m[2];                   /* local free nodes per axis = full_hi - full_lo - 1 */
+    /* factor storage (band LU, O7) */
+    zc *band;                   /* n x (2p+1), NULL until factored */
+    int factored;
+} orc_sub;
+
+typedef struct {
+    orc_params p;
+    int N[2];        /* cells per axis incl. PML */
+    int nf[2];       /* free nodes per axis = N - 1 */
+    int64_t nfree;
+    int nsub;
+    int *split[2];   /* block starts s_0..s_P (cells == nodes) */
+    orc_sub *sub;
+    zc *A7;          /* global matrix, 7 slots per free row (see slot_of) */
+} orc_ctx;
+
+/* ------------------------------------------------------------------------------------------------
+ * PML scaling function (BASELINE.json configs[0]; P:37-43 properties):
+ *   g(t) = sigma0 t^3 / (3 kappa^2)              0 <= t <= kappa
+ *   g(t) = sigma0 kappa / 3 + sigma0 (t - kappa)  t > kappa      ("linear beyond", C^1 at kappa)
+ * out[0..2] = g, g', g''.
+ * ----------------------------------------------------------------------------------------------*/
+void orc_gfun(double t, double kappa, double sigma0, double *out)
+{
+    if (t <= 0.0) { out[0] = out[1] = out[2] = 0.0; return; }
+    if (t <= kappa) {
+        out[0] = sigma0 * t * t * t / (3.0 * kappa * kappa);
+        out[1] = sigma0 * t * t / (kappa * kappa);
+        out[2] = 2.0 * sigma0 * t / (kappa * kappa);
+    } else {
+        out[0] = sigma0 * kappa / 3.0 + sigma0 * (t - kappa);
+        out[1] = sigma0;
+        out[2] = 0.0;
+    }
+}
+
+/* gamma = 1 + i g'(t), gamma' = (+/-) i g''(t): upper ramps g_i(x) = g(x - b), lower ramps
+ * g_i(x) = -g(a - x) so g_i'(x) = g'(a - x) and g_i''(x) = -g''(a - x)  (D4). */
+static void ramp(double t, int upper, const orc_params *p, zc *gam, zc *dgam)
+{
+    double g[3];
+    orc_gfun(t, p->kappa, p->sigma0, g);
+    *gam = 1.0 + I * g[1];
+    *dgam = upper ? I * g[2] : -I * g[2];
+}
+
+/* Global gamma along one axis at a position given in thirds of a cell: x = X3 * h / 3 in node units
+ * (node 0 at X3 = 0).  Omega_int spans nodes [ng, ng + ni].  Depth is formed from integer offsets (D5). */
+static void gamma_global(const orc_ctx *c, int axis, long X3, zc *gam, zc *dgam)
+{
+    const orc_params *p = &c->p;
+    long lo = 3L * p->ng, hi = 3L * (p->ng + (axis == 0 ? p->nix : p->niy));
+    double h3 = p->h / 3.0;
+    if (X3 > hi) ramp((double)(X3 - hi) * h3, 1, p, gam, dgam);
+    else if (X3 < lo) ramp((double)(lo - X3) * h3, 0, p, gam, dgam);
+    else { *gam = 1.0; *dgam = 0.0; }
+}
+
+/* Local scaling g_j^i: upper ramp from b_j above the int box, lower ramp from a_j below it,
+ * the global g_i inside.  Ramps exist only on faces that carry a local PML. */
+static void gamma_local(const orc_ctx *c, const orc_sub *s, int axis, long X3, zc *gam, zc *dgam)
+{
+    long a = 3L * s->int_lo[axis], b = 3L * s->int_hi[axis];
+    double h3 = c->p.h / 3.0;
+    if (s->has_hi[axis] && X3 > b) ramp((double)(X3 - b) * h3, 1, &c->p, gam, dgam);
+    else if (s->has_lo[axis] && X3 < a) ramp((double)(a - X3) * h3, 0, &c->p, gam, dgam);
+    else gamma_global(c, axis, X3, gam, dgam);
+}
+
+/* exported for the PML pins: sub < 0 -> global */
+void orc_gamma(const orc_ctx *c, int sub, int axis, long X3, zc *gam, zc *dgam)
+{
+    if (sub < 0) gamma_global(c, axis, X3, gam, dgam);
+    else gamma_local(c, &c->sub[sub], axis, X3, gam, dgam);
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * P1 element matrix (weak form eq. (weak)):
+ *   a(u,v) = int D grad u . grad v - (beta . grad u) v - k^2 u v,
+ *   D = diag(gamma_x^-2, gamma_y^-2), beta = (gamma_x'/gamma_x^3, gamma_y'/gamma_y^3),
+ * with D, beta frozen at the triangle centroid (BASELINE.json configs[0]; D5).  Bilinear, no
+ * conjugation (D6).  Row = test function phi_p, column = trial phi_q:
+ *   A_T[p][q] = |T| (D11 dx phi_p dx phi_q + D22 dy phi_p dy phi_q) - beta . grad phi_q * |T|/3
+ *               - k^2 |T| (1 + delta_pq) / 12.
+ * Cell (i,j) is split on its SW->NE diagonal (D1):
+ *   T_lo = {(i,j),(i+1,j),(i+1,j+1)}  centroid (i+2/3, j+1/3)  h*grad: (-1,0) (1,-1) (0,1)
+ *   T_up = {(i,j),(i+1,j+1),(i,j+1)}  centroid (i+1/3, j+2/3)  h*grad: (0,-1) (1,0) (-1,1)
+ * ----------------------------------------------------------------------------------------------*/
+static const int TRI_V[2][3][2] = { { {0, 0}, {1, 0}, {1, 1} }, { {0, 0}, {1, 1}, {0, 1} } };
+static const double TRI_G[2][3][2] = { { {-1, 0}, {1, -1}, {0, 1} }, { {0, -1}, {1, 0}, {-1, 1} } };
+static const int TRI_C3[2][2] = { {2, 1}, {1, 2} }; /* centroid offset in thirds (x, y) */
+
+static void element_matrix(const orc_params *p, zc gx, zc dgx, zc gy, zc dgy, int tri, zc Ae[3][3])
+{
+    double h = p->h, area = 0.5 * h * h;
+    zc D11 = 1.0 / (gx * gx), D22 = 1.0 / (gy * gy);
+    zc b1 = dgx / (gx * gx * gx), b2 = dgy / (gy * gy * gy);
+    for (int a = 0; a < 3; a++)
+        for (int q = 0; q < 3; q++) {
+            double dxa = TRI_G[tri][a][0] / h, dya = TRI_G[tri][a][1] / h;
+            double dxq = TRI_G[tri][q][0] / h, dyq = TRI_G[tri][q][1] / h;
+            zc stiff = area * (D11 * dxa * dxq + D22 * dya * dyq);
+            zc conv = (b1 * dxq + b2 * dyq) * (area / 3.0);
+            double mass = p->k * p->k * area * (a == q ? 2.0 : 1.0) / 12.0;
+            Ae[a][q] = stiff - conv - mass;
+        }
+}
+
+/* global free-row slot of neighbour (dx,dy); 7-point pattern of the SW->NE split (D1) */
+static int slot_of(int dx, int dy)
+{
+    if (dx == 0 && dy == 0) return 0;
+    if (dx == 1 && dy == 0) return 1;   /* E  */
+    if (dx == -1 && dy == 0) return 2;  /* W  */
+    if (dx == 0 && dy == 1) return 3;   /* N  */
+    if (dx == 0 && dy == -1) return 4;  /* S  */
+    if (dx == 1 && dy == 1) return 5;   /* NE */
+    if (dx == -1 && dy == -1) return 6; /* SW */
+    fprintf(stderr, "orc: neighbour (%d,%d) outside the 7-point pattern\n", dx, dy);
+    abort();
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Decomposition (D8, D10).  Cells 0..N-1 of each axis are cut into P blocks of floor/ceil
+ * size, larger blocks first.  Int box = block extended by delta cells on every side not on dOmega;
+ * full box = int box extended by kappa cells on the same sides.  Local free nodes = nodes strictly
+ * inside the full box (Dirichlet on dOmega_j, RAS-PML-Drch; D9).
+ * Owner of node i: the block p with s_p <= i < s_{p+1}.
+ * ----------------------------------------------------------------------------------------------*/
+orc_ctx *orc_create(const orc_params *p, char *err, int errlen)
+{
+    orc_ctx *c = calloc(1, sizeof(orc_ctx));
+    c->p = *p;
+    c->N[0] = p->nix + 2 * p->ng;
+    c->N[1] = p->niy + 2 * p->ng;
+    c->nf[0] = c->N[0] - 1;
+    c->nf[1] = c->N[1] - 1;
+    c->nfree = (int64_t)c->nf[0] * c->nf[1];
+    int P[2] = { p->px, p->py };
+    c->nsub = P[0] * P[1];
+    int w = p->novlp + p->npml;
+    if (P[0] < 1 || P[1] < 1 || c->N[0] < 2 || c->N[1] < 2) {
+        snprintf(err, errlen, "empty grid or subdomain count");
+        free(c); return NULL;
+    }
+    c->split[0] = malloc(sizeof(int) * (P[0] + 1));
+    c->split[1] = malloc(sizeof(int) * (P[1] + 1));
+    for (int ax = 0; ax < 2; ax++) {
+        int q = c->N[ax] / P[ax], r = c->N[ax] % P[ax];
+        c->split[ax][0] = 0;
+        for (int b = 0; b < P[ax]; b++) c->split[ax][b + 1] = c->split[ax][b] + q + (b < r ? 1 : 0);
+        for (int b = 0; b < P[ax]; b++) {
+            int sz = c->split[ax][b + 1] - c->split[ax][b];
+            if ((P[ax] > 1 && sz < w) || sz < 2) {
+                snprintf(err, errlen, "block %d on axis %d has %d cells (< delta+kappa = %d or < 2)", b, ax, sz, w);
+                free(c->split[0]); free(c->split[1]); free(c); return NULL;
+            }
+        }
+    }
+    c->sub = calloc(c->nsub, sizeof(orc_sub));
+    for (int jy = 0; jy < P[1]; jy++)
+        for (int jx = 0; jx < P[0]; jx++) {
+            orc_sub *s = &c->sub[jx + P[0] * jy];
+            int jj[2] = { jx, jy };
+            for (int ax = 0; ax < 2; ax++) {
+                int b = jj[ax];
+                s->own_lo[ax] = c->split[ax][b];
+                s->own_hi[ax] = c->split[ax][b + 1];
+                s->has_lo[ax] = b > 0;
+                s->has_hi[ax] = b < P[ax] - 1;
+                s->int_lo[ax] = s->own_lo[ax] - (s->has_lo[ax] ? p->novlp : 0);
+                s->int_hi[ax] = s->own_hi[ax] + (s->has_hi[ax] ? p->novlp : 0);
+                s->full_lo[ax] = s->int_lo[ax] - (s->has_lo[ax] ? p->npml : 0);
+                s->full_hi[ax] = s->int_hi[ax] + (s->has_hi[ax] ? p->npml : 0);
+                s->m[ax] = s->full_hi[ax] - s->full_lo[ax] - 1;
+                if (s->full_lo[ax] < 0 || s->full_hi[ax] > c->N[ax]) {
+                    snprintf(err, errlen, "full box of subdomain (%d,%d) leaves Omega", jx, jy);
+                    free(c->sub); free(c->split[0]); free(c->split[1]); free(c); return NULL;
+                }
+            }
+        }
+    return c;
+}
+
+void orc_destroy(orc_ctx *c)
+{
+    if (!c) return;
+    for (int j = 0; j < c->nsub; j++) free(c->sub[j].band);
+    free(c->sub);
+    free(c->split[0]);
+    free(c->split[1]);
+    free(c->A7);
+    free(c);
+}
+
+/* dims: N[0], N[1], nf[0], nf[1], nsub, px, py */
+void orc_dims(const orc_ctx *c, int *out)
+{
+    out[0] = c->N[0]; out[1] = c->N[1]; out[2] = c->nf[0]; out[3] = c->nf[1];
+    out[4] = c->nsub; out[5] = c->p.px; out[6] = c->p.py;
+}
+
+/* subdomain j: own_lo/hi, int_lo/hi, full_lo/hi, has_lo/hi, m  per axis -> 18 ints (x then y) */
+void orc_subdomain(const orc_ctx *c, int j, int *out)
+{
+    const orc_sub *s = &c->sub[j];
+    for (int ax = 0; ax < 2; ax++) {
+        int *o = out + 9 * ax;
+        o[0] = s->own_lo[ax]; o[1] = s->own_hi[ax]; o[2] = s->int_lo[ax]; o[3] = s->int_hi[ax];
+        o[4] = s->full_lo[ax]; o[5] = s->full_hi[ax]; o[6] = s->has_lo[ax]; o[7] = s->has_hi[ax];
+        o[8] = s->m[ax];
+    }
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Global assembly (eq. (weak) on V_h subset H^1_0(Omega)): element loop over all
+ * N x N cells with the global coefficients; rows/columns of Dirichlet nodes dropped.
+ * Free node (i,j), 1 <= i,j <= N-1, has index (i-1) + nf (j-1).
+ * ----------------------------------------------------------------------------------------------*/
+static void assemble_global(orc_ctx *c)
+{
+    if (c->A7) return;
+    c->A7 = calloc((size_t)c->nfree * 7, sizeof(zc));
+    for (int cj = 0; cj < c->N[1]; cj++)
+        for (int ci = 0; ci < c->N[0]; ci++)
+            for (int tri = 0; tri < 2; tri++) {
+                zc gx, dgx, gy, dgy, Ae[3][3];
+                gamma_global(c, 0, 3L * ci + TRI_C3[tri][0], &gx, &dgx);
+                gamma_global(c, 1, 3L * cj + TRI_C3[tri][1], &gy, &dgy);
+                element_matrix(&c->p, gx, dgx, gy, dgy, tri, Ae);
+                for (int a = 0; a < 3; a++) {
+                    int pi = ci + TRI_V[tri][a][0], pj = cj + TRI_V[tri][a][1];
+                    if (pi < 1 || pi > c->nf[0] || pj < 1 || pj > c->nf[1]) continue;
+                    int64_t row = (pi - 1) + (int64_t)c->nf[0] * (pj - 1);
+                    for (int q = 0; q < 3; q++) {
+                        int qi = ci + TRI_V[tri][q][0], qj = cj + TRI_V[tri][q][1];
+                        if (qi < 1 || qi > c->nf[0] || qj < 1 || qj > c->nf[1]) continue;
+                        c->A7[row * 7 + slot_of(qi - pi, qj - pj)] += Ae[a][q];
+                    }
+                }
+            }
+}
+
+/* 7 slots per free row: 0 centre, 1 E, 2 W, 3 N, 4 S, 5 NE, 6 SW (row-major [nfree][7]) */
+void orc_global_stencil(orc_ctx *c, zc *out)
+{
+    assemble_global(c);
+    memcpy(out, c->A7, sizeof(zc) * 7 * (size_t)c->nfree);
+}
+
+/* y = A x (S: matvec; eq. (weak)) */
+void orc_matvec(orc_ctx *c, const zc *x, zc *y)
+{
+    assemble_global(c);
+    int nfx = c->nf[0], nfy = c->nf[1];
+    static const int DX[7] = { 0, 1, -1, 0, 0, 1, -1 }, DY[7] = { 0, 0, 0, 1, -1, 1, -1 };
+#pragma omp parallel for schedule(static)
+    for (int j = 1; j <= nfy; j++)
+        for (int i = 1; i <= nfx; i++) {
+            int64_t row = (i - 1) + (int64_t)nfx * (j - 1);
+            zc acc = 0;
+            for (int s = 0; s < 7; s++) {
+                int qi = i + DX[s], qj = j + DY[s];
+                if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
+                acc += c->A7[row * 7 + s] * x[(qi - 1) + (int64_t)nfx * (qj - 1)];
+            }
+            y[row] = acc;
+        }
+}
+
+/* y[rows[r]] = (A x)[rows[r]] for a sample of rows (full-size parity on sampled outputs) */
+void orc_matvec_rows(orc_ctx *c, const zc *x, const int64_t *rows, int nrows, zc *y)
+{
+    assemble_global(c);
+    int nfx = c->nf[0], nfy = c->nf[1];
+    static const int DX[7] = { 0, 1, -1, 0, 0, 1, -1 }, DY[7] = { 0, 0, 0, 1, -1, 1, -1 };
+    for (int r = 0; r < nrows; r++) {
+        int64_t row = rows[r];
+        int i = (int)(row % nfx) + 1, j = (int)(row / nfx) + 1;
+        zc acc = 0;
+        for (int s = 0; s < 7; s++) {
+            int qi = i + DX[s], qj = j + DY[s];
+            if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
+            acc += c->A7[row * 7 + s] * x[(qi - 1) + (int64_t)nfx * (qj - 1)];
+        }
+        y[r] = acc;
+    }
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Right-hand side (D14): f(x) = sum_s a_s (2 pi sigma^2)^-1 exp(-|x - x_s|^2 / (2 sigma^2)), nodal
+ * interpolation at the free nodes, b = M_ff f_I with the consistent P1 mass matrix
+ * (int_T phi_p phi_q = |T| (1 + delta_pq) / 12), assembled element by element.
+ * Node (i,j) sits at ((i - ng) h, (j - ng) h).
+ * ----------------------------------------------------------------------------------------------*/
+void orc_rhs(orc_ctx *c, int nsrc, const double *xy, const zc *amp, double sigma, zc *b)
+{
+    int nfx = c->nf[0], nfy = c->nf[1];
+    double h = c->p.h, area = 0.5 * h * h;
+    zc *f = calloc((size_t)c->nfree, sizeof(zc));
+#pragma omp parallel for schedule(static)
+    for (int j = 1; j <= nfy; j++)
+        for (int i = 1; i <= nfx; i++) {
+            double x = (i - c->p.ng) * h, y = (j - c->p.ng) * h;
+            zc acc = 0;
+            for (int s = 0; s < nsrc; s++) {
+                double dx = x - xy[2 * s], dy = y - xy[2 * s + 1];
+                acc += amp[s] * exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma)) / (2.0 * M_PI * sigma * sigma);
+            }
+            f[(i - 1) + (int64_t)nfx * (j - 1)] = acc;
+        }
+    memset(b, 0, sizeof(zc) * (size_t)c->nfree);
+    for (int cj = 0; cj < c->N[1]; cj++)
+        for (int ci = 0; ci < c->N[0]; ci++)
+            for (int tri = 0; tri < 2; tri++)
+                for (int a = 0; a < 3; a++) {
+                    int pi = ci + TRI_V[tri][a][0], pj = cj + TRI_V[tri][a][1];
+                    if (pi < 1 || pi > nfx || pj < 1 || pj > nfy) continue;
+                    for (int q = 0; q < 3; q++) {
+                        int qi = ci + TRI_V[tri][q][0], qj = cj + TRI_V[tri][q][1];
+                        if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
+                        b[(pi - 1) + (int64_t)nfx * (pj - 1)] +=
+                            area * (a == q ? 2.0 : 1.0) / 12.0 * f[(qi - 1) + (int64_t)nfx * (qj - 1)];
+                    }
+                }
+    free(f);
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Local operator A_j (a_j = a restricted to H^1_0(Omega_j) with the local scaling g_j),
+ * assembled element by element over the cells of the full box into band storage.
+ * Local free node (lx,ly), 1 <= lx <= mx, 1 <= ly <= my, is global node (full_lo + lx, ...) and has
+ * local index (lx-1) + mx (ly-1); half-bandwidth p = mx + 1 (D1).  band[r*(2p+1) + (col - r + p)].
+ * ----------------------------------------------------------------------------------------------*/
+static void assemble_local(const orc_ctx *c, int j, zc *band)
+{
+    const orc_sub *s = &c->sub[j];
+    int mx = s->m[0], my = s->m[1], p = mx + 1, bw = 2 * p + 1;
+    int64_t n = (int64_t)mx * my;
+    memset(band, 0, sizeof(zc) * (size_t)n * bw);
+    for (int cj = s->full_lo[1]; cj < s->full_hi[1]; cj++)
+        for (int ci = s->full_lo[0]; ci < s->full_hi[0]; ci++)
+            for (int tri = 0; tri < 2; tri++) {
+                zc gx, dgx, gy, dgy, Ae[3][3];
+                gamma_local(c, s, 0, 3L * ci + TRI_C3[tri][0], &gx, &dgx);
+                gamma_local(c, s, 1, 3L * cj + TRI_C3[tri][1], &gy, &dgy);
+                element_matrix(&c->p, gx, dgx, gy, dgy, tri, Ae);
+                for (int a = 0; a < 3; a++) {
+                    int lx = ci + TRI_V[tri][a][0] - s->full_lo[0], ly = cj + TRI_V[tri][a][1] - s->full_lo[1];
+                    if (lx < 1 || lx > mx || ly < 1 || ly > my) continue;
+                    int64_t r = (lx - 1) + (int64_t)mx * (ly - 1);
+                    for (int q = 0; q < 3; q++) {
+                        int qx = ci + TRI_V[tri][q][0] - s->full_lo[0], qy = cj + TRI_V[tri][q][1] - s->full_lo[1];
+                        if (qx < 1 || qx > mx || qy < 1 || qy > my) continue;
+                        int64_t col = (qx - 1) + (int64_t)mx * (qy - 1);
+                        band[r * bw + (col - r + p)] += Ae[a][q];
+                    }
+                }
+            }
+}
+
+/* export the local band (n x (2p+1)) for pins; returns n */
+int64_t orc_local_band(const orc_ctx *c, int j, zc *band)
+{
+    assemble_local(c, j, band);
+    return (int64_t)c->sub[j].m[0] * c->sub[j].m[1];
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Naive banded LU without pivoting (D12; exact local solves), in place on band storage.
+ *   for kk: u = a[kk][kk]; if u == 0 -> zero pivot at row kk
+ *           for i in kk+1..kk+p: l = a[i][kk]/u; a[i][kk] = l; a[i][kk+1..kk+p] -= l a[kk][kk+1..kk+p]
+ * Returns -1 on success, else the zero-pivot row.
+ * ----------------------------------------------------------------------------------------------*/
+int64_t orc_band_lu(int64_t n, int p, zc *a)
+{
+    int bw = 2 * p + 1;
+#define AB(r, col) a[(r) * bw + ((col) - (r) + p)]
+    for (int64_t kk = 0; kk < n; kk++) {
+        zc u = AB(kk, kk);
+        if (u == 0) return kk;
+        int64_t iend = kk + p < n - 1 ? kk + p : n - 1;
+        for (int64_t i = kk + 1; i <= iend; i++) {
+            zc l = AB(i, kk) / u;
+            AB(i, kk) = l;
+            if (l == 0) continue;
+            for (int64_t col = kk + 1; col <= iend; col++) AB(i, col) -= l * AB(kk, col);
+        }
+    }
+    return -1;
+}
+
+/* forward (unit L) then backward (U) substitution, x in/out */
+void orc_band_solve(int64_t n, int p, const zc *a, zc *x)
+{
+    int bw = 2 * p + 1;
+    for (int64_t i = 0; i < n; i++) {
+        zc acc = x[i];
+        for (int64_t col = (i - p > 0 ? i - p : 0); col < i; col++) acc -= AB(i, col) * x[col];
+        x[i] = acc;
+    }
+    for (int64_t i = n - 1; i >= 0; i--) {
+        zc acc = x[i];
+        int64_t cend = i + p < n - 1 ? i + p : n - 1;
+        for (int64_t col = i + 1; col <= cend; col++) acc -= AB(i, col) * x[col];
+        x[i] = acc / AB(i, i);
+    }
+#undef AB
+}
+
+/* Factor the listed subdomains (list == NULL -> all).  Returns 0, or -(1 + j) with *zero_row set on
+ * a zero pivot in subdomain j. */
+int orc_factor(orc_ctx *c, const int *list, int nlist, int64_t *zero_row)
+{
+    int cnt = list ? nlist : c->nsub;
+    int bad = -1;
+    int64_t badrow = -1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < cnt; t++) {
+        int j = list ? list[t] : t;
+        orc_sub *s = &c->sub[j];
+        if (s->factored) continue;
+        int mx = s->m[0], p = mx + 1;
+        int64_t n = (int64_t)mx * s->m[1];
+        zc *band = malloc(sizeof(zc) * (size_t)n * (2 * p + 1));
+        assemble_local(c, j, band);
+        int64_t zr = orc_band_lu(n, p, band);
+        if (zr >= 0) {
+#pragma omp critical
+            { if (bad < 0) { bad = j; badrow = zr; } }
+            free(band);
+            continue;
+        }
+        s->band = band;
+        s->factored = 1;
+    }
+    if (bad >= 0) { if (zero_row) *zero_row = badrow; return -(1 + bad); }
+    return 0;
+}
+
+/* drop factors (bench / memory control) */
+void orc_release(orc_ctx *c)
+{
+    for (int j = 0; j < c->nsub; j++) { free(c->sub[j].band); c->sub[j].band = NULL; c->sub[j].factored = 0; }
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * RAS-PML preconditioner: z = sum_j R~_j^T A_j^-1 R_j v, with
+ *   R_j    = restriction to all local free nodes of Omega_j (D11),
+ *   R~_j^T = extension by the 0/1 owner indicator chi_j = 1 on block j (D10).
+ * Only the listed subdomains are applied (list == NULL -> all); z is written at their owned nodes.
+ * Returns 0, or -1 if a listed subdomain is not factored.
+ * ----------------------------------------------------------------------------------------------*/
+int orc_apply(orc_ctx *c, const zc *v, zc *z, const int *list, int nlist)
+{
+    int cnt = list ? nlist : c->nsub;
+    int nfx = c->nf[0];
+    int missing = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < cnt; t++) {
+        int j = list ? list[t] : t;
+        orc_sub *s = &c->sub[j];
+        if (!s->factored) { missing = 1; continue; }
+        int mx = s->m[0], my = s->m[1];
+        int64_t n = (int64_t)mx * my;
+        zc *x = malloc(sizeof(zc) * (size_t)n);
+        for (int ly = 1; ly <= my; ly++)
+            for (int lx = 1; lx <= mx; lx++) {
+                int gi = s->full_lo[0] + lx, gj = s->full_lo[1] + ly;
+                x[(lx - 1) + (int64_t)mx * (ly - 1)] = v[(gi - 1) + (int64_t)nfx * (gj - 1)];
+            }
+        orc_band_solve(n, mx + 1, s->band, x);
+        for (int gj = s->own_lo[1]; gj < s->own_hi[1]; gj++)
+            for (int gi = s->own_lo[0]; gi < s->own_hi[0]; gi++) {
+                if (gi < 1 || gi > c->nf[0] || gj < 1 || gj > c->nf[1]) continue; /* Dirichlet node */
+                int lx = gi - s->full_lo[0], ly = gj - s->full_lo[1];
+                z[(gi - 1) + (int64_t)nfx * (gj - 1)] = x[(lx - 1) + (int64_t)mx * (ly - 1)];
+            }
+        free(x);
+    }
+    return missing ? -1 : 0;
+}
