@@ -1,0 +1,143 @@
+/*
+ * helm.h -- C ABI of libhelm: the B200-native (sm_100a) hot path of the one-level restricted additive
+ * Schwarz method with PML transmission conditions (RAS-PML) of arXiv 2602.00735 for P1, complex-valued,
+ * high-frequency 2D Helmholtz systems, used as a right preconditioner inside restarted GMRES.
+ *
+ * Citations: "P:n" = the paper's text line n with the section / equation named; D-numbers are
+ * the readings in DESIGN.md section 3.  All vectors are complex128 (IEEE fp64 re/im interleaved,
+ * == cuDoubleComplex == torch.complex128), indexed over the free nodes (i, j), 1 <= i, j <= N-1, of the
+ * uniform mesh, x-fastest: g = (i - 1) + (N - 1) (j - 1).
+ *
+ * Ownership: the context owns every device allocation it makes (operators, factors, Krylov basis,
+ * scratch).  The caller owns every vector argument; "_dev" pointers are device memory holding this
+ * rank's owned rectangle (helm_layout), "_host" pointers are host memory.  Work is ordered on the CUDA
+ * stream given to helm_setup; functions return once the work is enqueued unless stated otherwise.
+ *
+ * Errors: every int-returning function returns HELM_OK (0), a positive solver status, or a negative
+ * error code; helm_last_error() then describes it.  A context stays destroyable after any error.
+ *
+ * No CPU fallback: every arithmetic step runs in the library's own CUDA kernels.
+ */
+#ifndef HELM_H
+#define HELM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } helm_z;
+typedef struct helm_ctx helm_ctx;
+
+enum {
+    HELM_OK = 0,
+    HELM_NOT_CONVERGED = 2,   /* maxit reached; x holds the last iterate */
+    HELM_BREAKDOWN = 3,       /* NaN / Inf in the Arnoldi process */
+    HELM_EINVAL = -1,         /* bad argument or unsupported parameter combination */
+    HELM_ENOMEM = -2,         /* device allocation failed */
+    HELM_ECUDA = -3,          /* CUDA runtime error */
+    HELM_ENCCL = -4,          /* multi-rank communication error / not built with NCCL */
+    HELM_EZEROPIVOT = -5,     /* singular Schur complement block: message names subdomain, block, row */
+    HELM_ELAYOUT = -6,        /* a subdomain extension leaves Omega (blocks smaller than delta + kappa) */
+    HELM_ESTATE = -7          /* apply / gmres before helm_factor */
+};
+
+enum { HELM_BC_DIRICHLET = 0 /* RAS-PML-Drch: u = 0 on dOmega_j, P:131-137, P:152 (D9) */ };
+
+/* Problem and decomposition (P:36-62 problem, P:71-92 covering; BASELINE.json configs). */
+typedef struct {
+    double k;            /* wavenumber (> 0); constant wave speed c = 1 */
+    int ppw;             /* points per wavelength: n_int = round(ppw k / 2 pi) cells on (0,1), h = 1/n_int (D2) */
+    int n_pml_global;    /* global PML cells per side; PML profile width kappa_g = n_pml_global * h (D3) */
+    double sigma0;       /* profile g(t) = sigma0 t^3 / (3 kappa_g^2), linear beyond kappa_g */
+    int nsub_x, nsub_y;  /* Cartesian subdomain grid */
+    int n_ovlp, n_pml;   /* overlap delta / local PML kappa in cells per interior face; < 0 => max(2, round(1.59 ln k)) */
+    int local_bc;        /* HELM_BC_DIRICHLET */
+    int gpu_grid_x, gpu_grid_y;   /* rank grid over the subdomain grid; product == nranks (0,0 => 1 x nranks) */
+} helm_params;
+
+typedef struct {
+    long long n_free_global;  /* (N-1)^2 */
+    int N_cells;              /* cells per side including the global PML: n_int + 2 n_pml_global */
+    int n_int;                /* cells across Omega_int = (0,1) */
+    int n_ovlp, n_pml;        /* resolved widths */
+    int owned_i0, owned_i1;   /* this rank's owned free nodes: i in [owned_i0, owned_i1) (1-based node index) */
+    int owned_j0, owned_j1;   /* ... and j in [owned_j0, owned_j1) */
+    long long n_local;        /* (owned_i1 - owned_i0) * (owned_j1 - owned_j0): length of every _dev vector */
+    int n_sub;                /* total subdomains */
+    int n_sub_local;          /* subdomains whose factors this rank holds */
+    int m_max;                /* largest local block size (free nodes per local row) */
+    long long local_unknowns; /* sum over local subdomains of n_j */
+    long long factor_bytes;   /* bytes of explicit Schur-complement inverses held by this rank */
+    long long apply_bytes;    /* algorithmic DRAM bytes one helm_precond_apply moves on this rank */
+    long long band_bytes;     /* the same operator as band L+U factors + gather + write (SURVEY 8(d) B_apply) */
+    long long spmv_bytes;     /* algorithmic bytes of one helm_matvec on this rank */
+} helm_layout;
+
+typedef struct {
+    int iterations;      /* Arnoldi steps (one A B^-1 product each) */
+    int restarts;        /* completed cycles minus one */
+    int status;          /* HELM_OK, HELM_NOT_CONVERGED, HELM_BREAKDOWN */
+    int applies;         /* preconditioner applications issued (iterations + one per cycle end) */
+    double relres_est;   /* |g_{j+1}| / ||b|| of the last Givens step */
+    double relres_true;  /* ||b - A x|| / ||b|| recomputed at the last cycle end */
+    double* history;     /* caller-owned host buffer for relres_est per iteration, or NULL */
+    int history_cap;
+} helm_gmres_info;
+
+/* Create a context: grid, decomposition, device assembly of the global operator A (eq. (weak))
+ * and of every local operator A_j.  rank / nranks: this process's place in the job; nranks > 1
+ * needs nccl_unique_id (128 bytes, identical on all ranks) and a library built with NCCL.  cuda_stream:
+ * cudaStream_t or NULL (legacy default stream).  Allocates the global operator and local stencils. */
+int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id,
+               void* cuda_stream, helm_ctx** out);
+
+/* Fill *out with the layout of this rank.  Synchronous, host only. */
+int helm_get_layout(const helm_ctx* ctx, helm_layout* out);
+
+/* b = M f_I: f = sum_s amp_s (2 pi sigma^2)^-1 exp(-|x - xy_s|^2 / (2 sigma^2)) at the free nodes, M the
+ * consistent P1 mass matrix (D14).  xy_host: 2*nsrc doubles (x0,y0,x1,y1,...), amp_host: nsrc values,
+ * both host memory; b_dev: n_local values. */
+int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_host, double sigma, helm_z* b_dev);
+
+/* Factor every local operator of this rank once (setup; P:143-147 A_j^-1): twisted block-tridiagonal
+ * LU with explicit inverses of the Schur-complement blocks.  Synchronises the stream;
+ * HELM_EZEROPIVOT names the first singular block.  Idempotent. */
+int helm_factor(helm_ctx* ctx);
+
+/* y = A x (7-point P1 stencil of eq. (weak)).  x_dev, y_dev: n_local values, distinct. */
+int helm_matvec(helm_ctx* ctx, const helm_z* x_dev, helm_z* y_dev);
+
+/* z = B^-1 r = sum_j R~_j^T A_j^-1 R_j r: restrict to every PML-extended subdomain, exact local
+ * solves, restricted owner write (chi_j = indicator of block j, D10).  r_dev, z_dev: n_local values, distinct. */
+int helm_precond_apply(helm_ctx* ctx, const helm_z* r_dev, helm_z* z_dev);
+
+/* Same with host buffers: r_host -> device, apply, device -> z_host; synchronous (end-to-end path). */
+int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host);
+
+/* Right-preconditioned restarted GMRES(restart) on A (B^-1 u) = b, x = B^-1 u (D13):
+ * x_dev in: initial guess, out: solution.  rtol on ||b - A x|| / ||b||; rtol <= 0 runs exactly maxit
+ * iterations.  Synchronous.  Returns HELM_OK / HELM_NOT_CONVERGED / HELM_BREAKDOWN or an error. */
+int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, double rtol, int maxit,
+               helm_gmres_info* info);
+
+/* Same with host b / x (copied in and out inside the call). */
+int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int restart, double rtol, int maxit,
+                    helm_gmres_info* info);
+
+/* Parity export: the global operator as 7 slot arrays [7][n_local] (slot order centre, E, W, N, S, NE, SW;
+ * a slot pointing at a Dirichlet node is 0).  out_dev: 7 * n_local values. */
+int helm_export_stencil(helm_ctx* ctx, helm_z* out_dev);
+
+/* Kernel timing of the apply kernel: when enabled, CUDA events bracket every launch of the fused apply
+ * kernel on the context's stream; helm_profile_read synchronises and returns the summed milliseconds
+ * and the launch count since the last read (then resets). */
+int helm_profile_enable(helm_ctx* ctx, int on);
+int helm_profile_read(helm_ctx* ctx, double* apply_ms, int* apply_launches, int* total_launches);
+
+const char* helm_last_error(const helm_ctx* ctx);
+void helm_destroy(helm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELM_H */

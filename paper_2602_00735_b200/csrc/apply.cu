@@ -1,0 +1,301 @@
+// apply.cu -- K4: the fused RAS-PML preconditioner application z = sum_j R~_j^T A_j^-1 R_j r.
+//
+// One persistent CTA per (SM x occupancy) walks a static list of subdomains.  Per subdomain it performs
+//   restrict   b_i = (R_j r) on block row i, read straight from r (rows are contiguous: x-fastest),
+//   solve      the twisted block-tridiagonal substitution with the explicit Schur-complement inverses
+//              written by factor.cu:
+//                T  z_i = Q_i^-1 (b_i - U_i z_{i+1})           i = nb-1 .. tw+1
+//                B  y_i = P_i^-1 (b_i - L_i y_{i-1})           i = 0 .. tw-1
+//                Z  x_tw = Z^-1 (b_tw - L_tw y_{tw-1} - U_tw z_{tw+1})
+//                D  x_i = y_i - P_i^-1 (U_i x_{i+1})           i = tw-1 .. lo   (owned rows only)
+//                U  x_i = z_i - Q_i^-1 (L_i x_{i-1})           i = tw+1 .. hi   (owned rows only)
+//   prolong    z[g] = x_i[t] for the owned nodes of block j only (restricted owner write, D10) -- no
+//              atomics, each global node written exactly once.
+// The dense m x m inverse blocks dominate the bytes.  They are streamed HBM -> shared
+// memory by one producer thread with cp.async.bulk (TMA bulk copies) into an NS-slot ring guarded by
+// mbarriers (full: complete_tx, empty: one arrive per consumer warp), so the stream runs ahead of the
+// serial block-row dependency chain.  Consumer thread t owns row t of every block: the GEMV reads column
+// c of the column-major block (consecutive lanes -> consecutive 16-byte words, conflict-free) and the
+// broadcast operand rhs[c].
+#include "internal.cuh"
+
+namespace {
+
+constexpr int NS = 8;              // ring slots
+constexpr int SLOT_TARGET = 12288; // bytes per slot (rounded down to whole columns of m_max)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    uint32_t ok = 0;
+    const uint32_t a = smem_u32(bar);
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_bar(int nthreads)
+{
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+enum { PH_T = 0, PH_B = 1, PH_Z = 2, PH_D = 3, PH_U = 4 };
+
+struct Step { int ph, i; };
+
+__device__ __forceinline__ int nsteps(const SubDesc& d) { return d.nb + d.hi - d.lo; }
+
+__device__ __forceinline__ Step step_of(const SubDesc& d, int s)
+{
+    const int nT = d.nb - 1 - d.tw, nB = d.tw, nD = d.tw - d.lo;
+    if (s < nT) return {PH_T, d.nb - 1 - s};
+    s -= nT;
+    if (s < nB) return {PH_B, s};
+    s -= nB;
+    if (s == 0) return {PH_Z, d.tw};
+    s -= 1;
+    if (s < nD) return {PH_D, d.tw - 1 - s};
+    s -= nD;
+    return {PH_U, d.tw + 1 + s};
+}
+
+// operands a consumer thread needs for one step, loaded one step ahead
+struct Pre {
+    z2 b;         // restricted input b_i[t]      (T, B, Z)
+    z2 c0, c1;    // coupling pair                (T: N,NE  B: S,SW  D: N,NE  U: S,SW  Z: S,SW)
+    z2 c2, c3;    // second pair for Z            (N, NE)
+    z2 yz;        // y_i / z_i from scratch       (D, U)
+};
+
+__device__ __forceinline__ void prefetch(Pre& p, const SubDesc& d, Step st, int t, const ApplyArgs& a,
+                                         const z2* scr)
+{
+    if (t >= d.m) return;
+    const z2* row = a.stencil + d.stc_off + (long long)st.i * 7 * d.m;
+    if (st.ph <= PH_Z) {
+        const long long gi = d.gx0 + t - a.in_i0, gj = d.gy0 + st.i - a.in_j0;
+        p.b = __ldg(a.in + gi + a.in_stride * gj);
+    }
+    if (st.ph == PH_T || st.ph == PH_D) {
+        p.c0 = __ldg(row + SL_N * d.m + t);
+        p.c1 = __ldg(row + SL_NE * d.m + t);
+    } else {
+        p.c0 = __ldg(row + SL_S * d.m + t);
+        p.c1 = __ldg(row + SL_SW * d.m + t);
+    }
+    if (st.ph == PH_Z) {
+        p.c2 = __ldg(row + SL_N * d.m + t);
+        p.c3 = __ldg(row + SL_NE * d.m + t);
+    }
+    if (st.ph >= PH_D) p.yz = scr[(long long)(st.i - d.lo) * d.m + t];
+}
+
+__global__ void k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * slot_bytes);
+    uint64_t* empty = full + NS;
+    z2* vb = reinterpret_cast<z2*>(empty + NS);   // bottom chain carry / down-expansion carry
+    const int nct = nc_warps * 32;                // consumer threads
+    z2* vt = vb + nct + 1;                        // top chain carry / up-expansion carry
+    z2* rhs = vt + nct + 1;                       // GEMV operand
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < NS; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], nc_warps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == nc_warps) {
+        // ---------------------------------------------------------------- producer: stream the factors
+        if (lane != 0) return;
+        uint32_t k = 0;
+        for (int w = blockIdx.x; w < a.nsub; w += gridDim.x) {
+            const SubDesc d = a.desc[a.order[w]];
+            const int kc = slot_bytes / (d.m * (int)sizeof(z2));
+            const int S = nsteps(d);
+            for (int s = 0; s < S; s++) {
+                const Step st = step_of(d, s);
+                const z2* blk = a.dinv + d.fac_off + (long long)st.i * d.m * d.m;
+                for (int c0 = 0; c0 < d.m; c0 += kc, k++) {
+                    const int nc = min(kc, d.m - c0);
+                    const uint32_t slot = k % NS, ph = (k / NS) & 1;
+                    mbar_wait(&empty[slot], ph ^ 1);
+                    const uint32_t bytes = (uint32_t)(nc * d.m * sizeof(z2));
+                    mbar_arrive_expect_tx(&full[slot], bytes);
+                    bulk_g2s(ring + (size_t)slot * slot_bytes, blk + (long long)c0 * d.m, bytes, &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+
+    // -------------------------------------------------------------------- consumers: solve the chain
+    const int t = tid;
+    uint32_t k = 0;
+    z2* scr = a.scratch + (long long)blockIdx.x * a.scratch_per_cta;
+    for (int w = blockIdx.x; w < a.nsub; w += gridDim.x) {
+        const SubDesc d = a.desc[a.order[w]];
+        const int m = d.m;
+        const bool act = t < m;
+        const int kc = slot_bytes / (m * (int)sizeof(z2));
+        const int S = nsteps(d);
+        Pre cur, nxt;
+        prefetch(cur, d, step_of(d, 0), t, a, scr);
+        for (int s = 0; s < S; s++) {
+            const Step st = step_of(d, s);
+            if (s + 1 < S) prefetch(nxt, d, step_of(d, s + 1), t, a, scr);
+            // ---- right-hand side of this block step
+            z2 r = zmk(0, 0);
+            if (act) {
+                switch (st.ph) {
+                case PH_T:
+                    r = cur.b;
+                    if (st.i < d.nb - 1) {
+                        zfma(r, zmk(-cur.c0.x, -cur.c0.y), vt[t]);
+                        if (t + 1 < m) zfma(r, zmk(-cur.c1.x, -cur.c1.y), vt[t + 1]);
+                    }
+                    break;
+                case PH_B:
+                    r = cur.b;
+                    if (st.i > 0) {
+                        zfma(r, zmk(-cur.c0.x, -cur.c0.y), vb[t]);
+                        if (t > 0) zfma(r, zmk(-cur.c1.x, -cur.c1.y), vb[t - 1]);
+                    }
+                    break;
+                case PH_Z:
+                    r = cur.b;
+                    if (st.i > 0) {
+                        zfma(r, zmk(-cur.c0.x, -cur.c0.y), vb[t]);
+                        if (t > 0) zfma(r, zmk(-cur.c1.x, -cur.c1.y), vb[t - 1]);
+                    }
+                    if (st.i < d.nb - 1) {
+                        zfma(r, zmk(-cur.c2.x, -cur.c2.y), vt[t]);
+                        if (t + 1 < m) zfma(r, zmk(-cur.c3.x, -cur.c3.y), vt[t + 1]);
+                    }
+                    break;
+                case PH_D:   // U_i x_{i+1}
+                    zfma(r, cur.c0, vb[t]);
+                    if (t + 1 < m) zfma(r, cur.c1, vb[t + 1]);
+                    break;
+                default:     // PH_U: L_i x_{i-1}
+                    zfma(r, cur.c0, vt[t]);
+                    if (t > 0) zfma(r, cur.c1, vt[t - 1]);
+                    break;
+                }
+                rhs[t] = r;
+            }
+            consumer_bar(nct);
+            // ---- GEMV with the streamed block: acc = Dinv_i rhs
+            z2 acc0 = zmk(0, 0), acc1 = zmk(0, 0);
+            for (int c0 = 0; c0 < m; c0 += kc, k++) {
+                const int nc = min(kc, m - c0);
+                const uint32_t slot = k % NS, ph = (k / NS) & 1;
+                mbar_wait(&full[slot], ph);
+                const z2* col = reinterpret_cast<const z2*>(ring + (size_t)slot * slot_bytes);
+                if (act) {
+                    int c = 0;
+#pragma unroll 4
+                    for (; c + 1 < nc; c += 2) {
+                        zfma(acc0, col[(size_t)c * m + t], rhs[c0 + c]);
+                        zfma(acc1, col[(size_t)(c + 1) * m + t], rhs[c0 + c + 1]);
+                    }
+                    if (c < nc) zfma(acc0, col[(size_t)c * m + t], rhs[c0 + c]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+            }
+            const z2 acc = zadd(acc0, acc1);
+            // ---- finish the step
+            if (act) {
+                z2 x;
+                switch (st.ph) {
+                case PH_T:
+                    vt[t] = acc;
+                    if (st.i <= d.hi) scr[(long long)(st.i - d.lo) * m + t] = acc;
+                    break;
+                case PH_B:
+                    vb[t] = acc;
+                    if (st.i >= d.lo) scr[(long long)(st.i - d.lo) * m + t] = acc;
+                    break;
+                default:
+                    if (st.ph == PH_Z) {
+                        x = acc;
+                        vb[t] = x;
+                        vt[t] = x;
+                    } else if (st.ph == PH_D) {
+                        x = zsub(cur.yz, acc);
+                        vb[t] = x;
+                    } else {
+                        x = zsub(cur.yz, acc);
+                        vt[t] = x;
+                    }
+                    if (t >= d.olo && t <= d.ohi) {
+                        const long long gi = d.gx0 + t - a.out_i0, gj = d.gy0 + st.i - a.out_j0;
+                        a.out[gi + a.out_stride * gj] = x;
+                    }
+                    break;
+                }
+            }
+            consumer_bar(nct);
+            cur = nxt;
+        }
+    }
+}
+
+int slot_bytes_for(int m_max)
+{
+    int kc = SLOT_TARGET / (m_max * (int)sizeof(z2));
+    if (kc < 1) kc = 1;
+    return kc * m_max * (int)sizeof(z2);
+}
+
+}  // namespace
+
+int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm)
+{
+    const int ncw = (m_max + 31) / 32;
+    *block_threads = 32 * (ncw + 1);
+    *slot_bytes = slot_bytes_for(m_max);
+    *smem_bytes = NS * *slot_bytes + 2 * NS * 8 + 3 * (32 * ncw + 1) * (int)sizeof(z2);
+    cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem_bytes);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply, *block_threads, *smem_bytes);
+    *ctas_per_sm = occ;
+    return ncw;
+}
+
+void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s)
+{
+    k_apply<<<grid, block, smem, s>>>(a, block / 32 - 1, slot_bytes);
+}

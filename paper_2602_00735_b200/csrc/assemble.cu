@@ -1,0 +1,213 @@
+// assemble.cu -- structured-mesh assembly of the PML P1 operators on the device.
+//
+//   K1 assemble_global : 7 coefficients per free row of A (eq. (weak)), SoA slots [7][n_local]
+//   K2 assemble_local  : 7 coefficients per local free node of every A_j, [nb][7][m] per subdomain
+//   K10 rhs            : f at the free nodes (sum of Gaussians, D14) then b = M f with the P1 mass stencil
+//
+// Each row is gathered from the six triangles around its node (a per-row formulation; the oracle
+// scatters element matrices instead).  PML coefficients D = diag(gamma^-2), beta = gamma'/gamma^3
+// are frozen at the triangle centroid (D5); gamma_i = 1 + i g_i' with the profile
+// g(t) = sigma0 t^3/(3 kappa^2), linear beyond kappa (BASELINE.json configs[0]; D3).  Lower-side ramps
+// are g_i(x) = -g(a - x), so gamma' = -i g''(a - x) there (D4).
+#include "internal.cuh"
+
+namespace {
+
+__device__ __forceinline__ void ramp_d(long d3, bool upper, const Geom& g, z2& gam, z2& dgam)
+{
+    double t = (double)d3 * g.h3;
+    double g1, g2;
+    if (t <= g.kappa) {
+        g1 = g.sigma0 * t * t / (g.kappa * g.kappa);
+        g2 = 2.0 * g.sigma0 * t / (g.kappa * g.kappa);
+    } else {
+        g1 = g.sigma0;
+        g2 = 0.0;
+    }
+    gam = zmk(1.0, g1);
+    dgam = zmk(0.0, upper ? g2 : -g2);
+}
+
+// global scaling g_i: ramps above node N - n_g and below node n_g
+__device__ __forceinline__ void gamma_global(long X3, const Geom& g, z2& gam, z2& dgam)
+{
+    if (X3 > g.hi3) ramp_d(X3 - g.hi3, true, g, gam, dgam);
+    else if (X3 < g.lo3) ramp_d(g.lo3 - X3, false, g, gam, dgam);
+    else { gam = zmk(1.0, 0.0); dgam = zmk(0.0, 0.0); }
+}
+
+// local scaling g_j^i: upper ramp from b_j, lower ramp from a_j, global g_i in between; only on
+// faces carrying a local PML (kappa_{j,l/u} != 0)
+__device__ __forceinline__ void gamma_local(long X3, long a3, long b3, bool has_lo, bool has_hi, const Geom& g,
+                                            z2& gam, z2& dgam)
+{
+    if (has_hi && X3 > b3) ramp_d(X3 - b3, true, g, gam, dgam);
+    else if (has_lo && X3 < a3) ramp_d(a3 - X3, false, g, gam, dgam);
+    else gamma_global(X3, g, gam, dgam);
+}
+
+// The six triangles around node (i, j): cell offset, triangle (0 = lower SW->NE half, 1 = upper half) and
+// the node's vertex index in that triangle.  Triangle vertices relative to the cell corner:
+//   lower {(0,0),(1,0),(1,1)}, upper {(0,0),(1,1),(0,1)}  (D1); h * grad phi: see TG.
+struct TriRef { int cdx, cdy, tri, a; };
+__constant__ TriRef c_tris[6] = { {-1, -1, 0, 2}, {-1, -1, 1, 1}, {0, -1, 1, 2},
+                                  {-1, 0, 0, 1},  {0, 0, 0, 0},   {0, 0, 1, 0} };
+__constant__ int c_tv[2][3][2] = { { {0, 0}, {1, 0}, {1, 1} }, { {0, 0}, {1, 1}, {0, 1} } };
+__constant__ double c_tg[2][3][2] = { { {-1, 0}, {1, -1}, {0, 1} }, { {0, -1}, {1, 0}, {-1, 1} } };
+__constant__ int c_c3[2][2] = { {2, 1}, {1, 2} };   // centroid offset in thirds
+
+__device__ __forceinline__ int slot_of(int dx, int dy)
+{
+    // (0,0) C, (1,0) E, (-1,0) W, (0,1) N, (0,-1) S, (1,1) NE, (-1,-1) SW
+    if (dy == 0) return dx == 0 ? SL_C : (dx > 0 ? SL_E : SL_W);
+    if (dx == 0) return dy > 0 ? SL_N : SL_S;
+    return dx > 0 ? SL_NE : SL_SW;
+}
+
+// Row of node (i, j) (global node indices): A[p][q] = 1/2 (D11 gx_p gx_q + D22 gy_p gy_q)
+//   - h/6 (beta1 gx_q + beta2 gy_q) - k^2 h^2 / 24 (1 + delta_pq), with g = h grad phi.
+template <class GammaFn>
+__device__ void node_row(int i, int j, const Geom& g, GammaFn gam_at, z2 row[7])
+{
+    for (int s = 0; s < 7; s++) row[s] = zmk(0.0, 0.0);
+    const double kh2_24 = g.k * g.k * g.h * g.h / 24.0;
+    const double h6 = g.h / 6.0;
+#pragma unroll
+    for (int e = 0; e < 6; e++) {
+        const TriRef T = c_tris[e];
+        const int ci = i + T.cdx, cj = j + T.cdy, tri = T.tri, a = T.a;
+        z2 gx, dgx, gy, dgy;
+        gam_at(0, 3L * ci + c_c3[tri][0], gx, dgx);
+        gam_at(1, 3L * cj + c_c3[tri][1], gy, dgy);
+        const z2 ix = zinv(gx), iy = zinv(gy);
+        const z2 D11 = zmul(ix, ix), D22 = zmul(iy, iy);
+        const z2 b1 = zmul(dgx, zmul(D11, ix)), b2 = zmul(dgy, zmul(D22, iy));
+        const double gxa = c_tg[tri][a][0], gya = c_tg[tri][a][1];
+        for (int q = 0; q < 3; q++) {
+            const double gxq = c_tg[tri][q][0], gyq = c_tg[tri][q][1];
+            z2 v = zadd(zscale(D11, 0.5 * gxa * gxq), zscale(D22, 0.5 * gya * gyq));
+            v = zsub(v, zscale(zadd(zscale(b1, gxq), zscale(b2, gyq)), h6));
+            v.x -= kh2_24 * (q == a ? 2.0 : 1.0);
+            const int dx = T.cdx + c_tv[tri][q][0], dy = T.cdy + c_tv[tri][q][1];
+            const int s = slot_of(dx, dy);
+            row[s] = zadd(row[s], v);
+        }
+    }
+}
+
+__constant__ int c_sdx[7] = { 0, 1, -1, 0, 0, 1, -1 };
+__constant__ int c_sdy[7] = { 0, 0, 0, 1, -1, 1, -1 };
+
+__global__ void k_assemble_global(Geom g, z2* __restrict__ A7, int i0, int i1, int j0, int j1)
+{
+    const long long w = i1 - i0, n = w * (long long)(j1 - j0);
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        const int i = i0 + (int)(r % w), j = j0 + (int)(r / w);
+        z2 row[7];
+        node_row(i, j, g, [&](int, long X3, z2& ga, z2& dga) { gamma_global(X3, g, ga, dga); }, row);
+#pragma unroll
+        for (int s = 0; s < 7; s++) {
+            const int qi = i + c_sdx[s], qj = j + c_sdy[s];
+            const bool free_q = qi >= 1 && qi <= g.nf && qj >= 1 && qj <= g.nf;
+            A7[s * n + r] = free_q ? row[s] : zmk(0.0, 0.0);
+        }
+    }
+}
+
+__global__ void k_assemble_local(Geom g, const SubDesc* __restrict__ desc, z2* __restrict__ stc)
+{
+    const SubDesc d = desc[blockIdx.y];
+    const int n = d.m * d.nb;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int t = r % d.m, row_i = r / d.m;
+        const int i = d.gx0 + t, j = d.gy0 + row_i;
+        z2 rowv[7];
+        node_row(i, j, g,
+                 [&](int axis, long X3, z2& ga, z2& dga) {
+                     if (axis == 0) gamma_local(X3, d.ilo3, d.ihi3, d.flags & 1, d.flags & 2, g, ga, dga);
+                     else gamma_local(X3, d.jlo3, d.jhi3, d.flags & 4, d.flags & 8, g, ga, dga);
+                 },
+                 rowv);
+        z2* out = stc + d.stc_off + (long long)row_i * 7 * d.m + t;
+#pragma unroll
+        for (int s = 0; s < 7; s++) {
+            const int qt = t + c_sdx[s], qr = row_i + c_sdy[s];
+            const bool inside = qt >= 0 && qt < d.m && qr >= 0 && qr < d.nb;   // Dirichlet on dOmega_j (D9)
+            out[s * d.m] = inside ? rowv[s] : zmk(0.0, 0.0);
+        }
+    }
+}
+
+// f at the free nodes of [i0-1, i1] x [j0-1, j1] (clipped), stored with a one-node frame
+__global__ void k_rhs_f(Geom g, int nsrc, const double* __restrict__ xy, const z2* __restrict__ amp, double sigma,
+                        z2* __restrict__ f, int i0, int i1, int j0, int j1)
+{
+    const int fw = i1 - i0 + 2, fh = j1 - j0 + 2;
+    const long long n = (long long)fw * fh;
+    const double c = 1.0 / (2.0 * M_PI * sigma * sigma), e = 1.0 / (2.0 * sigma * sigma);
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        const int i = i0 - 1 + (int)(r % fw), j = j0 - 1 + (int)(r / fw);
+        z2 acc = zmk(0.0, 0.0);
+        if (i >= 1 && i <= g.nf && j >= 1 && j <= g.nf) {
+            const double x = (i - g.ng) * g.h, y = (j - g.ng) * g.h;
+            for (int s = 0; s < nsrc; s++) {
+                const double dx = x - xy[2 * s], dy = y - xy[2 * s + 1];
+                const double w = c * exp(-(dx * dx + dy * dy) * e);
+                acc = zadd(acc, zscale(amp[s], w));
+            }
+        }
+        f[r] = acc;
+    }
+}
+
+// b = M f: consistent P1 mass stencil on the SW->NE mesh: centre h^2/2, E W N S NE SW h^2/12 (PML-free,
+// the k^2 u v term of eq. (weak) carries no gamma)
+__global__ void k_rhs_b(Geom g, const z2* __restrict__ f, z2* __restrict__ b, int i0, int i1, int j0, int j1)
+{
+    const int w = i1 - i0, fw = w + 2;
+    const long long n = (long long)w * (j1 - j0);
+    const double mc = g.h * g.h / 2.0, mo = g.h * g.h / 12.0;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        const int li = (int)(r % w) + 1, lj = (int)(r / w) + 1;
+        const z2* fc = f + li + (long long)fw * lj;
+        z2 acc = zscale(fc[0], mc);
+        z2 o = zadd(zadd(fc[1], fc[-1]), zadd(fc[fw], fc[-fw]));
+        o = zadd(o, zadd(fc[fw + 1], fc[-fw - 1]));
+        b[r] = zadd(acc, zscale(o, mo));   // f is 0 at Dirichlet nodes (frame filled with zeros there)
+    }
+}
+
+int grid_for(long long n, int threads)
+{
+    long long b = (n + threads - 1) / threads;
+    if (b > 148LL * 32) b = 148LL * 32;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+void launch_assemble_global(const Geom& g, z2* A7, int i0, int i1, int j0, int j1, cudaStream_t s)
+{
+    const long long n = (long long)(i1 - i0) * (j1 - j0);
+    k_assemble_global<<<grid_for(n, 256), 256, 0, s>>>(g, A7, i0, i1, j0, j1);
+}
+
+void launch_assemble_local(const Geom& g, const SubDesc* d_desc, int nsub, z2* stencil, int max_n, cudaStream_t s)
+{
+    // blockIdx.y = subdomain (nsub <= 65535 per launch chunk)
+    const int per = 256;
+    for (int base = 0; base < nsub; base += 65535) {
+        const int cnt = nsub - base < 65535 ? nsub - base : 65535;
+        dim3 grid((max_n + per - 1) / per, cnt);
+        k_assemble_local<<<grid, per, 0, s>>>(g, d_desc + base, stencil);
+    }
+}
+
+void launch_rhs(const Geom& g, int nsrc, const double* d_xy, const z2* d_amp, double sigma, z2* f_work, z2* b,
+                int i0, int i1, int j0, int j1, cudaStream_t s)
+{
+    const long long nf = (long long)(i1 - i0 + 2) * (j1 - j0 + 2);
+    k_rhs_f<<<grid_for(nf, 256), 256, 0, s>>>(g, nsrc, d_xy, d_amp, sigma, f_work, i0, i1, j0, j1);
+    const long long n = (long long)(i1 - i0) * (j1 - j0);
+    k_rhs_b<<<grid_for(n, 256), 256, 0, s>>>(g, f_work, b, i0, i1, j0, j1);
+}

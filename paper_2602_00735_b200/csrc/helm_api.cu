@@ -1,0 +1,694 @@
+// helm_api.cu -- host side of libhelm: the C ABI of include/helm.h, grid and decomposition, device memory,
+// and the restarted GMRES driver.  Every arithmetic step on vectors runs in this library's kernels; the host
+// only sizes the problem, launches, and performs the O(restart^2) Givens / triangular-solve bookkeeping of
+// GMRES on at most restart+1 scalars per iteration (D13).
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <complex>
+#include <vector>
+
+#include "internal.cuh"
+
+typedef std::complex<double> cplx;
+
+struct helm_ctx {
+    helm_params p{};
+    int rank = 0, nranks = 1;
+    cudaStream_t stream = nullptr;
+    char err[512] = {0};
+
+    // grid (D2) and widths
+    int n_int = 0, N = 0, nf = 0, ng = 0, wo = 0, wp = 0;
+    double h = 0;
+    Geom geom{};
+    // this rank's owned rectangle of free nodes, [i0,i1) x [j0,j1), 1-based node indices
+    int i0 = 1, i1 = 1, j0 = 1, j1 = 1;
+    long long n_local = 0;
+
+    // subdomains held by this rank
+    std::vector<SubDesc> subs;
+    int n_sub_total = 0, m_max = 0;
+    long long max_n = 0, local_unknowns = 0, n_dinv = 0, n_stc = 0;
+    long long apply_bytes = 0, band_bytes = 0;
+    SubDesc* d_desc = nullptr;
+    int* d_order = nullptr;
+    z2* d_A7 = nullptr;
+    z2* d_stc = nullptr;
+    z2* d_dinv = nullptr;
+    z2* d_scratch = nullptr;
+    long long scratch_per_cta = 0;
+    int* d_err = nullptr;
+    bool factored = false;
+
+    // apply launch configuration
+    int ap_block = 0, ap_smem = 0, ap_slot = 0, ap_grid = 0, ap_occ = 0;
+
+    // Krylov workspace
+    z2* d_V = nullptr;
+    int V_cap = 0;
+    z2 *d_w = nullptr, *d_z = nullptr, *d_t = nullptr, *d_r = nullptr, *d_xb = nullptr, *d_bb = nullptr;
+    z2 *d_h1 = nullptr, *d_h2 = nullptr, *d_Hcol = nullptr, *d_y = nullptr;
+    double* d_norm = nullptr;
+    z2* d_zpart = nullptr;
+    double* d_dpart = nullptr;
+    int nblk = 148 * 4;
+    z2* h_pin = nullptr;   // pinned host staging for H columns / y (NVMAX complex)
+
+    // profiling of the apply kernel
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_free;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
+    int launches = 0;
+};
+
+static int set_err(helm_ctx* ctx, int code, const char* fmt, ...)
+{
+    if (ctx) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CK(expr) HELM_CUDA_OK(expr)
+
+namespace {
+
+constexpr int NVMAX = 64;
+constexpr int M_LIMIT = 112;   // factor kernel keeps an m x m complex block in shared memory
+
+int round_half_up(double x) { return (int)floor(x + 0.5); }
+
+template <class T>
+int dalloc(helm_ctx* ctx, T** p, size_t count)
+{
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(ctx, HELM_ENOMEM, "cudaMalloc of %.3f GB failed: %s", count * sizeof(T) / 1e9,
+                       cudaGetErrorString(e));
+    }
+    return HELM_OK;
+}
+
+// Cartesian block starts: N cells into P blocks of floor/ceil size, larger blocks first (D8)
+std::vector<int> block_starts(int N, int P)
+{
+    std::vector<int> s(P + 1, 0);
+    const int q = N / P, r = N % P;
+    for (int b = 0; b < P; b++) s[b + 1] = s[b] + q + (b < r ? 1 : 0);
+    return s;
+}
+
+int build_layout(helm_ctx* ctx)
+{
+    const helm_params& p = ctx->p;
+    if (!(p.k > 0) || p.ppw < 1 || p.n_pml_global < 1 || p.nsub_x < 1 || p.nsub_y < 1 || p.sigma0 < 0)
+        return set_err(ctx, HELM_EINVAL, "invalid parameters (k, ppw, n_pml_global, nsub, sigma0)");
+    if (p.local_bc != HELM_BC_DIRICHLET)
+        return set_err(ctx, HELM_EINVAL, "only HELM_BC_DIRICHLET (RAS-PML-Drch) is implemented");
+    // O1 / D2: n_int = round(ppw k / 2 pi) cells on (0,1), h = 1 / n_int, N = n_int + 2 n_g
+    ctx->n_int = round_half_up(p.ppw * p.k / (2.0 * M_PI));
+    if (ctx->n_int < 1) return set_err(ctx, HELM_EINVAL, "k * ppw too small: no interior cell");
+    ctx->h = 1.0 / ctx->n_int;
+    ctx->ng = p.n_pml_global;
+    ctx->N = ctx->n_int + 2 * ctx->ng;
+    ctx->nf = ctx->N - 1;
+    // BJ configs[0]: delta = kappa = max(2, round(1.59 ln k)) cells unless given
+    const int wdef = std::max(2, round_half_up(1.59 * log(p.k)));
+    ctx->wo = p.n_ovlp < 0 ? wdef : p.n_ovlp;
+    ctx->wp = p.n_pml < 0 ? wdef : p.n_pml;
+
+    Geom& g = ctx->geom;
+    g.k = p.k;
+    g.h = ctx->h;
+    g.h3 = ctx->h / 3.0;
+    g.sigma0 = p.sigma0;
+    g.kappa = ctx->ng * ctx->h;   // D3: one profile, kappa = kappa_g
+    g.N = ctx->N;
+    g.nf = ctx->nf;
+    g.ng = ctx->ng;
+    g.lo3 = 3L * ctx->ng;
+    g.hi3 = 3L * (ctx->N - ctx->ng);
+
+    // covering (D8)
+    const int P[2] = {p.nsub_x, p.nsub_y};
+    std::vector<int> st[2] = {block_starts(ctx->N, P[0]), block_starts(ctx->N, P[1])};
+    const int w = ctx->wo + ctx->wp;
+    for (int ax = 0; ax < 2; ax++)
+        for (int b = 0; b < P[ax]; b++) {
+            const int sz = st[ax][b + 1] - st[ax][b];
+            if (sz < 2 || (P[ax] > 1 && sz < w))
+                return set_err(ctx, HELM_ELAYOUT,
+                               "block %d on axis %d has %d cells; needs >= delta + kappa = %d (and >= 2)", b, ax, sz, w);
+        }
+    ctx->n_sub_total = P[0] * P[1];
+
+    // rank grid over the subdomain grid
+    int gx = p.gpu_grid_x, gy = p.gpu_grid_y;
+    if (gx <= 0 || gy <= 0) { gx = 1; gy = ctx->nranks; }
+    if (gx * gy != ctx->nranks || gx > P[0] || gy > P[1])
+        return set_err(ctx, HELM_EINVAL, "gpu grid %dx%d does not match %d ranks / %dx%d subdomains", gx, gy,
+                       ctx->nranks, P[0], P[1]);
+    const int rx = ctx->rank % gx, ry = ctx->rank / gx;
+    const std::vector<int> sbx = block_starts(P[0], gx), sby = block_starts(P[1], gy);
+    const int bx0 = sbx[rx], bx1 = sbx[rx + 1], by0 = sby[ry], by1 = sby[ry + 1];
+    // owned free nodes of this rank: union of its blocks' owned nodes (D10)
+    ctx->i0 = std::max(st[0][bx0], 1);
+    ctx->i1 = std::min(st[0][bx1], ctx->N);
+    ctx->j0 = std::max(st[1][by0], 1);
+    ctx->j1 = std::min(st[1][by1], ctx->N);
+    ctx->n_local = (long long)(ctx->i1 - ctx->i0) * (ctx->j1 - ctx->j0);
+
+    long long fac = 0, stc = 0;
+    ctx->subs.clear();
+    ctx->m_max = 0;
+    ctx->max_n = 0;
+    ctx->local_unknowns = 0;
+    ctx->apply_bytes = 0;
+    ctx->band_bytes = 0;
+    long long owned_total = 0;
+    for (int by = by0; by < by1; by++)
+        for (int bx = bx0; bx < bx1; bx++) {
+            const int bb[2] = {bx, by};
+            int own_lo[2], own_hi[2], int_lo[2], int_hi[2], full_lo[2], full_hi[2], has_lo[2], has_hi[2];
+            for (int ax = 0; ax < 2; ax++) {
+                const int b = bb[ax];
+                own_lo[ax] = st[ax][b];
+                own_hi[ax] = st[ax][b + 1];
+                has_lo[ax] = b > 0;
+                has_hi[ax] = b < P[ax] - 1;
+                int_lo[ax] = own_lo[ax] - (has_lo[ax] ? ctx->wo : 0);
+                int_hi[ax] = own_hi[ax] + (has_hi[ax] ? ctx->wo : 0);
+                full_lo[ax] = int_lo[ax] - (has_lo[ax] ? ctx->wp : 0);
+                full_hi[ax] = int_hi[ax] + (has_hi[ax] ? ctx->wp : 0);
+                if (full_lo[ax] < 0 || full_hi[ax] > ctx->N)
+                    return set_err(ctx, HELM_ELAYOUT, "full box of subdomain (%d,%d) leaves Omega", bx, by);
+            }
+            SubDesc d{};
+            d.m = full_hi[0] - full_lo[0] - 1;
+            d.nb = full_hi[1] - full_lo[1] - 1;
+            d.gx0 = full_lo[0] + 1;
+            d.gy0 = full_lo[1] + 1;
+            d.olo = std::max(own_lo[0], 1) - d.gx0;
+            d.ohi = std::min(own_hi[0], ctx->N) - 1 - d.gx0;
+            d.lo = std::max(own_lo[1], 1) - d.gy0;
+            d.hi = std::min(own_hi[1], ctx->N) - 1 - d.gy0;
+            d.tw = (d.lo + d.hi) / 2;
+            d.ilo3 = 3 * int_lo[0];
+            d.ihi3 = 3 * int_hi[0];
+            d.jlo3 = 3 * int_lo[1];
+            d.jhi3 = 3 * int_hi[1];
+            d.flags = (has_lo[0] ? 1 : 0) | (has_hi[0] ? 2 : 0) | (has_lo[1] ? 4 : 0) | (has_hi[1] ? 8 : 0);
+            d.fac_off = fac;
+            d.stc_off = stc;
+            if (d.m > M_LIMIT)
+                return set_err(ctx, HELM_EINVAL, "local block width %d exceeds %d (use more subdomains)", d.m, M_LIMIT);
+            fac += (long long)d.nb * d.m * d.m;
+            stc += (long long)d.nb * 7 * d.m;
+            ctx->m_max = std::max(ctx->m_max, d.m);
+            const long long n = (long long)d.m * d.nb;
+            ctx->max_n = std::max(ctx->max_n, n);
+            ctx->local_unknowns += n;
+            ctx->scratch_per_cta = std::max(ctx->scratch_per_cta, (long long)(d.hi - d.lo + 1) * d.m);
+            // algorithmic bytes of one apply of this subdomain
+            const long long nblocks = d.nb + d.hi - d.lo;
+            const long long owned = (long long)(d.ohi - d.olo + 1) * (d.hi - d.lo + 1);
+            owned_total += owned;
+            ctx->apply_bytes += 16 * (nblocks * d.m * d.m      // explicit inverse blocks streamed
+                                      + n                      // restriction gather
+                                      + 2LL * nblocks * d.m    // two coupling vectors per block step
+                                      + 2LL * (d.hi - d.lo) * d.m   // y / z scratch written + read
+                                      + owned);                // owner write
+            ctx->band_bytes += 16 * (n * (2LL * (d.m + 1) + 1) + n + owned);
+            ctx->subs.push_back(d);
+        }
+    (void)owned_total;
+    ctx->n_dinv = fac;
+    ctx->n_stc = stc;
+    return HELM_OK;
+}
+
+int ensure_krylov(helm_ctx* ctx, int restart)
+{
+    int rc;
+    const long long n = ctx->n_local;
+    if (!ctx->d_w) {
+        if ((rc = dalloc(ctx, &ctx->d_w, n)) || (rc = dalloc(ctx, &ctx->d_z, n)) || (rc = dalloc(ctx, &ctx->d_t, n)) ||
+            (rc = dalloc(ctx, &ctx->d_r, n)) || (rc = dalloc(ctx, &ctx->d_h1, NVMAX)) ||
+            (rc = dalloc(ctx, &ctx->d_h2, NVMAX)) || (rc = dalloc(ctx, &ctx->d_Hcol, NVMAX)) ||
+            (rc = dalloc(ctx, &ctx->d_y, NVMAX)) || (rc = dalloc(ctx, &ctx->d_norm, 4)) ||
+            (rc = dalloc(ctx, &ctx->d_zpart, (size_t)ctx->nblk * NVMAX)) || (rc = dalloc(ctx, &ctx->d_dpart, ctx->nblk)))
+            return rc;
+        CK(cudaMallocHost((void**)&ctx->h_pin, sizeof(z2) * NVMAX));
+    }
+    if (restart + 1 > ctx->V_cap) {
+        if (ctx->d_V) cudaFree(ctx->d_V);
+        ctx->d_V = nullptr;
+        ctx->V_cap = 0;
+        if ((rc = dalloc(ctx, &ctx->d_V, (size_t)(restart + 1) * n))) return rc;
+        ctx->V_cap = restart + 1;
+    }
+    return HELM_OK;
+}
+
+int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
+{
+    if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
+    ApplyArgs a{};
+    a.desc = ctx->d_desc;
+    a.order = ctx->d_order;
+    a.nsub = (int)ctx->subs.size();
+    a.dinv = ctx->d_dinv;
+    a.stencil = ctx->d_stc;
+    a.in = r;
+    a.in_i0 = ctx->i0;
+    a.in_j0 = ctx->j0;
+    a.in_stride = ctx->i1 - ctx->i0;
+    a.out = z;
+    a.out_i0 = ctx->i0;
+    a.out_j0 = ctx->j0;
+    a.out_stride = ctx->i1 - ctx->i0;
+    a.scratch = ctx->d_scratch;
+    a.scratch_per_cta = ctx->scratch_per_cta;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof) {
+        if (ctx->ev_free.size() < 2) {
+            cudaEvent_t a0, a1;
+            CK(cudaEventCreate(&a0));
+            CK(cudaEventCreate(&a1));
+            ctx->ev_free.push_back(a0);
+            ctx->ev_free.push_back(a1);
+        }
+        e1 = ctx->ev_free.back();
+        ctx->ev_free.pop_back();
+        e0 = ctx->ev_free.back();
+        ctx->ev_free.pop_back();
+        CK(cudaEventRecord(e0, ctx->stream));
+    }
+    launch_apply(a, ctx->ap_grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->stream);
+    CK(cudaGetLastError());
+    ctx->launches++;
+    if (ctx->prof) {
+        CK(cudaEventRecord(e1, ctx->stream));
+        ctx->ev_used.push_back({e0, e1});
+    }
+    return HELM_OK;
+}
+
+// ||v|| on the device, copied to the host (synchronises)
+int norm_host(helm_ctx* ctx, const z2* v, double* out)
+{
+    launch_norm_partial(v, ctx->n_local, ctx->d_dpart, ctx->nblk, ctx->stream);
+    launch_reduce_norm(ctx->d_dpart, ctx->nblk, nullptr, ctx->d_norm, ctx->stream);
+    CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_norm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    memcpy(out, ctx->h_pin, sizeof(double));
+    return HELM_OK;
+}
+
+// r = b - A x and ||r|| (host)
+int residual_host(helm_ctx* ctx, const z2* b, const z2* x, z2* r, double* out)
+{
+    const int nx = ctx->i1 - ctx->i0, ny = ctx->j1 - ctx->j0;
+    launch_residual(ctx->d_A7, x, b, r, nx, ny, ctx->d_dpart, ctx->nblk, ctx->stream);
+    launch_reduce_norm(ctx->d_dpart, ctx->nblk, nullptr, ctx->d_norm, ctx->stream);
+    CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_norm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    memcpy(out, ctx->h_pin, sizeof(double));
+    return HELM_OK;
+}
+
+// Right-preconditioned restarted GMRES (O9 of DESIGN.md), classical Gram-Schmidt with one
+// re-orthogonalisation pass (CGS2) on the device, Givens rotations on the host.
+int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int maxit, helm_gmres_info* info)
+{
+    if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "gmres before helm_factor");
+    if (restart < 1 || restart + 1 > NVMAX || maxit < 0)
+        return set_err(ctx, HELM_EINVAL, "restart must be in [1, %d], maxit >= 0", NVMAX - 1);
+    int rc;
+    if ((rc = ensure_krylov(ctx, restart))) return rc;
+    const long long n = ctx->n_local;
+    const int nx = ctx->i1 - ctx->i0, ny = ctx->j1 - ctx->j0;
+    cudaStream_t s = ctx->stream;
+    helm_gmres_info loc{};
+    helm_gmres_info* inf = info ? info : &loc;
+    inf->iterations = inf->restarts = inf->applies = 0;
+    inf->status = HELM_OK;
+    inf->relres_est = inf->relres_true = 0.0;
+
+    double beta0;
+    if ((rc = norm_host(ctx, b, &beta0))) return rc;
+    if (!(beta0 > 0.0)) {
+        if (beta0 == 0.0) {   // b = 0 -> x = 0, no iteration
+            CK(cudaMemsetAsync(x, 0, sizeof(z2) * n, s));
+            CK(cudaStreamSynchronize(s));
+            return HELM_OK;
+        }
+        inf->status = HELM_BREAKDOWN;
+        return HELM_BREAKDOWN;
+    }
+    double beta;
+    if ((rc = residual_host(ctx, b, x, ctx->d_r, &beta))) return rc;
+    const int m = restart;
+    std::vector<cplx> H((size_t)(m + 1) * m), g(m + 1), sn(m), y(m);
+    std::vector<double> cs(m);
+    auto Hij = [&](int i, int j) -> cplx& { return H[(size_t)i * m + j]; };
+    int its = 0, cycles = 0;
+    double est = beta / beta0;
+    z2* V = ctx->d_V;
+    while (true) {
+        // v_0 = r / ||r||
+        CK(cudaMemcpyAsync(ctx->d_norm, &beta, sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_scale_by_norm(ctx->d_r, ctx->d_norm, V, n, s);
+        std::fill(g.begin(), g.end(), cplx(0, 0));
+        g[0] = beta;
+        int jend = 0;
+        for (int j = 0; j < m; j++) {
+            z2* vj = V + (long long)j * n;
+            if ((rc = apply_impl(ctx, vj, ctx->d_z))) return rc;
+            inf->applies++;
+            launch_spmv(ctx->d_A7, ctx->d_z, ctx->d_w, nx, ny, s);
+            its++;
+            // CGS2: h1 = V^H w; w -= V h1; h2 = V^H w; w -= V h2; H(:,j) = h1 + h2; H(j+1,j) = ||w||
+            launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+            launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h1, nullptr, nullptr, s);
+            launch_multiaxpy(V, n, j + 1, ctx->d_h1, ctx->d_w, n, nullptr, ctx->nblk, s);
+            launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+            launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, ctx->d_Hcol, ctx->d_h1, s);
+            launch_multiaxpy(V, n, j + 1, ctx->d_h2, ctx->d_w, n, ctx->d_dpart, ctx->nblk, s);
+            launch_reduce_norm(ctx->d_dpart, ctx->nblk, ctx->d_Hcol + j + 1, ctx->d_norm, s);
+            launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_Hcol, sizeof(z2) * (j + 2), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (int i = 0; i <= j + 1; i++) Hij(i, j) = cplx(ctx->h_pin[i].x, ctx->h_pin[i].y);
+            const double hn = Hij(j + 1, j).real();
+            if (!std::isfinite(hn)) {
+                inf->iterations = its;
+                inf->status = HELM_BREAKDOWN;
+                return set_err(ctx, HELM_BREAKDOWN, "non-finite Arnoldi norm at iteration %d", its);
+            }
+            for (int i = 0; i < j; i++) {   // previous rotations
+                const cplx a = Hij(i, j), c = Hij(i + 1, j);
+                Hij(i, j) = cs[i] * a + sn[i] * c;
+                Hij(i + 1, j) = -std::conj(sn[i]) * a + cs[i] * c;
+            }
+            const cplx a = Hij(j, j), bb = Hij(j + 1, j);   // new rotation
+            if (a == cplx(0, 0)) {
+                cs[j] = 0.0;
+                sn[j] = 1.0;
+                Hij(j, j) = bb;
+            } else {
+                const double rho = sqrt(std::norm(a) + std::norm(bb));
+                const cplx ph = a / std::abs(a);
+                cs[j] = std::abs(a) / rho;
+                sn[j] = ph * std::conj(bb) / rho;
+                Hij(j, j) = ph * rho;
+            }
+            Hij(j + 1, j) = 0.0;
+            g[j + 1] = -std::conj(sn[j]) * g[j];
+            g[j] = cs[j] * g[j];
+            est = std::abs(g[j + 1]) / beta0;
+            if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
+            jend = j + 1;
+            if ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || hn == 0.0 || its >= maxit) break;
+        }
+        // H y = g (upper triangular), t = V y, x += B^-1 t
+        for (int i = jend - 1; i >= 0; i--) {
+            cplx acc = g[i];
+            for (int c = i + 1; c < jend; c++) acc -= Hij(i, c) * y[c];
+            y[i] = acc / Hij(i, i);
+        }
+        for (int i = 0; i < jend; i++) ctx->h_pin[i] = zmk(y[i].real(), y[i].imag());
+        CK(cudaMemcpyAsync(ctx->d_y, ctx->h_pin, sizeof(z2) * jend, cudaMemcpyHostToDevice, s));
+        launch_combine(V, n, jend, ctx->d_y, ctx->d_t, n, s);
+        if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
+        inf->applies++;
+        launch_axpy(x, ctx->d_z, n, s);
+        double rn;
+        if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
+        cycles++;
+        const double tr = rn / beta0;
+        inf->iterations = its;
+        inf->restarts = cycles - 1;
+        inf->relres_est = est;
+        inf->relres_true = tr;
+        if (!std::isfinite(tr)) {
+            inf->status = HELM_BREAKDOWN;
+            return set_err(ctx, HELM_BREAKDOWN, "non-finite residual");
+        }
+        if (rtol > 0 && tr <= rtol) {
+            inf->status = HELM_OK;
+            return HELM_OK;
+        }
+        if (its >= maxit) {
+            inf->status = HELM_NOT_CONVERGED;
+            return HELM_NOT_CONVERGED;
+        }
+        beta = rn;
+    }
+}
+
+}  // namespace
+
+// ===================================================================================================== C ABI
+extern "C" {
+
+int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id, void* cuda_stream,
+               helm_ctx** out)
+{
+    if (!params || !out) return HELM_EINVAL;
+    *out = nullptr;
+    helm_ctx* ctx = new helm_ctx();
+    ctx->p = *params;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    *out = ctx;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(ctx, HELM_EINVAL, "bad rank %d / %d", rank, nranks);
+    if (nranks > 1) {
+        (void)nccl_unique_id;
+        return set_err(ctx, HELM_ENCCL, "multi-rank execution is not built into this library yet");
+    }
+    int rc = build_layout(ctx);
+    if (rc) return rc;
+    // device buffers: global stencil, local stencils, descriptors
+    const int nsub = (int)ctx->subs.size();
+    if ((rc = dalloc(ctx, &ctx->d_A7, 7 * (size_t)ctx->n_local)) || (rc = dalloc(ctx, &ctx->d_stc, ctx->n_stc)) ||
+        (rc = dalloc(ctx, &ctx->d_desc, nsub)) || (rc = dalloc(ctx, &ctx->d_order, nsub)) ||
+        (rc = dalloc(ctx, &ctx->d_err, 4)))
+        return rc;
+    // processing order: most expensive first (static round-robin over persistent CTAs)
+    std::vector<int> order(nsub);
+    for (int i = 0; i < nsub; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        const SubDesc &x = ctx->subs[a], &y = ctx->subs[b];
+        return (long long)(x.nb + x.hi - x.lo) * x.m * x.m > (long long)(y.nb + y.hi - y.lo) * y.m * y.m;
+    });
+    CK(cudaMemcpyAsync(ctx->d_desc, ctx->subs.data(), sizeof(SubDesc) * nsub, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_order, order.data(), sizeof(int) * nsub, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4 * sizeof(int), ctx->stream));
+    launch_assemble_global(ctx->geom, ctx->d_A7, ctx->i0, ctx->i1, ctx->j0, ctx->j1, ctx->stream);
+    launch_assemble_local(ctx->geom, ctx->d_desc, nsub, ctx->d_stc, (int)ctx->max_n, ctx->stream);
+    CK(cudaGetLastError());
+    // apply launch configuration
+    int nsm = 148;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    apply_configure(ctx->m_max, &ctx->ap_block, &ctx->ap_smem, &ctx->ap_slot, &ctx->ap_occ);
+    CK(cudaGetLastError());
+    if (ctx->ap_occ < 1) return set_err(ctx, HELM_ECUDA, "apply kernel does not fit on an SM (smem %d)", ctx->ap_smem);
+    ctx->ap_grid = std::min(nsub, nsm * ctx->ap_occ);
+    ctx->nblk = nsm * 4;
+    if ((rc = dalloc(ctx, &ctx->d_scratch, (size_t)ctx->ap_grid * ctx->scratch_per_cta))) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HELM_OK;
+}
+
+int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
+{
+    if (!ctx || !out) return HELM_EINVAL;
+    out->n_free_global = (long long)ctx->nf * ctx->nf;
+    out->N_cells = ctx->N;
+    out->n_int = ctx->n_int;
+    out->n_ovlp = ctx->wo;
+    out->n_pml = ctx->wp;
+    out->owned_i0 = ctx->i0;
+    out->owned_i1 = ctx->i1;
+    out->owned_j0 = ctx->j0;
+    out->owned_j1 = ctx->j1;
+    out->n_local = ctx->n_local;
+    out->n_sub = ctx->n_sub_total;
+    out->n_sub_local = (int)ctx->subs.size();
+    out->m_max = ctx->m_max;
+    out->local_unknowns = ctx->local_unknowns;
+    out->factor_bytes = ctx->n_dinv * 16;
+    out->apply_bytes = ctx->apply_bytes;
+    out->band_bytes = ctx->band_bytes + 16LL * ctx->n_local;
+    out->spmv_bytes = 16LL * 9 * ctx->n_local;
+    return HELM_OK;
+}
+
+int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_host, double sigma, helm_z* b_dev)
+{
+    if (!ctx || nsrc < 0 || (nsrc > 0 && (!xy_host || !amp_host)) || !b_dev || !(sigma > 0))
+        return set_err(ctx, HELM_EINVAL, "helm_rhs: bad arguments");
+    double* d_xy = nullptr;
+    z2* d_amp = nullptr;
+    z2* d_f = nullptr;
+    const long long nfw = (long long)(ctx->i1 - ctx->i0 + 2) * (ctx->j1 - ctx->j0 + 2);
+    int rc;
+    if ((rc = dalloc(ctx, &d_xy, 2 * (size_t)std::max(nsrc, 1))) || (rc = dalloc(ctx, &d_amp, std::max(nsrc, 1))) ||
+        (rc = dalloc(ctx, &d_f, nfw)))
+        return rc;
+    if (nsrc > 0) {
+        CK(cudaMemcpyAsync(d_xy, xy_host, sizeof(double) * 2 * nsrc, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d_amp, amp_host, sizeof(z2) * nsrc, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    launch_rhs(ctx->geom, nsrc, d_xy, d_amp, sigma, d_f, (z2*)b_dev, ctx->i0, ctx->i1, ctx->j0, ctx->j1, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_xy);
+    cudaFree(d_amp);
+    cudaFree(d_f);
+    return HELM_OK;
+}
+
+int helm_factor(helm_ctx* ctx)
+{
+    if (!ctx) return HELM_EINVAL;
+    if (ctx->factored) return HELM_OK;
+    int rc;
+    if (!ctx->d_dinv && (rc = dalloc(ctx, &ctx->d_dinv, ctx->n_dinv))) return rc;
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4 * sizeof(int), ctx->stream));
+    launch_factor(ctx->d_desc, ctx->subs.data(), (int)ctx->subs.size(), ctx->m_max, ctx->d_stc, ctx->d_dinv,
+                  ctx->d_err, ctx->stream);
+    CK(cudaGetLastError());
+    int herr[4];
+    CK(cudaMemcpyAsync(herr, ctx->d_err, sizeof(herr), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (herr[0])
+        return set_err(ctx, HELM_EZEROPIVOT, "zero pivot: subdomain %d, block %d, row %d", herr[1], herr[2], herr[3]);
+    ctx->factored = true;
+    return HELM_OK;
+}
+
+int helm_matvec(helm_ctx* ctx, const helm_z* x_dev, helm_z* y_dev)
+{
+    if (!ctx || !x_dev || !y_dev || (const void*)x_dev == (void*)y_dev)
+        return set_err(ctx, HELM_EINVAL, "helm_matvec: bad arguments");
+    launch_spmv(ctx->d_A7, (const z2*)x_dev, (z2*)y_dev, ctx->i1 - ctx->i0, ctx->j1 - ctx->j0, ctx->stream);
+    CK(cudaGetLastError());
+    return HELM_OK;
+}
+
+int helm_precond_apply(helm_ctx* ctx, const helm_z* r_dev, helm_z* z_dev)
+{
+    if (!ctx || !r_dev || !z_dev || (const void*)r_dev == (void*)z_dev)
+        return set_err(ctx, HELM_EINVAL, "helm_precond_apply: bad arguments");
+    return apply_impl(ctx, (const z2*)r_dev, (z2*)z_dev);
+}
+
+int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host)
+{
+    if (!ctx || !r_host || !z_host) return set_err(ctx, HELM_EINVAL, "helm_precond_apply_host: bad arguments");
+    int rc;
+    if ((rc = ensure_krylov(ctx, 1))) return rc;
+    const size_t bytes = sizeof(z2) * ctx->n_local;
+    CK(cudaMemcpyAsync(ctx->d_t, r_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
+    CK(cudaMemcpyAsync(z_host, ctx->d_z, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HELM_OK;
+}
+
+int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, double rtol, int maxit,
+               helm_gmres_info* info)
+{
+    if (!ctx || !b_dev || !x_dev || (const void*)b_dev == (void*)x_dev)
+        return set_err(ctx, HELM_EINVAL, "helm_gmres: bad arguments");
+    return gmres_impl(ctx, (const z2*)b_dev, (z2*)x_dev, restart, rtol, maxit, info);
+}
+
+int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int restart, double rtol, int maxit,
+                    helm_gmres_info* info)
+{
+    if (!ctx || !b_host || !x_host) return set_err(ctx, HELM_EINVAL, "helm_gmres_host: bad arguments");
+    int rc;
+    if (!ctx->d_bb && ((rc = dalloc(ctx, &ctx->d_bb, ctx->n_local)) || (rc = dalloc(ctx, &ctx->d_xb, ctx->n_local))))
+        return rc;
+    const size_t bytes = sizeof(z2) * ctx->n_local;
+    CK(cudaMemcpyAsync(ctx->d_bb, b_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_xb, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    rc = gmres_impl(ctx, ctx->d_bb, ctx->d_xb, restart, rtol, maxit, info);
+    if (rc < 0) return rc;
+    CK(cudaMemcpyAsync(x_host, ctx->d_xb, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return rc;
+}
+
+int helm_export_stencil(helm_ctx* ctx, helm_z* out_dev)
+{
+    if (!ctx || !out_dev) return set_err(ctx, HELM_EINVAL, "helm_export_stencil: bad arguments");
+    CK(cudaMemcpyAsync(out_dev, ctx->d_A7, sizeof(z2) * 7 * ctx->n_local, cudaMemcpyDeviceToDevice, ctx->stream));
+    return HELM_OK;
+}
+
+int helm_profile_enable(helm_ctx* ctx, int on)
+{
+    if (!ctx) return HELM_EINVAL;
+    ctx->prof = on != 0;
+    return HELM_OK;
+}
+
+int helm_profile_read(helm_ctx* ctx, double* apply_ms, int* apply_launches, int* total_launches)
+{
+    if (!ctx) return HELM_EINVAL;
+    CK(cudaStreamSynchronize(ctx->stream));
+    double ms = 0.0;
+    for (auto& pr : ctx->ev_used) {
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, pr.first, pr.second));
+        ms += f;
+        ctx->ev_free.push_back(pr.first);
+        ctx->ev_free.push_back(pr.second);
+    }
+    if (apply_ms) *apply_ms = ms;
+    if (apply_launches) *apply_launches = (int)ctx->ev_used.size();
+    if (total_launches) *total_launches = ctx->launches;
+    ctx->ev_used.clear();
+    ctx->launches = 0;
+    return HELM_OK;
+}
+
+const char* helm_last_error(const helm_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+void helm_destroy(helm_ctx* ctx)
+{
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    else cudaDeviceSynchronize();
+    void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
+                    ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
+                    ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    for (auto e : ctx->ev_free) cudaEventDestroy(e);
+    for (auto& pr : ctx->ev_used) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    delete ctx;
+}
+
+}  // extern "C"

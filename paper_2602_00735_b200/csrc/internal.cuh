@@ -1,0 +1,121 @@
+// internal.cuh -- shared device/host definitions of libhelm (product code; independent of oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "helm.h"
+
+// ---------------------------------------------------------------------------------------------------
+// complex128 helpers (double2 = (re, im))
+// ---------------------------------------------------------------------------------------------------
+typedef double2 z2;
+
+__host__ __device__ __forceinline__ z2 zmk(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ z2 zadd(z2 a, z2 b) { return zmk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ z2 zsub(z2 a, z2 b) { return zmk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ z2 zmul(z2 a, z2 b) { return zmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__host__ __device__ __forceinline__ z2 zscale(z2 a, double s) { return zmk(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ z2 zconj(z2 a) { return zmk(a.x, -a.y); }
+__host__ __device__ __forceinline__ double zabs2(z2 a) { return a.x * a.x + a.y * a.y; }
+__host__ __device__ __forceinline__ z2 zinv(z2 a)
+{
+    double d = a.x * a.x + a.y * a.y;
+    return zmk(a.x / d, -a.y / d);
+}
+__host__ __device__ __forceinline__ z2 zdiv(z2 a, z2 b) { return zmul(a, zinv(b)); }
+// acc += a * b
+__device__ __forceinline__ void zfma(z2& acc, z2 a, z2 b)
+{
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void zfma_conj(z2& acc, z2 a, z2 b)
+{
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(-a.y, b.x, acc.y);
+}
+
+// ---------------------------------------------------------------------------------------------------
+// Problem geometry on the device (global PML ramps) and per-subdomain descriptors.
+// Positions along an axis are integers in thirds of a cell ("X3"): triangle centroids sit at 3i+1 or
+// 3i+2, node n at 3n, so PML depth is an integer times h/3 (D5).
+// ---------------------------------------------------------------------------------------------------
+struct Geom {
+    double k, h, h3, sigma0, kappa;   // h3 = h / 3; kappa = profile width kappa_g
+    int N;                            // cells per side
+    int nf;                           // free nodes per side = N - 1
+    int ng;                           // global PML cells per side
+    long lo3, hi3;                    // Omega_int = nodes [n_g, N - n_g]  -> 3 n_g, 3 (N - n_g)
+};
+
+// One subdomain as seen by the local operator / factor / apply kernels.
+struct SubDesc {
+    int m;          // block size: local free nodes per row (x)
+    int nb;         // number of block rows (local free nodes per column, y)
+    int tw;         // twist block row
+    int lo, hi;     // owned block rows [lo, hi]
+    int olo, ohi;   // owned columns [olo, ohi] within a row
+    int gx0, gy0;   // global node index of local node (t = 0, row 0)
+    int ilo3, ihi3; // int box x-range in thirds (local ramps start there) ...
+    int jlo3, jhi3; // ... and y-range
+    int flags;      // bit0 x-lower PML, bit1 x-upper, bit2 y-lower, bit3 y-upper
+    int pad;
+    long long fac_off;   // complex offset of block 0 of the explicit inverses (blocks m x m, column-major)
+    long long stc_off;   // complex offset of the local stencil [nb][7][m]
+};
+
+enum { SL_C = 0, SL_E = 1, SL_W = 2, SL_N = 3, SL_S = 4, SL_NE = 5, SL_SW = 6 };
+
+#define HELM_CUDA_OK(expr)                                                                   \
+    do {                                                                                     \
+        cudaError_t e__ = (expr);                                                            \
+        if (e__ != cudaSuccess) return set_err(ctx, HELM_ECUDA, "%s: %s (%s:%d)", #expr,     \
+                                               cudaGetErrorString(e__), __FILE__, __LINE__); \
+    } while (0)
+
+// kernel launchers (defined in the .cu files)
+void launch_assemble_global(const Geom& g, z2* A7, int i0, int i1, int j0, int j1, cudaStream_t s);
+void launch_assemble_local(const Geom& g, const SubDesc* d_desc, int nsub, z2* stencil, int max_n, cudaStream_t s);
+void launch_rhs(const Geom& g, int nsrc, const double* d_xy, const z2* d_amp, double sigma, z2* f_work, z2* b,
+                int i0, int i1, int j0, int j1, cudaStream_t s);
+int factor_smem_bytes(int m_max);
+void launch_factor(const SubDesc* d_desc, const SubDesc* h_desc, int nsub, int m_max, const z2* stencil, z2* dinv,
+                   int* d_err, cudaStream_t s);
+
+struct ApplyArgs {
+    const SubDesc* desc;
+    const int* order;       // subdomains in processing order
+    int nsub;
+    const z2* dinv;
+    const z2* stencil;
+    const z2* in;           // input vector (possibly with ghost frame)
+    int in_i0, in_j0;       // node index of in[0]
+    long long in_stride;
+    z2* out;                // owned output
+    int out_i0, out_j0;
+    long long out_stride;
+    z2* scratch;            // per-CTA [max_rows][m_max]
+    long long scratch_per_cta;
+};
+int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
+void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
+
+void launch_spmv(const z2* A7, const z2* x, z2* y, int nx, int ny, cudaStream_t s);
+void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, int nx, int ny, double* partial, int nblk,
+                     cudaStream_t s);
+void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long n, z2* partial, int nblk,
+                     cudaStream_t s);
+void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, double* partial_norm,
+                      int nblk, cudaStream_t s);
+void launch_reduce_z(const z2* partial, int nblk, int nv, z2* out, z2* out_plus, const z2* add, cudaStream_t s);
+void launch_reduce_norm(const double* partial, int nblk, z2* out_slot, double* out_norm, cudaStream_t s);
+void launch_scale_by_norm(const z2* w, const double* norm, z2* v, long long n, cudaStream_t s);
+void launch_combine(const z2* V, long long ldv, int nv, const z2* y, z2* t, long long n, cudaStream_t s);
+void launch_axpy(z2* x, const z2* z, long long n, cudaStream_t s);
+void launch_copy(z2* dst, const z2* src, long long n, cudaStream_t s);
+void launch_norm_partial(const z2* x, long long n, double* partial, int nblk, cudaStream_t s);

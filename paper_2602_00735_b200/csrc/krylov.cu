@@ -1,0 +1,280 @@
+// krylov.cu -- K5 SpMV (7-point P1 stencil) and the GMRES vector kernels (K6-K8): multi-dot, multi-axpy
+// with fused norm, normalisation, basis combination.  All reductions are deterministic: a fixed row
+// partition per CTA, warp-shuffle trees inside a CTA, and a single-CTA pass over the CTA partials in
+// index order (D15).  No floating-point atomics.
+#include "internal.cuh"
+
+namespace {
+
+constexpr int KT = 256;          // threads per CTA
+constexpr int NVMAX = 64;        // max vectors in one multi-dot / multi-axpy (restart + 1 <= 64)
+
+__device__ __forceinline__ z2 warp_sum(z2 v)
+{
+    for (int off = 16; off; off >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+    }
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v)
+{
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+__device__ __forceinline__ void chunk_of(long long n, long long& r0, long long& r1)
+{
+    const long long per = ((n + gridDim.x - 1) / gridDim.x + 31) / 32 * 32;
+    r0 = (long long)blockIdx.x * per;
+    r1 = r0 + per < n ? r0 + per : n;
+}
+
+// CTA-wide deterministic sum of a per-thread double -> thread 0
+__device__ double block_sum(double v, double* sh)
+{
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += sh[w];
+    __syncthreads();
+    return s;
+}
+
+__constant__ int c_dx[7] = { 0, 1, -1, 0, 0, 1, -1 };
+__constant__ int c_dy[7] = { 0, 0, 0, 1, -1, 1, -1 };
+
+__device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* __restrict__ x, long long r, long long n,
+                                          int nx, int ny)
+{
+    const int i = (int)(r % nx), j = (int)(r / nx);
+    z2 acc = zmk(0, 0);
+#pragma unroll
+    for (int s = 0; s < 7; s++) {
+        const int qi = i + c_dx[s], qj = j + c_dy[s];
+        if (qi >= 0 && qi < nx && qj >= 0 && qj < ny)
+            zfma(acc, __ldg(A7 + s * n + r), __ldg(x + qi + (long long)nx * qj));
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(KT) k_spmv(const z2* __restrict__ A7, const z2* __restrict__ x, z2* __restrict__ y,
+                                             int nx, int ny)
+{
+    const long long n = (long long)nx * ny;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        y[r] = stencil_row(A7, x, r, n, nx, ny);
+}
+
+// r = b - A x, partial[blk] = ||r||^2 over the CTA's rows
+__global__ void __launch_bounds__(KT) k_residual(const z2* __restrict__ A7, const z2* __restrict__ x,
+                                                 const z2* __restrict__ b, z2* __restrict__ r, int nx, int ny,
+                                                 double* __restrict__ partial)
+{
+    __shared__ double sh[KT / 32];
+    const long long n = (long long)nx * ny;
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    double s = 0.0;
+    for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
+        const z2 v = zsub(__ldg(b + e), stencil_row(A7, x, e, n, nx, ny));
+        r[e] = v;
+        s += zabs2(v);
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// partial[blk][v] = sum_{e in blk} conj(V_v[e]) w[e],  v < nv
+template <int R>
+__global__ void __launch_bounds__(KT) k_multidot(const z2* __restrict__ V, long long ldv, int nv,
+                                                 const z2* __restrict__ w, long long n, z2* __restrict__ partial)
+{
+    __shared__ z2 acc[KT / 32][NVMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int v = lane; v < NVMAX; v += 32) acc[warp][v] = zmk(0, 0);
+    __syncwarp();
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    for (long long base = r0; base < r1; base += (long long)KT * R) {
+        z2 wv[R];
+        long long e[R];
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+            e[q] = base + q * KT + threadIdx.x;
+            wv[q] = e[q] < r1 ? __ldg(w + e[q]) : zmk(0, 0);
+        }
+        for (int v = 0; v < nv; v++) {
+            const z2* Vv = V + v * ldv;
+            z2 s = zmk(0, 0);
+#pragma unroll
+            for (int q = 0; q < R; q++)
+                if (e[q] < r1) zfma_conj(s, __ldg(Vv + e[q]), wv[q]);
+            s = warp_sum(s);
+            if (lane == 0) acc[warp][v] = zadd(acc[warp][v], s);
+        }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        z2 s = zmk(0, 0);
+        for (int q = 0; q < KT / 32; q++) s = zadd(s, acc[q][v]);
+        partial[(long long)blockIdx.x * NVMAX + v] = s;
+    }
+}
+
+// w -= sum_v h[v] V_v ; partial[blk] = ||w_new||^2
+__global__ void __launch_bounds__(KT) k_multiaxpy(const z2* __restrict__ V, long long ldv, int nv,
+                                                  const z2* __restrict__ h, z2* __restrict__ w, long long n,
+                                                  double* __restrict__ partial)
+{
+    __shared__ z2 hs[NVMAX];
+    __shared__ double sh[KT / 32];
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) hs[v] = h[v];
+    __syncthreads();
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    double s = 0.0;
+    for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
+        z2 acc = w[e];
+        for (int v = 0; v < nv; v++) {
+            const z2 hv = hs[v];
+            zfma(acc, zmk(-hv.x, -hv.y), __ldg(V + v * ldv + e));
+        }
+        w[e] = acc;
+        s += zabs2(acc);
+    }
+    if (partial) {
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) partial[blockIdx.x] = s;
+    }
+}
+
+// out[v] = sum_blk partial[blk][v]; out_plus[v] = add[v] + out[v] (if given); one CTA, index order
+__global__ void k_reduce_z(const z2* __restrict__ partial, int nblk, int nv, z2* __restrict__ out,
+                           z2* __restrict__ out_plus, const z2* __restrict__ add)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int v = warp; v < nv; v += blockDim.x >> 5) {
+        z2 s = zmk(0, 0);
+        for (int b = lane; b < nblk; b += 32) s = zadd(s, partial[(long long)b * NVMAX + v]);
+        s = warp_sum(s);
+        if (lane == 0) {
+            out[v] = s;
+            if (out_plus) out_plus[v] = zadd(add[v], s);
+        }
+    }
+}
+
+// norm = sqrt(sum partial); out_slot (complex) = (norm, 0)
+__global__ void k_reduce_norm(const double* __restrict__ partial, int nblk, z2* out_slot, double* out_norm)
+{
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += partial[b];
+    s = warp_sum(s);
+    if (lane == 0) {
+        const double nrm = sqrt(s);
+        if (out_slot) *out_slot = zmk(nrm, 0.0);
+        if (out_norm) *out_norm = nrm;
+    }
+}
+
+__global__ void __launch_bounds__(KT) k_scale(const z2* __restrict__ w, const double* __restrict__ norm,
+                                              z2* __restrict__ v, long long n)
+{
+    const double nr = *norm;
+    const double inv = nr != 0.0 ? 1.0 / nr : 0.0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        v[e] = zscale(w[e], inv);
+}
+
+// t = sum_v y[v] V_v
+__global__ void __launch_bounds__(KT) k_combine(const z2* __restrict__ V, long long ldv, int nv,
+                                                const z2* __restrict__ y, z2* __restrict__ t, long long n)
+{
+    __shared__ z2 ys[NVMAX];
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) ys[v] = y[v];
+    __syncthreads();
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        z2 acc = zmk(0, 0);
+        for (int v = 0; v < nv; v++) zfma(acc, ys[v], __ldg(V + v * ldv + e));
+        t[e] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(KT) k_axpy(z2* __restrict__ x, const z2* __restrict__ z, long long n)
+{
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        x[e] = zadd(x[e], z[e]);
+}
+
+__global__ void __launch_bounds__(KT) k_copy(z2* __restrict__ d, const z2* __restrict__ s, long long n)
+{
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        d[e] = s[e];
+}
+
+__global__ void __launch_bounds__(KT) k_norm_partial(const z2* __restrict__ x, long long n, double* __restrict__ partial)
+{
+    __shared__ double sh[KT / 32];
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    double s = 0.0;
+    for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) s += zabs2(x[e]);
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+int ew_grid(long long n)
+{
+    long long b = (n + KT - 1) / KT;
+    if (b > 148LL * 8) b = 148LL * 8;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+void launch_spmv(const z2* A7, const z2* x, z2* y, int nx, int ny, cudaStream_t s)
+{
+    k_spmv<<<ew_grid((long long)nx * ny), KT, 0, s>>>(A7, x, y, nx, ny);
+}
+void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, int nx, int ny, double* partial, int nblk,
+                     cudaStream_t s)
+{
+    k_residual<<<nblk, KT, 0, s>>>(A7, x, b, r, nx, ny, partial);
+}
+void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long n, z2* partial, int nblk,
+                     cudaStream_t s)
+{
+    k_multidot<4><<<nblk, KT, 0, s>>>(V, ldv, nv, w, n, partial);
+}
+void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, double* partial_norm,
+                      int nblk, cudaStream_t s)
+{
+    k_multiaxpy<<<nblk, KT, 0, s>>>(V, ldv, nv, h, w, n, partial_norm);
+}
+void launch_reduce_z(const z2* partial, int nblk, int nv, z2* out, z2* out_plus, const z2* add, cudaStream_t s)
+{
+    k_reduce_z<<<1, 512, 0, s>>>(partial, nblk, nv, out, out_plus, add);
+}
+void launch_reduce_norm(const double* partial, int nblk, z2* out_slot, double* out_norm, cudaStream_t s)
+{
+    k_reduce_norm<<<1, 32, 0, s>>>(partial, nblk, out_slot, out_norm);
+}
+void launch_scale_by_norm(const z2* w, const double* norm, z2* v, long long n, cudaStream_t s)
+{
+    k_scale<<<ew_grid(n), KT, 0, s>>>(w, norm, v, n);
+}
+void launch_combine(const z2* V, long long ldv, int nv, const z2* y, z2* t, long long n, cudaStream_t s)
+{
+    k_combine<<<ew_grid(n), KT, 0, s>>>(V, ldv, nv, y, t, n);
+}
+void launch_axpy(z2* x, const z2* z, long long n, cudaStream_t s) { k_axpy<<<ew_grid(n), KT, 0, s>>>(x, z, n); }
+void launch_copy(z2* dst, const z2* src, long long n, cudaStream_t s) { k_copy<<<ew_grid(n), KT, 0, s>>>(dst, src, n); }
+void launch_norm_partial(const z2* x, long long n, double* partial, int nblk, cudaStream_t s)
+{
+    k_norm_partial<<<nblk, KT, 0, s>>>(x, n, partial);
+}

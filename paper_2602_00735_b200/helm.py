@@ -1,0 +1,211 @@
+"""Thin Python binding of libhelm (include/helm.h): argument marshalling only.
+
+Every step of the hot path runs in libhelm's CUDA kernels; this module converts torch tensors to device
+pointers and ctypes structs.  PyTorch is used for device memory, streams and process groups only.  There is
+no CPU fallback: if libhelm.so is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import build as _build
+
+_LIB = None
+
+
+class HelmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"helm error {code}: {msg}")
+        self.code = code
+
+
+HELM_OK, HELM_NOT_CONVERGED, HELM_BREAKDOWN = 0, 2, 3
+
+
+class Params(C.Structure):
+    _fields_ = [("k", C.c_double), ("ppw", C.c_int), ("n_pml_global", C.c_int), ("sigma0", C.c_double),
+                ("nsub_x", C.c_int), ("nsub_y", C.c_int), ("n_ovlp", C.c_int), ("n_pml", C.c_int),
+                ("local_bc", C.c_int), ("gpu_grid_x", C.c_int), ("gpu_grid_y", C.c_int)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("n_free_global", C.c_longlong), ("N_cells", C.c_int), ("n_int", C.c_int),
+                ("n_ovlp", C.c_int), ("n_pml", C.c_int),
+                ("owned_i0", C.c_int), ("owned_i1", C.c_int), ("owned_j0", C.c_int), ("owned_j1", C.c_int),
+                ("n_local", C.c_longlong), ("n_sub", C.c_int), ("n_sub_local", C.c_int), ("m_max", C.c_int),
+                ("local_unknowns", C.c_longlong), ("factor_bytes", C.c_longlong), ("apply_bytes", C.c_longlong),
+                ("band_bytes", C.c_longlong), ("spmv_bytes", C.c_longlong)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class GmresInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int), ("applies", C.c_int),
+                ("relres_est", C.c_double), ("relres_true", C.c_double),
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
+
+
+EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_matvec", "helm_precond_apply",
+           "helm_precond_apply_host", "helm_gmres", "helm_gmres_host", "helm_export_stencil",
+           "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy"]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libhelm.so (building it in-tree if needed).  Raises if it cannot be built or loaded."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if build_if_missing:
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise RuntimeError(f"libhelm.so missing at {_build.LIB}; run __graft_entry__.build()")
+    L = C.CDLL(_build.LIB)
+    vp, i, d = C.c_void_p, C.c_int, C.c_double
+    L.helm_setup.argtypes = [C.POINTER(Params), i, i, vp, vp, C.POINTER(vp)]
+    L.helm_get_layout.argtypes = [vp, C.POINTER(Layout)]
+    L.helm_rhs.argtypes = [vp, i, vp, vp, d, vp]
+    L.helm_factor.argtypes = [vp]
+    L.helm_matvec.argtypes = [vp, vp, vp]
+    L.helm_precond_apply.argtypes = [vp, vp, vp]
+    L.helm_precond_apply_host.argtypes = [vp, vp, vp]
+    L.helm_gmres.argtypes = [vp, vp, vp, i, d, i, C.POINTER(GmresInfo)]
+    L.helm_gmres_host.argtypes = [vp, vp, vp, i, d, i, C.POINTER(GmresInfo)]
+    L.helm_export_stencil.argtypes = [vp, vp]
+    L.helm_profile_enable.argtypes = [vp, i]
+    L.helm_profile_read.argtypes = [vp, C.POINTER(d), C.POINTER(i), C.POINTER(i)]
+    L.helm_last_error.argtypes = [vp]
+    L.helm_last_error.restype = C.c_char_p
+    L.helm_destroy.argtypes = [vp]
+    for name in EXPORTS:
+        if name not in ("helm_last_error", "helm_destroy"):
+            getattr(L, name).restype = C.c_int
+    L.helm_destroy.restype = None
+    _LIB = L
+    return L
+
+
+def _ptr(t) -> int:
+    """Device (or host) address of a contiguous complex128 tensor / numpy array."""
+    import numpy as np
+    if isinstance(t, np.ndarray):
+        assert t.dtype == np.complex128 and t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    import torch
+    assert t.dtype == torch.complex128 and t.is_contiguous(), "complex128 contiguous tensors only"
+    return t.data_ptr()
+
+
+class Context:
+    """One rank's RAS-PML problem: owns the libhelm context (operators, factors, Krylov workspace)."""
+
+    def __init__(self, k: float, nsub_x: int, nsub_y: int | None = None, *, ppw: int = 10, n_pml_global: int = 10,
+                 sigma0: float = 5.0, n_ovlp: int = -1, n_pml: int = -1, rank: int = 0, nranks: int = 1,
+                 gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libhelm needs a CUDA device (no CPU fallback)")
+        self.L = load()
+        self.params = Params(float(k), ppw, n_pml_global, float(sigma0), nsub_x,
+                             nsub_y if nsub_y is not None else nsub_x, n_ovlp, n_pml, 0, gpu_grid[0], gpu_grid[1])
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self._h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        rc = self.L.helm_setup(C.byref(self.params), rank, nranks, idbuf, C.c_void_p(self.stream.cuda_stream),
+                               C.byref(self._h))
+        self._check(rc)
+        self.layout = self._layout()
+        self.n = self.layout.n_local
+
+    # ------------------------------------------------------------------------------------------ plumbing
+    def _check(self, rc: int, ok=(0,)):
+        if rc in ok:
+            return rc
+        msg = self.L.helm_last_error(self._h).decode() if self._h else ""
+        raise HelmError(rc, msg)
+
+    def _layout(self) -> Layout:
+        lay = Layout()
+        self._check(self.L.helm_get_layout(self._h, C.byref(lay)))
+        return lay
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self.L.helm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def empty(self):
+        import torch
+        return torch.empty(self.n, dtype=torch.complex128, device="cuda")
+
+    # ------------------------------------------------------------------------------------------ API
+    def rhs(self, xy, amp, sigma: float, out=None):
+        import numpy as np
+        xy = np.ascontiguousarray(xy, np.float64)
+        amp = np.ascontiguousarray(amp, np.complex128)
+        b = self.empty() if out is None else out
+        self._check(self.L.helm_rhs(self._h, len(amp), xy.ctypes.data, amp.ctypes.data, float(sigma), _ptr(b)))
+        return b
+
+    def factor(self):
+        self._check(self.L.helm_factor(self._h))
+
+    def matvec(self, x, out=None):
+        y = self.empty() if out is None else out
+        self._check(self.L.helm_matvec(self._h, _ptr(x), _ptr(y)))
+        return y
+
+    def precond_apply(self, r, out=None):
+        z = self.empty() if out is None else out
+        self._check(self.L.helm_precond_apply(self._h, _ptr(r), _ptr(z)))
+        return z
+
+    def precond_apply_host(self, r_host, z_host):
+        self._check(self.L.helm_precond_apply_host(self._h, _ptr(r_host), _ptr(z_host)))
+        return z_host
+
+    def gmres(self, b, x=None, restart: int = 50, rtol: float = 1e-6, maxit: int = 5000, history: bool = False):
+        import numpy as np
+        if x is None:
+            x = self.empty()
+            x.zero_()
+        info = GmresInfo()
+        hist = None
+        if history:
+            hist = np.zeros(maxit, np.float64)
+            info.history = hist.ctypes.data_as(C.POINTER(C.c_double))
+            info.history_cap = maxit
+        rc = self.L.helm_gmres(self._h, _ptr(b), _ptr(x), restart, float(rtol), maxit, C.byref(info))
+        self._check(rc, ok=(0, 2))
+        return x, info, (hist[:info.iterations].copy() if hist is not None else None)
+
+    def gmres_host(self, b_host, x_host, restart: int = 50, rtol: float = 1e-6, maxit: int = 5000):
+        info = GmresInfo()
+        rc = self.L.helm_gmres_host(self._h, _ptr(b_host), _ptr(x_host), restart, float(rtol), maxit, C.byref(info))
+        self._check(rc, ok=(0, 2))
+        return x_host, info
+
+    def export_stencil(self):
+        import torch
+        out = torch.empty(7 * self.n, dtype=torch.complex128, device="cuda")
+        self._check(self.L.helm_export_stencil(self._h, _ptr(out)))
+        return out.view(7, self.n)
+
+    def profile(self, on: bool = True):
+        self._check(self.L.helm_profile_enable(self._h, int(on)))
+
+    def profile_read(self):
+        ms, na, nt = C.c_double(), C.c_int(), C.c_int()
+        self._check(self.L.helm_profile_read(self._h, C.byref(ms), C.byref(na), C.byref(nt)))
+        return ms.value, na.value, nt.value
