@@ -130,7 +130,8 @@ int helm_export_stencil(helm_ctx* ctx, helm_z* out_dev);
 
 /* Kernel timing of the apply kernel: when enabled, CUDA events bracket every launch of the fused apply
  * kernel on the context's stream; helm_profile_read synchronises and returns the summed milliseconds
- * and the launch count since the last read (then resets). */
+ * and count of the timed apply launches, and the number of libhelm kernels launched by helm_matvec /
+ * helm_precond_apply / helm_gmres since the last read (then resets both). */
 int helm_profile_enable(helm_ctx* ctx, int on);
 int helm_profile_read(helm_ctx* ctx, double* apply_ms, int* apply_launches, int* total_launches);
 

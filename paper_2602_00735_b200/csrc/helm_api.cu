@@ -307,6 +307,7 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
 int norm_host(helm_ctx* ctx, const z2* v, double* out)
 {
     launch_norm_partial(v, ctx->n_local, ctx->d_dpart, ctx->nblk, ctx->stream);
+    ctx->launches += 2;
     launch_reduce_norm(ctx->d_dpart, ctx->nblk, nullptr, ctx->d_norm, ctx->stream);
     CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_norm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -319,6 +320,7 @@ int residual_host(helm_ctx* ctx, const z2* b, const z2* x, z2* r, double* out)
 {
     const int nx = ctx->i1 - ctx->i0, ny = ctx->j1 - ctx->j0;
     launch_residual(ctx->d_A7, x, b, r, nx, ny, ctx->d_dpart, ctx->nblk, ctx->stream);
+    ctx->launches += 2;
     launch_reduce_norm(ctx->d_dpart, ctx->nblk, nullptr, ctx->d_norm, ctx->stream);
     CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_norm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -368,6 +370,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         // v_0 = r / ||r||
         CK(cudaMemcpyAsync(ctx->d_norm, &beta, sizeof(double), cudaMemcpyHostToDevice, s));
         launch_scale_by_norm(ctx->d_r, ctx->d_norm, V, n, s);
+        ctx->launches++;
         std::fill(g.begin(), g.end(), cplx(0, 0));
         g[0] = beta;
         int jend = 0;
@@ -386,6 +389,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             launch_multiaxpy(V, n, j + 1, ctx->d_h2, ctx->d_w, n, ctx->d_dpart, ctx->nblk, s);
             launch_reduce_norm(ctx->d_dpart, ctx->nblk, ctx->d_Hcol + j + 1, ctx->d_norm, s);
             launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
+            ctx->launches += 9;   // spmv, 2x multidot, 2x reduce, 2x multiaxpy, norm, scale
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_Hcol, sizeof(z2) * (j + 2), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -433,6 +437,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
         inf->applies++;
         launch_axpy(x, ctx->d_z, n, s);
+        ctx->launches += 2;   // combine, axpy
         double rn;
         if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
         cycles++;
@@ -587,6 +592,7 @@ int helm_matvec(helm_ctx* ctx, const helm_z* x_dev, helm_z* y_dev)
     if (!ctx || !x_dev || !y_dev || (const void*)x_dev == (void*)y_dev)
         return set_err(ctx, HELM_EINVAL, "helm_matvec: bad arguments");
     launch_spmv(ctx->d_A7, (const z2*)x_dev, (z2*)y_dev, ctx->i1 - ctx->i0, ctx->j1 - ctx->j0, ctx->stream);
+    ctx->launches++;
     CK(cudaGetLastError());
     return HELM_OK;
 }
