@@ -288,7 +288,10 @@ int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_by
     *block_threads = 32 * (ncw + 1);
     *slot_bytes = slot_bytes_for(m_max);
     *smem_bytes = NS * *slot_bytes + 2 * NS * 8 + 3 * (32 * ncw + 1) * (int)sizeof(z2);
-    cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem_bytes);
+    int cur = 0;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k_apply) == cudaSuccess) cur = fa.maxDynamicSharedSizeBytes;
+    if (*smem_bytes > cur) cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem_bytes);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply, *block_threads, *smem_bytes);
     *ctas_per_sm = occ;
@@ -297,5 +300,12 @@ int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_by
 
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s)
 {
+    // the dynamic-smem limit is a per-function attribute shared by every context in the process: raise it
+    // whenever a context needs more than any earlier one
+    static int smem_set = 0;
+    if (smem > smem_set) {
+        cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        smem_set = smem;
+    }
     k_apply<<<grid, block, smem, s>>>(a, block / 32 - 1, slot_bytes);
 }
