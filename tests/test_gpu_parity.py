@@ -100,8 +100,10 @@ def test_gmres_parity(name):
 
 
 def test_single_subdomain_is_exact_inverse_and_one_iteration():
-    ctx, o = pair("c1", nsub=(1, 1))
-    xy, amp, sig = sources(CONFIGS["c1"])
+    """north_star: a single subdomain equal to Omega makes B^-1 = A^-1 and GMRES converge in 1 iteration
+    (c0: one 51 x 51-node subdomain)."""
+    ctx, o = pair("c0", nsub=(1, 1))
+    xy, amp, sig = sources(CONFIGS["c0"])
     b = o.rhs(xy, amp, sig)
     import scipy.sparse.linalg as sla
     xd = sla.spsolve(o.matrix().tocsc(), b)
@@ -171,6 +173,9 @@ def test_errors():
     with pytest.raises(HelmError) as e:
         ctx.precond_apply(torch.zeros(ctx.n, dtype=torch.complex128, device="cuda"))
     assert e.value.code == -7
+    with pytest.raises(HelmError) as e:
+        Context(100.0, 1, 1)                      # one 178-node-wide block: above the 112 limit
+    assert e.value.code == -1
 
 
 def test_c3_full_size_sampled_parity():
