@@ -86,8 +86,10 @@ typedef struct {
 
 /* Create a context: grid, decomposition, device assembly of the global operator A (eq. (weak))
  * and of every local operator A_j.  rank / nranks: this process's place in the job; nranks > 1
- * needs nccl_unique_id (128 bytes, identical on all ranks) and a library built with NCCL.  cuda_stream:
- * cudaStream_t or NULL (legacy default stream).  Allocates the global operator and local stencils. */
+ * with nccl_unique_id (128 bytes from helm_nccl_unique_id, identical on all ranks) creates an NCCL
+ * communicator over which halos and GMRES inner products are exchanged (collective: every rank calls it);
+ * nranks > 1 with nccl_unique_id == NULL creates a communication-free shard (see the _ext entry points).
+ * cuda_stream: cudaStream_t or NULL (legacy default stream).  Allocates the operators. */
 int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id,
                void* cuda_stream, helm_ctx** out);
 
@@ -134,6 +136,48 @@ int helm_export_stencil(helm_ctx* ctx, helm_z* out_dev);
  * helm_precond_apply / helm_gmres since the last read (then resets both). */
 int helm_profile_enable(helm_ctx* ctx, int on);
 int helm_profile_read(helm_ctx* ctx, double* apply_ms, int* apply_launches, int* total_launches);
+
+/* ---------------------------------------------------------------------------------------------------
+ * Multi-rank layout (one process per GPU).  The P_x x P_y subdomain grid is cut into a
+ * gpu_grid_x x gpu_grid_y rank grid (rank = rx + gpu_grid_x * ry); each rank owns the union of its blocks'
+ * owned nodes (a rectangle) and the factors of its subdomains.  Before an apply a rank needs its input on
+ * ext = owned rectangle grown toward every neighbouring rank by delta + kappa - 1 nodes below and
+ * delta + kappa above (the full boxes of its edge subdomains reach that far, with half-open
+ * ownership, D10); the SpMV needs 1 node.  Exchanges run in two phases (x, then y over the x-extended
+ * range, which carries the corners).  These two functions are pure host logic (no CUDA) so that the
+ * exchange schedule can be verified on CPU.
+ * ------------------------------------------------------------------------------------------------- */
+typedef struct {
+    int gx, gy, rx, ry;
+    int owned_i0, owned_i1, owned_j0, owned_j1;   /* free nodes [i0,i1) x [j0,j1), 1-based node index */
+    int ext_i0, ext_i1, ext_j0, ext_j1;           /* apply input rectangle incl. ghosts */
+    int halo_lo, halo_hi;                         /* ghost layers below / above: delta+kappa-1, delta+kappa */
+    int nbr[4];                                   /* neighbour ranks: -x, +x, -y, +y (-1: none) */
+    int n_sub_local;
+} helm_plan;
+
+typedef struct {
+    int phase;                  /* 0: x exchange, 1: y exchange (after phase 0 is unpacked) */
+    int peer;                   /* rank to send to and receive from */
+    int send_i0, send_i1, send_j0, send_j1;   /* rectangle (node indices) packed and sent to peer */
+    int recv_i0, recv_i1, recv_j0, recv_j1;   /* rectangle received from peer into the ghost frame */
+} helm_msg;
+
+int helm_plan_rank(const helm_params* params, int rank, int nranks, helm_plan* out);
+/* Messages of one exchange for `rank`: width 0 = the apply frame (halo_lo below, halo_hi above), width W in
+ * [1, halo_hi] = W layers on both sides.  Returns the count (<= 4) or a negative error.  A message's send
+ * and receive rectangles may differ in shape (a rank sends halo_hi layers down, receives halo_lo). */
+int helm_halo_schedule(const helm_params* params, int rank, int nranks, int width, helm_msg* out, int cap);
+
+/* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it); HELM_ENCCL without NCCL. */
+int helm_nccl_unique_id(void* out128);
+
+/* Communication-free sharded entry points: the caller supplies the input already extended with ghosts.
+ * ext_dev covers the plan's ext rectangle (apply) / the owned rectangle grown by one node toward every
+ * neighbour (matvec), x-fastest.  Valid on every context, including nranks > 1 contexts created with
+ * nccl_unique_id == NULL (which cannot run helm_gmres / helm_precond_apply / helm_matvec). */
+int helm_precond_apply_ext(helm_ctx* ctx, const helm_z* ext_dev, helm_z* z_dev);
+int helm_matvec_ext(helm_ctx* ctx, const helm_z* ext1_dev, helm_z* y_dev);
 
 const char* helm_last_error(const helm_ctx* ctx);
 void helm_destroy(helm_ctx* ctx);

@@ -21,6 +21,21 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_dirs():
+    """(include, lib) of the NCCL that torch's wheel set ships (nvidia-nccl), or None."""
+    try:
+        import nvidia.nccl as m
+        base = list(m.__path__)[0]
+    except Exception:
+        base = None
+    for b in [base, "/usr"]:
+        if b and os.path.exists(os.path.join(b, "include", "nccl.h")):
+            lib = os.path.join(b, "lib")
+            if os.path.exists(os.path.join(lib, "libnccl.so")) or os.path.exists(os.path.join(lib, "libnccl.so.2")):
+                return os.path.join(b, "include"), lib
+    return None
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -37,7 +52,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, *sources(), "-o", LIB + ".tmp"]
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC]
+    nd = nccl_dirs()
+    if nd:
+        inc, lib = nd
+        libname = "nccl" if os.path.exists(os.path.join(lib, "libnccl.so")) else ":libnccl.so.2"
+        cmd += ["-DHELM_HAVE_NCCL", "-I", inc]
+        link = ["-L", lib, "-l" + libname, "-Xlinker", "-rpath=" + lib]
+    else:
+        link = []
+    cmd += [*sources(), *link, "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:

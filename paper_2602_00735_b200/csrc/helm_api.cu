@@ -1,7 +1,7 @@
-// helm_api.cu -- host side of libhelm: the C ABI of include/helm.h, grid and decomposition, device memory,
-// and the restarted GMRES driver.  Every arithmetic step on vectors runs in this library's kernels; the host
-// only sizes the problem, launches, and performs the O(restart^2) Givens / triangular-solve bookkeeping of
-// GMRES on at most restart+1 scalars per iteration (D13).
+// helm_api.cu -- host side of libhelm: the C ABI of include/helm.h, grid / decomposition / rank plan, device
+// memory, the NCCL halo exchange, and the restarted GMRES driver.  Every arithmetic step on vectors runs in
+// this library's kernels; the host only sizes the problem, launches, and performs the O(restart^2) Givens /
+// triangular-solve bookkeeping of GMRES on at most restart+1 scalars per iteration (D13).
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -13,7 +13,154 @@
 
 #include "internal.cuh"
 
+#ifdef HELM_HAVE_NCCL
+#include <nccl.h>
+#endif
+
 typedef std::complex<double> cplx;
+
+namespace {
+
+constexpr int NVMAX = 64;
+constexpr int M_LIMIT = 112;   // factor kernel keeps an m x m complex block in shared memory
+
+int round_half_up(double x) { return (int)floor(x + 0.5); }
+
+// Cartesian block starts: N cells into P blocks of floor/ceil size, larger blocks first (D8)
+std::vector<int> block_starts(int N, int P)
+{
+    std::vector<int> s(P + 1, 0);
+    const int q = N / P, r = N % P;
+    for (int b = 0; b < P; b++) s[b + 1] = s[b] + q + (b < r ? 1 : 0);
+    return s;
+}
+
+// Grid (O1/D2), covering (P:71-84/D8) and this rank's place in the rank grid -- pure host logic.
+struct GridInfo {
+    int n_int = 0, N = 0, nf = 0, ng = 0, wo = 0, wp = 0;
+    double h = 0;
+    int P[2] = {1, 1};
+    std::vector<int> st[2];
+    int gx = 1, gy = 1, rx = 0, ry = 0;
+    int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0;
+    int i0 = 1, i1 = 1, j0 = 1, j1 = 1;       // owned free nodes
+    int halo_lo = 0, halo_hi = 0;             // ghost nodes below / above: delta + kappa - 1, delta + kappa
+    int nbr[4] = {-1, -1, -1, -1};            // -x, +x, -y, +y
+    int e_i0 = 1, e_i1 = 1, e_j0 = 1, e_j1 = 1;   // ext rectangle (apply input)
+};
+
+int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* err, size_t errlen)
+{
+    if (!(p.k > 0) || p.ppw < 1 || p.n_pml_global < 1 || p.nsub_x < 1 || p.nsub_y < 1 || p.sigma0 < 0) {
+        snprintf(err, errlen, "invalid parameters (k, ppw, n_pml_global, nsub, sigma0)");
+        return HELM_EINVAL;
+    }
+    if (p.local_bc != HELM_BC_DIRICHLET) {
+        snprintf(err, errlen, "only HELM_BC_DIRICHLET (RAS-PML-Drch) is implemented");
+        return HELM_EINVAL;
+    }
+    if (nranks < 1 || rank < 0 || rank >= nranks) {
+        snprintf(err, errlen, "bad rank %d / %d", rank, nranks);
+        return HELM_EINVAL;
+    }
+    // O1 / D2: n_int = round(ppw k / 2 pi) cells on (0,1), h = 1 / n_int, N = n_int + 2 n_g
+    G.n_int = round_half_up(p.ppw * p.k / (2.0 * M_PI));
+    if (G.n_int < 1) {
+        snprintf(err, errlen, "k * ppw too small: no interior cell");
+        return HELM_EINVAL;
+    }
+    G.h = 1.0 / G.n_int;
+    G.ng = p.n_pml_global;
+    G.N = G.n_int + 2 * G.ng;
+    G.nf = G.N - 1;
+    // BJ configs[0]: delta = kappa = max(2, round(1.59 ln k)) cells unless given
+    const int wdef = std::max(2, round_half_up(1.59 * log(p.k)));
+    G.wo = p.n_ovlp < 0 ? wdef : p.n_ovlp;
+    G.wp = p.n_pml < 0 ? wdef : p.n_pml;
+    G.P[0] = p.nsub_x;
+    G.P[1] = p.nsub_y;
+    G.st[0] = block_starts(G.N, G.P[0]);
+    G.st[1] = block_starts(G.N, G.P[1]);
+    const int w = G.wo + G.wp;
+    for (int ax = 0; ax < 2; ax++)
+        for (int b = 0; b < G.P[ax]; b++) {
+            const int sz = G.st[ax][b + 1] - G.st[ax][b];
+            if (sz < 2 || (G.P[ax] > 1 && sz < w)) {
+                snprintf(err, errlen, "block %d on axis %d has %d cells; needs >= delta + kappa = %d (and >= 2)", b, ax,
+                         sz, w);
+                return HELM_ELAYOUT;
+            }
+        }
+    // rank grid: default = most square factorisation with gx >= gy
+    int gx = p.gpu_grid_x, gy = p.gpu_grid_y;
+    if (gx <= 0 || gy <= 0) {
+        gy = 1;
+        for (int d = 1; d * d <= nranks; d++)
+            if (nranks % d == 0) gy = d;
+        gx = nranks / gy;
+        if (gx > G.P[0] && gy <= G.P[0] && gx <= G.P[1]) std::swap(gx, gy);
+    }
+    if (gx * gy != nranks || gx > G.P[0] || gy > G.P[1]) {
+        snprintf(err, errlen, "gpu grid %dx%d does not match %d ranks / %dx%d subdomains", gx, gy, nranks, G.P[0], G.P[1]);
+        return HELM_EINVAL;
+    }
+    G.gx = gx;
+    G.gy = gy;
+    G.rx = rank % gx;
+    G.ry = rank / gx;
+    const std::vector<int> sbx = block_starts(G.P[0], gx), sby = block_starts(G.P[1], gy);
+    G.bx0 = sbx[G.rx];
+    G.bx1 = sbx[G.rx + 1];
+    G.by0 = sby[G.ry];
+    G.by1 = sby[G.ry + 1];
+    // owned free nodes of this rank: union of its blocks' owned nodes (D10)
+    G.i0 = std::max(G.st[0][G.bx0], 1);
+    G.i1 = std::min(G.st[0][G.bx1], G.N);
+    G.j0 = std::max(G.st[1][G.by0], 1);
+    G.j1 = std::min(G.st[1][G.by1], G.N);
+    // the full box of a block's subdomain spans nodes s_p - w + 1 .. s_{p+1} + w - 1 while the block owns
+    // s_p .. s_{p+1} - 1 (half-open ownership, D10): w - 1 ghost nodes below, w above
+    G.halo_lo = w - 1;
+    G.halo_hi = w;
+    G.nbr[0] = G.rx > 0 ? rank - 1 : -1;
+    G.nbr[1] = G.rx < gx - 1 ? rank + 1 : -1;
+    G.nbr[2] = G.ry > 0 ? rank - gx : -1;
+    G.nbr[3] = G.ry < gy - 1 ? rank + gx : -1;
+    G.e_i0 = G.i0 - (G.nbr[0] >= 0 ? G.halo_lo : 0);
+    G.e_i1 = G.i1 + (G.nbr[1] >= 0 ? G.halo_hi : 0);
+    G.e_j0 = G.j0 - (G.nbr[2] >= 0 ? G.halo_lo : 0);
+    G.e_j1 = G.j1 + (G.nbr[3] >= 0 ? G.halo_hi : 0);
+    return HELM_OK;
+}
+
+// Two-phase halo exchange filling lo ghost layers below and hi above the owned rectangle (x first, then y
+// over the x-extended range, which carries the corners).  width 0 = the apply frame (halo_lo, halo_hi),
+// width W > 0 = W layers on both sides.  A message's send and receive rectangles may differ in shape: a
+// rank sends `hi` layers down (the lower neighbour's upper ghosts) and receives `lo` layers from below.
+int halo_schedule(const GridInfo& G, int width, helm_msg* out, int cap)
+{
+    int lo, hi;
+    if (width == 0) {
+        lo = G.halo_lo;
+        hi = G.halo_hi;
+    } else {
+        lo = hi = width;
+    }
+    if (width < 0 || lo < 0 || hi < 1 || hi > G.halo_hi) return HELM_EINVAL;
+    int n = 0;
+    auto add = [&](int phase, int peer, int s0, int s1, int t0, int t1, int r0, int r1, int q0, int q1) {
+        if (n < cap) out[n] = helm_msg{phase, peer, s0, s1, t0, t1, r0, r1, q0, q1};
+        n++;
+    };
+    if (G.nbr[0] >= 0) add(0, G.nbr[0], G.i0, G.i0 + hi, G.j0, G.j1, G.i0 - lo, G.i0, G.j0, G.j1);
+    if (G.nbr[1] >= 0) add(0, G.nbr[1], G.i1 - lo, G.i1, G.j0, G.j1, G.i1, G.i1 + hi, G.j0, G.j1);
+    const int x0 = G.i0 - (G.nbr[0] >= 0 ? lo : 0), x1 = G.i1 + (G.nbr[1] >= 0 ? hi : 0);
+    if (G.nbr[2] >= 0) add(1, G.nbr[2], x0, x1, G.j0, G.j0 + hi, x0, x1, G.j0 - lo, G.j0);
+    if (G.nbr[3] >= 0) add(1, G.nbr[3], x0, x1, G.j1 - lo, G.j1, x0, x1, G.j1, G.j1 + hi);
+    return n;
+}
+
+}  // namespace
 
 struct helm_ctx {
     helm_params p{};
@@ -21,17 +168,13 @@ struct helm_ctx {
     cudaStream_t stream = nullptr;
     char err[512] = {0};
 
-    // grid (D2) and widths
-    int n_int = 0, N = 0, nf = 0, ng = 0, wo = 0, wp = 0;
-    double h = 0;
+    GridInfo G;
     Geom geom{};
-    // this rank's owned rectangle of free nodes, [i0,i1) x [j0,j1), 1-based node indices
-    int i0 = 1, i1 = 1, j0 = 1, j1 = 1;
     long long n_local = 0;
 
     // subdomains held by this rank
     std::vector<SubDesc> subs;
-    int n_sub_total = 0, m_max = 0;
+    int m_max = 0;
     long long max_n = 0, local_unknowns = 0, n_dinv = 0, n_stc = 0;
     long long apply_bytes = 0, band_bytes = 0;
     SubDesc* d_desc = nullptr;
@@ -46,6 +189,18 @@ struct helm_ctx {
 
     // apply launch configuration
     int ap_block = 0, ap_smem = 0, ap_slot = 0, ap_grid = 0, ap_occ = 0;
+
+    // multi-rank: ghost-framed buffer (ext rectangle), pack / unpack buffers, communicator
+    bool multi = false, has_comm = false;
+    z2* d_ext = nullptr;
+    long long ext_stride = 0, n_ext = 0;
+    z2* d_sendbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+    z2* d_recvbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+    long long msg_cap = 0;
+    double* d_sq = nullptr;
+#ifdef HELM_HAVE_NCCL
+    ncclComm_t comm = nullptr;
+#endif
 
     // Krylov workspace
     z2* d_V = nullptr;
@@ -63,6 +218,17 @@ struct helm_ctx {
     std::vector<cudaEvent_t> ev_free;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
     int launches = 0;
+
+    StencilGeom owned_geom() const
+    {
+        StencilGeom s{G.i0, G.j0, G.i1 - G.i0, G.j1 - G.j0, G.nf, G.i0, G.j0, (long long)(G.i1 - G.i0)};
+        return s;
+    }
+    StencilGeom ext_geom() const
+    {
+        StencilGeom s{G.i0, G.j0, G.i1 - G.i0, G.j1 - G.j0, G.nf, G.e_i0, G.e_j0, ext_stride};
+        return s;
+    }
 };
 
 static int set_err(helm_ctx* ctx, int code, const char* fmt, ...)
@@ -78,12 +244,15 @@ static int set_err(helm_ctx* ctx, int code, const char* fmt, ...)
 
 #define CK(expr) HELM_CUDA_OK(expr)
 
+#ifdef HELM_HAVE_NCCL
+#define NK(expr)                                                                                              \
+    do {                                                                                                      \
+        ncclResult_t r__ = (expr);                                                                            \
+        if (r__ != ncclSuccess) return set_err(ctx, HELM_ENCCL, "%s: %s", #expr, ncclGetErrorString(r__));   \
+    } while (0)
+#endif
+
 namespace {
-
-constexpr int NVMAX = 64;
-constexpr int M_LIMIT = 112;   // factor kernel keeps an m x m complex block in shared memory
-
-int round_half_up(double x) { return (int)floor(x + 0.5); }
 
 template <class T>
 int dalloc(helm_ctx* ctx, T** p, size_t count)
@@ -98,98 +267,41 @@ int dalloc(helm_ctx* ctx, T** p, size_t count)
     return HELM_OK;
 }
 
-// Cartesian block starts: N cells into P blocks of floor/ceil size, larger blocks first (D8)
-std::vector<int> block_starts(int N, int P)
-{
-    std::vector<int> s(P + 1, 0);
-    const int q = N / P, r = N % P;
-    for (int b = 0; b < P; b++) s[b + 1] = s[b] + q + (b < r ? 1 : 0);
-    return s;
-}
-
 int build_layout(helm_ctx* ctx)
 {
-    const helm_params& p = ctx->p;
-    if (!(p.k > 0) || p.ppw < 1 || p.n_pml_global < 1 || p.nsub_x < 1 || p.nsub_y < 1 || p.sigma0 < 0)
-        return set_err(ctx, HELM_EINVAL, "invalid parameters (k, ppw, n_pml_global, nsub, sigma0)");
-    if (p.local_bc != HELM_BC_DIRICHLET)
-        return set_err(ctx, HELM_EINVAL, "only HELM_BC_DIRICHLET (RAS-PML-Drch) is implemented");
-    // O1 / D2: n_int = round(ppw k / 2 pi) cells on (0,1), h = 1 / n_int, N = n_int + 2 n_g
-    ctx->n_int = round_half_up(p.ppw * p.k / (2.0 * M_PI));
-    if (ctx->n_int < 1) return set_err(ctx, HELM_EINVAL, "k * ppw too small: no interior cell");
-    ctx->h = 1.0 / ctx->n_int;
-    ctx->ng = p.n_pml_global;
-    ctx->N = ctx->n_int + 2 * ctx->ng;
-    ctx->nf = ctx->N - 1;
-    // BJ configs[0]: delta = kappa = max(2, round(1.59 ln k)) cells unless given
-    const int wdef = std::max(2, round_half_up(1.59 * log(p.k)));
-    ctx->wo = p.n_ovlp < 0 ? wdef : p.n_ovlp;
-    ctx->wp = p.n_pml < 0 ? wdef : p.n_pml;
-
+    GridInfo& G = ctx->G;
+    int rc = compute_grid(ctx->p, ctx->rank, ctx->nranks, G, ctx->err, sizeof(ctx->err));
+    if (rc) return rc;
     Geom& g = ctx->geom;
-    g.k = p.k;
-    g.h = ctx->h;
-    g.h3 = ctx->h / 3.0;
-    g.sigma0 = p.sigma0;
-    g.kappa = ctx->ng * ctx->h;   // D3: one profile, kappa = kappa_g
-    g.N = ctx->N;
-    g.nf = ctx->nf;
-    g.ng = ctx->ng;
-    g.lo3 = 3L * ctx->ng;
-    g.hi3 = 3L * (ctx->N - ctx->ng);
-
-    // covering (D8)
-    const int P[2] = {p.nsub_x, p.nsub_y};
-    std::vector<int> st[2] = {block_starts(ctx->N, P[0]), block_starts(ctx->N, P[1])};
-    const int w = ctx->wo + ctx->wp;
-    for (int ax = 0; ax < 2; ax++)
-        for (int b = 0; b < P[ax]; b++) {
-            const int sz = st[ax][b + 1] - st[ax][b];
-            if (sz < 2 || (P[ax] > 1 && sz < w))
-                return set_err(ctx, HELM_ELAYOUT,
-                               "block %d on axis %d has %d cells; needs >= delta + kappa = %d (and >= 2)", b, ax, sz, w);
-        }
-    ctx->n_sub_total = P[0] * P[1];
-
-    // rank grid over the subdomain grid
-    int gx = p.gpu_grid_x, gy = p.gpu_grid_y;
-    if (gx <= 0 || gy <= 0) { gx = 1; gy = ctx->nranks; }
-    if (gx * gy != ctx->nranks || gx > P[0] || gy > P[1])
-        return set_err(ctx, HELM_EINVAL, "gpu grid %dx%d does not match %d ranks / %dx%d subdomains", gx, gy,
-                       ctx->nranks, P[0], P[1]);
-    const int rx = ctx->rank % gx, ry = ctx->rank / gx;
-    const std::vector<int> sbx = block_starts(P[0], gx), sby = block_starts(P[1], gy);
-    const int bx0 = sbx[rx], bx1 = sbx[rx + 1], by0 = sby[ry], by1 = sby[ry + 1];
-    // owned free nodes of this rank: union of its blocks' owned nodes (D10)
-    ctx->i0 = std::max(st[0][bx0], 1);
-    ctx->i1 = std::min(st[0][bx1], ctx->N);
-    ctx->j0 = std::max(st[1][by0], 1);
-    ctx->j1 = std::min(st[1][by1], ctx->N);
-    ctx->n_local = (long long)(ctx->i1 - ctx->i0) * (ctx->j1 - ctx->j0);
+    g.k = ctx->p.k;
+    g.h = G.h;
+    g.h3 = G.h / 3.0;
+    g.sigma0 = ctx->p.sigma0;
+    g.kappa = G.ng * G.h;   // D3: one profile, kappa = kappa_g
+    g.N = G.N;
+    g.nf = G.nf;
+    g.ng = G.ng;
+    g.lo3 = 3L * G.ng;
+    g.hi3 = 3L * (G.N - G.ng);
+    ctx->n_local = (long long)(G.i1 - G.i0) * (G.j1 - G.j0);
 
     long long fac = 0, stc = 0;
     ctx->subs.clear();
-    ctx->m_max = 0;
-    ctx->max_n = 0;
-    ctx->local_unknowns = 0;
-    ctx->apply_bytes = 0;
-    ctx->band_bytes = 0;
-    long long owned_total = 0;
-    for (int by = by0; by < by1; by++)
-        for (int bx = bx0; bx < bx1; bx++) {
+    for (int by = G.by0; by < G.by1; by++)
+        for (int bx = G.bx0; bx < G.bx1; bx++) {
             const int bb[2] = {bx, by};
             int own_lo[2], own_hi[2], int_lo[2], int_hi[2], full_lo[2], full_hi[2], has_lo[2], has_hi[2];
             for (int ax = 0; ax < 2; ax++) {
                 const int b = bb[ax];
-                own_lo[ax] = st[ax][b];
-                own_hi[ax] = st[ax][b + 1];
+                own_lo[ax] = G.st[ax][b];
+                own_hi[ax] = G.st[ax][b + 1];
                 has_lo[ax] = b > 0;
-                has_hi[ax] = b < P[ax] - 1;
-                int_lo[ax] = own_lo[ax] - (has_lo[ax] ? ctx->wo : 0);
-                int_hi[ax] = own_hi[ax] + (has_hi[ax] ? ctx->wo : 0);
-                full_lo[ax] = int_lo[ax] - (has_lo[ax] ? ctx->wp : 0);
-                full_hi[ax] = int_hi[ax] + (has_hi[ax] ? ctx->wp : 0);
-                if (full_lo[ax] < 0 || full_hi[ax] > ctx->N)
+                has_hi[ax] = b < G.P[ax] - 1;
+                int_lo[ax] = own_lo[ax] - (has_lo[ax] ? G.wo : 0);
+                int_hi[ax] = own_hi[ax] + (has_hi[ax] ? G.wo : 0);
+                full_lo[ax] = int_lo[ax] - (has_lo[ax] ? G.wp : 0);
+                full_hi[ax] = int_hi[ax] + (has_hi[ax] ? G.wp : 0);
+                if (full_lo[ax] < 0 || full_hi[ax] > G.N)
                     return set_err(ctx, HELM_ELAYOUT, "full box of subdomain (%d,%d) leaves Omega", bx, by);
             }
             SubDesc d{};
@@ -198,9 +310,9 @@ int build_layout(helm_ctx* ctx)
             d.gx0 = full_lo[0] + 1;
             d.gy0 = full_lo[1] + 1;
             d.olo = std::max(own_lo[0], 1) - d.gx0;
-            d.ohi = std::min(own_hi[0], ctx->N) - 1 - d.gx0;
+            d.ohi = std::min(own_hi[0], G.N) - 1 - d.gx0;
             d.lo = std::max(own_lo[1], 1) - d.gy0;
-            d.hi = std::min(own_hi[1], ctx->N) - 1 - d.gy0;
+            d.hi = std::min(own_hi[1], G.N) - 1 - d.gy0;
             d.tw = (d.lo + d.hi) / 2;
             d.ilo3 = 3 * int_lo[0];
             d.ihi3 = 3 * int_hi[0];
@@ -211,6 +323,10 @@ int build_layout(helm_ctx* ctx)
             d.stc_off = stc;
             if (d.m > M_LIMIT)
                 return set_err(ctx, HELM_EINVAL, "local block width %d exceeds %d (use more subdomains)", d.m, M_LIMIT);
+            // every node the subdomain reads must lie in this rank's ext rectangle
+            if (d.gx0 < G.e_i0 || d.gx0 + d.m > G.e_i1 || d.gy0 < G.e_j0 || d.gy0 + d.nb > G.e_j1)
+                return set_err(ctx, HELM_ELAYOUT, "subdomain (%d,%d) reaches beyond the halo of rank %d", bx, by,
+                               ctx->rank);
             fac += (long long)d.nb * d.m * d.m;
             stc += (long long)d.nb * 7 * d.m;
             ctx->m_max = std::max(ctx->m_max, d.m);
@@ -221,16 +337,14 @@ int build_layout(helm_ctx* ctx)
             // algorithmic bytes of one apply of this subdomain
             const long long nblocks = d.nb + d.hi - d.lo;
             const long long owned = (long long)(d.ohi - d.olo + 1) * (d.hi - d.lo + 1);
-            owned_total += owned;
-            ctx->apply_bytes += 16 * (nblocks * d.m * d.m      // explicit inverse blocks streamed
-                                      + n                      // restriction gather
-                                      + 2LL * nblocks * d.m    // two coupling vectors per block step
+            ctx->apply_bytes += 16 * (nblocks * d.m * d.m       // explicit inverse blocks streamed
+                                      + n                       // restriction gather
+                                      + 2LL * nblocks * d.m     // two coupling vectors per block step
                                       + 2LL * (d.hi - d.lo) * d.m   // y / z scratch written + read
-                                      + owned);                // owner write
+                                      + owned);                 // owner write
             ctx->band_bytes += 16 * (n * (2LL * (d.m + 1) + 1) + n + owned);
             ctx->subs.push_back(d);
         }
-    (void)owned_total;
     ctx->n_dinv = fac;
     ctx->n_stc = stc;
     return HELM_OK;
@@ -259,7 +373,81 @@ int ensure_krylov(helm_ctx* ctx, int restart)
     return HELM_OK;
 }
 
-int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
+int need_comm(helm_ctx* ctx)
+{
+    if (ctx->multi && !ctx->has_comm)
+        return set_err(ctx, HELM_ENCCL, "communication-free shard: use the _ext entry points");
+    return HELM_OK;
+}
+
+// ---------------------------------------------------------------------------------------- collectives
+// halo exchange of width W on the ghost-framed buffer d_ext (ext rectangle layout)
+int exchange(helm_ctx* ctx, int W)
+{
+#ifdef HELM_HAVE_NCCL
+    helm_msg msgs[4];
+    const int nm = halo_schedule(ctx->G, W, msgs, 4);
+    const GridInfo& G = ctx->G;
+    for (int phase = 0; phase < 2; phase++) {
+        int idx[4], k = 0;
+        for (int q = 0; q < nm; q++)
+            if (msgs[q].phase == phase) idx[k++] = q;
+        if (!k) continue;
+        for (int a = 0; a < k; a++) {
+            const helm_msg& m = msgs[idx[a]];
+            launch_copy_rect(ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], m.send_i0, m.send_j0,
+                             m.send_i1 - m.send_i0, m.send_i0, m.send_i1, m.send_j0, m.send_j1, ctx->stream);
+            ctx->launches++;
+        }
+        NK(ncclGroupStart());
+        for (int a = 0; a < k; a++) {
+            const helm_msg& m = msgs[idx[a]];
+            const size_t scnt = 2 * (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
+            const size_t rcnt = 2 * (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+            NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
+            NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
+        }
+        NK(ncclGroupEnd());
+        for (int a = 0; a < k; a++) {
+            const helm_msg& m = msgs[idx[a]];
+            launch_copy_rect(ctx->d_recvbuf[a], m.recv_i0, m.recv_j0, m.recv_i1 - m.recv_i0, ctx->d_ext, G.e_i0,
+                             G.e_j0, ctx->ext_stride, m.recv_i0, m.recv_i1, m.recv_j0, m.recv_j1, ctx->stream);
+            ctx->launches++;
+        }
+    }
+    return HELM_OK;
+#else
+    (void)W;
+    return set_err(ctx, HELM_ENCCL, "library built without NCCL");
+#endif
+}
+
+// in-place sum over ranks of `count` doubles on the device
+int allreduce(helm_ctx* ctx, double* buf, size_t count)
+{
+    if (!ctx->multi) return HELM_OK;
+#ifdef HELM_HAVE_NCCL
+    NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    return HELM_OK;
+#else
+    (void)buf;
+    (void)count;
+    return set_err(ctx, HELM_ENCCL, "library built without NCCL");
+#endif
+}
+
+// owned vector -> interior of d_ext, then exchange ghost layers (W = 0: the apply frame)
+int fill_ext(helm_ctx* ctx, const z2* v, int W)
+{
+    const GridInfo& G = ctx->G;
+    launch_copy_rect(v, G.i0, G.j0, G.i1 - G.i0, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, G.i0, G.i1, G.j0, G.j1,
+                     ctx->stream);
+    ctx->launches++;
+    return exchange(ctx, W);
+}
+
+// ------------------------------------------------------------------------------------------- operators
+int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z)
 {
     if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
     ApplyArgs a{};
@@ -268,14 +456,14 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
     a.nsub = (int)ctx->subs.size();
     a.dinv = ctx->d_dinv;
     a.stencil = ctx->d_stc;
-    a.in = r;
-    a.in_i0 = ctx->i0;
-    a.in_j0 = ctx->j0;
-    a.in_stride = ctx->i1 - ctx->i0;
+    a.in = in;
+    a.in_i0 = in_i0;
+    a.in_j0 = in_j0;
+    a.in_stride = in_stride;
     a.out = z;
-    a.out_i0 = ctx->i0;
-    a.out_j0 = ctx->j0;
-    a.out_stride = ctx->i1 - ctx->i0;
+    a.out_i0 = ctx->G.i0;
+    a.out_j0 = ctx->G.j0;
+    a.out_stride = ctx->G.i1 - ctx->G.i0;
     a.scratch = ctx->d_scratch;
     a.scratch_per_cta = ctx->scratch_per_cta;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -303,29 +491,78 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
     return HELM_OK;
 }
 
-// ||v|| on the device, copied to the host (synchronises)
-int norm_host(helm_ctx* ctx, const z2* v, double* out)
+// z = B^-1 r for an owned input vector (exchanging the halo when sharded)
+int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
 {
-    launch_norm_partial(v, ctx->n_local, ctx->d_dpart, ctx->nblk, ctx->stream);
+    int rc;
+    if ((rc = need_comm(ctx))) return rc;
+    if (!ctx->multi) return apply_raw(ctx, r, ctx->G.i0, ctx->G.j0, ctx->G.i1 - ctx->G.i0, z);
+    if ((rc = fill_ext(ctx, r, 0))) return rc;
+    return apply_raw(ctx, ctx->d_ext, ctx->G.e_i0, ctx->G.e_j0, ctx->ext_stride, z);
+}
+
+// y = A x for an owned input vector
+int spmv_impl(helm_ctx* ctx, const z2* x, z2* y)
+{
+    int rc;
+    if ((rc = need_comm(ctx))) return rc;
+    if (!ctx->multi) {
+        launch_spmv(ctx->d_A7, x, y, ctx->owned_geom(), ctx->stream);
+    } else {
+        if ((rc = fill_ext(ctx, x, 1))) return rc;
+        launch_spmv(ctx->d_A7, ctx->d_ext, y, ctx->ext_geom(), ctx->stream);
+    }
+    ctx->launches++;
+    return HELM_OK;
+}
+
+// global ||.||^2 partials -> norm on the device (d_norm) and optionally a Hessenberg slot
+int finish_norm(helm_ctx* ctx, z2* slot)
+{
+    if (!ctx->multi) {
+        launch_reduce_norm(ctx->d_dpart, ctx->nblk, slot, ctx->d_norm, ctx->stream);
+        ctx->launches++;
+        return HELM_OK;
+    }
+    launch_reduce_sq(ctx->d_dpart, ctx->nblk, ctx->d_sq, ctx->stream);
+    int rc;
+    if ((rc = allreduce(ctx, ctx->d_sq, 1))) return rc;
+    launch_finish_norm(ctx->d_sq, slot, ctx->d_norm, ctx->stream);
     ctx->launches += 2;
-    launch_reduce_norm(ctx->d_dpart, ctx->nblk, nullptr, ctx->d_norm, ctx->stream);
+    return HELM_OK;
+}
+
+int fetch_norm(helm_ctx* ctx, double* out)
+{
     CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_norm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     memcpy(out, ctx->h_pin, sizeof(double));
     return HELM_OK;
 }
 
+// ||v|| (global) to the host (synchronises)
+int norm_host(helm_ctx* ctx, const z2* v, double* out)
+{
+    launch_norm_partial(v, ctx->n_local, ctx->d_dpart, ctx->nblk, ctx->stream);
+    ctx->launches++;
+    int rc;
+    if ((rc = finish_norm(ctx, nullptr))) return rc;
+    return fetch_norm(ctx, out);
+}
+
 // r = b - A x and ||r|| (host)
 int residual_host(helm_ctx* ctx, const z2* b, const z2* x, z2* r, double* out)
 {
-    const int nx = ctx->i1 - ctx->i0, ny = ctx->j1 - ctx->j0;
-    launch_residual(ctx->d_A7, x, b, r, nx, ny, ctx->d_dpart, ctx->nblk, ctx->stream);
-    ctx->launches += 2;
-    launch_reduce_norm(ctx->d_dpart, ctx->nblk, nullptr, ctx->d_norm, ctx->stream);
-    CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_norm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    memcpy(out, ctx->h_pin, sizeof(double));
-    return HELM_OK;
+    int rc;
+    if (!ctx->multi) {
+        launch_residual(ctx->d_A7, x, b, r, ctx->owned_geom(), ctx->d_dpart, ctx->nblk, ctx->stream);
+    } else {
+        if ((rc = fill_ext(ctx, x, 1))) return rc;
+        launch_residual(ctx->d_A7, ctx->d_ext, b, r, ctx->ext_geom(), ctx->d_dpart, ctx->nblk, ctx->stream);
+    }
+    ctx->launches++;
+    if ((rc = finish_norm(ctx, nullptr))) return rc;
+    return fetch_norm(ctx, out);
 }
 
 // Right-preconditioned restarted GMRES (O9 of DESIGN.md), classical Gram-Schmidt with one
@@ -336,9 +573,9 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
     if (restart < 1 || restart + 1 > NVMAX || maxit < 0)
         return set_err(ctx, HELM_EINVAL, "restart must be in [1, %d], maxit >= 0", NVMAX - 1);
     int rc;
+    if ((rc = need_comm(ctx))) return rc;
     if ((rc = ensure_krylov(ctx, restart))) return rc;
     const long long n = ctx->n_local;
-    const int nx = ctx->i1 - ctx->i0, ny = ctx->j1 - ctx->j0;
     cudaStream_t s = ctx->stream;
     helm_gmres_info loc{};
     helm_gmres_info* inf = info ? info : &loc;
@@ -355,7 +592,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             return HELM_OK;
         }
         inf->status = HELM_BREAKDOWN;
-        return HELM_BREAKDOWN;
+        return set_err(ctx, HELM_BREAKDOWN, "non-finite ||b||");
     }
     double beta;
     if ((rc = residual_host(ctx, b, x, ctx->d_r, &beta))) return rc;
@@ -368,7 +605,8 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
     z2* V = ctx->d_V;
     while (true) {
         // v_0 = r / ||r||
-        CK(cudaMemcpyAsync(ctx->d_norm, &beta, sizeof(double), cudaMemcpyHostToDevice, s));
+        memcpy(ctx->h_pin, &beta, sizeof(double));
+        CK(cudaMemcpyAsync(ctx->d_norm, ctx->h_pin, sizeof(double), cudaMemcpyHostToDevice, s));
         launch_scale_by_norm(ctx->d_r, ctx->d_norm, V, n, s);
         ctx->launches++;
         std::fill(g.begin(), g.end(), cplx(0, 0));
@@ -378,18 +616,27 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             z2* vj = V + (long long)j * n;
             if ((rc = apply_impl(ctx, vj, ctx->d_z))) return rc;
             inf->applies++;
-            launch_spmv(ctx->d_A7, ctx->d_z, ctx->d_w, nx, ny, s);
+            if ((rc = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc;
             its++;
             // CGS2: h1 = V^H w; w -= V h1; h2 = V^H w; w -= V h2; H(:,j) = h1 + h2; H(j+1,j) = ||w||
             launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
             launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h1, nullptr, nullptr, s);
+            if ((rc = allreduce(ctx, (double*)ctx->d_h1, 2 * (size_t)(j + 1)))) return rc;
             launch_multiaxpy(V, n, j + 1, ctx->d_h1, ctx->d_w, n, nullptr, ctx->nblk, s);
             launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
-            launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, ctx->d_Hcol, ctx->d_h1, s);
+            if (!ctx->multi) {
+                launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, ctx->d_Hcol, ctx->d_h1, s);
+            } else {
+                launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, nullptr, nullptr, s);
+                if ((rc = allreduce(ctx, (double*)ctx->d_h2, 2 * (size_t)(j + 1)))) return rc;
+                launch_zadd(ctx->d_h1, ctx->d_h2, ctx->d_Hcol, j + 1, s);
+                ctx->launches++;
+            }
             launch_multiaxpy(V, n, j + 1, ctx->d_h2, ctx->d_w, n, ctx->d_dpart, ctx->nblk, s);
-            launch_reduce_norm(ctx->d_dpart, ctx->nblk, ctx->d_Hcol + j + 1, ctx->d_norm, s);
+            ctx->launches += 6;   // 2x multidot, 2x reduce, 2x multiaxpy
+            if ((rc = finish_norm(ctx, ctx->d_Hcol + j + 1))) return rc;
             launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
-            ctx->launches += 9;   // spmv, 2x multidot, 2x reduce, 2x multiaxpy, norm, scale
+            ctx->launches++;
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_Hcol, sizeof(z2) * (j + 2), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -434,10 +681,11 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         for (int i = 0; i < jend; i++) ctx->h_pin[i] = zmk(y[i].real(), y[i].imag());
         CK(cudaMemcpyAsync(ctx->d_y, ctx->h_pin, sizeof(z2) * jend, cudaMemcpyHostToDevice, s));
         launch_combine(V, n, jend, ctx->d_y, ctx->d_t, n, s);
+        ctx->launches++;
         if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
         inf->applies++;
         launch_axpy(x, ctx->d_z, n, s);
-        ctx->launches += 2;   // combine, axpy
+        ctx->launches++;
         double rn;
         if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
         cycles++;
@@ -467,6 +715,57 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
 // ===================================================================================================== C ABI
 extern "C" {
 
+int helm_plan_rank(const helm_params* params, int rank, int nranks, helm_plan* out)
+{
+    if (!params || !out) return HELM_EINVAL;
+    GridInfo G;
+    char err[256];
+    int rc = compute_grid(*params, rank, nranks, G, err, sizeof(err));
+    if (rc) return rc;
+    out->gx = G.gx;
+    out->gy = G.gy;
+    out->rx = G.rx;
+    out->ry = G.ry;
+    out->owned_i0 = G.i0;
+    out->owned_i1 = G.i1;
+    out->owned_j0 = G.j0;
+    out->owned_j1 = G.j1;
+    out->ext_i0 = G.e_i0;
+    out->ext_i1 = G.e_i1;
+    out->ext_j0 = G.e_j0;
+    out->ext_j1 = G.e_j1;
+    out->halo_lo = G.halo_lo;
+    out->halo_hi = G.halo_hi;
+    for (int q = 0; q < 4; q++) out->nbr[q] = G.nbr[q];
+    out->n_sub_local = (G.bx1 - G.bx0) * (G.by1 - G.by0);
+    return HELM_OK;
+}
+
+int helm_halo_schedule(const helm_params* params, int rank, int nranks, int width, helm_msg* out, int cap)
+{
+    if (!params || (!out && cap > 0)) return HELM_EINVAL;
+    GridInfo G;
+    char err[256];
+    int rc = compute_grid(*params, rank, nranks, G, err, sizeof(err));
+    if (rc) return rc;
+    return halo_schedule(G, width, out, cap);
+}
+
+int helm_nccl_unique_id(void* out128)
+{
+#ifdef HELM_HAVE_NCCL
+    if (!out128) return HELM_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return HELM_ENCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    memcpy(out128, &id, sizeof(id));
+    return HELM_OK;
+#else
+    (void)out128;
+    return HELM_ENCCL;
+#endif
+}
+
 int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id, void* cuda_stream,
                helm_ctx** out)
 {
@@ -478,19 +777,36 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     ctx->nranks = nranks;
     ctx->stream = (cudaStream_t)cuda_stream;
     *out = ctx;
-    if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(ctx, HELM_EINVAL, "bad rank %d / %d", rank, nranks);
-    if (nranks > 1) {
-        (void)nccl_unique_id;
-        return set_err(ctx, HELM_ENCCL, "multi-rank execution is not built into this library yet");
-    }
     int rc = build_layout(ctx);
     if (rc) return rc;
+    ctx->multi = nranks > 1;
+    if (ctx->multi && nccl_unique_id) {
+#ifdef HELM_HAVE_NCCL
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+        ctx->has_comm = true;
+#else
+        return set_err(ctx, HELM_ENCCL, "library built without NCCL");
+#endif
+    }
     // device buffers: global stencil, local stencils, descriptors
     const int nsub = (int)ctx->subs.size();
     if ((rc = dalloc(ctx, &ctx->d_A7, 7 * (size_t)ctx->n_local)) || (rc = dalloc(ctx, &ctx->d_stc, ctx->n_stc)) ||
         (rc = dalloc(ctx, &ctx->d_desc, nsub)) || (rc = dalloc(ctx, &ctx->d_order, nsub)) ||
-        (rc = dalloc(ctx, &ctx->d_err, 4)))
+        (rc = dalloc(ctx, &ctx->d_err, 4)) || (rc = dalloc(ctx, &ctx->d_sq, 2)))
         return rc;
+    if (ctx->multi) {
+        const GridInfo& G = ctx->G;
+        ctx->ext_stride = G.e_i1 - G.e_i0;
+        ctx->n_ext = ctx->ext_stride * (G.e_j1 - G.e_j0);
+        ctx->msg_cap = (long long)std::max(G.i1 - G.i0 + G.halo_lo + G.halo_hi, G.j1 - G.j0) * G.halo_hi;
+        if ((rc = dalloc(ctx, &ctx->d_ext, ctx->n_ext))) return rc;
+        CK(cudaMemsetAsync(ctx->d_ext, 0, sizeof(z2) * ctx->n_ext, ctx->stream));
+        for (int q = 0; q < 4; q++)
+            if ((rc = dalloc(ctx, &ctx->d_sendbuf[q], ctx->msg_cap)) || (rc = dalloc(ctx, &ctx->d_recvbuf[q], ctx->msg_cap)))
+                return rc;
+    }
     // processing order: most expensive first (static round-robin over persistent CTAs)
     std::vector<int> order(nsub);
     for (int i = 0; i < nsub; i++) order[i] = i;
@@ -501,7 +817,7 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     CK(cudaMemcpyAsync(ctx->d_desc, ctx->subs.data(), sizeof(SubDesc) * nsub, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_order, order.data(), sizeof(int) * nsub, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(ctx->d_err, 0, 4 * sizeof(int), ctx->stream));
-    launch_assemble_global(ctx->geom, ctx->d_A7, ctx->i0, ctx->i1, ctx->j0, ctx->j1, ctx->stream);
+    launch_assemble_global(ctx->geom, ctx->d_A7, ctx->G.i0, ctx->G.i1, ctx->G.j0, ctx->G.j1, ctx->stream);
     launch_assemble_local(ctx->geom, ctx->d_desc, nsub, ctx->d_stc, (int)ctx->max_n, ctx->stream);
     CK(cudaGetLastError());
     // apply launch configuration
@@ -522,17 +838,18 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
 int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
 {
     if (!ctx || !out) return HELM_EINVAL;
-    out->n_free_global = (long long)ctx->nf * ctx->nf;
-    out->N_cells = ctx->N;
-    out->n_int = ctx->n_int;
-    out->n_ovlp = ctx->wo;
-    out->n_pml = ctx->wp;
-    out->owned_i0 = ctx->i0;
-    out->owned_i1 = ctx->i1;
-    out->owned_j0 = ctx->j0;
-    out->owned_j1 = ctx->j1;
+    const GridInfo& G = ctx->G;
+    out->n_free_global = (long long)G.nf * G.nf;
+    out->N_cells = G.N;
+    out->n_int = G.n_int;
+    out->n_ovlp = G.wo;
+    out->n_pml = G.wp;
+    out->owned_i0 = G.i0;
+    out->owned_i1 = G.i1;
+    out->owned_j0 = G.j0;
+    out->owned_j1 = G.j1;
     out->n_local = ctx->n_local;
-    out->n_sub = ctx->n_sub_total;
+    out->n_sub = G.P[0] * G.P[1];
     out->n_sub_local = (int)ctx->subs.size();
     out->m_max = ctx->m_max;
     out->local_unknowns = ctx->local_unknowns;
@@ -547,10 +864,11 @@ int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_h
 {
     if (!ctx || nsrc < 0 || (nsrc > 0 && (!xy_host || !amp_host)) || !b_dev || !(sigma > 0))
         return set_err(ctx, HELM_EINVAL, "helm_rhs: bad arguments");
+    const GridInfo& G = ctx->G;
     double* d_xy = nullptr;
     z2* d_amp = nullptr;
     z2* d_f = nullptr;
-    const long long nfw = (long long)(ctx->i1 - ctx->i0 + 2) * (ctx->j1 - ctx->j0 + 2);
+    const long long nfw = (long long)(G.i1 - G.i0 + 2) * (G.j1 - G.j0 + 2);
     int rc;
     if ((rc = dalloc(ctx, &d_xy, 2 * (size_t)std::max(nsrc, 1))) || (rc = dalloc(ctx, &d_amp, std::max(nsrc, 1))) ||
         (rc = dalloc(ctx, &d_f, nfw)))
@@ -559,7 +877,7 @@ int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_h
         CK(cudaMemcpyAsync(d_xy, xy_host, sizeof(double) * 2 * nsrc, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(d_amp, amp_host, sizeof(z2) * nsrc, cudaMemcpyHostToDevice, ctx->stream));
     }
-    launch_rhs(ctx->geom, nsrc, d_xy, d_amp, sigma, d_f, (z2*)b_dev, ctx->i0, ctx->i1, ctx->j0, ctx->j1, ctx->stream);
+    launch_rhs(ctx->geom, nsrc, d_xy, d_amp, sigma, d_f, (z2*)b_dev, G.i0, G.i1, G.j0, G.j1, ctx->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     cudaFree(d_xy);
@@ -591,7 +909,19 @@ int helm_matvec(helm_ctx* ctx, const helm_z* x_dev, helm_z* y_dev)
 {
     if (!ctx || !x_dev || !y_dev || (const void*)x_dev == (void*)y_dev)
         return set_err(ctx, HELM_EINVAL, "helm_matvec: bad arguments");
-    launch_spmv(ctx->d_A7, (const z2*)x_dev, (z2*)y_dev, ctx->i1 - ctx->i0, ctx->j1 - ctx->j0, ctx->stream);
+    int rc = spmv_impl(ctx, (const z2*)x_dev, (z2*)y_dev);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    return HELM_OK;
+}
+
+int helm_matvec_ext(helm_ctx* ctx, const helm_z* ext1_dev, helm_z* y_dev)
+{
+    if (!ctx || !ext1_dev || !y_dev) return set_err(ctx, HELM_EINVAL, "helm_matvec_ext: bad arguments");
+    const GridInfo& G = ctx->G;
+    const int li = G.nbr[0] >= 0, ri = G.nbr[1] >= 0, dj = G.nbr[2] >= 0;
+    StencilGeom sg{G.i0, G.j0, G.i1 - G.i0, G.j1 - G.j0, G.nf, G.i0 - li, G.j0 - dj, (long long)(G.i1 - G.i0 + li + ri)};
+    launch_spmv(ctx->d_A7, (const z2*)ext1_dev, (z2*)y_dev, sg, ctx->stream);
     ctx->launches++;
     CK(cudaGetLastError());
     return HELM_OK;
@@ -602,6 +932,13 @@ int helm_precond_apply(helm_ctx* ctx, const helm_z* r_dev, helm_z* z_dev)
     if (!ctx || !r_dev || !z_dev || (const void*)r_dev == (void*)z_dev)
         return set_err(ctx, HELM_EINVAL, "helm_precond_apply: bad arguments");
     return apply_impl(ctx, (const z2*)r_dev, (z2*)z_dev);
+}
+
+int helm_precond_apply_ext(helm_ctx* ctx, const helm_z* ext_dev, helm_z* z_dev)
+{
+    if (!ctx || !ext_dev || !z_dev) return set_err(ctx, HELM_EINVAL, "helm_precond_apply_ext: bad arguments");
+    const GridInfo& G = ctx->G;
+    return apply_raw(ctx, (const z2*)ext_dev, G.e_i0, G.e_j0, G.e_i1 - G.e_i0, (z2*)z_dev);
 }
 
 int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host)
@@ -683,11 +1020,18 @@ void helm_destroy(helm_ctx* ctx)
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
+#ifdef HELM_HAVE_NCCL
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+#endif
     void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
-                    ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart};
+                    ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    for (int q = 0; q < 4; q++) {
+        if (ctx->d_sendbuf[q]) cudaFree(ctx->d_sendbuf[q]);
+        if (ctx->d_recvbuf[q]) cudaFree(ctx->d_recvbuf[q]);
+    }
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     for (auto e : ctx->ev_free) cudaEventDestroy(e);
     for (auto& pr : ctx->ev_used) {

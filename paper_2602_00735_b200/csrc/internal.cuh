@@ -105,9 +105,20 @@ struct ApplyArgs {
 int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
 
-void launch_spmv(const z2* A7, const z2* x, z2* y, int nx, int ny, cudaStream_t s);
-void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, int nx, int ny, double* partial, int nblk,
+// owned rows [i0, i0+nx) x [j0, j0+ny) of the 7-point operator; x read from a buffer with origin (xi0, xj0)
+struct StencilGeom {
+    int i0, j0, nx, ny, nf;
+    int xi0, xj0;
+    long long xstride;
+};
+void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s);
+void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s);
+void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,
+                      int i0, int i1, int j0, int j1, cudaStream_t s);
+void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t s);
+void launch_finish_norm(const double* sq, z2* out_slot, double* out_norm, cudaStream_t s);
+void launch_zadd(const z2* a, const z2* b, z2* out, int nv, cudaStream_t s);
 void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long n, z2* partial, int nblk,
                      cudaStream_t s);
 void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, double* partial_norm,

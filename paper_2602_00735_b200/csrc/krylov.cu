@@ -47,45 +47,85 @@ __device__ double block_sum(double v, double* sh)
 __constant__ int c_dx[7] = { 0, 1, -1, 0, 0, 1, -1 };
 __constant__ int c_dy[7] = { 0, 0, 0, 1, -1, 1, -1 };
 
-__device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* __restrict__ x, long long r, long long n,
-                                          int nx, int ny)
+// Row r of the owned rectangle (x-fastest): y = sum_s A7[s][r] x(neighbour_s); x is read from a buffer
+// covering the owned rectangle plus whatever ghost frame the caller provides (origin xi0, xj0; stride).
+__device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* __restrict__ x, long long r,
+                                          const StencilGeom& G)
 {
-    const int i = (int)(r % nx), j = (int)(r / nx);
+    const long long n = (long long)G.nx * G.ny;
+    const int i = G.i0 + (int)(r % G.nx), j = G.j0 + (int)(r / G.nx);
     z2 acc = zmk(0, 0);
 #pragma unroll
     for (int s = 0; s < 7; s++) {
         const int qi = i + c_dx[s], qj = j + c_dy[s];
-        if (qi >= 0 && qi < nx && qj >= 0 && qj < ny)
-            zfma(acc, __ldg(A7 + s * n + r), __ldg(x + qi + (long long)nx * qj));
+        if (qi >= 1 && qi <= G.nf && qj >= 1 && qj <= G.nf)
+            zfma(acc, __ldg(A7 + s * n + r), __ldg(x + (qi - G.xi0) + G.xstride * (qj - G.xj0)));
     }
     return acc;
 }
 
 __global__ void __launch_bounds__(KT) k_spmv(const z2* __restrict__ A7, const z2* __restrict__ x, z2* __restrict__ y,
-                                             int nx, int ny)
+                                             StencilGeom G)
 {
-    const long long n = (long long)nx * ny;
+    const long long n = (long long)G.nx * G.ny;
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
-        y[r] = stencil_row(A7, x, r, n, nx, ny);
+        y[r] = stencil_row(A7, x, r, G);
 }
 
 // r = b - A x, partial[blk] = ||r||^2 over the CTA's rows
 __global__ void __launch_bounds__(KT) k_residual(const z2* __restrict__ A7, const z2* __restrict__ x,
-                                                 const z2* __restrict__ b, z2* __restrict__ r, int nx, int ny,
+                                                 const z2* __restrict__ b, z2* __restrict__ r, StencilGeom G,
                                                  double* __restrict__ partial)
 {
     __shared__ double sh[KT / 32];
-    const long long n = (long long)nx * ny;
+    const long long n = (long long)G.nx * G.ny;
     long long r0, r1;
     chunk_of(n, r0, r1);
     double s = 0.0;
     for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
-        const z2 v = zsub(__ldg(b + e), stencil_row(A7, x, e, n, nx, ny));
+        const z2 v = zsub(__ldg(b + e), stencil_row(A7, x, e, G));
         r[e] = v;
         s += zabs2(v);
     }
     s = block_sum(s, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// dst(rect) = src(rect): strided 2-D copy between vectors with different origins / strides (halo pack,
+// unpack, owned -> ghost-framed buffer)
+__global__ void __launch_bounds__(KT) k_copy_rect(const z2* __restrict__ src, int si0, int sj0, long long sstride,
+                                                  z2* __restrict__ dst, int di0, int dj0, long long dstride,
+                                                  int i0, int i1, int j0, int j1)
+{
+    const int w = i1 - i0;
+    const long long n = (long long)w * (j1 - j0);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int i = i0 + (int)(e % w), j = j0 + (int)(e / w);
+        dst[(i - di0) + dstride * (j - dj0)] = src[(i - si0) + sstride * (j - sj0)];
+    }
+}
+
+// sum of squares (no sqrt) -> *sq; used before a cross-rank allreduce
+__global__ void k_reduce_sq(const double* __restrict__ partial, int nblk, double* sq)
+{
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += partial[b];
+    s = warp_sum(s);
+    if (lane == 0) *sq = s;
+}
+
+__global__ void k_finish_norm(const double* sq, z2* out_slot, double* out_norm)
+{
+    const double nrm = sqrt(*sq);
+    if (out_slot) *out_slot = zmk(nrm, 0.0);
+    if (out_norm) *out_norm = nrm;
+}
+
+// out[v] = a[v] + b[v]
+__global__ void k_zadd(const z2* __restrict__ a, const z2* __restrict__ b, z2* __restrict__ out, int nv)
+{
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) out[v] = zadd(a[v], b[v]);
 }
 
 // partial[blk][v] = sum_{e in blk} conj(V_v[e]) w[e],  v < nv
@@ -237,15 +277,31 @@ int ew_grid(long long n)
 
 }  // namespace
 
-void launch_spmv(const z2* A7, const z2* x, z2* y, int nx, int ny, cudaStream_t s)
+void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s)
 {
-    k_spmv<<<ew_grid((long long)nx * ny), KT, 0, s>>>(A7, x, y, nx, ny);
+    k_spmv<<<ew_grid((long long)G.nx * G.ny), KT, 0, s>>>(A7, x, y, G);
 }
-void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, int nx, int ny, double* partial, int nblk,
+void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s)
 {
-    k_residual<<<nblk, KT, 0, s>>>(A7, x, b, r, nx, ny, partial);
+    k_residual<<<nblk, KT, 0, s>>>(A7, x, b, r, G, partial);
 }
+void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,
+                      int i0, int i1, int j0, int j1, cudaStream_t s)
+{
+    const long long n = (long long)(i1 - i0) * (j1 - j0);
+    if (n <= 0) return;
+    k_copy_rect<<<ew_grid(n), KT, 0, s>>>(src, si0, sj0, sstride, dst, di0, dj0, dstride, i0, i1, j0, j1);
+}
+void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t s)
+{
+    k_reduce_sq<<<1, 32, 0, s>>>(partial, nblk, sq);
+}
+void launch_finish_norm(const double* sq, z2* out_slot, double* out_norm, cudaStream_t s)
+{
+    k_finish_norm<<<1, 1, 0, s>>>(sq, out_slot, out_norm);
+}
+void launch_zadd(const z2* a, const z2* b, z2* out, int nv, cudaStream_t s) { k_zadd<<<1, 64, 0, s>>>(a, b, out, nv); }
 void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long n, z2* partial, int nblk,
                      cudaStream_t s)
 {

@@ -47,9 +47,32 @@ class GmresInfo(C.Structure):
                 ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
 
 
+class Plan(C.Structure):
+    _fields_ = [("gx", C.c_int), ("gy", C.c_int), ("rx", C.c_int), ("ry", C.c_int),
+                ("owned_i0", C.c_int), ("owned_i1", C.c_int), ("owned_j0", C.c_int), ("owned_j1", C.c_int),
+                ("ext_i0", C.c_int), ("ext_i1", C.c_int), ("ext_j0", C.c_int), ("ext_j1", C.c_int),
+                ("halo_lo", C.c_int), ("halo_hi", C.c_int), ("nbr", C.c_int * 4), ("n_sub_local", C.c_int)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "nbr"}
+        d["nbr"] = list(self.nbr)
+        return d
+
+
+class Msg(C.Structure):
+    _fields_ = [("phase", C.c_int), ("peer", C.c_int),
+                ("send_i0", C.c_int), ("send_i1", C.c_int), ("send_j0", C.c_int), ("send_j1", C.c_int),
+                ("recv_i0", C.c_int), ("recv_i1", C.c_int), ("recv_j0", C.c_int), ("recv_j1", C.c_int)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_matvec", "helm_precond_apply",
            "helm_precond_apply_host", "helm_gmres", "helm_gmres_host", "helm_export_stencil",
-           "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy"]
+           "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy",
+           "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
+           "helm_matvec_ext"]
 
 
 def lib_path() -> str:
@@ -79,6 +102,11 @@ def load(build_if_missing: bool = True):
     L.helm_export_stencil.argtypes = [vp, vp]
     L.helm_profile_enable.argtypes = [vp, i]
     L.helm_profile_read.argtypes = [vp, C.POINTER(d), C.POINTER(i), C.POINTER(i)]
+    L.helm_plan_rank.argtypes = [C.POINTER(Params), i, i, C.POINTER(Plan)]
+    L.helm_halo_schedule.argtypes = [C.POINTER(Params), i, i, i, C.POINTER(Msg), i]
+    L.helm_nccl_unique_id.argtypes = [vp]
+    L.helm_precond_apply_ext.argtypes = [vp, vp, vp]
+    L.helm_matvec_ext.argtypes = [vp, vp, vp]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
     L.helm_destroy.argtypes = [vp]
@@ -101,6 +129,41 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def make_params(k, nsub_x, nsub_y=None, ppw=10, n_pml_global=10, sigma0=5.0, n_ovlp=-1, n_pml=-1,
+                gpu_grid=(0, 0)) -> Params:
+    return Params(float(k), ppw, n_pml_global, float(sigma0), nsub_x, nsub_y if nsub_y is not None else nsub_x,
+                  n_ovlp, n_pml, 0, gpu_grid[0], gpu_grid[1])
+
+
+def plan_rank(params: Params, rank: int, nranks: int) -> dict:
+    """This rank's owned / ghost-framed rectangles and neighbours (host logic of libhelm, no GPU needed)."""
+    L = load()
+    pl = Plan()
+    rc = L.helm_plan_rank(C.byref(params), rank, nranks, C.byref(pl))
+    if rc != 0:
+        raise HelmError(rc, "helm_plan_rank")
+    return pl.as_dict()
+
+
+def halo_schedule(params: Params, rank: int, nranks: int, width: int) -> list:
+    """The two-phase halo exchange libhelm performs for `rank` (list of message dicts)."""
+    L = load()
+    msgs = (Msg * 4)()
+    n = L.helm_halo_schedule(C.byref(params), rank, nranks, width, msgs, 4)
+    if n < 0:
+        raise HelmError(n, "helm_halo_schedule")
+    return [msgs[q].as_dict() for q in range(n)]
+
+
+def nccl_unique_id() -> bytes:
+    L = load()
+    buf = C.create_string_buffer(128)
+    rc = L.helm_nccl_unique_id(buf)
+    if rc != 0:
+        raise HelmError(rc, "helm_nccl_unique_id (library built without NCCL?)")
+    return buf.raw
+
+
 class Context:
     """One rank's RAS-PML problem: owns the libhelm context (operators, factors, Krylov workspace)."""
 
@@ -111,8 +174,8 @@ class Context:
         if not torch.cuda.is_available():
             raise RuntimeError("libhelm needs a CUDA device (no CPU fallback)")
         self.L = load()
-        self.params = Params(float(k), ppw, n_pml_global, float(sigma0), nsub_x,
-                             nsub_y if nsub_y is not None else nsub_x, n_ovlp, n_pml, 0, gpu_grid[0], gpu_grid[1])
+        self.params = make_params(k, nsub_x, nsub_y, ppw, n_pml_global, sigma0, n_ovlp, n_pml, gpu_grid)
+        self.rank, self.nranks = rank, nranks
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._h = C.c_void_p()
         idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
@@ -121,6 +184,7 @@ class Context:
         self._check(rc)
         self.layout = self._layout()
         self.n = self.layout.n_local
+        self.plan = plan_rank(self.params, rank, nranks)
 
     # ------------------------------------------------------------------------------------------ plumbing
     def _check(self, rc: int, ok=(0,)):
@@ -170,6 +234,18 @@ class Context:
         z = self.empty() if out is None else out
         self._check(self.L.helm_precond_apply(self._h, _ptr(r), _ptr(z)))
         return z
+
+    def precond_apply_ext(self, ext, out=None):
+        """Apply with a caller-filled ghost-framed input covering plan['ext_*'] (no communication)."""
+        z = self.empty() if out is None else out
+        self._check(self.L.helm_precond_apply_ext(self._h, _ptr(ext), _ptr(z)))
+        return z
+
+    def matvec_ext(self, ext1, out=None):
+        """matvec with a caller-filled input covering the owned rectangle grown by 1 toward neighbours."""
+        y = self.empty() if out is None else out
+        self._check(self.L.helm_matvec_ext(self._h, _ptr(ext1), _ptr(y)))
+        return y
 
     def precond_apply_host(self, r_host, z_host):
         self._check(self.L.helm_precond_apply_host(self._h, _ptr(r_host), _ptr(z_host)))

@@ -1,0 +1,134 @@
+"""Multi-rank host logic of libhelm (rank plan + two-phase halo schedule), checked on CPU: partition of the free
+nodes, message pairing, coverage of every subdomain's full box, and the exchange itself executed over a gloo
+process group (world size 2 and 4) on a synthetic global vector.  -m "not gpu"."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from paper_2602_00735_b200.helm import make_params, plan_rank, halo_schedule
+
+CASES = [(100.0, 4, 2), (100.0, 4, 4), (400.0, 16, 2), (400.0, 16, 4), (400.0, 16, 8), (400.0, 16, 6),
+         (1600.0, 64, 8), (100.0, 5, 3)]
+
+
+@pytest.mark.parametrize("k,nsub,nranks", CASES)
+def test_owned_rectangles_partition_the_free_nodes(k, nsub, nranks):
+    p = make_params(k, nsub)
+    plans = [plan_rank(p, r, nranks) for r in range(nranks)]
+    nf = plans[0]["owned_i1"] if False else None
+    o = Oracle.from_config(k=k, nsub_x=nsub, nsub_y=nsub)
+    nfx, nfy = o.nf
+    cover = np.zeros((nfy + 2, nfx + 2), int)
+    for pl in plans:
+        cover[pl["owned_j0"]:pl["owned_j1"], pl["owned_i0"]:pl["owned_i1"]] += 1
+        assert pl["gx"] * pl["gy"] == nranks
+    assert np.all(cover[1:nfy + 1, 1:nfx + 1] == 1) and cover.sum() == nfx * nfy
+    assert sum(pl["n_sub_local"] for pl in plans) == nsub * nsub
+
+
+@pytest.mark.parametrize("k,nsub,nranks", CASES)
+def test_every_full_box_inside_its_ranks_ghost_frame(k, nsub, nranks):
+    """The halo width delta + kappa - 1 is exactly what the edge subdomains' full boxes need."""
+    p = make_params(k, nsub)
+    o = Oracle.from_config(k=k, nsub_x=nsub, nsub_y=nsub)
+    need = {r: [10 ** 9, -1, 10 ** 9, -1] for r in range(nranks)}
+    plans = [plan_rank(p, r, nranks) for r in range(nranks)]
+    for j in range(o.nsub):
+        s = o.subdomain(j)
+        gi, gj = max(s["own_lo"][0], 1), max(s["own_lo"][1], 1)
+        r = next(q for q, pl in enumerate(plans) if pl["owned_i0"] <= gi < pl["owned_i1"] and pl["owned_j0"] <= gj < pl["owned_j1"])
+        pl = plans[r]
+        # local free nodes: full_lo+1 .. full_hi-1 per axis
+        assert pl["ext_i0"] <= s["full_lo"][0] + 1 and s["full_hi"][0] - 1 < pl["ext_i1"]
+        assert pl["ext_j0"] <= s["full_lo"][1] + 1 and s["full_hi"][1] - 1 < pl["ext_j1"]
+        n = need[r]
+        n[0] = min(n[0], s["full_lo"][0] + 1); n[1] = max(n[1], s["full_hi"][0] - 1)
+        n[2] = min(n[2], s["full_lo"][1] + 1); n[3] = max(n[3], s["full_hi"][1] - 1)
+    for r, pl in enumerate(plans):   # and no wider than needed
+        assert need[r] == [pl["ext_i0"], pl["ext_i1"] - 1, pl["ext_j0"], pl["ext_j1"] - 1]
+
+
+@pytest.mark.parametrize("k,nsub,nranks", CASES)
+@pytest.mark.parametrize("W", [0, 1])
+def test_messages_pair_up(k, nsub, nranks, W):
+    p = make_params(k, nsub)
+    sched = {r: halo_schedule(p, r, nranks, W) for r in range(nranks)}
+    for r, msgs in sched.items():
+        for m in msgs:
+            back = [q for q in sched[m["peer"]] if q["peer"] == r and q["phase"] == m["phase"]]
+            assert len(back) == 1
+            q = back[0]
+            # what r sends is exactly what the peer receives, node for node
+            assert (m["send_i0"], m["send_i1"], m["send_j0"], m["send_j1"]) == \
+                   (q["recv_i0"], q["recv_i1"], q["recv_j0"], q["recv_j1"])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _exchange_worker(rank, nranks, port, k, nsub, result_q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    try:
+        p = make_params(k, nsub)
+        pl = plan_rank(p, rank, nranks)
+        N = int(round(10 * k / (2 * np.pi))) + 20
+        nf = N - 1
+        gid = lambda i, j: (i - 1) + nf * (j - 1)   # noqa: E731  synthetic global vector value = index
+        ok = True
+        for W in (0, 1):
+            lo, hi = (pl["halo_lo"], pl["halo_hi"]) if W == 0 else (W, W)
+            e_i0, e_j0 = pl["ext_i0"], pl["ext_j0"]
+            ew, eh = pl["ext_i1"] - e_i0, pl["ext_j1"] - e_j0
+            buf = torch.full((eh, ew), -1.0, dtype=torch.float64)
+            for j in range(pl["owned_j0"], pl["owned_j1"]):
+                buf[j - e_j0, pl["owned_i0"] - e_i0:pl["owned_i1"] - e_i0] = torch.tensor(
+                    [float(gid(i, j)) for i in range(pl["owned_i0"], pl["owned_i1"])])
+            msgs = halo_schedule(p, rank, nranks, W)
+            for phase in (0, 1):
+                ops, recvs = [], []
+                for m in msgs:
+                    if m["phase"] != phase:
+                        continue
+                    send = buf[m["send_j0"] - e_j0:m["send_j1"] - e_j0, m["send_i0"] - e_i0:m["send_i1"] - e_i0].contiguous()
+                    recv = torch.empty((m["recv_j1"] - m["recv_j0"], m["recv_i1"] - m["recv_i0"]), dtype=torch.float64)
+                    ops.append(dist.P2POp(dist.isend, send, m["peer"]))
+                    ops.append(dist.P2POp(dist.irecv, recv, m["peer"]))
+                    recvs.append((m, recv))
+                if ops:
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                for m, recv in recvs:
+                    buf[m["recv_j0"] - e_j0:m["recv_j1"] - e_j0, m["recv_i0"] - e_i0:m["recv_i1"] - e_i0] = recv
+            # the (lo, hi) frame (incl. corners) must now hold the global values
+            for j in range(pl["owned_j0"] - (lo if pl["nbr"][2] >= 0 else 0), pl["owned_j1"] + (hi if pl["nbr"][3] >= 0 else 0)):
+                for i in range(pl["owned_i0"] - (lo if pl["nbr"][0] >= 0 else 0), pl["owned_i1"] + (hi if pl["nbr"][1] >= 0 else 0)):
+                    if buf[j - e_j0, i - e_i0].item() != gid(i, j):
+                        ok = False
+        result_q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_two_phase_exchange_over_gloo(nranks):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, nranks, port, 100.0, 4, q)) for r in range(nranks)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=240) for _ in range(nranks))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(res[r] for r in range(nranks)), res
