@@ -124,7 +124,13 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     nccl_id = None
     if world > 1:
-        raise SystemExit("multi-GPU bench requires the NCCL build of libhelm (not in this build)")
+        # libhelm owns its NCCL communicator; rank 0 makes the id, torch.distributed only broadcasts it
+        from paper_2602_00735_b200.helm import nccl_unique_id
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, src=0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
 
     t0 = time.time()
     ctx = Context(cfg.k, cfg.nsub, cfg.nsub, rank=rank, nranks=world, stream=stream, nccl_id=nccl_id)
@@ -204,7 +210,7 @@ def run_ours(args):
     achieved = lay["apply_bytes"] / (apply_avg_ms / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k_apply_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         with open(prof) as f:
             tj = json.load(f)
         traffic = tj.get(cfg.name, {}).get("dram_bytes_per_launch")

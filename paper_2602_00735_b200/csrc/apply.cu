@@ -101,16 +101,27 @@ __device__ __forceinline__ void prefetch(Pre& p, const SubDesc& d, Step st, int 
         const long long gi = d.gx0 + t - a.in_i0, gj = d.gy0 + st.i - a.in_j0;
         p.b = __ldg(a.in + gi + a.in_stride * gj);
     }
-    if (st.ph == PH_T || st.ph == PH_D) {
-        p.c0 = __ldg(row + SL_N * d.m + t);
-        p.c1 = __ldg(row + SL_NE * d.m + t);
-    } else {
-        p.c0 = __ldg(row + SL_S * d.m + t);
-        p.c1 = __ldg(row + SL_SW * d.m + t);
-    }
+    // nodes whose six triangles all have gamma = 1 carry the constant interior couplings: no load
+    const bool cst = t >= d.cx0 && t < d.cx1 && st.i >= d.cy0 && st.i < d.cy1;
+    // the first step of each chain has no coupling term
+    if ((st.ph == PH_T && st.i == d.nb - 1) || (st.ph == PH_B && st.i == 0)) return;
     if (st.ph == PH_Z) {
-        p.c2 = __ldg(row + SL_N * d.m + t);
-        p.c3 = __ldg(row + SL_NE * d.m + t);
+        if (st.i > 0) {
+            p.c0 = cst ? a.cS : __ldg(row + SL_S * d.m + t);
+            p.c1 = cst ? a.cSW : __ldg(row + SL_SW * d.m + t);
+        }
+        if (st.i < d.nb - 1) {
+            p.c2 = cst ? a.cN : __ldg(row + SL_N * d.m + t);
+            p.c3 = cst ? a.cNE : __ldg(row + SL_NE * d.m + t);
+        }
+        return;
+    }
+    if (st.ph == PH_T || st.ph == PH_D) {
+        p.c0 = cst ? a.cN : __ldg(row + SL_N * d.m + t);
+        p.c1 = cst ? a.cNE : __ldg(row + SL_NE * d.m + t);
+    } else {
+        p.c0 = cst ? a.cS : __ldg(row + SL_S * d.m + t);
+        p.c1 = cst ? a.cSW : __ldg(row + SL_SW * d.m + t);
     }
     if (st.ph >= PH_D) p.yz = scr[(long long)(st.i - d.lo) * d.m + t];
 }

@@ -219,16 +219,31 @@ struct helm_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
     int launches = 0;
 
-    StencilGeom owned_geom() const
+    // constant interior stencil (rows with gamma = 1 on all six triangles) and its node range
+    int cst[4] = {0, 0, 0, 0};
+    z2 c7[7] = {};
+    z2 lcS{}, lcSW{}, lcN{}, lcNE{};   // constant local couplings (apply)
+
+    StencilGeom geom_for(int xi0, int xj0, long long xstride) const
     {
-        StencilGeom s{G.i0, G.j0, G.i1 - G.i0, G.j1 - G.j0, G.nf, G.i0, G.j0, (long long)(G.i1 - G.i0)};
+        StencilGeom s{};
+        s.i0 = G.i0;
+        s.j0 = G.j0;
+        s.nx = G.i1 - G.i0;
+        s.ny = G.j1 - G.j0;
+        s.nf = G.nf;
+        s.xi0 = xi0;
+        s.xj0 = xj0;
+        s.xstride = xstride;
+        s.ci0 = cst[0];
+        s.ci1 = cst[1];
+        s.cj0 = cst[2];
+        s.cj1 = cst[3];
+        for (int q = 0; q < 7; q++) s.c7[q] = c7[q];
         return s;
     }
-    StencilGeom ext_geom() const
-    {
-        StencilGeom s{G.i0, G.j0, G.i1 - G.i0, G.j1 - G.j0, G.nf, G.e_i0, G.e_j0, ext_stride};
-        return s;
-    }
+    StencilGeom owned_geom() const { return geom_for(G.i0, G.j0, G.i1 - G.i0); }
+    StencilGeom ext_geom() const { return geom_for(G.e_i0, G.e_j0, ext_stride); }
 };
 
 static int set_err(helm_ctx* ctx, int code, const char* fmt, ...)
@@ -319,6 +334,22 @@ int build_layout(helm_ctx* ctx)
             d.jlo3 = 3 * int_lo[1];
             d.jhi3 = 3 * int_hi[1];
             d.flags = (has_lo[0] ? 1 : 0) | (has_hi[0] ? 2 : 0) | (has_lo[1] ? 4 : 0) | (has_hi[1] ? 8 : 0);
+            {
+                // constant-coupling node range: cells [max(a_j, n_g), min(b_j, N - n_g)) have local gamma = 1
+                // (inside the int box where g_j = g_i, and inside Omega_int where g_i = 0)
+                int c0[2], c1[2];
+                for (int ax = 0; ax < 2; ax++) {
+                    const int lo_cell = std::max(has_lo[ax] ? int_lo[ax] : 0, G.ng);
+                    const int hi_cell = std::min(has_hi[ax] ? int_hi[ax] : G.N, G.N - G.ng);
+                    // nodes with both adjacent cells inside, and all neighbours free in Omega_j
+                    c0[ax] = std::max(lo_cell + 1, full_lo[ax] + 2);
+                    c1[ax] = std::min(hi_cell, full_hi[ax] - 1);
+                }
+                d.cx0 = std::max(c0[0] - d.gx0, 0);
+                d.cx1 = std::max(std::min(c1[0] - d.gx0, d.m), d.cx0);
+                d.cy0 = std::max(c0[1] - d.gy0, 0);
+                d.cy1 = std::max(std::min(c1[1] - d.gy0, d.nb), d.cy0);
+            }
             d.fac_off = fac;
             d.stc_off = stc;
             if (d.m > M_LIMIT)
@@ -337,9 +368,22 @@ int build_layout(helm_ctx* ctx)
             // algorithmic bytes of one apply of this subdomain
             const long long nblocks = d.nb + d.hi - d.lo;
             const long long owned = (long long)(d.ohi - d.olo + 1) * (d.hi - d.lo + 1);
+            // coupling vectors loaded per block step (two; four at the twist), except at constant-stencil nodes;
+            // the first step of each chain reads none (T: i = nb-1, B: i = 0)
+            long long cpl = 0;
+            auto loaded = [&](int i) { return (long long)d.m - ((i >= d.cy0 && i < d.cy1) ? (d.cx1 - d.cx0) : 0); };
+            for (int i = 0; i < d.nb; i++) {
+                int uses = 0;
+                if (i > d.tw && i < d.nb - 1) uses += 2;        // T: U_i
+                if (i < d.tw && i > 0) uses += 2;               // B: L_i
+                if (i == d.tw) uses += (i > 0 ? 2 : 0) + (i < d.nb - 1 ? 2 : 0);   // Z: L and U
+                if (i < d.tw && i >= d.lo) uses += 2;           // D: U_i
+                if (i > d.tw && i <= d.hi) uses += 2;           // U: L_i
+                cpl += uses * loaded(i);
+            }
             ctx->apply_bytes += 16 * (nblocks * d.m * d.m       // explicit inverse blocks streamed
                                       + n                       // restriction gather
-                                      + 2LL * nblocks * d.m     // two coupling vectors per block step
+                                      + cpl                     // coupling vectors
                                       + 2LL * (d.hi - d.lo) * d.m   // y / z scratch written + read
                                       + owned);                 // owner write
             ctx->band_bytes += 16 * (n * (2LL * (d.m + 1) + 1) + n + owned);
@@ -466,6 +510,10 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     a.out_stride = ctx->G.i1 - ctx->G.i0;
     a.scratch = ctx->d_scratch;
     a.scratch_per_cta = ctx->scratch_per_cta;
+    a.cS = ctx->lcS;
+    a.cSW = ctx->lcSW;
+    a.cN = ctx->lcN;
+    a.cNE = ctx->lcNE;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof) {
         if (ctx->ev_free.size() < 2) {
@@ -619,11 +667,11 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             if ((rc = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc;
             its++;
             // CGS2: h1 = V^H w; w -= V h1; h2 = V^H w; w -= V h2; H(:,j) = h1 + h2; H(j+1,j) = ||w||
+            // (the first update and the second projection share one sweep over V: k_axpy_dot)
             launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
             launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h1, nullptr, nullptr, s);
             if ((rc = allreduce(ctx, (double*)ctx->d_h1, 2 * (size_t)(j + 1)))) return rc;
-            launch_multiaxpy(V, n, j + 1, ctx->d_h1, ctx->d_w, n, nullptr, ctx->nblk, s);
-            launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+            launch_axpy_dot(V, n, j + 1, ctx->d_h1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
             if (!ctx->multi) {
                 launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, ctx->d_Hcol, ctx->d_h1, s);
             } else {
@@ -633,7 +681,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
                 ctx->launches++;
             }
             launch_multiaxpy(V, n, j + 1, ctx->d_h2, ctx->d_w, n, ctx->d_dpart, ctx->nblk, s);
-            ctx->launches += 6;   // 2x multidot, 2x reduce, 2x multiaxpy
+            ctx->launches += 5;   // multidot, axpy_dot, 2x reduce, multiaxpy
             if ((rc = finish_norm(ctx, ctx->d_Hcol + j + 1))) return rc;
             launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
             ctx->launches++;
@@ -820,6 +868,36 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     launch_assemble_global(ctx->geom, ctx->d_A7, ctx->G.i0, ctx->G.i1, ctx->G.j0, ctx->G.j1, ctx->stream);
     launch_assemble_local(ctx->geom, ctx->d_desc, nsub, ctx->d_stc, (int)ctx->max_n, ctx->stream);
     CK(cudaGetLastError());
+    {
+        // constant interior stencil: nodes ng+1 .. N-ng-1 have gamma = 1 on all six triangles; copy the 7
+        // coefficients of one such owned row from A7 so the SpMV fast path is bitwise identical to A7
+        const GridInfo& G = ctx->G;
+        const int a = std::max(G.i0, G.ng + 1), b = std::min(G.i1, G.N - G.ng);
+        const int c = std::max(G.j0, G.ng + 1), d = std::min(G.j1, G.N - G.ng);
+        if (a < b && c < d) {
+            const long long r = (long long)(a - G.i0) + (long long)(G.i1 - G.i0) * (c - G.j0);
+            for (int q = 0; q < 7; q++)
+                CK(cudaMemcpyAsync(&ctx->c7[q], ctx->d_A7 + q * ctx->n_local + r, sizeof(z2), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            ctx->cst[0] = a;
+            ctx->cst[1] = b;
+            ctx->cst[2] = c;
+            ctx->cst[3] = d;
+        }
+        // the same for the local operators: couplings of one constant-range node of the first subdomain that
+        // has one (all such nodes are computed from gamma = 1 with exact arithmetic: identical bits)
+        for (const SubDesc& sd : ctx->subs) {
+            if (sd.cx0 >= sd.cx1 || sd.cy0 >= sd.cy1) continue;
+            const z2* row = ctx->d_stc + sd.stc_off + (long long)sd.cy0 * 7 * sd.m + sd.cx0;
+            z2* dst[4] = {&ctx->lcS, &ctx->lcSW, &ctx->lcN, &ctx->lcNE};
+            const int sl[4] = {SL_S, SL_SW, SL_N, SL_NE};
+            for (int q = 0; q < 4; q++)
+                CK(cudaMemcpyAsync(dst[q], row + sl[q] * sd.m, sizeof(z2), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            break;
+        }
+    }
     // apply launch configuration
     int nsm = 148;
     int dev = 0;
@@ -856,7 +934,9 @@ int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
     out->factor_bytes = ctx->n_dinv * 16;
     out->apply_bytes = ctx->apply_bytes;
     out->band_bytes = ctx->band_bytes + 16LL * ctx->n_local;
-    out->spmv_bytes = 16LL * 9 * ctx->n_local;
+    // SpMV: x read + y write per row; rows off the constant interior stencil also read 7 coefficients
+    const long long ncst = (long long)std::max(0, ctx->cst[1] - ctx->cst[0]) * std::max(0, ctx->cst[3] - ctx->cst[2]);
+    out->spmv_bytes = 16LL * 2 * ctx->n_local + 16LL * 7 * (ctx->n_local - ncst);
     return HELM_OK;
 }
 
@@ -920,7 +1000,7 @@ int helm_matvec_ext(helm_ctx* ctx, const helm_z* ext1_dev, helm_z* y_dev)
     if (!ctx || !ext1_dev || !y_dev) return set_err(ctx, HELM_EINVAL, "helm_matvec_ext: bad arguments");
     const GridInfo& G = ctx->G;
     const int li = G.nbr[0] >= 0, ri = G.nbr[1] >= 0, dj = G.nbr[2] >= 0;
-    StencilGeom sg{G.i0, G.j0, G.i1 - G.i0, G.j1 - G.j0, G.nf, G.i0 - li, G.j0 - dj, (long long)(G.i1 - G.i0 + li + ri)};
+    const StencilGeom sg = ctx->geom_for(G.i0 - li, G.j0 - dj, (long long)(G.i1 - G.i0 + li + ri));
     launch_spmv(ctx->d_A7, (const z2*)ext1_dev, (z2*)y_dev, sg, ctx->stream);
     ctx->launches++;
     CK(cudaGetLastError());

@@ -64,6 +64,8 @@ struct SubDesc {
     int ilo3, ihi3; // int box x-range in thirds (local ramps start there) ...
     int jlo3, jhi3; // ... and y-range
     int flags;      // bit0 x-lower PML, bit1 x-upper, bit2 y-lower, bit3 y-upper
+    int cx0, cx1;   // local columns [cx0, cx1) and rows [cy0, cy1) whose six triangles all have gamma = 1:
+    int cy0, cy1;   //   their couplings equal the constant interior stencil (apply skips those loads)
     int pad;
     long long fac_off;   // complex offset of block 0 of the explicit inverses (blocks m x m, column-major)
     long long stc_off;   // complex offset of the local stencil [nb][7][m]
@@ -101,15 +103,21 @@ struct ApplyArgs {
     long long out_stride;
     z2* scratch;            // per-CTA [max_rows][m_max]
     long long scratch_per_cta;
+    z2 cS, cSW, cN, cNE;    // couplings of the constant interior stencil
 };
 int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
 
-// owned rows [i0, i0+nx) x [j0, j0+ny) of the 7-point operator; x read from a buffer with origin (xi0, xj0)
+// owned rows [i0, i0+nx) x [j0, j0+ny) of the 7-point operator; x read from a buffer with origin (xi0, xj0).
+// Rows whose node lies in [ci0, ci1) x [cj0, cj1) -- all six triangles inside Omega_int, gamma = 1 --
+// share one stencil c7 (copied from an assembled interior row, so bitwise equal to A7 there) and skip the
+// seven coefficient loads.
 struct StencilGeom {
     int i0, j0, nx, ny, nf;
     int xi0, xj0;
     long long xstride;
+    int ci0, ci1, cj0, cj1;
+    z2 c7[7];
 };
 void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s);
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
@@ -120,6 +128,8 @@ void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t 
 void launch_finish_norm(const double* sq, z2* out_slot, double* out_norm, cudaStream_t s);
 void launch_zadd(const z2* a, const z2* b, z2* out, int nv, cudaStream_t s);
 void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long n, z2* partial, int nblk,
+                     cudaStream_t s);
+void launch_axpy_dot(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, z2* partial, int nblk,
                      cudaStream_t s);
 void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, double* partial_norm,
                       int nblk, cudaStream_t s);

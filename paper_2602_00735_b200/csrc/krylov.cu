@@ -53,8 +53,17 @@ __device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* _
                                           const StencilGeom& G)
 {
     const long long n = (long long)G.nx * G.ny;
-    const int i = G.i0 + (int)(r % G.nx), j = G.j0 + (int)(r / G.nx);
+    // rows of one rank fit in 32 bits (< 2^31 nodes): 32-bit division
+    const unsigned ru = (unsigned)r;
+    const int lj = (int)(ru / (unsigned)G.nx);
+    const int i = G.i0 + (int)(ru - (unsigned)lj * (unsigned)G.nx), j = G.j0 + lj;
     z2 acc = zmk(0, 0);
+    if (i >= G.ci0 && i < G.ci1 && j >= G.cj0 && j < G.cj1) {   // constant interior stencil (all neighbours free)
+        const z2* xc = x + (i - G.xi0) + G.xstride * (j - G.xj0);
+#pragma unroll
+        for (int s = 0; s < 7; s++) zfma(acc, G.c7[s], __ldg(xc + c_dx[s] + G.xstride * c_dy[s]));
+        return acc;
+    }
 #pragma unroll
     for (int s = 0; s < 7; s++) {
         const int qi = i + c_dx[s], qj = j + c_dy[s];
@@ -64,12 +73,16 @@ __device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* _
     return acc;
 }
 
+// 2-D launch: blockIdx.y strides over rows j, x-threads over i (no 64-bit division per row)
 __global__ void __launch_bounds__(KT) k_spmv(const z2* __restrict__ A7, const z2* __restrict__ x, z2* __restrict__ y,
                                              StencilGeom G)
 {
-    const long long n = (long long)G.nx * G.ny;
-    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= G.nx) return;
+    for (int lj = blockIdx.y; lj < G.ny; lj += gridDim.y) {
+        const long long r = li + (long long)G.nx * lj;
         y[r] = stencil_row(A7, x, r, G);
+    }
 }
 
 // r = b - A x, partial[blk] = ||r||^2 over the CTA's rows
@@ -147,6 +160,57 @@ __global__ void __launch_bounds__(KT) k_multidot(const z2* __restrict__ V, long 
             e[q] = base + q * KT + threadIdx.x;
             wv[q] = e[q] < r1 ? __ldg(w + e[q]) : zmk(0, 0);
         }
+        for (int v = 0; v < nv; v++) {
+            const z2* Vv = V + v * ldv;
+            z2 s = zmk(0, 0);
+#pragma unroll
+            for (int q = 0; q < R; q++)
+                if (e[q] < r1) zfma_conj(s, __ldg(Vv + e[q]), wv[q]);
+            s = warp_sum(s);
+            if (lane == 0) acc[warp][v] = zadd(acc[warp][v], s);
+        }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        z2 s = zmk(0, 0);
+        for (int q = 0; q < KT / 32; q++) s = zadd(s, acc[q][v]);
+        partial[(long long)blockIdx.x * NVMAX + v] = s;
+    }
+}
+
+// Fused second CGS pass: w -= sum_v h[v] V_v and partial[blk][v] = sum_e conj(V_v[e]) w_new[e] in one sweep
+// (V is read from HBM once; the second touch of each tile hits L1/L2).
+template <int R>
+__global__ void __launch_bounds__(KT) k_axpy_dot(const z2* __restrict__ V, long long ldv, int nv,
+                                                 const z2* __restrict__ h, z2* __restrict__ w, long long n,
+                                                 z2* __restrict__ partial)
+{
+    __shared__ z2 hs[NVMAX];
+    __shared__ z2 acc[KT / 32][NVMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) hs[v] = h[v];
+    for (int v = lane; v < NVMAX; v += 32) acc[warp][v] = zmk(0, 0);
+    __syncthreads();
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    for (long long base = r0; base < r1; base += (long long)KT * R) {
+        z2 wv[R];
+        long long e[R];
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+            e[q] = base + q * KT + threadIdx.x;
+            wv[q] = e[q] < r1 ? w[e[q]] : zmk(0, 0);
+        }
+        for (int v = 0; v < nv; v++) {
+            const z2 hv = zmk(-hs[v].x, -hs[v].y);
+            const z2* Vv = V + v * ldv;
+#pragma unroll
+            for (int q = 0; q < R; q++)
+                if (e[q] < r1) zfma(wv[q], hv, __ldg(Vv + e[q]));
+        }
+#pragma unroll
+        for (int q = 0; q < R; q++)
+            if (e[q] < r1) w[e[q]] = wv[q];
         for (int v = 0; v < nv; v++) {
             const z2* Vv = V + v * ldv;
             z2 s = zmk(0, 0);
@@ -279,7 +343,9 @@ int ew_grid(long long n)
 
 void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s)
 {
-    k_spmv<<<ew_grid((long long)G.nx * G.ny), KT, 0, s>>>(A7, x, y, G);
+    const int gx = (G.nx + KT - 1) / KT;
+    const int gy = G.ny < 65535 ? G.ny : 65535;
+    k_spmv<<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
 }
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s)
@@ -306,6 +372,11 @@ void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long 
                      cudaStream_t s)
 {
     k_multidot<4><<<nblk, KT, 0, s>>>(V, ldv, nv, w, n, partial);
+}
+void launch_axpy_dot(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, z2* partial, int nblk,
+                     cudaStream_t s)
+{
+    k_axpy_dot<4><<<nblk, KT, 0, s>>>(V, ldv, nv, h, w, n, partial);
 }
 void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, double* partial_norm,
                       int nblk, cudaStream_t s)
