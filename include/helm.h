@@ -32,6 +32,7 @@ enum {
     HELM_OK = 0,
     HELM_NOT_CONVERGED = 2,   /* maxit reached; x holds the last iterate */
     HELM_BREAKDOWN = 3,       /* NaN / Inf in the Arnoldi process */
+    HELM_DIVERGED = 4,        /* Richardson: relative residual above 1e6 or not finite */
     HELM_EINVAL = -1,         /* bad argument or unsupported parameter combination */
     HELM_ENOMEM = -2,         /* device allocation failed */
     HELM_ECUDA = -3,          /* CUDA runtime error */
@@ -125,6 +126,19 @@ int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, d
 /* Same with host b / x (copied in and out inside the call). */
 int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int restart, double rtol, int maxit,
                     helm_gmres_info* info);
+
+/* Algorithm 1 RAS_IterSolve in discrete form: u <- u + B^-1 (b - A u) from the
+ * initial guess in x_dev until ||b - A u|| <= rtol ||b|| (HELM_OK), maxit steps (HELM_NOT_CONVERGED), or the
+ * relative residual exceeds 1e6 / is not finite (HELM_DIVERGED).  One apply, one SpMV per step; synchronous. */
+typedef struct {
+    int iterations;
+    int status;
+    double relres;       /* final ||b - A u|| / ||b|| */
+    double* history;     /* caller-owned host buffer for the relative residual after each step, or NULL */
+    int history_cap;
+} helm_richardson_info;
+int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rtol, int maxit,
+                    helm_richardson_info* info);
 
 /* Parity export: the global operator as 7 slot arrays [7][n_local] (slot order centre, E, W, N, S, NE, SW;
  * a slot pointing at a Dirichlet node is 0).  out_dev: 7 * n_local values. */

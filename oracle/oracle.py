@@ -278,6 +278,42 @@ class Oracle:
 
 
 # ------------------------------------------------------------------------------------------------
+# Algorithm 1 RAS_IterSolve in its discrete form (eq. local-ras-discrete + eq. update1,
+# P:130-142): u^{n+1} = u^n + sum_j R~_j^T A_j^{-1} R_j (f - A u^n) = u^n + B^{-1}(f - A u^n).
+# Stops when ||f - A u|| <= rtol ||f||, at maxit, or flags divergence when the relative residual exceeds
+# 1e6 or is not finite.
+# ------------------------------------------------------------------------------------------------
+@dataclass
+class RichardsonResult:
+    x: np.ndarray
+    iterations: int
+    status: int          # 0 converged, 2 maxit, 3 diverged
+    relres: float
+    history: list
+
+
+def richardson(A, M, b: np.ndarray, rtol: float = 1e-6, maxit: int = 500, x0: np.ndarray | None = None,
+               diverge: float = 1e6) -> RichardsonResult:
+    b = np.asarray(b, np.complex128)
+    x = np.zeros_like(b) if x0 is None else np.array(x0, np.complex128)
+    beta0 = np.linalg.norm(b)
+    if beta0 == 0.0:
+        return RichardsonResult(np.zeros_like(b), 0, 0, 0.0, [])
+    r = b - A(x)
+    rel = np.linalg.norm(r) / beta0
+    its, hist = 0, []
+    while rel > rtol and its < maxit:
+        x = x + M(r)                       # u^{n+1} = u^n + sum_j chi_j c_j
+        its += 1
+        r = b - A(x)
+        rel = np.linalg.norm(r) / beta0
+        hist.append(rel)
+        if not np.isfinite(rel) or rel > diverge:
+            return RichardsonResult(x, its, 3, rel, hist)
+    return RichardsonResult(x, its, 0 if rel <= rtol else 2, rel, hist)
+
+
+# ------------------------------------------------------------------------------------------------
 # O9: right-preconditioned restarted GMRES(m), modified Gram-Schmidt, Hermitian inner products
 # ("Algorithm 1 as a preconditioner for GMRES"; D13).
 # ------------------------------------------------------------------------------------------------

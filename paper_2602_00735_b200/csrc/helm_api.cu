@@ -758,9 +758,62 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
     }
 }
 
+// Algorithm 1: u <- u + B^-1 (b - A u)
+int richardson_impl(helm_ctx* ctx, const z2* b, z2* x, double rtol, int maxit, helm_richardson_info* info)
+{
+    if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "richardson before helm_factor");
+    if (maxit < 0) return set_err(ctx, HELM_EINVAL, "maxit >= 0");
+    int rc;
+    if ((rc = need_comm(ctx))) return rc;
+    if ((rc = ensure_krylov(ctx, 1))) return rc;
+    helm_richardson_info loc{};
+    helm_richardson_info* inf = info ? info : &loc;
+    inf->iterations = 0;
+    inf->status = HELM_OK;
+    inf->relres = 0.0;
+    double beta0;
+    if ((rc = norm_host(ctx, b, &beta0))) return rc;
+    if (beta0 == 0.0) {
+        CK(cudaMemsetAsync(x, 0, sizeof(z2) * ctx->n_local, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return HELM_OK;
+    }
+    double rn;
+    if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
+    double rel = rn / beta0;
+    int its = 0;
+    while (rel > rtol && its < maxit) {
+        if ((rc = apply_impl(ctx, ctx->d_r, ctx->d_z))) return rc;   // sum_j chi_j c_j
+        launch_axpy(x, ctx->d_z, ctx->n_local, ctx->stream);
+        ctx->launches++;
+        its++;
+        if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
+        rel = rn / beta0;
+        if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = rel;
+        if (!std::isfinite(rel) || rel > 1e6) {
+            inf->iterations = its;
+            inf->relres = rel;
+            inf->status = HELM_DIVERGED;
+            return HELM_DIVERGED;
+        }
+    }
+    inf->iterations = its;
+    inf->relres = rel;
+    inf->status = rel <= rtol ? HELM_OK : HELM_NOT_CONVERGED;
+    return inf->status;
+}
+
 }  // namespace
 
 // ===================================================================================================== C ABI
+
+int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rtol, int maxit,
+                    helm_richardson_info* info)
+{
+    if (!ctx || !b_dev || !x_dev || (const void*)b_dev == (void*)x_dev)
+        return set_err(ctx, HELM_EINVAL, "helm_richardson: bad arguments");
+    return richardson_impl(ctx, (const z2*)b_dev, (z2*)x_dev, rtol, maxit, info);
+}
 extern "C" {
 
 int helm_plan_rank(const helm_params* params, int rank, int nranks, helm_plan* out)

@@ -47,6 +47,11 @@ class GmresInfo(C.Structure):
                 ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
 
 
+class RichardsonInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("status", C.c_int), ("relres", C.c_double),
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
+
+
 class Plan(C.Structure):
     _fields_ = [("gx", C.c_int), ("gy", C.c_int), ("rx", C.c_int), ("ry", C.c_int),
                 ("owned_i0", C.c_int), ("owned_i1", C.c_int), ("owned_j0", C.c_int), ("owned_j1", C.c_int),
@@ -72,7 +77,7 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_precond_apply_host", "helm_gmres", "helm_gmres_host", "helm_export_stencil",
            "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy",
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
-           "helm_matvec_ext"]
+           "helm_matvec_ext", "helm_richardson"]
 
 
 def lib_path() -> str:
@@ -107,6 +112,7 @@ def load(build_if_missing: bool = True):
     L.helm_nccl_unique_id.argtypes = [vp]
     L.helm_precond_apply_ext.argtypes = [vp, vp, vp]
     L.helm_matvec_ext.argtypes = [vp, vp, vp]
+    L.helm_richardson.argtypes = [vp, vp, vp, d, i, C.POINTER(RichardsonInfo)]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
     L.helm_destroy.argtypes = [vp]
@@ -264,6 +270,22 @@ class Context:
             info.history_cap = maxit
         rc = self.L.helm_gmres(self._h, _ptr(b), _ptr(x), restart, float(rtol), maxit, C.byref(info))
         self._check(rc, ok=(0, 2))
+        return x, info, (hist[:info.iterations].copy() if hist is not None else None)
+
+    def richardson(self, b, x=None, rtol: float = 1e-6, maxit: int = 500, history: bool = False):
+        """Algorithm 1 (RAS_IterSolve) on the device; returns (x, info, history or None)."""
+        import numpy as np
+        if x is None:
+            x = self.empty()
+            x.zero_()
+        info = RichardsonInfo()
+        hist = None
+        if history:
+            hist = np.zeros(max(maxit, 1), np.float64)
+            info.history = hist.ctypes.data_as(C.POINTER(C.c_double))
+            info.history_cap = maxit
+        rc = self.L.helm_richardson(self._h, _ptr(b), _ptr(x), float(rtol), maxit, C.byref(info))
+        self._check(rc, ok=(0, 2, 4))
         return x, info, (hist[:info.iterations].copy() if hist is not None else None)
 
     def gmres_host(self, b_host, x_host, restart: int = 50, rtol: float = 1e-6, maxit: int = 5000):

@@ -1,0 +1,76 @@
+"""GPU parity for Algorithm 1 (RAS_IterSolve) against the oracle: iteration count +-1, final
+solution <= 1e-6, residual history; the single-subdomain case; the interface-band residual structure of the
+paper's improvement (i) reproduced by the GPU iterates.  -m gpu."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, richardson
+from paper_2602_00735_b200.workloads import CONFIGS, sources
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a B200", allow_module_level=True)
+
+from paper_2602_00735_b200 import Context  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+def test_richardson_parity(name):
+    cfg = CONFIGS[name]
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub)
+    ctx.factor()
+    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    o.factor()
+    xy, amp, sig = sources(cfg)
+    b = o.rhs(xy, amp, sig)
+    ref = richardson(o.matvec, o.apply, b, rtol=cfg.rtol, maxit=500)
+    x, info, hist = ctx.richardson(torch.from_numpy(b).cuda(), rtol=cfg.rtol, maxit=500, history=True)
+    assert info.status == 0 and ref.status == 0
+    assert abs(info.iterations - ref.iterations) <= 1
+    assert rel(x.cpu().numpy(), ref.x) <= 1e-6
+    n = min(len(hist), len(ref.history))
+    assert np.allclose(hist[:n], ref.history[:n], rtol=1e-6, atol=0)
+    ctx.close()
+
+
+def test_richardson_single_subdomain_one_step():
+    cfg = CONFIGS["c0"]
+    ctx = Context(cfg.k, 1, 1)
+    ctx.factor()
+    o = Oracle.from_config(k=cfg.k, nsub_x=1, nsub_y=1)
+    xy, amp, sig = sources(cfg)
+    b = torch.from_numpy(o.rhs(xy, amp, sig)).cuda()
+    x, info, _ = ctx.richardson(b, rtol=1e-10)
+    assert info.iterations == 1 and info.relres < 1e-12
+
+
+def test_gpu_iterates_keep_residual_on_interfaces():
+    cfg = CONFIGS["c1"]
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub)
+    ctx.factor()
+    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    xy, amp, sig = sources(cfg)
+    b = o.rhs(xy, amp, sig)
+    bd = torch.from_numpy(b).cuda()
+    x, info, _ = ctx.richardson(bd, rtol=0.0, maxit=2)
+    r = (bd - ctx.matvec(x)).cpu().numpy()
+    nfx, nfy = o.nf
+    owner = np.full((nfy + 2, nfx + 2), -1)
+    for j in range(o.nsub):
+        s = o.subdomain(j)
+        owner[s["own_lo"][1]:s["own_hi"][1], s["own_lo"][0]:s["own_hi"][0]] = j
+    O = owner[1:nfy + 1, 1:nfx + 1]
+    band = np.zeros_like(O, bool)
+    P = np.pad(O, 1, constant_values=-2)
+    for dx, dy in [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1)]:
+        Q = P[1 + dy:1 + dy + nfy, 1 + dx:1 + dx + nfx]
+        band |= (Q != O) & (Q != -2)
+    band = band.ravel()
+    assert np.max(np.abs(r[~band])) <= 1e-12 * np.linalg.norm(b)
+    assert np.max(np.abs(r[band])) > 1e-6 * np.linalg.norm(b)
