@@ -42,7 +42,10 @@ enum {
     HELM_ESTATE = -7          /* apply / gmres before helm_factor */
 };
 
-enum { HELM_BC_DIRICHLET = 0 /* RAS-PML-Drch: u = 0 on dOmega_j, P:131-137, P:152 (D9) */ };
+enum {
+    HELM_BC_DIRICHLET = 0,   /* RAS-PML-Drch: u = 0 on dOmega_j, P:131-137, P:152 (D9); the hot path */
+    HELM_BC_IMPEDANCE = 1    /* RAS-PML-Imp: d_nu u - i k u = 0 on the faces of Omega_j not on dOmega */
+};
 
 /* Problem and decomposition (P:36-62 problem, P:71-92 covering; BASELINE.json configs). */
 typedef struct {
@@ -52,7 +55,7 @@ typedef struct {
     double sigma0;       /* profile g(t) = sigma0 t^3 / (3 kappa_g^2), linear beyond kappa_g */
     int nsub_x, nsub_y;  /* Cartesian subdomain grid */
     int n_ovlp, n_pml;   /* overlap delta / local PML kappa in cells per interior face; < 0 => max(2, round(1.59 ln k)) */
-    int local_bc;        /* HELM_BC_DIRICHLET */
+    int local_bc;        /* HELM_BC_DIRICHLET or HELM_BC_IMPEDANCE */
     int gpu_grid_x, gpu_grid_y;   /* rank grid over the subdomain grid; product == nranks (0,0 => 1 x nranks) */
 } helm_params;
 

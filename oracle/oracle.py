@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
 class _Params(C.Structure):
     _fields_ = [("k", C.c_double), ("sigma0", C.c_double), ("h", C.c_double),
                 ("nix", C.c_int), ("niy", C.c_int), ("ng", C.c_int), ("kappa", C.c_double),
-                ("px", C.c_int), ("py", C.c_int), ("novlp", C.c_int), ("npml", C.c_int)]
+                ("px", C.c_int), ("py", C.c_int), ("novlp", C.c_int), ("npml", C.c_int), ("local_bc", C.c_int)]
 
 
 _lib = None
@@ -119,17 +119,18 @@ class Problem:
     py: int
     novlp: int
     npml: int
+    local_bc: int = 0    # 0 RAS-PML-Drch, 1 RAS-PML-Imp
 
 
 def problem_from_config(k, ppw=10, n_pml_global=10, sigma0=5.0, nsub_x=1, nsub_y=1,
-                        n_ovlp=-1, n_pml=-1) -> Problem:
+                        n_ovlp=-1, n_pml=-1, local_bc=0) -> Problem:
     n_int = n_int_from(k, ppw)
     h = 1.0 / n_int
     w = width_from(k)
     return Problem(k=float(k), sigma0=float(sigma0), h=h, nix=n_int, niy=n_int, ng=n_pml_global,
                    kappa=n_pml_global * h,  # D3: kappa_g = 1 wavelength ~ 10 cells at 10 ppw
                    px=nsub_x, py=nsub_y,
-                   novlp=w if n_ovlp < 0 else n_ovlp, npml=w if n_pml < 0 else n_pml)
+                   novlp=w if n_ovlp < 0 else n_ovlp, npml=w if n_pml < 0 else n_pml, local_bc=local_bc)
 
 
 class OracleError(RuntimeError):
@@ -140,7 +141,7 @@ class Oracle:
     def __init__(self, prob: Problem):
         self.prob = prob
         p = _Params(prob.k, prob.sigma0, prob.h, prob.nix, prob.niy, prob.ng, prob.kappa,
-                    prob.px, prob.py, prob.novlp, prob.npml)
+                    prob.px, prob.py, prob.novlp, prob.npml, prob.local_bc)
         err = C.create_string_buffer(256)
         self._h = lib().orc_create(C.byref(p), err, 256)
         if not self._h:
@@ -165,10 +166,10 @@ class Oracle:
 
     # -- layout ---------------------------------------------------------------------------------
     def subdomain(self, j: int) -> dict:
-        o = (C.c_int * 18)()
+        o = (C.c_int * 20)()
         lib().orc_subdomain(self._h, j, o)
-        keys = ["own_lo", "own_hi", "int_lo", "int_hi", "full_lo", "full_hi", "has_lo", "has_hi", "m"]
-        return {k: (o[i], o[9 + i]) for i, k in enumerate(keys)}
+        keys = ["own_lo", "own_hi", "int_lo", "int_hi", "full_lo", "full_hi", "has_lo", "has_hi", "m", "node0"]
+        return {k: (o[i], o[10 + i]) for i, k in enumerate(keys)}
 
     # -- PML ------------------------------------------------------------------------------------
     def gamma(self, axis: int, X3: int, sub: int = -1):

@@ -43,6 +43,7 @@ typedef struct {
     int px, py;     /* subdomains per axis (Cartesian covering) */
     int novlp;      /* overlap delta in cells, per side of every interior face (D8) */
     int npml;       /* local PML kappa in cells on every interior face */
+    int local_bc;   /* 0: RAS-PML-Drch (u = 0 on dOmega_j); 1: RAS-PML-Imp */
 } orc_params;
 
 typedef struct {
@@ -51,7 +52,8 @@ typedef struct {
     int int_lo[2], int_hi[2];   /* int box nodes a_j, b_j */
     int full_lo[2], full_hi[2]; /* full box nodes */
     int has_lo[2], has_hi[2];   /* local PML on lower / upper face (kappa_{j,l/u} != 0) */
-    int m[2];                   /* local free nodes per axis = full_hi - full_lo - 1 */
+    int m[2];                   /* local free nodes per axis */
+    int node0[2];               /* global index of the first local free node per axis */
     /* factor storage (band LU, O7) */
     zc *band;                   /* n x (2p+1), NULL until factored */
     int factored;
@@ -226,7 +228,12 @@ orc_ctx *orc_create(const orc_params *p, char *err, int errlen)
                 s->int_hi[ax] = s->own_hi[ax] + (s->has_hi[ax] ? p->novlp : 0);
                 s->full_lo[ax] = s->int_lo[ax] - (s->has_lo[ax] ? p->npml : 0);
                 s->full_hi[ax] = s->int_hi[ax] + (s->has_hi[ax] ? p->npml : 0);
-                s->m[ax] = s->full_hi[ax] - s->full_lo[ax] - 1;
+                /* local free nodes: strictly inside the full box (Dirichlet on dOmega_j), plus the
+                   nodes on faces that carry the impedance condition (RAS-PML-Imp) */
+                int imp = p->local_bc == 1;
+                s->node0[ax] = s->full_lo[ax] + ((imp && s->has_lo[ax]) ? 0 : 1);
+                int last = s->full_hi[ax] - ((imp && s->has_hi[ax]) ? 0 : 1);
+                s->m[ax] = last - s->node0[ax] + 1;
                 if (s->full_lo[ax] < 0 || s->full_hi[ax] > c->N[ax]) {
                     snprintf(err, errlen, "full box of subdomain (%d,%d) leaves Omega", jx, jy);
                     free(c->sub); free(c->split[0]); free(c->split[1]); free(c); return NULL;
@@ -254,15 +261,15 @@ void orc_dims(const orc_ctx *c, int *out)
     out[4] = c->nsub; out[5] = c->p.px; out[6] = c->p.py;
 }
 
-/* subdomain j: own_lo/hi, int_lo/hi, full_lo/hi, has_lo/hi, m  per axis -> 18 ints (x then y) */
+/* subdomain j: own_lo/hi, int_lo/hi, full_lo/hi, has_lo/hi, m, node0 per axis -> 20 ints (x then y) */
 void orc_subdomain(const orc_ctx *c, int j, int *out)
 {
     const orc_sub *s = &c->sub[j];
     for (int ax = 0; ax < 2; ax++) {
-        int *o = out + 9 * ax;
+        int *o = out + 10 * ax;
         o[0] = s->own_lo[ax]; o[1] = s->own_hi[ax]; o[2] = s->int_lo[ax]; o[3] = s->int_hi[ax];
         o[4] = s->full_lo[ax]; o[5] = s->full_hi[ax]; o[6] = s->has_lo[ax]; o[7] = s->has_hi[ax];
-        o[8] = s->m[ax];
+        o[8] = s->m[ax]; o[9] = s->node0[ax];
     }
 }
 
@@ -383,9 +390,22 @@ void orc_rhs(orc_ctx *c, int nsrc, const double *xy, const zc *amp, double sigma
 /* ------------------------------------------------------------------------------------------------
  * Local operator A_j (a_j = a restricted to H^1_0(Omega_j) with the local scaling g_j),
  * assembled element by element over the cells of the full box into band storage.
- * Local free node (lx,ly), 1 <= lx <= mx, 1 <= ly <= my, is global node (full_lo + lx, ...) and has
- * local index (lx-1) + mx (ly-1); half-bandwidth p = mx + 1 (D1).  band[r*(2p+1) + (col - r + p)].
+ * The local free nodes are the global nodes node0 .. node0 + m - 1 per axis (node0 = full_lo + 1 for a
+ * Dirichlet face; = full_lo when the face carries the impedance condition of P:185-195); global node
+ * (gi, gj) has local index (gi - node0x) + mx (gj - node0y); half-bandwidth p = mx + 1 (D1).
+ * band[r*(2p+1) + (col - r + p)].
+ * RAS-PML-Imp (eq. impedance): on every face of Omega_j that is not on dOmega the condition
+ * d_nu u - i k u = 0 is imposed as a natural boundary condition, i.e. a_j gains -i k int_face u v; with P1
+ * on an edge of length h: -i k (h/6) [[2,1],[1,2]] (no PML metric).
  * ----------------------------------------------------------------------------------------------*/
+static int local_index(const orc_sub *s, int gi, int gj, int64_t *idx)
+{
+    int lx = gi - s->node0[0], ly = gj - s->node0[1];
+    if (lx < 0 || lx >= s->m[0] || ly < 0 || ly >= s->m[1]) return 0;
+    *idx = lx + (int64_t)s->m[0] * ly;
+    return 1;
+}
+
 static void assemble_local(const orc_ctx *c, int j, zc *band)
 {
     const orc_sub *s = &c->sub[j];
@@ -400,17 +420,36 @@ static void assemble_local(const orc_ctx *c, int j, zc *band)
                 gamma_local(c, s, 1, 3L * cj + TRI_C3[tri][1], &gy, &dgy);
                 element_matrix(&c->p, gx, dgx, gy, dgy, tri, Ae);
                 for (int a = 0; a < 3; a++) {
-                    int lx = ci + TRI_V[tri][a][0] - s->full_lo[0], ly = cj + TRI_V[tri][a][1] - s->full_lo[1];
-                    if (lx < 1 || lx > mx || ly < 1 || ly > my) continue;
-                    int64_t r = (lx - 1) + (int64_t)mx * (ly - 1);
+                    int64_t r, col;
+                    if (!local_index(s, ci + TRI_V[tri][a][0], cj + TRI_V[tri][a][1], &r)) continue;
                     for (int q = 0; q < 3; q++) {
-                        int qx = ci + TRI_V[tri][q][0] - s->full_lo[0], qy = cj + TRI_V[tri][q][1] - s->full_lo[1];
-                        if (qx < 1 || qx > mx || qy < 1 || qy > my) continue;
-                        int64_t col = (qx - 1) + (int64_t)mx * (qy - 1);
+                        if (!local_index(s, ci + TRI_V[tri][q][0], cj + TRI_V[tri][q][1], &col)) continue;
                         band[r * bw + (col - r + p)] += Ae[a][q];
                     }
                 }
             }
+    if (c->p.local_bc != 1) return;
+    /* impedance faces: x = full_lo / full_hi (edges along y) and y = full_lo / full_hi (edges along x) */
+    for (int ax = 0; ax < 2; ax++)
+        for (int side = 0; side < 2; side++) {
+            if (!(side ? s->has_hi[ax] : s->has_lo[ax])) continue;
+            int f = side ? s->full_hi[ax] : s->full_lo[ax];
+            int o = 1 - ax;
+            for (int e = s->full_lo[o]; e < s->full_hi[o]; e++) {   /* edge between nodes e and e+1 */
+                int pts[2][2];
+                for (int q = 0; q < 2; q++) {
+                    pts[q][ax] = f;
+                    pts[q][o] = e + q;
+                }
+                for (int a = 0; a < 2; a++)
+                    for (int q = 0; q < 2; q++) {
+                        int64_t r, col;
+                        if (!local_index(s, pts[a][0], pts[a][1], &r)) continue;
+                        if (!local_index(s, pts[q][0], pts[q][1], &col)) continue;
+                        band[r * bw + (col - r + p)] += -I * c->p.k * (c->p.h / 6.0) * (a == q ? 2.0 : 1.0);
+                    }
+            }
+        }
 }
 
 /* export the local band (n x (2p+1)) for pins; returns n */
@@ -518,17 +557,18 @@ int orc_apply(orc_ctx *c, const zc *v, zc *z, const int *list, int nlist)
         int mx = s->m[0], my = s->m[1];
         int64_t n = (int64_t)mx * my;
         zc *x = malloc(sizeof(zc) * (size_t)n);
-        for (int ly = 1; ly <= my; ly++)
-            for (int lx = 1; lx <= mx; lx++) {
-                int gi = s->full_lo[0] + lx, gj = s->full_lo[1] + ly;
-                x[(lx - 1) + (int64_t)mx * (ly - 1)] = v[(gi - 1) + (int64_t)nfx * (gj - 1)];
+        for (int ly = 0; ly < my; ly++)
+            for (int lx = 0; lx < mx; lx++) {
+                int gi = s->node0[0] + lx, gj = s->node0[1] + ly;
+                x[lx + (int64_t)mx * ly] = v[(gi - 1) + (int64_t)nfx * (gj - 1)];
             }
         orc_band_solve(n, mx + 1, s->band, x);
         for (int gj = s->own_lo[1]; gj < s->own_hi[1]; gj++)
             for (int gi = s->own_lo[0]; gi < s->own_hi[0]; gi++) {
                 if (gi < 1 || gi > c->nf[0] || gj < 1 || gj > c->nf[1]) continue; /* Dirichlet node */
-                int lx = gi - s->full_lo[0], ly = gj - s->full_lo[1];
-                z[(gi - 1) + (int64_t)nfx * (gj - 1)] = x[(lx - 1) + (int64_t)mx * (ly - 1)];
+                int64_t r;
+                local_index(s, gi, gj, &r);
+                z[(gi - 1) + (int64_t)nfx * (gj - 1)] = x[r];
             }
         free(x);
     }

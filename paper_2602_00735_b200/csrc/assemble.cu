@@ -66,8 +66,10 @@ __device__ __forceinline__ int slot_of(int dx, int dy)
 
 // Row of node (i, j) (global node indices): A[p][q] = 1/2 (D11 gx_p gx_q + D22 gy_p gy_q)
 //   - h/6 (beta1 gx_q + beta2 gy_q) - k^2 h^2 / 24 (1 + delta_pq), with g = h grad phi.
+// Only triangles of cells in [cx0, cx1) x [cy0, cy1) contribute (the domain of the form: Omega, or the full
+// box of a subdomain -- relevant for nodes on an impedance face).
 template <class GammaFn>
-__device__ void node_row(int i, int j, const Geom& g, GammaFn gam_at, z2 row[7])
+__device__ void node_row(int i, int j, const Geom& g, GammaFn gam_at, z2 row[7], int cx0, int cx1, int cy0, int cy1)
 {
     for (int s = 0; s < 7; s++) row[s] = zmk(0.0, 0.0);
     const double kh2_24 = g.k * g.k * g.h * g.h / 24.0;
@@ -76,6 +78,7 @@ __device__ void node_row(int i, int j, const Geom& g, GammaFn gam_at, z2 row[7])
     for (int e = 0; e < 6; e++) {
         const TriRef T = c_tris[e];
         const int ci = i + T.cdx, cj = j + T.cdy, tri = T.tri, a = T.a;
+        if (ci < cx0 || ci >= cx1 || cj < cy0 || cj >= cy1) continue;
         z2 gx, dgx, gy, dgy;
         gam_at(0, 3L * ci + c_c3[tri][0], gx, dgx);
         gam_at(1, 3L * cj + c_c3[tri][1], gy, dgy);
@@ -104,7 +107,7 @@ __global__ void k_assemble_global(Geom g, z2* __restrict__ A7, int i0, int i1, i
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
         const int i = i0 + (int)(r % w), j = j0 + (int)(r / w);
         z2 row[7];
-        node_row(i, j, g, [&](int, long X3, z2& ga, z2& dga) { gamma_global(X3, g, ga, dga); }, row);
+        node_row(i, j, g, [&](int, long X3, z2& ga, z2& dga) { gamma_global(X3, g, ga, dga); }, row, 0, g.N, 0, g.N);
 #pragma unroll
         for (int s = 0; s < 7; s++) {
             const int qi = i + c_sdx[s], qj = j + c_sdy[s];
@@ -127,7 +130,24 @@ __global__ void k_assemble_local(Geom g, const SubDesc* __restrict__ desc, z2* _
                      if (axis == 0) gamma_local(X3, d.ilo3, d.ihi3, d.flags & 1, d.flags & 2, g, ga, dga);
                      else gamma_local(X3, d.jlo3, d.jhi3, d.flags & 4, d.flags & 8, g, ga, dga);
                  },
-                 rowv);
+                 rowv, d.fx0, d.fx1, d.fy0, d.fy1);
+        if (d.imp) {
+            // RAS-PML-Imp: -i k int_face u v on faces of Omega_j not on dOmega; P1 edge mass
+            // (h/6)[[2,1],[1,2]] per edge of length h (no PML metric)
+            const double w1 = g.k * g.h / 6.0;   // -i k h/6 = (0, -w1)
+            auto edge = [&](int slot) {
+                rowv[SL_C].y -= 2.0 * w1;
+                rowv[slot].y -= w1;
+            };
+            if (((d.imp & 1) && i == d.fx0) || ((d.imp & 2) && i == d.fx1)) {   // face x = const: edges along y
+                if (j - 1 >= d.fy0) edge(SL_S);
+                if (j + 1 <= d.fy1) edge(SL_N);
+            }
+            if (((d.imp & 4) && j == d.fy0) || ((d.imp & 8) && j == d.fy1)) {   // face y = const: edges along x
+                if (i - 1 >= d.fx0) edge(SL_W);
+                if (i + 1 <= d.fx1) edge(SL_E);
+            }
+        }
         z2* out = stc + d.stc_off + (long long)row_i * 7 * d.m + t;
 #pragma unroll
         for (int s = 0; s < 7; s++) {

@@ -55,8 +55,8 @@ int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* 
         snprintf(err, errlen, "invalid parameters (k, ppw, n_pml_global, nsub, sigma0)");
         return HELM_EINVAL;
     }
-    if (p.local_bc != HELM_BC_DIRICHLET) {
-        snprintf(err, errlen, "only HELM_BC_DIRICHLET (RAS-PML-Drch) is implemented");
+    if (p.local_bc != HELM_BC_DIRICHLET && p.local_bc != HELM_BC_IMPEDANCE) {
+        snprintf(err, errlen, "local_bc must be HELM_BC_DIRICHLET or HELM_BC_IMPEDANCE");
         return HELM_EINVAL;
     }
     if (nranks < 1 || rank < 0 || rank >= nranks) {
@@ -120,8 +120,10 @@ int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* 
     G.j1 = std::min(G.st[1][G.by1], G.N);
     // the full box of a block's subdomain spans nodes s_p - w + 1 .. s_{p+1} + w - 1 while the block owns
     // s_p .. s_{p+1} - 1 (half-open ownership, D10): w - 1 ghost nodes below, w above
-    G.halo_lo = w - 1;
-    G.halo_hi = w;
+    // (with the impedance variant the face nodes themselves are unknowns: one more on each side)
+    const int imp = p.local_bc == HELM_BC_IMPEDANCE;
+    G.halo_lo = w - 1 + imp;
+    G.halo_hi = w + imp;
     G.nbr[0] = G.rx > 0 ? rank - 1 : -1;
     G.nbr[1] = G.rx < gx - 1 ? rank + 1 : -1;
     G.nbr[2] = G.ry > 0 ? rank - gx : -1;
@@ -320,10 +322,23 @@ int build_layout(helm_ctx* ctx)
                     return set_err(ctx, HELM_ELAYOUT, "full box of subdomain (%d,%d) leaves Omega", bx, by);
             }
             SubDesc d{};
-            d.m = full_hi[0] - full_lo[0] - 1;
-            d.nb = full_hi[1] - full_lo[1] - 1;
-            d.gx0 = full_lo[0] + 1;
-            d.gy0 = full_lo[1] + 1;
+            // local unknowns: nodes strictly inside the full box (Dirichlet on dOmega_j) plus, for
+            // RAS-PML-Imp, the nodes on faces carrying the impedance condition
+            const int imp = ctx->p.local_bc == HELM_BC_IMPEDANCE;
+            int node0[2], node1[2];
+            for (int ax = 0; ax < 2; ax++) {
+                node0[ax] = full_lo[ax] + ((imp && has_lo[ax]) ? 0 : 1);
+                node1[ax] = full_hi[ax] - ((imp && has_hi[ax]) ? 0 : 1);
+            }
+            d.m = node1[0] - node0[0] + 1;
+            d.nb = node1[1] - node0[1] + 1;
+            d.gx0 = node0[0];
+            d.gy0 = node0[1];
+            d.fx0 = full_lo[0];
+            d.fx1 = full_hi[0];
+            d.fy0 = full_lo[1];
+            d.fy1 = full_hi[1];
+            d.imp = imp ? ((has_lo[0] ? 1 : 0) | (has_hi[0] ? 2 : 0) | (has_lo[1] ? 4 : 0) | (has_hi[1] ? 8 : 0)) : 0;
             d.olo = std::max(own_lo[0], 1) - d.gx0;
             d.ohi = std::min(own_hi[0], G.N) - 1 - d.gx0;
             d.lo = std::max(own_lo[1], 1) - d.gy0;

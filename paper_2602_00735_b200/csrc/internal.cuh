@@ -66,6 +66,9 @@ struct SubDesc {
     int flags;      // bit0 x-lower PML, bit1 x-upper, bit2 y-lower, bit3 y-upper
     int cx0, cx1;   // local columns [cx0, cx1) and rows [cy0, cy1) whose six triangles all have gamma = 1:
     int cy0, cy1;   //   their couplings equal the constant interior stencil (apply skips those loads)
+    int fx0, fx1;   // full box in cells (= node indices of its faces): only triangles of these cells count
+    int fy0, fy1;
+    int imp;        // impedance faces: bit0 x-lower, bit1 x-upper, bit2 y-lower, bit3 y-upper
     int pad;
     long long fac_off;   // complex offset of block 0 of the explicit inverses (blocks m x m, column-major)
     long long stc_off;   // complex offset of the local stencil [nb][7][m]

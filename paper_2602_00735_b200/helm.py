@@ -135,10 +135,13 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+BC_DIRICHLET, BC_IMPEDANCE = 0, 1
+
+
 def make_params(k, nsub_x, nsub_y=None, ppw=10, n_pml_global=10, sigma0=5.0, n_ovlp=-1, n_pml=-1,
-                gpu_grid=(0, 0)) -> Params:
+                gpu_grid=(0, 0), local_bc=BC_DIRICHLET) -> Params:
     return Params(float(k), ppw, n_pml_global, float(sigma0), nsub_x, nsub_y if nsub_y is not None else nsub_x,
-                  n_ovlp, n_pml, 0, gpu_grid[0], gpu_grid[1])
+                  n_ovlp, n_pml, local_bc, gpu_grid[0], gpu_grid[1])
 
 
 def plan_rank(params: Params, rank: int, nranks: int) -> dict:
@@ -175,12 +178,12 @@ class Context:
 
     def __init__(self, k: float, nsub_x: int, nsub_y: int | None = None, *, ppw: int = 10, n_pml_global: int = 10,
                  sigma0: float = 5.0, n_ovlp: int = -1, n_pml: int = -1, rank: int = 0, nranks: int = 1,
-                 gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None):
+                 gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None, local_bc: int = BC_DIRICHLET):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libhelm needs a CUDA device (no CPU fallback)")
         self.L = load()
-        self.params = make_params(k, nsub_x, nsub_y, ppw, n_pml_global, sigma0, n_ovlp, n_pml, gpu_grid)
+        self.params = make_params(k, nsub_x, nsub_y, ppw, n_pml_global, sigma0, n_ovlp, n_pml, gpu_grid, local_bc)
         self.rank, self.nranks = rank, nranks
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._h = C.c_void_p()

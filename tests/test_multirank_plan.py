@@ -30,10 +30,12 @@ def test_owned_rectangles_partition_the_free_nodes(k, nsub, nranks):
 
 
 @pytest.mark.parametrize("k,nsub,nranks", CASES)
-def test_every_full_box_inside_its_ranks_ghost_frame(k, nsub, nranks):
-    """The halo width delta + kappa - 1 is exactly what the edge subdomains' full boxes need."""
-    p = make_params(k, nsub)
-    o = Oracle.from_config(k=k, nsub_x=nsub, nsub_y=nsub)
+@pytest.mark.parametrize("bc", [0, 1])
+def test_every_full_box_inside_its_ranks_ghost_frame(k, nsub, nranks, bc):
+    """The ghost frame (delta + kappa - 1 below, delta + kappa above; one more each side for RAS-PML-Imp, whose
+    face nodes are unknowns) is exactly what the edge subdomains' local unknowns need."""
+    p = make_params(k, nsub, local_bc=bc)
+    o = Oracle.from_config(k=k, nsub_x=nsub, nsub_y=nsub, local_bc=bc)
     need = {r: [10 ** 9, -1, 10 ** 9, -1] for r in range(nranks)}
     plans = [plan_rank(p, r, nranks) for r in range(nranks)]
     for j in range(o.nsub):
@@ -41,12 +43,13 @@ def test_every_full_box_inside_its_ranks_ghost_frame(k, nsub, nranks):
         gi, gj = max(s["own_lo"][0], 1), max(s["own_lo"][1], 1)
         r = next(q for q, pl in enumerate(plans) if pl["owned_i0"] <= gi < pl["owned_i1"] and pl["owned_j0"] <= gj < pl["owned_j1"])
         pl = plans[r]
-        # local free nodes: full_lo+1 .. full_hi-1 per axis
-        assert pl["ext_i0"] <= s["full_lo"][0] + 1 and s["full_hi"][0] - 1 < pl["ext_i1"]
-        assert pl["ext_j0"] <= s["full_lo"][1] + 1 and s["full_hi"][1] - 1 < pl["ext_j1"]
+        lo = s["node0"]
+        hi = (s["node0"][0] + s["m"][0] - 1, s["node0"][1] + s["m"][1] - 1)
+        assert pl["ext_i0"] <= lo[0] and hi[0] < pl["ext_i1"]
+        assert pl["ext_j0"] <= lo[1] and hi[1] < pl["ext_j1"]
         n = need[r]
-        n[0] = min(n[0], s["full_lo"][0] + 1); n[1] = max(n[1], s["full_hi"][0] - 1)
-        n[2] = min(n[2], s["full_lo"][1] + 1); n[3] = max(n[3], s["full_hi"][1] - 1)
+        n[0] = min(n[0], lo[0]); n[1] = max(n[1], hi[0])
+        n[2] = min(n[2], lo[1]); n[3] = max(n[3], hi[1])
     for r, pl in enumerate(plans):   # and no wider than needed
         assert need[r] == [pl["ext_i0"], pl["ext_i1"] - 1, pl["ext_j0"], pl["ext_j1"] - 1]
 
