@@ -56,8 +56,12 @@ typedef struct {
     int nsub_x, nsub_y;  /* Cartesian subdomain grid */
     int n_ovlp, n_pml;   /* overlap delta / local PML kappa in cells per interior face; < 0 => max(2, round(1.59 ln k)) */
     int local_bc;        /* HELM_BC_DIRICHLET or HELM_BC_IMPEDANCE */
-    int gpu_grid_x, gpu_grid_y;   /* rank grid over the subdomain grid; product == nranks (0,0 => 1 x nranks) */
+    int gpu_grid_x, gpu_grid_y;   /* rank grid over the subdomain grid; product == nranks (0,0 => most square) */
+    int pou;             /* HELM_POU_OWNER: restricted owner write (D10, the hot path); HELM_POU_RAMP: linear
+                            ramps across the overlaps, one rank only, blocks >= 2 delta cells */
 } helm_params;
+
+enum { HELM_POU_OWNER = 0, HELM_POU_RAMP = 1 };
 
 typedef struct {
     long long n_free_global;  /* (N-1)^2 */

@@ -40,7 +40,8 @@ def build(force: bool = False) -> str:
 class _Params(C.Structure):
     _fields_ = [("k", C.c_double), ("sigma0", C.c_double), ("h", C.c_double),
                 ("nix", C.c_int), ("niy", C.c_int), ("ng", C.c_int), ("kappa", C.c_double),
-                ("px", C.c_int), ("py", C.c_int), ("novlp", C.c_int), ("npml", C.c_int), ("local_bc", C.c_int)]
+                ("px", C.c_int), ("py", C.c_int), ("novlp", C.c_int), ("npml", C.c_int), ("local_bc", C.c_int),
+                ("pou", C.c_int)]
 
 
 _lib = None
@@ -70,6 +71,8 @@ def lib():
         L.orc_factor.restype = C.c_int
         L.orc_factor.argtypes = [vp, ip, C.c_int, i64p]
         L.orc_release.argtypes = [vp]
+        L.orc_chi1.restype = C.c_double
+        L.orc_chi1.argtypes = [vp, C.c_int, C.c_int, C.c_int]
         L.orc_apply.restype = C.c_int
         L.orc_apply.argtypes = [vp, vp, vp, ip, C.c_int]
         _lib = L
@@ -120,17 +123,18 @@ class Problem:
     novlp: int
     npml: int
     local_bc: int = 0    # 0 RAS-PML-Drch, 1 RAS-PML-Imp
+    pou: int = 0         # 0 owner indicator (D10), 1 linear ramps
 
 
 def problem_from_config(k, ppw=10, n_pml_global=10, sigma0=5.0, nsub_x=1, nsub_y=1,
-                        n_ovlp=-1, n_pml=-1, local_bc=0) -> Problem:
+                        n_ovlp=-1, n_pml=-1, local_bc=0, pou=0) -> Problem:
     n_int = n_int_from(k, ppw)
     h = 1.0 / n_int
     w = width_from(k)
     return Problem(k=float(k), sigma0=float(sigma0), h=h, nix=n_int, niy=n_int, ng=n_pml_global,
                    kappa=n_pml_global * h,  # D3: kappa_g = 1 wavelength ~ 10 cells at 10 ppw
                    px=nsub_x, py=nsub_y,
-                   novlp=w if n_ovlp < 0 else n_ovlp, npml=w if n_pml < 0 else n_pml, local_bc=local_bc)
+                   novlp=w if n_ovlp < 0 else n_ovlp, npml=w if n_pml < 0 else n_pml, local_bc=local_bc, pou=pou)
 
 
 class OracleError(RuntimeError):
@@ -141,7 +145,7 @@ class Oracle:
     def __init__(self, prob: Problem):
         self.prob = prob
         p = _Params(prob.k, prob.sigma0, prob.h, prob.nix, prob.niy, prob.ng, prob.kappa,
-                    prob.px, prob.py, prob.novlp, prob.npml, prob.local_bc)
+                    prob.px, prob.py, prob.novlp, prob.npml, prob.local_bc, prob.pou)
         err = C.create_string_buffer(256)
         self._h = lib().orc_create(C.byref(p), err, 256)
         if not self._h:
@@ -170,6 +174,10 @@ class Oracle:
         lib().orc_subdomain(self._h, j, o)
         keys = ["own_lo", "own_hi", "int_lo", "int_hi", "full_lo", "full_hi", "has_lo", "has_hi", "m", "node0"]
         return {k: (o[i], o[10 + i]) for i, k in enumerate(keys)}
+
+    def chi(self, axis: int, block: int, x: int) -> float:
+        """1-D partition-of-unity factor of `block` at node x (owner indicator or linear ramp)."""
+        return lib().orc_chi1(self._h, axis, block, x)
 
     # -- PML ------------------------------------------------------------------------------------
     def gamma(self, axis: int, X3: int, sub: int = -1):

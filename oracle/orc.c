@@ -44,6 +44,7 @@ typedef struct {
     int novlp;      /* overlap delta in cells, per side of every interior face (D8) */
     int npml;       /* local PML kappa in cells on every interior face */
     int local_bc;   /* 0: RAS-PML-Drch (u = 0 on dOmega_j); 1: RAS-PML-Imp */
+    int pou;        /* 0: owner indicator chi_j = 1 on block j (D10); 1: linear ramps across overlaps */
 } orc_params;
 
 typedef struct {
@@ -207,8 +208,9 @@ orc_ctx *orc_create(const orc_params *p, char *err, int errlen)
         for (int b = 0; b < P[ax]; b++) c->split[ax][b + 1] = c->split[ax][b] + q + (b < r ? 1 : 0);
         for (int b = 0; b < P[ax]; b++) {
             int sz = c->split[ax][b + 1] - c->split[ax][b];
-            if ((P[ax] > 1 && sz < w) || sz < 2) {
-                snprintf(err, errlen, "block %d on axis %d has %d cells (< delta+kappa = %d or < 2)", b, ax, sz, w);
+            if ((P[ax] > 1 && sz < w) || sz < 2 || (p->pou == 1 && P[ax] > 1 && sz < 2 * p->novlp)) {
+                snprintf(err, errlen, "block %d on axis %d has %d cells (< delta+kappa = %d, < 2, or < 2 delta for "
+                         "ramps)", b, ax, sz, w);
                 free(c->split[0]); free(c->split[1]); free(c); return NULL;
             }
         }
@@ -544,11 +546,68 @@ void orc_release(orc_ctx *c)
  * Only the listed subdomains are applied (list == NULL -> all); z is written at their owned nodes.
  * Returns 0, or -1 if a listed subdomain is not factored.
  * ----------------------------------------------------------------------------------------------*/
+/* ------------------------------------------------------------------------------------------------
+ * Partition of unity chi_j.  pou = 0: the owner indicator (D10).  pou = 1: the paper's
+ * experiments, "tensor products of the 1D PoU functions which vary linearly across the overlap
+ * regions": along an axis, block b = cells [s_b, s_{b+1}) with int box [s_b - delta, s_{b+1} + delta]
+ * on sides with a neighbour; chi rises linearly from 0 at s_b - delta to 1 at s_b + delta, falls from 1 at
+ * s_{b+1} - delta to 0 at s_{b+1} + delta, and is 1 up to dOmega on sides without a neighbour.  The two
+ * ramps of an overlap of width 2 delta sum to 1.  Evaluated at node x (integer).
+ * ----------------------------------------------------------------------------------------------*/
+double orc_chi1(const orc_ctx *c, int ax, int b, int x)
+{
+    int P = ax ? c->p.py : c->p.px, d = c->p.novlp;
+    int s0 = c->split[ax][b], s1 = c->split[ax][b + 1];
+    int lo = b > 0, hi = b < P - 1;
+    if (c->p.pou != 1 || d == 0) return (x >= s0 && x < s1) ? 1.0 : 0.0;   /* owner indicator */
+    if (lo && x <= s0 - d) return 0.0;
+    if (hi && x >= s1 + d) return 0.0;
+    if (lo && x < s0 + d) return (double)(x - (s0 - d)) / (2.0 * d);
+    if (hi && x > s1 - d) return (double)(s1 + d - x) / (2.0 * d);
+    return 1.0;
+}
+
 int orc_apply(orc_ctx *c, const zc *v, zc *z, const int *list, int nlist)
 {
     int cnt = list ? nlist : c->nsub;
     int nfx = c->nf[0];
     int missing = 0;
+    if (c->p.pou == 1) {
+        /* z += sum_j chi_j R_j^T A_j^-1 R_j v: local solves in parallel, accumulation in subdomain order */
+        zc **sol = calloc(cnt, sizeof(zc *));
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int t = 0; t < cnt; t++) {
+            int j = list ? list[t] : t;
+            orc_sub *s = &c->sub[j];
+            if (!s->factored) { missing = 1; continue; }
+            int mx = s->m[0], my = s->m[1];
+            int64_t n = (int64_t)mx * my;
+            zc *x = malloc(sizeof(zc) * (size_t)n);
+            for (int ly = 0; ly < my; ly++)
+                for (int lx = 0; lx < mx; lx++)
+                    x[lx + (int64_t)mx * ly] = v[(s->node0[0] + lx - 1) + (int64_t)nfx * (s->node0[1] + ly - 1)];
+            orc_band_solve(n, mx + 1, s->band, x);
+            sol[t] = x;
+        }
+        if (!list) memset(z, 0, sizeof(zc) * (size_t)c->nfree);
+        for (int t = 0; t < cnt && !missing; t++) {
+            int j = list ? list[t] : t;
+            orc_sub *s = &c->sub[j];
+            int bx = j % c->p.px, by = j / c->p.px;
+            for (int gj = s->int_lo[1]; gj <= s->int_hi[1]; gj++)
+                for (int gi = s->int_lo[0]; gi <= s->int_hi[0]; gi++) {
+                    if (gi < 1 || gi > c->nf[0] || gj < 1 || gj > c->nf[1]) continue;
+                    double w = orc_chi1(c, 0, bx, gi) * orc_chi1(c, 1, by, gj);
+                    if (w == 0.0) continue;
+                    int64_t r;
+                    local_index(s, gi, gj, &r);
+                    z[(gi - 1) + (int64_t)nfx * (gj - 1)] += w * sol[t][r];
+                }
+        }
+        for (int t = 0; t < cnt; t++) free(sol[t]);
+        free(sol);
+        return missing ? -1 : 0;
+    }
 #pragma omp parallel for schedule(dynamic, 1)
     for (int t = 0; t < cnt; t++) {
         int j = list ? list[t] : t;

@@ -272,8 +272,17 @@ __global__ void k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
                         vt[t] = x;
                     }
                     if (t >= d.olo && t <= d.ohi) {
-                        const long long gi = d.gx0 + t - a.out_i0, gj = d.gy0 + st.i - a.out_j0;
-                        a.out[gi + a.out_stride * gj] = x;
+                        if (a.pou_buf) {
+                            // linear-ramp PoU: chi_j-weighted solution into the subdomain's slot; the
+                            // gather kernel sums the <= 4 covering subdomains in index order
+                            const double w = chi_ramp(d.gx0 + t, d.s0x, d.s1x, a.delta, d.flags & 1, d.flags & 2) *
+                                             chi_ramp(d.gy0 + st.i, d.s0y, d.s1y, a.delta, d.flags & 4, d.flags & 8);
+                            a.pou_buf[d.pou_off + (t - d.olo) + (long long)(d.ohi - d.olo + 1) * (st.i - d.lo)] =
+                                zscale(x, w);
+                        } else {
+                            const long long gi = d.gx0 + t - a.out_i0, gj = d.gy0 + st.i - a.out_j0;
+                            a.out[gi + a.out_stride * gj] = x;
+                        }
                     }
                     break;
                 }
@@ -281,6 +290,33 @@ __global__ void k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
             consumer_bar(nct);
             cur = nxt;
         }
+    }
+}
+
+// Ramp-PoU prolongation: z[g] = sum over the <= 2 x 2 subdomains whose chi is positive at
+// g of their weighted local solutions, summed in ascending subdomain index (deterministic).
+// candx / candy: per node index, the (up to) two blocks along that axis, -1 padded.
+__global__ void k_pou_gather(const SubDesc* __restrict__ desc, const int* __restrict__ candx,
+                             const int* __restrict__ candy, int px, const z2* __restrict__ buf, z2* __restrict__ z,
+                             int i0, int i1, int j0, int j1)
+{
+    const int w = i1 - i0;
+    const long long n = (long long)w * (j1 - j0);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int i = i0 + (int)(e % w), j = j0 + (int)(e / w);
+        z2 acc = zmk(0, 0);
+        for (int b = 0; b < 2; b++) {
+            const int by = candy[2 * j + b];
+            if (by < 0) continue;
+            for (int a = 0; a < 2; a++) {
+                const int bx = candx[2 * i + a];
+                if (bx < 0) continue;
+                const SubDesc d = desc[bx + px * by];
+                const long long off = d.pou_off + (i - (d.gx0 + d.olo)) + (long long)(d.ohi - d.olo + 1) * (j - (d.gy0 + d.lo));
+                acc = zadd(acc, buf[off]);
+            }
+        }
+        z[e] = acc;
     }
 }
 
@@ -307,6 +343,15 @@ int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_by
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply, *block_threads, *smem_bytes);
     *ctas_per_sm = occ;
     return ncw;
+}
+
+void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int px, const z2* pou_buf, z2* z,
+                       int i0, int i1, int j0, int j1, cudaStream_t s)
+{
+    const long long n = (long long)(i1 - i0) * (j1 - j0);
+    long long g = (n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    k_pou_gather<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(desc, candx, candy, px, pou_buf, z, i0, i1, j0, j1);
 }
 
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s)

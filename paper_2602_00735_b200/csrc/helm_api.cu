@@ -90,7 +90,19 @@ int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* 
                          sz, w);
                 return HELM_ELAYOUT;
             }
+            if (p.pou == HELM_POU_RAMP && G.P[ax] > 1 && sz < 2 * G.wo) {
+                snprintf(err, errlen, "ramp PoU: block %d on axis %d has %d cells < 2 delta = %d", b, ax, sz, 2 * G.wo);
+                return HELM_ELAYOUT;
+            }
         }
+    if (p.pou != HELM_POU_OWNER && p.pou != HELM_POU_RAMP) {
+        snprintf(err, errlen, "pou must be HELM_POU_OWNER or HELM_POU_RAMP");
+        return HELM_EINVAL;
+    }
+    if (p.pou == HELM_POU_RAMP && (nranks > 1 || G.wo < 1)) {
+        snprintf(err, errlen, "ramp PoU needs one rank and delta >= 1");
+        return HELM_EINVAL;
+    }
     // rank grid: default = most square factorisation with gx >= gy
     int gx = p.gpu_grid_x, gy = p.gpu_grid_y;
     if (gx <= 0 || gy <= 0) {
@@ -191,6 +203,12 @@ struct helm_ctx {
 
     // apply launch configuration
     int ap_block = 0, ap_smem = 0, ap_slot = 0, ap_grid = 0, ap_occ = 0;
+
+    // ramp partition of unity: weighted local solutions + per-axis covering blocks
+    long long pou_len = 0;
+    z2* d_pou = nullptr;
+    int* d_candx = nullptr;
+    int* d_candy = nullptr;
 
     // multi-rank: ghost-framed buffer (ext rectangle), pack / unpack buffers, communicator
     bool multi = false, has_comm = false;
@@ -339,11 +357,26 @@ int build_layout(helm_ctx* ctx)
             d.fy0 = full_lo[1];
             d.fy1 = full_hi[1];
             d.imp = imp ? ((has_lo[0] ? 1 : 0) | (has_hi[0] ? 2 : 0) | (has_lo[1] ? 4 : 0) | (has_hi[1] ? 8 : 0)) : 0;
-            d.olo = std::max(own_lo[0], 1) - d.gx0;
-            d.ohi = std::min(own_hi[0], G.N) - 1 - d.gx0;
-            d.lo = std::max(own_lo[1], 1) - d.gy0;
-            d.hi = std::min(own_hi[1], G.N) - 1 - d.gy0;
+            if (ctx->p.pou == HELM_POU_RAMP) {
+                // the solution is needed wherever chi_j > 0: the int box interior
+                d.olo = std::max(int_lo[0] + (has_lo[0] ? 1 : 0), 1) - d.gx0;
+                d.ohi = std::min(int_hi[0] - (has_hi[0] ? 1 : 0), G.N - 1) - d.gx0;
+                d.lo = std::max(int_lo[1] + (has_lo[1] ? 1 : 0), 1) - d.gy0;
+                d.hi = std::min(int_hi[1] - (has_hi[1] ? 1 : 0), G.N - 1) - d.gy0;
+            } else {
+                // restricted owner write (D10): the block's own nodes
+                d.olo = std::max(own_lo[0], 1) - d.gx0;
+                d.ohi = std::min(own_hi[0], G.N) - 1 - d.gx0;
+                d.lo = std::max(own_lo[1], 1) - d.gy0;
+                d.hi = std::min(own_hi[1], G.N) - 1 - d.gy0;
+            }
             d.tw = (d.lo + d.hi) / 2;
+            d.s0x = own_lo[0];
+            d.s1x = own_hi[0];
+            d.s0y = own_lo[1];
+            d.s1y = own_hi[1];
+            d.pou_off = ctx->pou_len;
+            if (ctx->p.pou == HELM_POU_RAMP) ctx->pou_len += (long long)(d.ohi - d.olo + 1) * (d.hi - d.lo + 1);
             d.ilo3 = 3 * int_lo[0];
             d.ihi3 = 3 * int_hi[0];
             d.jlo3 = 3 * int_lo[1];
@@ -406,6 +439,8 @@ int build_layout(helm_ctx* ctx)
         }
     ctx->n_dinv = fac;
     ctx->n_stc = stc;
+    // ramp PoU: the gather re-reads every weighted value once and writes z once
+    if (ctx->p.pou == HELM_POU_RAMP) ctx->apply_bytes += 16 * (ctx->pou_len + ctx->n_local);
     return HELM_OK;
 }
 
@@ -529,6 +564,8 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     a.cSW = ctx->lcSW;
     a.cN = ctx->lcN;
     a.cNE = ctx->lcNE;
+    a.pou_buf = ctx->d_pou;
+    a.delta = ctx->G.wo;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof) {
         if (ctx->ev_free.size() < 2) {
@@ -547,6 +584,12 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     launch_apply(a, ctx->ap_grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->stream);
     CK(cudaGetLastError());
     ctx->launches++;
+    if (ctx->d_pou) {
+        launch_pou_gather(ctx->d_desc, ctx->d_candx, ctx->d_candy, ctx->G.P[0], ctx->d_pou, z, ctx->G.i0, ctx->G.i1,
+                          ctx->G.j0, ctx->G.j1, ctx->stream);
+        CK(cudaGetLastError());
+        ctx->launches++;
+    }
     if (ctx->prof) {
         CK(cudaEventRecord(e1, ctx->stream));
         ctx->ev_used.push_back({e0, e1});
@@ -977,6 +1020,23 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     ctx->ap_grid = std::min(nsub, nsm * ctx->ap_occ);
     ctx->nblk = nsm * 4;
     if ((rc = dalloc(ctx, &ctx->d_scratch, (size_t)ctx->ap_grid * ctx->scratch_per_cta))) return rc;
+    if (ctx->p.pou == HELM_POU_RAMP) {
+        // per axis and node index: the (<= 2, ascending) blocks whose ramp chi is positive there
+        const GridInfo& G = ctx->G;
+        if ((rc = dalloc(ctx, &ctx->d_pou, ctx->pou_len)) || (rc = dalloc(ctx, &ctx->d_candx, 2 * (G.N + 1))) ||
+            (rc = dalloc(ctx, &ctx->d_candy, 2 * (G.N + 1))))
+            return rc;
+        for (int ax = 0; ax < 2; ax++) {
+            std::vector<int> cand(2 * (G.N + 1), -1);
+            for (int x = 0; x <= G.N; x++) {
+                int k = 0;
+                for (int b = 0; b < G.P[ax] && k < 2; b++)
+                    if (chi_ramp(x, G.st[ax][b], G.st[ax][b + 1], G.wo, b > 0, b < G.P[ax] - 1) > 0.0) cand[2 * x + k++] = b;
+            }
+            CK(cudaMemcpyAsync(ax ? ctx->d_candy : ctx->d_candx, cand.data(), sizeof(int) * cand.size(),
+                               cudaMemcpyHostToDevice, ctx->stream));
+        }
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     return HELM_OK;
 }
@@ -1173,7 +1233,8 @@ void helm_destroy(helm_ctx* ctx)
 #endif
     void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
-                    ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq};
+                    ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq,
+                    ctx->d_pou, ctx->d_candx, ctx->d_candy};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int q = 0; q < 4; q++) {

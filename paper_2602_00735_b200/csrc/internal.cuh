@@ -69,10 +69,24 @@ struct SubDesc {
     int fx0, fx1;   // full box in cells (= node indices of its faces): only triangles of these cells count
     int fy0, fy1;
     int imp;        // impedance faces: bit0 x-lower, bit1 x-upper, bit2 y-lower, bit3 y-upper
+    int s0x, s1x;   // block cells [s0, s1) per axis (linear-ramp partition of unity)
+    int s0y, s1y;
     int pad;
     long long fac_off;   // complex offset of block 0 of the explicit inverses (blocks m x m, column-major)
     long long stc_off;   // complex offset of the local stencil [nb][7][m]
+    long long pou_off;   // ramp-PoU mode: offset of this subdomain's weighted solution [lo..hi][olo..ohi]
 };
+
+// linear-ramp PoU factor along one axis at node x: 0 -> 1 across [s0-d, s0+d], 1 -> 0 across
+// [s1-d, s1+d], 1 toward dOmega; d = overlap delta
+__host__ __device__ __forceinline__ double chi_ramp(int x, int s0, int s1, int d, bool lo, bool hi)
+{
+    if (lo && x <= s0 - d) return 0.0;
+    if (hi && x >= s1 + d) return 0.0;
+    if (lo && x < s0 + d) return (double)(x - (s0 - d)) / (2.0 * d);
+    if (hi && x > s1 - d) return (double)(s1 + d - x) / (2.0 * d);
+    return 1.0;
+}
 
 enum { SL_C = 0, SL_E = 1, SL_W = 2, SL_N = 3, SL_S = 4, SL_NE = 5, SL_SW = 6 };
 
@@ -107,7 +121,11 @@ struct ApplyArgs {
     z2* scratch;            // per-CTA [max_rows][m_max]
     long long scratch_per_cta;
     z2 cS, cSW, cN, cNE;    // couplings of the constant interior stencil
+    z2* pou_buf;            // ramp-PoU mode: weighted local solutions (else nullptr: owner write to out)
+    int delta;              // overlap width (ramp half-width)
 };
+void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int px, const z2* pou_buf, z2* z,
+                       int i0, int i1, int j0, int j1, cudaStream_t s);
 int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
 

@@ -26,7 +26,7 @@ HELM_OK, HELM_NOT_CONVERGED, HELM_BREAKDOWN = 0, 2, 3
 class Params(C.Structure):
     _fields_ = [("k", C.c_double), ("ppw", C.c_int), ("n_pml_global", C.c_int), ("sigma0", C.c_double),
                 ("nsub_x", C.c_int), ("nsub_y", C.c_int), ("n_ovlp", C.c_int), ("n_pml", C.c_int),
-                ("local_bc", C.c_int), ("gpu_grid_x", C.c_int), ("gpu_grid_y", C.c_int)]
+                ("local_bc", C.c_int), ("gpu_grid_x", C.c_int), ("gpu_grid_y", C.c_int), ("pou", C.c_int)]
 
 
 class Layout(C.Structure):
@@ -136,12 +136,13 @@ def _ptr(t) -> int:
 
 
 BC_DIRICHLET, BC_IMPEDANCE = 0, 1
+POU_OWNER, POU_RAMP = 0, 1
 
 
 def make_params(k, nsub_x, nsub_y=None, ppw=10, n_pml_global=10, sigma0=5.0, n_ovlp=-1, n_pml=-1,
-                gpu_grid=(0, 0), local_bc=BC_DIRICHLET) -> Params:
+                gpu_grid=(0, 0), local_bc=BC_DIRICHLET, pou=POU_OWNER) -> Params:
     return Params(float(k), ppw, n_pml_global, float(sigma0), nsub_x, nsub_y if nsub_y is not None else nsub_x,
-                  n_ovlp, n_pml, local_bc, gpu_grid[0], gpu_grid[1])
+                  n_ovlp, n_pml, local_bc, gpu_grid[0], gpu_grid[1], pou)
 
 
 def plan_rank(params: Params, rank: int, nranks: int) -> dict:
@@ -178,12 +179,14 @@ class Context:
 
     def __init__(self, k: float, nsub_x: int, nsub_y: int | None = None, *, ppw: int = 10, n_pml_global: int = 10,
                  sigma0: float = 5.0, n_ovlp: int = -1, n_pml: int = -1, rank: int = 0, nranks: int = 1,
-                 gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None, local_bc: int = BC_DIRICHLET):
+                 gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None, local_bc: int = BC_DIRICHLET,
+                 pou: int = POU_OWNER):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libhelm needs a CUDA device (no CPU fallback)")
         self.L = load()
-        self.params = make_params(k, nsub_x, nsub_y, ppw, n_pml_global, sigma0, n_ovlp, n_pml, gpu_grid, local_bc)
+        self.params = make_params(k, nsub_x, nsub_y, ppw, n_pml_global, sigma0, n_ovlp, n_pml, gpu_grid, local_bc,
+                                  pou)
         self.rank, self.nranks = rank, nranks
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._h = C.c_void_p()
