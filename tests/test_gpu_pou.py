@@ -22,7 +22,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("name,nsub,bc", [("c0", None, 0), ("c1", None, 0), ("c2", None, 0), ("c1", (5, 3), 0),
-                                          ("c1", None, 1), ("c2", (9, 13), 1)])
+                                          ("c1", None, 1), ("c2", (11, 13), 1)])
 def test_pou_apply_and_gmres_parity(name, nsub, bc):
     cfg = CONFIGS[name]
     nsub = nsub or (cfg.nsub, cfg.nsub)
