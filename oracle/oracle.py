@@ -41,7 +41,7 @@ class _Params(C.Structure):
     _fields_ = [("k", C.c_double), ("sigma0", C.c_double), ("h", C.c_double),
                 ("nix", C.c_int), ("niy", C.c_int), ("ng", C.c_int), ("kappa", C.c_double),
                 ("px", C.c_int), ("py", C.c_int), ("novlp", C.c_int), ("npml", C.c_int), ("local_bc", C.c_int),
-                ("pou", C.c_int)]
+                ("pou", C.c_int), ("elem", C.c_int), ("frame", C.c_int), ("pml_c", C.c_double)]
 
 
 _lib = None
@@ -59,6 +59,7 @@ def lib():
         L.orc_subdomain.argtypes = [vp, C.c_int, ip]
         L.orc_gfun.argtypes = [C.c_double, C.c_double, C.c_double, dp]
         L.orc_gamma.argtypes = [vp, C.c_int, C.c_int, C.c_long, vp, vp]
+        L.orc_gamma_q.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, vp, vp]
         L.orc_global_stencil.argtypes = [vp, vp]
         L.orc_matvec.argtypes = [vp, vp, vp]
         L.orc_matvec_rows.argtypes = [vp, vp, i64p, C.c_int, vp]
@@ -124,6 +125,9 @@ class Problem:
     npml: int
     local_bc: int = 0    # 0 RAS-PML-Drch, 1 RAS-PML-Imp
     pou: int = 0         # 0 owner indicator (D10), 1 linear ramps
+    elem: int = 0        # 0 P1 (D1), 1 Q1 bilinear (D18)
+    frame: int = 0       # 0 BJ frame (Omega_int = (0,1)^2 + ng PML cells), 1 paper frame (Omega = (0,1)^2; D19)
+    pml_c: float = 0.0   # paper frame: g(t) = pml_c t^3
 
 
 def problem_from_config(k, ppw=10, n_pml_global=10, sigma0=5.0, nsub_x=1, nsub_y=1,
@@ -137,6 +141,19 @@ def problem_from_config(k, ppw=10, n_pml_global=10, sigma0=5.0, nsub_x=1, nsub_y
                    novlp=w if n_ovlp < 0 else n_ovlp, npml=w if n_pml < 0 else n_pml, local_bc=local_bc, pou=pou)
 
 
+def problem_from_paper(k, nsub, pml, ovlp, local_bc=1, pou=1, n_cells=None, kappa_wavelengths=3.0,
+                       pml_c=None) -> Problem:
+    """The paper's own experiment (Tables 1-4): Omega = (0,1)^2 is a uniform n x n grid of Q1 cells
+    (grid "600^2" at k = 300, i.e. n = 2k: D19), global PML of width kappa_g = 3 wavelengths inside Omega with
+    g(x) = 10 k x^3, N = nsub^2 subdomains, `pml` / `ovlp` cells of local PML / overlap (the integers
+    printed in the tables; D20), impedance (RAS-PML-Imp) or Dirichlet local faces, linear-ramp PoU."""
+    n = int(round(2 * k)) if n_cells is None else int(n_cells)
+    lam = 2.0 * math.pi / k
+    return Problem(k=float(k), sigma0=0.0, h=1.0 / n, nix=n, niy=n, ng=0, kappa=kappa_wavelengths * lam,
+                   px=nsub, py=nsub, novlp=ovlp, npml=pml, local_bc=local_bc, pou=pou, elem=1, frame=1,
+                   pml_c=10.0 * k if pml_c is None else float(pml_c))
+
+
 class OracleError(RuntimeError):
     pass
 
@@ -145,7 +162,9 @@ class Oracle:
     def __init__(self, prob: Problem):
         self.prob = prob
         p = _Params(prob.k, prob.sigma0, prob.h, prob.nix, prob.niy, prob.ng, prob.kappa,
-                    prob.px, prob.py, prob.novlp, prob.npml, prob.local_bc, prob.pou)
+                    prob.px, prob.py, prob.novlp, prob.npml, prob.local_bc, prob.pou, prob.elem, prob.frame,
+                    prob.pml_c)
+        self.ns = 9 if prob.elem == 1 else 7
         err = C.create_string_buffer(256)
         self._h = lib().orc_create(C.byref(p), err, 256)
         if not self._h:
@@ -160,6 +179,10 @@ class Oracle:
     @classmethod
     def from_config(cls, **kw) -> "Oracle":
         return cls(problem_from_config(**kw))
+
+    @classmethod
+    def from_paper(cls, **kw) -> "Oracle":
+        return cls(problem_from_paper(**kw))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -186,10 +209,19 @@ class Oracle:
         lib().orc_gamma(self._h, sub, axis, X3, _ptr(g), _ptr(dg))
         return complex(g[0]), complex(dg[0])
 
+    def gamma_q(self, axis: int, ci: int, xi: float, sub: int = -1):
+        """(gamma, gamma') at x = (ci + xi) h on the Q1 path (global, or subdomain `sub`'s local scaling)."""
+        g = np.zeros(1, np.complex128)
+        dg = np.zeros(1, np.complex128)
+        lib().orc_gamma_q(self._h, sub, axis, ci, xi, _ptr(g), _ptr(dg))
+        return complex(g[0]), complex(dg[0])
+
     # -- operators ------------------------------------------------------------------------------
+    OFFSETS = [(0, 0), (1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1), (-1, 1), (1, -1)]
+
     def stencil(self) -> np.ndarray:
-        """Global matrix as [nfree, 7] slots: centre, E, W, N, S, NE, SW."""
-        out = np.zeros((self.nfree, 7), np.complex128)
+        """Global matrix as [nfree, ns] slots: centre, E, W, N, S, NE, SW (+ NW, SE for Q1)."""
+        out = np.zeros((self.nfree, self.ns), np.complex128)
         lib().orc_global_stencil(self._h, _ptr(out))
         return out
 
@@ -202,7 +234,7 @@ class Oracle:
         i = idx % nfx
         j = idx // nfx
         rows, cols, vals = [], [], []
-        for s, (dx, dy) in enumerate([(0, 0), (1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1)]):
+        for s, (dx, dy) in enumerate(self.OFFSETS[:self.ns]):
             qi, qj = i + dx, j + dy
             ok = (qi >= 0) & (qi < nfx) & (qj >= 0) & (qj < nfy)
             rows.append(idx[ok]); cols.append((qi + nfx * qj)[ok]); vals.append(A7[ok, s])

@@ -16,7 +16,11 @@
  * stencil closed form; PML closed forms / finite differences; A = A^T when sigma0 = 0; interior local
  * matrix = global matrix of the (int box + kappa PML) problem; band LU vs numpy.linalg.solve;
  * dense sum_j R~_j^T A_j^-1 R_j vs the apply; single subdomain => B^-1 = A^-1; Hankel far field;
- * FEM order 2.  No function here is "parity unpinned".
+ * FEM order 2.  Q1 / paper frame (tests/test_oracle_q1.py): the bilinear interior stencil closed form,
+ * symmetry without PML, the g = 10 k t^3 profile closed forms / finite differences / local restarts, local rows =
+ * global rows in the int box, Q1 FEM order 2, band LU vs zgesv, dense ramp-PoU RAS vs the apply, single subdomain
+ * => exact inverse, unit mass of the smoothed delta, and the iteration counts printed in the paper's Tables 1 and 4
+ * at k = 300 (tests/golden/paper_iterations.txt).  No function here is "parity unpinned".
  */
 #include <complex.h>
 #include <math.h>
@@ -45,6 +49,12 @@ typedef struct {
     int npml;       /* local PML kappa in cells on every interior face */
     int local_bc;   /* 0: RAS-PML-Drch (u = 0 on dOmega_j); 1: RAS-PML-Imp */
     int pou;        /* 0: owner indicator chi_j = 1 on block j (D10); 1: linear ramps across overlaps */
+    /* paper-faithful workload (D18-D22) */
+    int elem;       /* 0: P1 on the SW->NE split (D1); 1: Q1 bilinear elements, 2x2 Gauss quadrature */
+    int frame;      /* 0: BJ frame -- Omega_int = (0, nix h) x (0, niy h) inside ng PML cells per side;
+                       1: paper frame -- Omega = (0, nix h) x (0, niy h) itself (ng = 0) and
+                          Omega_int = Omega shrunk by kappa (= kappa_g = 3 lambda) on every side */
+    double pml_c;   /* frame 1: g(t) = pml_c t^3 (g(x) = 10 k x^3) */
 } orc_params;
 
 typedef struct {
@@ -68,7 +78,9 @@ typedef struct {
     int nsub;
     int *split[2];   /* block starts s_0..s_P (cells == nodes) */
     orc_sub *sub;
-    zc *A7;          /* global matrix, 7 slots per free row (see slot_of) */
+    int ns;          /* slots per global row: 7 (P1) or 9 (Q1) */
+    double lo_u[2], hi_u[2];   /* Omega_int per axis in cell units (node 0 at 0): where the global ramps start */
+    zc *A7;          /* global matrix, ns slots per free row (see slot_of) */
 } orc_ctx;
 
 /* ------------------------------------------------------------------------------------------------
@@ -132,6 +144,90 @@ void orc_gamma(const orc_ctx *c, int sub, int axis, long X3, zc *gam, zc *dgam)
 }
 
 /* ------------------------------------------------------------------------------------------------
+ * Q1 path (elem = 1): PML coefficients at arbitrary points x = (ci + xi) h of cell ci (xi in [0,1]).
+ * Depth below / above a ramp start r (cell units) is formed as (r - ci) - xi resp. (ci - r) + xi, then
+ * scaled by h, so identical relative positions give identical bits whenever r is a node (D5 carried over).
+ * Profile: frame 0 -> the BJ profile (orc_gfun); frame 1 -> the paper's g(t) = pml_c t^3, with
+ * g' = 3 pml_c t^2 and g'' = 6 pml_c t.  Signs of gamma' as in D4.
+ * ----------------------------------------------------------------------------------------------*/
+static void ramp_q(double t, int upper, const orc_params *p, zc *gam, zc *dgam)
+{
+    double g1, g2;
+    if (p->frame == 1) {
+        g1 = 3.0 * p->pml_c * t * t;
+        g2 = 6.0 * p->pml_c * t;
+    } else {
+        double g[3];
+        orc_gfun(t, p->kappa, p->sigma0, g);
+        g1 = g[1];
+        g2 = g[2];
+    }
+    *gam = 1.0 + I * g1;
+    *dgam = upper ? I * g2 : -I * g2;
+}
+
+static void gamma_global_q(const orc_ctx *c, int axis, int ci, double xi, zc *gam, zc *dgam)
+{
+    double up = ((double)ci - c->hi_u[axis]) + xi, dn = (c->lo_u[axis] - (double)ci) - xi;
+    if (up > 0.0) ramp_q(up * c->p.h, 1, &c->p, gam, dgam);
+    else if (dn > 0.0) ramp_q(dn * c->p.h, 0, &c->p, gam, dgam);
+    else { *gam = 1.0; *dgam = 0.0; }
+}
+
+/* local scaling g_j^i at a Q1 quadrature point */
+static void gamma_local_q(const orc_ctx *c, const orc_sub *s, int axis, int ci, double xi, zc *gam, zc *dgam)
+{
+    double up = (double)(ci - s->int_hi[axis]) + xi, dn = (double)(s->int_lo[axis] - ci) - xi;
+    if (s->has_hi[axis] && up > 0.0) ramp_q(up * c->p.h, 1, &c->p, gam, dgam);
+    else if (s->has_lo[axis] && dn > 0.0) ramp_q(dn * c->p.h, 0, &c->p, gam, dgam);
+    else gamma_global_q(c, axis, ci, xi, gam, dgam);
+}
+
+/* exported for the PML pins (Q1 path): sub < 0 -> global */
+void orc_gamma_q(const orc_ctx *c, int sub, int axis, int ci, double xi, zc *gam, zc *dgam)
+{
+    if (sub < 0) gamma_global_q(c, axis, ci, xi, gam, dgam);
+    else gamma_local_q(c, &c->sub[sub], axis, ci, xi, gam, dgam);
+}
+
+/* 2-point Gauss-Legendre abscissae on [0, 1]; weights 1/2 each */
+static double gauss_xi(int q) { return q == 0 ? 0.5 - 0.5 / sqrt(3.0) : 0.5 + 0.5 / sqrt(3.0); }
+
+/* ------------------------------------------------------------------------------------------------
+ * Q1 element matrix of eq. (weak) on a square cell of side h, bilinear basis
+ *   phi_a(x, y) = N_{ax}(xi) N_{ay}(eta),  N_0 = 1 - xi, N_1 = xi,  a = ax + 2 ay  (vertex (ci+ax, cj+ay)),
+ * integrated with the 2 x 2 Gauss rule (weight h^2/4 per point; exact for the mass and for constant D):
+ *   A_e[a][b] = sum_q h^2/4 [ D11 dx phi_a dx phi_b + D22 dy phi_a dy phi_b - (beta . grad phi_b) phi_a
+ *                             - k^2 phi_a phi_b ]   (row = test phi_a, column = trial phi_b; bilinear, D6),
+ * D11 = gamma_x^-2, D22 = gamma_y^-2, beta_i = gamma_i' / gamma_i^3 at the quadrature point.
+ * gx[q], dgx[q]: gamma_x, gamma_x' at xi = gauss_xi(q); gy, dgy likewise in y.
+ * ----------------------------------------------------------------------------------------------*/
+static void element_matrix_q1(const orc_params *p, const zc gx[2], const zc dgx[2], const zc gy[2], const zc dgy[2],
+                              zc Ae[4][4])
+{
+    double h = p->h, w = 0.25 * h * h;
+    for (int a = 0; a < 4; a++)
+        for (int b = 0; b < 4; b++) Ae[a][b] = 0;
+    for (int qx = 0; qx < 2; qx++)
+        for (int qy = 0; qy < 2; qy++) {
+            double xi = gauss_xi(qx), eta = gauss_xi(qy);
+            double Nx[2] = { 1.0 - xi, xi }, Ny[2] = { 1.0 - eta, eta }, dN[2] = { -1.0 / h, 1.0 / h };
+            zc D11 = 1.0 / (gx[qx] * gx[qx]), D22 = 1.0 / (gy[qy] * gy[qy]);
+            zc b1 = dgx[qx] / (gx[qx] * gx[qx] * gx[qx]), b2 = dgy[qy] / (gy[qy] * gy[qy] * gy[qy]);
+            for (int a = 0; a < 4; a++) {
+                int ax = a & 1, ay = a >> 1;
+                double pa = Nx[ax] * Ny[ay], pax = dN[ax] * Ny[ay], pay = Nx[ax] * dN[ay];
+                for (int b = 0; b < 4; b++) {
+                    int bx = b & 1, by = b >> 1;
+                    double pb = Nx[bx] * Ny[by], pbx = dN[bx] * Ny[by], pby = Nx[bx] * dN[by];
+                    Ae[a][b] += w * (D11 * pax * pbx + D22 * pay * pby - (b1 * pbx + b2 * pby) * pa
+                                     - p->k * p->k * pa * pb);
+                }
+            }
+        }
+}
+
+/* ------------------------------------------------------------------------------------------------
  * P1 element matrix (weak form eq. (weak)):
  *   a(u,v) = int D grad u . grad v - (beta . grad u) v - k^2 u v,
  *   D = diag(gamma_x^-2, gamma_y^-2), beta = (gamma_x'/gamma_x^3, gamma_y'/gamma_y^3),
@@ -173,7 +269,9 @@ static int slot_of(int dx, int dy)
     if (dx == 0 && dy == -1) return 4;  /* S  */
     if (dx == 1 && dy == 1) return 5;   /* NE */
     if (dx == -1 && dy == -1) return 6; /* SW */
-    fprintf(stderr, "orc: neighbour (%d,%d) outside the 7-point pattern\n", dx, dy);
+    if (dx == -1 && dy == 1) return 7;  /* NW (Q1 only) */
+    if (dx == 1 && dy == -1) return 8;  /* SE (Q1 only) */
+    fprintf(stderr, "orc: neighbour (%d,%d) outside the 9-point pattern\n", dx, dy);
     abort();
 }
 
@@ -199,6 +297,20 @@ orc_ctx *orc_create(const orc_params *p, char *err, int errlen)
     if (P[0] < 1 || P[1] < 1 || c->N[0] < 2 || c->N[1] < 2) {
         snprintf(err, errlen, "empty grid or subdomain count");
         free(c); return NULL;
+    }
+    if (p->elem != 0 && p->elem != 1) { snprintf(err, errlen, "elem must be 0 (P1) or 1 (Q1)"); free(c); return NULL; }
+    if (p->frame == 1 && (p->elem != 1 || p->ng != 0)) {
+        snprintf(err, errlen, "the paper frame is Q1 with ng = 0"); free(c); return NULL;
+    }
+    c->ns = p->elem == 1 ? 9 : 7;
+    for (int ax = 0; ax < 2; ax++) {
+        if (p->frame == 1) {     /* Omega_int = (kappa_g, L - kappa_g) in cell units */
+            c->lo_u[ax] = p->kappa / p->h;
+            c->hi_u[ax] = (double)c->N[ax] - p->kappa / p->h;
+        } else {                 /* Omega_int = nodes [ng, ng + ni] */
+            c->lo_u[ax] = (double)p->ng;
+            c->hi_u[ax] = (double)(p->ng + (ax == 0 ? p->nix : p->niy));
+        }
     }
     c->split[0] = malloc(sizeof(int) * (P[0] + 1));
     c->split[1] = malloc(sizeof(int) * (P[1] + 1));
@@ -280,81 +392,91 @@ void orc_subdomain(const orc_ctx *c, int j, int *out)
  * N x N cells with the global coefficients; rows/columns of Dirichlet nodes dropped.
  * Free node (i,j), 1 <= i,j <= N-1, has index (i-1) + nf (j-1).
  * ----------------------------------------------------------------------------------------------*/
+static void scatter_global(orc_ctx *c, int ci, int cj, int nv, const int (*V)[2], const zc *Ae /* nv x nv */)
+{
+    for (int a = 0; a < nv; a++) {
+        int pi = ci + V[a][0], pj = cj + V[a][1];
+        if (pi < 1 || pi > c->nf[0] || pj < 1 || pj > c->nf[1]) continue;
+        int64_t row = (pi - 1) + (int64_t)c->nf[0] * (pj - 1);
+        for (int q = 0; q < nv; q++) {
+            int qi = ci + V[q][0], qj = cj + V[q][1];
+            if (qi < 1 || qi > c->nf[0] || qj < 1 || qj > c->nf[1]) continue;
+            c->A7[row * c->ns + slot_of(qi - pi, qj - pj)] += Ae[a * nv + q];
+        }
+    }
+}
+
+static const int Q1_V[4][2] = { {0, 0}, {1, 0}, {0, 1}, {1, 1} };   /* a = ax + 2 ay */
+
 static void assemble_global(orc_ctx *c)
 {
     if (c->A7) return;
-    c->A7 = calloc((size_t)c->nfree * 7, sizeof(zc));
+    c->A7 = calloc((size_t)c->nfree * c->ns, sizeof(zc));
     for (int cj = 0; cj < c->N[1]; cj++)
-        for (int ci = 0; ci < c->N[0]; ci++)
+        for (int ci = 0; ci < c->N[0]; ci++) {
+            if (c->p.elem == 1) {
+                zc gx[2], dgx[2], gy[2], dgy[2], Ae[4][4];
+                for (int q = 0; q < 2; q++) {
+                    gamma_global_q(c, 0, ci, gauss_xi(q), &gx[q], &dgx[q]);
+                    gamma_global_q(c, 1, cj, gauss_xi(q), &gy[q], &dgy[q]);
+                }
+                element_matrix_q1(&c->p, gx, dgx, gy, dgy, Ae);
+                scatter_global(c, ci, cj, 4, Q1_V, &Ae[0][0]);
+                continue;
+            }
             for (int tri = 0; tri < 2; tri++) {
                 zc gx, dgx, gy, dgy, Ae[3][3];
                 gamma_global(c, 0, 3L * ci + TRI_C3[tri][0], &gx, &dgx);
                 gamma_global(c, 1, 3L * cj + TRI_C3[tri][1], &gy, &dgy);
                 element_matrix(&c->p, gx, dgx, gy, dgy, tri, Ae);
-                for (int a = 0; a < 3; a++) {
-                    int pi = ci + TRI_V[tri][a][0], pj = cj + TRI_V[tri][a][1];
-                    if (pi < 1 || pi > c->nf[0] || pj < 1 || pj > c->nf[1]) continue;
-                    int64_t row = (pi - 1) + (int64_t)c->nf[0] * (pj - 1);
-                    for (int q = 0; q < 3; q++) {
-                        int qi = ci + TRI_V[tri][q][0], qj = cj + TRI_V[tri][q][1];
-                        if (qi < 1 || qi > c->nf[0] || qj < 1 || qj > c->nf[1]) continue;
-                        c->A7[row * 7 + slot_of(qi - pi, qj - pj)] += Ae[a][q];
-                    }
-                }
+                scatter_global(c, ci, cj, 3, TRI_V[tri], &Ae[0][0]);
             }
+        }
 }
 
-/* 7 slots per free row: 0 centre, 1 E, 2 W, 3 N, 4 S, 5 NE, 6 SW (row-major [nfree][7]) */
+/* ns slots per free row: 0 centre, 1 E, 2 W, 3 N, 4 S, 5 NE, 6 SW [, 7 NW, 8 SE for Q1] (row-major [nfree][ns]) */
 void orc_global_stencil(orc_ctx *c, zc *out)
 {
     assemble_global(c);
-    memcpy(out, c->A7, sizeof(zc) * 7 * (size_t)c->nfree);
+    memcpy(out, c->A7, sizeof(zc) * c->ns * (size_t)c->nfree);
+}
+
+static const int SDX[9] = { 0, 1, -1, 0, 0, 1, -1, -1, 1 }, SDY[9] = { 0, 0, 0, 1, -1, 1, -1, 1, -1 };
+
+static zc matvec_row(const orc_ctx *c, const zc *x, int64_t row)
+{
+    int nfx = c->nf[0], nfy = c->nf[1];
+    int i = (int)(row % nfx) + 1, j = (int)(row / nfx) + 1;
+    zc acc = 0;
+    for (int s = 0; s < c->ns; s++) {
+        int qi = i + SDX[s], qj = j + SDY[s];
+        if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
+        acc += c->A7[row * c->ns + s] * x[(qi - 1) + (int64_t)nfx * (qj - 1)];
+    }
+    return acc;
 }
 
 /* y = A x (S: matvec; eq. (weak)) */
 void orc_matvec(orc_ctx *c, const zc *x, zc *y)
 {
     assemble_global(c);
-    int nfx = c->nf[0], nfy = c->nf[1];
-    static const int DX[7] = { 0, 1, -1, 0, 0, 1, -1 }, DY[7] = { 0, 0, 0, 1, -1, 1, -1 };
 #pragma omp parallel for schedule(static)
-    for (int j = 1; j <= nfy; j++)
-        for (int i = 1; i <= nfx; i++) {
-            int64_t row = (i - 1) + (int64_t)nfx * (j - 1);
-            zc acc = 0;
-            for (int s = 0; s < 7; s++) {
-                int qi = i + DX[s], qj = j + DY[s];
-                if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
-                acc += c->A7[row * 7 + s] * x[(qi - 1) + (int64_t)nfx * (qj - 1)];
-            }
-            y[row] = acc;
-        }
+    for (int64_t row = 0; row < c->nfree; row++) y[row] = matvec_row(c, x, row);
 }
 
 /* y[rows[r]] = (A x)[rows[r]] for a sample of rows (full-size parity on sampled outputs) */
 void orc_matvec_rows(orc_ctx *c, const zc *x, const int64_t *rows, int nrows, zc *y)
 {
     assemble_global(c);
-    int nfx = c->nf[0], nfy = c->nf[1];
-    static const int DX[7] = { 0, 1, -1, 0, 0, 1, -1 }, DY[7] = { 0, 0, 0, 1, -1, 1, -1 };
-    for (int r = 0; r < nrows; r++) {
-        int64_t row = rows[r];
-        int i = (int)(row % nfx) + 1, j = (int)(row / nfx) + 1;
-        zc acc = 0;
-        for (int s = 0; s < 7; s++) {
-            int qi = i + DX[s], qj = j + DY[s];
-            if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
-            acc += c->A7[row * 7 + s] * x[(qi - 1) + (int64_t)nfx * (qj - 1)];
-        }
-        y[r] = acc;
-    }
+    for (int r = 0; r < nrows; r++) y[r] = matvec_row(c, x, rows[r]);
 }
 
 /* ------------------------------------------------------------------------------------------------
  * Right-hand side (D14): f(x) = sum_s a_s (2 pi sigma^2)^-1 exp(-|x - x_s|^2 / (2 sigma^2)), nodal
- * interpolation at the free nodes, b = M_ff f_I with the consistent P1 mass matrix
+ * interpolation at the free nodes, b = M_ff f_I with the consistent P1 (or Q1) mass matrix
  * (int_T phi_p phi_q = |T| (1 + delta_pq) / 12), assembled element by element.
- * Node (i,j) sits at ((i - ng) h, (j - ng) h).
+ * Node (i,j) sits at ((i - ng) h, (j - ng) h): Omega_int's corner is the origin in the BJ frame, Omega's
+ * corner in the paper frame (ng = 0; the smoothed delta of P:217-218 is one unit-mass Gaussian).
  * ----------------------------------------------------------------------------------------------*/
 void orc_rhs(orc_ctx *c, int nsrc, const double *xy, const zc *amp, double sigma, zc *b)
 {
@@ -374,18 +496,26 @@ void orc_rhs(orc_ctx *c, int nsrc, const double *xy, const zc *amp, double sigma
         }
     memset(b, 0, sizeof(zc) * (size_t)c->nfree);
     for (int cj = 0; cj < c->N[1]; cj++)
-        for (int ci = 0; ci < c->N[0]; ci++)
-            for (int tri = 0; tri < 2; tri++)
-                for (int a = 0; a < 3; a++) {
-                    int pi = ci + TRI_V[tri][a][0], pj = cj + TRI_V[tri][a][1];
+        for (int ci = 0; ci < c->N[0]; ci++) {
+            /* element mass: P1 |T| (1 + delta_pq) / 12 per triangle; Q1 the tensor product of the 1D P1 mass
+               (h/6)[[2,1],[1,2]] (exact, = the 2 x 2 Gauss rule) */
+            int nt = c->p.elem == 1 ? 1 : 2, nv = c->p.elem == 1 ? 4 : 3;
+            for (int tri = 0; tri < nt; tri++)
+                for (int a = 0; a < nv; a++) {
+                    const int *va = c->p.elem == 1 ? Q1_V[a] : TRI_V[tri][a];
+                    int pi = ci + va[0], pj = cj + va[1];
                     if (pi < 1 || pi > nfx || pj < 1 || pj > nfy) continue;
-                    for (int q = 0; q < 3; q++) {
-                        int qi = ci + TRI_V[tri][q][0], qj = cj + TRI_V[tri][q][1];
+                    for (int q = 0; q < nv; q++) {
+                        const int *vq = c->p.elem == 1 ? Q1_V[q] : TRI_V[tri][q];
+                        int qi = ci + vq[0], qj = cj + vq[1];
                         if (qi < 1 || qi > nfx || qj < 1 || qj > nfy) continue;
-                        b[(pi - 1) + (int64_t)nfx * (pj - 1)] +=
-                            area * (a == q ? 2.0 : 1.0) / 12.0 * f[(qi - 1) + (int64_t)nfx * (qj - 1)];
+                        double mq = c->p.elem == 1
+                            ? (h / 6.0) * (va[0] == vq[0] ? 2.0 : 1.0) * (h / 6.0) * (va[1] == vq[1] ? 2.0 : 1.0)
+                            : area * (a == q ? 2.0 : 1.0) / 12.0;
+                        b[(pi - 1) + (int64_t)nfx * (pj - 1)] += mq * f[(qi - 1) + (int64_t)nfx * (qj - 1)];
                     }
                 }
+        }
     free(f);
 }
 
@@ -415,7 +545,24 @@ static void assemble_local(const orc_ctx *c, int j, zc *band)
     int64_t n = (int64_t)mx * my;
     memset(band, 0, sizeof(zc) * (size_t)n * bw);
     for (int cj = s->full_lo[1]; cj < s->full_hi[1]; cj++)
-        for (int ci = s->full_lo[0]; ci < s->full_hi[0]; ci++)
+        for (int ci = s->full_lo[0]; ci < s->full_hi[0]; ci++) {
+            if (c->p.elem == 1) {
+                zc gx[2], dgx[2], gy[2], dgy[2], Ae[4][4];
+                for (int q = 0; q < 2; q++) {
+                    gamma_local_q(c, s, 0, ci, gauss_xi(q), &gx[q], &dgx[q]);
+                    gamma_local_q(c, s, 1, cj, gauss_xi(q), &gy[q], &dgy[q]);
+                }
+                element_matrix_q1(&c->p, gx, dgx, gy, dgy, Ae);
+                for (int a = 0; a < 4; a++) {
+                    int64_t r, col;
+                    if (!local_index(s, ci + Q1_V[a][0], cj + Q1_V[a][1], &r)) continue;
+                    for (int q = 0; q < 4; q++) {
+                        if (!local_index(s, ci + Q1_V[q][0], cj + Q1_V[q][1], &col)) continue;
+                        band[r * bw + (col - r + p)] += Ae[a][q];
+                    }
+                }
+                continue;
+            }
             for (int tri = 0; tri < 2; tri++) {
                 zc gx, dgx, gy, dgy, Ae[3][3];
                 gamma_local(c, s, 0, 3L * ci + TRI_C3[tri][0], &gx, &dgx);
@@ -430,6 +577,7 @@ static void assemble_local(const orc_ctx *c, int j, zc *band)
                     }
                 }
             }
+        }
     if (c->p.local_bc != 1) return;
     /* impedance faces: x = full_lo / full_hi (edges along y) and y = full_lo / full_hi (edges along x) */
     for (int ax = 0; ax < 2; ax++)

@@ -62,3 +62,43 @@ def probe_vector(n: int, seed: int) -> np.ndarray:
     re = rng.standard_normal(n)
     im = rng.standard_normal(n)
     return (re + 1j * im).astype(np.complex128)
+
+
+# ------------------------------------------------------------------------------------------------------------------
+# The paper's own experiment (Tables 1-4): Omega = (0,1)^2 on an n x n grid of Q1
+# cells with n = 2k ("grid 600^2" at k = 300, ~12.6 points per wavelength), global PML of 3 wavelengths with
+# g(x) = 10 k x^3, one smoothed delta at (0.5, 0.5), N = nsub^2 subdomains with `pml` / `ovlp` cells of local PML /
+# overlap as printed in the tables, RAS-PML-Imp, linear-ramp PoU, rtol 1e-10.  Config literals only.
+# ------------------------------------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class PaperConfig:
+    name: str
+    k: float
+    nsub: int
+    pml: int
+    ovlp: int
+    n_cells: int
+    local_bc: int = 1      # 1 = impedance (RAS-PML-Imp), 0 = Dirichlet (RAS-PML-Drch)
+    rtol: float = 1e-10
+    maxit: int = 500
+
+
+PAPER_CONFIGS = {
+    # Table 1 / Table 2 rows (C_kappa = 3/8, C_delta = 1/6)
+    "p300": PaperConfig("p300", 300.0, 2, 8, 4, 600),
+    "p600": PaperConfig("p600", 600.0, 4, 11, 5, 1200),
+    "p1200": PaperConfig("p1200", 1200.0, 8, 15, 6, 2400),
+    "p2400": PaperConfig("p2400", 2400.0, 16, 18, 8, 4800),
+    # Table 4 rows (C_kappa = 1/2, C_delta = 1/6): the paper's timed runs
+    "t300": PaperConfig("t300", 300.0, 2, 12, 4, 600),
+    "t600": PaperConfig("t600", 600.0, 4, 16, 5, 1200),
+    "t1200": PaperConfig("t1200", 1200.0, 8, 21, 6, 2400),
+    "t2400": PaperConfig("t2400", 2400.0, 16, 26, 8, 4800),
+}
+
+
+def paper_source(k: float):
+    """The smoothed delta of P:217-218, f(x) = 16 k^2/pi^3 exp(-16 k^2 |x - x_c|^2 / pi^2), x_c = (0.5, 0.5),
+    written as one unit-mass Gaussian (2 pi s^2)^-1 exp(-|x - x_c|^2 / (2 s^2)) with s = pi / (k sqrt(32)):
+    returns (xy[1,2], amp[1], s) in the frame of Omega = (0,1)^2."""
+    return (np.array([[0.5, 0.5]]), np.array([1.0 + 0.0j]), math.pi / (k * math.sqrt(32.0)))
