@@ -59,9 +59,18 @@ typedef struct {
     int gpu_grid_x, gpu_grid_y;   /* rank grid over the subdomain grid; product == nranks (0,0 => most square) */
     int pou;             /* HELM_POU_OWNER: restricted owner write (D10, the hot path); HELM_POU_RAMP: linear
                             ramps across the overlaps, one rank only, blocks >= 2 delta cells */
+    /* The paper's own workload (D18-D22).  Zero-initialised fields give
+     * the BASELINE.json problem above. */
+    int elem;            /* HELM_ELEM_P1: P1 on the SW->NE split, 7-point stencil (D1); HELM_ELEM_Q1: bilinear
+                            elements, 9-point stencil, 2 x 2 Gauss quadrature of D and beta (D18) */
+    int n_cells;         /* > 0 selects the paper frame (D19): Omega = (0,1)^2 itself is n_cells x n_cells cells and
+                            the global PML lies inside it; ppw, n_pml_global and sigma0 are then unused.  Needs Q1. */
+    double kappa_g;      /* paper frame: global PML width; Omega_int = (kappa_g, 1 - kappa_g)^2 (3 lambda) */
+    double pml_c;        /* paper frame: PML profile g(t) = pml_c t^3 (10 k) */
 } helm_params;
 
 enum { HELM_POU_OWNER = 0, HELM_POU_RAMP = 1 };
+enum { HELM_ELEM_P1 = 0, HELM_ELEM_Q1 = 1 };
 
 typedef struct {
     long long n_free_global;  /* (N-1)^2 */
@@ -79,6 +88,7 @@ typedef struct {
     long long apply_bytes;    /* algorithmic DRAM bytes one helm_precond_apply moves on this rank */
     long long band_bytes;     /* the same operator as band L+U factors + gather + write (SURVEY 8(d) B_apply) */
     long long spmv_bytes;     /* algorithmic bytes of one helm_matvec on this rank */
+    int stencil_slots;        /* coefficients per row of A (helm_export_stencil): 7 (P1) or 9 (Q1) */
 } helm_layout;
 
 typedef struct {
@@ -147,8 +157,9 @@ typedef struct {
 int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rtol, int maxit,
                     helm_richardson_info* info);
 
-/* Parity export: the global operator as 7 slot arrays [7][n_local] (slot order centre, E, W, N, S, NE, SW;
- * a slot pointing at a Dirichlet node is 0).  out_dev: 7 * n_local values. */
+/* Parity export: the global operator as S slot arrays [S][n_local], S = helm_layout.stencil_slots (slot order
+ * centre, E, W, N, S, NE, SW, and for Q1 NW, SE; a slot pointing at a Dirichlet node is 0).  out_dev: S * n_local
+ * values. */
 int helm_export_stencil(helm_ctx* ctx, helm_z* out_dev);
 
 /* Kernel timing of the apply kernel: when enabled, CUDA events bracket every launch of the fused apply

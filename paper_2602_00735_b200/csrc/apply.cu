@@ -84,49 +84,68 @@ __device__ __forceinline__ Step step_of(const SubDesc& d, int s)
     return {PH_U, d.tw + 1 + s};
 }
 
+// A coupling row (L_i or U_i) at node t: r += d v[t] + lo v[t-1] + hi v[t+1].  U_i: d = N, lo = NW, hi = NE;
+// L_i: d = S, lo = SW, hi = SE (NW / SE exist for the 9-point Q1 stencil only, D18; zero for P1).
+struct Cp { z2 d, lo, hi; };
+
 // operands a consumer thread needs for one step, loaded one step ahead
 struct Pre {
     z2 b;         // restricted input b_i[t]      (T, B, Z)
-    z2 c0, c1;    // coupling pair                (T: N,NE  B: S,SW  D: N,NE  U: S,SW  Z: S,SW)
-    z2 c2, c3;    // second pair for Z            (N, NE)
+    Cp c;         // coupling: T, D -> U_i;  B, U, Z -> L_i
+    Cp c2;        // Z: U_i
     z2 yz;        // y_i / z_i from scratch       (D, U)
 };
+
+__device__ __forceinline__ Cp load_upper(const z2* row, int m, int t, bool cst, const ApplyArgs& a)
+{
+    Cp c;
+    c.d = cst ? a.cN : __ldg(row + SL_N * m + t);
+    c.hi = cst ? a.cNE : __ldg(row + SL_NE * m + t);
+    c.lo = a.ns == 9 ? (cst ? a.cNW : __ldg(row + SL_NW * m + t)) : zmk(0, 0);
+    return c;
+}
+__device__ __forceinline__ Cp load_lower(const z2* row, int m, int t, bool cst, const ApplyArgs& a)
+{
+    Cp c;
+    c.d = cst ? a.cS : __ldg(row + SL_S * m + t);
+    c.lo = cst ? a.cSW : __ldg(row + SL_SW * m + t);
+    c.hi = a.ns == 9 ? (cst ? a.cSE : __ldg(row + SL_SE * m + t)) : zmk(0, 0);
+    return c;
+}
+
+// r -= C v (sign < 0) or r += C v, in the fixed order d, lo, hi
+__device__ __forceinline__ void cpl_apply(z2& r, const Cp& c, const z2* v, int t, int m, bool minus)
+{
+    const double s = minus ? -1.0 : 1.0;
+    zfma(r, zmk(s * c.d.x, s * c.d.y), v[t]);
+    if (t > 0) zfma(r, zmk(s * c.lo.x, s * c.lo.y), v[t - 1]);
+    if (t + 1 < m) zfma(r, zmk(s * c.hi.x, s * c.hi.y), v[t + 1]);
+}
 
 __device__ __forceinline__ void prefetch(Pre& p, const SubDesc& d, Step st, int t, const ApplyArgs& a,
                                          const z2* scr)
 {
     if (t >= d.m) return;
-    const z2* row = a.stencil + d.stc_off + (long long)st.i * 7 * d.m;
+    const z2* row = a.stencil + d.stc_off + (long long)st.i * a.ns * d.m;
     if (st.ph <= PH_Z) {
         const long long gi = d.gx0 + t - a.in_i0, gj = d.gy0 + st.i - a.in_j0;
         p.b = __ldg(a.in + gi + a.in_stride * gj);
     }
-    // nodes whose six triangles all have gamma = 1 carry the constant interior couplings: no load
+    // nodes whose cells all have gamma = 1 carry the constant interior couplings: no load
     const bool cst = t >= d.cx0 && t < d.cx1 && st.i >= d.cy0 && st.i < d.cy1;
     // the first step of each chain has no coupling term
     if ((st.ph == PH_T && st.i == d.nb - 1) || (st.ph == PH_B && st.i == 0)) return;
     if (st.ph == PH_Z) {
-        if (st.i > 0) {
-            p.c0 = cst ? a.cS : __ldg(row + SL_S * d.m + t);
-            p.c1 = cst ? a.cSW : __ldg(row + SL_SW * d.m + t);
-        }
-        if (st.i < d.nb - 1) {
-            p.c2 = cst ? a.cN : __ldg(row + SL_N * d.m + t);
-            p.c3 = cst ? a.cNE : __ldg(row + SL_NE * d.m + t);
-        }
+        if (st.i > 0) p.c = load_lower(row, d.m, t, cst, a);
+        if (st.i < d.nb - 1) p.c2 = load_upper(row, d.m, t, cst, a);
         return;
     }
-    if (st.ph == PH_T || st.ph == PH_D) {
-        p.c0 = cst ? a.cN : __ldg(row + SL_N * d.m + t);
-        p.c1 = cst ? a.cNE : __ldg(row + SL_NE * d.m + t);
-    } else {
-        p.c0 = cst ? a.cS : __ldg(row + SL_S * d.m + t);
-        p.c1 = cst ? a.cSW : __ldg(row + SL_SW * d.m + t);
-    }
+    if (st.ph == PH_T || st.ph == PH_D) p.c = load_upper(row, d.m, t, cst, a);
+    else p.c = load_lower(row, d.m, t, cst, a);
     if (st.ph >= PH_D) p.yz = scr[(long long)(st.i - d.lo) * d.m + t];
 }
 
-__global__ void k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
+__device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int slot_bytes)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ring = smem;
@@ -190,38 +209,24 @@ __global__ void k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
             z2 r = zmk(0, 0);
             if (act) {
                 switch (st.ph) {
-                case PH_T:
+                case PH_T:   // b_i - U_i z_{i+1}
                     r = cur.b;
-                    if (st.i < d.nb - 1) {
-                        zfma(r, zmk(-cur.c0.x, -cur.c0.y), vt[t]);
-                        if (t + 1 < m) zfma(r, zmk(-cur.c1.x, -cur.c1.y), vt[t + 1]);
-                    }
+                    if (st.i < d.nb - 1) cpl_apply(r, cur.c, vt, t, m, true);
                     break;
-                case PH_B:
+                case PH_B:   // b_i - L_i y_{i-1}
                     r = cur.b;
-                    if (st.i > 0) {
-                        zfma(r, zmk(-cur.c0.x, -cur.c0.y), vb[t]);
-                        if (t > 0) zfma(r, zmk(-cur.c1.x, -cur.c1.y), vb[t - 1]);
-                    }
+                    if (st.i > 0) cpl_apply(r, cur.c, vb, t, m, true);
                     break;
                 case PH_Z:
                     r = cur.b;
-                    if (st.i > 0) {
-                        zfma(r, zmk(-cur.c0.x, -cur.c0.y), vb[t]);
-                        if (t > 0) zfma(r, zmk(-cur.c1.x, -cur.c1.y), vb[t - 1]);
-                    }
-                    if (st.i < d.nb - 1) {
-                        zfma(r, zmk(-cur.c2.x, -cur.c2.y), vt[t]);
-                        if (t + 1 < m) zfma(r, zmk(-cur.c3.x, -cur.c3.y), vt[t + 1]);
-                    }
+                    if (st.i > 0) cpl_apply(r, cur.c, vb, t, m, true);
+                    if (st.i < d.nb - 1) cpl_apply(r, cur.c2, vt, t, m, true);
                     break;
                 case PH_D:   // U_i x_{i+1}
-                    zfma(r, cur.c0, vb[t]);
-                    if (t + 1 < m) zfma(r, cur.c1, vb[t + 1]);
+                    cpl_apply(r, cur.c, vb, t, m, false);
                     break;
                 default:     // PH_U: L_i x_{i-1}
-                    zfma(r, cur.c0, vt[t]);
-                    if (t > 0) zfma(r, cur.c1, vt[t - 1]);
+                    cpl_apply(r, cur.c, vt, t, m, false);
                     break;
                 }
                 rhs[t] = r;
@@ -293,6 +298,21 @@ __global__ void k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
     }
 }
 
+// One instance per CTA-size class so that the register budget matches the block: m <= 224 (the BASELINE.json
+// configs, m <= 91), m <= 480, m <= 992 (the paper's ~300-400-node-wide subdomains, D21).
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
+{
+    apply_body(a, nc_warps, slot_bytes);
+}
+
+const void* apply_fn(int block)
+{
+    if (block <= 256) return (const void*)k_apply<256>;
+    if (block <= 512) return (const void*)k_apply<512>;
+    return (const void*)k_apply<1024>;
+}
+
 // Ramp-PoU prolongation: z[g] = sum over the <= 2 x 2 subdomains whose chi is positive at
 // g of their weighted local solutions, summed in ascending subdomain index (deterministic).
 // candx / candy: per node index, the (up to) two blocks along that axis, -1 padded.
@@ -335,12 +355,13 @@ int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_by
     *block_threads = 32 * (ncw + 1);
     *slot_bytes = slot_bytes_for(m_max);
     *smem_bytes = NS * *slot_bytes + 2 * NS * 8 + 3 * (32 * ncw + 1) * (int)sizeof(z2);
+    const void* fn = apply_fn(*block_threads);
     int cur = 0;
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, k_apply) == cudaSuccess) cur = fa.maxDynamicSharedSizeBytes;
-    if (*smem_bytes > cur) cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem_bytes);
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) cur = fa.maxDynamicSharedSizeBytes;
+    if (*smem_bytes > cur) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem_bytes);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply, *block_threads, *smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, *block_threads, *smem_bytes);
     *ctas_per_sm = occ;
     return ncw;
 }
@@ -358,10 +379,14 @@ void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_by
 {
     // the dynamic-smem limit is a per-function attribute shared by every context in the process: raise it
     // whenever a context needs more than any earlier one
-    static int smem_set = 0;
-    if (smem > smem_set) {
-        cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        smem_set = smem;
+    static int smem_set[3] = {0, 0, 0};
+    const int cls = block <= 256 ? 0 : (block <= 512 ? 1 : 2);
+    if (smem > smem_set[cls]) {
+        cudaFuncSetAttribute(apply_fn(block), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        smem_set[cls] = smem;
     }
-    k_apply<<<grid, block, smem, s>>>(a, block / 32 - 1, slot_bytes);
+    const int ncw = block / 32 - 1;
+    if (cls == 0) k_apply<256><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
+    else if (cls == 1) k_apply<512><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
+    else k_apply<1024><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
 }

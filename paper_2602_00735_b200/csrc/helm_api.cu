@@ -22,7 +22,7 @@ typedef std::complex<double> cplx;
 namespace {
 
 constexpr int NVMAX = 64;
-constexpr int M_LIMIT = 112;   // factor kernel keeps an m x m complex block in shared memory
+constexpr int M_LIMIT = 992;   // apply CTA: one consumer thread per block row entry, <= 31 consumer warps
 
 int round_half_up(double x) { return (int)floor(x + 0.5); }
 
@@ -39,6 +39,8 @@ std::vector<int> block_starts(int N, int P)
 struct GridInfo {
     int n_int = 0, N = 0, nf = 0, ng = 0, wo = 0, wp = 0;
     double h = 0;
+    int frame = 0, ns = 7;                    // paper frame (D19); stencil slots (7 P1, 9 Q1)
+    double lo_u = 0, hi_u = 0;                // Omega_int in cell units (node 0 at 0)
     int P[2] = {1, 1};
     std::vector<int> st[2];
     int gx = 1, gy = 1, rx = 0, ry = 0;
@@ -51,8 +53,8 @@ struct GridInfo {
 
 int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* err, size_t errlen)
 {
-    if (!(p.k > 0) || p.ppw < 1 || p.n_pml_global < 1 || p.nsub_x < 1 || p.nsub_y < 1 || p.sigma0 < 0) {
-        snprintf(err, errlen, "invalid parameters (k, ppw, n_pml_global, nsub, sigma0)");
+    if (!(p.k > 0) || p.nsub_x < 1 || p.nsub_y < 1 || p.sigma0 < 0) {
+        snprintf(err, errlen, "invalid parameters (k, nsub, sigma0)");
         return HELM_EINVAL;
     }
     if (p.local_bc != HELM_BC_DIRICHLET && p.local_bc != HELM_BC_IMPEDANCE) {
@@ -63,16 +65,42 @@ int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* 
         snprintf(err, errlen, "bad rank %d / %d", rank, nranks);
         return HELM_EINVAL;
     }
-    // O1 / D2: n_int = round(ppw k / 2 pi) cells on (0,1), h = 1 / n_int, N = n_int + 2 n_g
-    G.n_int = round_half_up(p.ppw * p.k / (2.0 * M_PI));
-    if (G.n_int < 1) {
-        snprintf(err, errlen, "k * ppw too small: no interior cell");
+    if (p.elem != HELM_ELEM_P1 && p.elem != HELM_ELEM_Q1) {
+        snprintf(err, errlen, "elem must be HELM_ELEM_P1 or HELM_ELEM_Q1");
         return HELM_EINVAL;
     }
-    G.h = 1.0 / G.n_int;
-    G.ng = p.n_pml_global;
-    G.N = G.n_int + 2 * G.ng;
-    G.nf = G.N - 1;
+    G.ns = p.elem == HELM_ELEM_Q1 ? 9 : 7;
+    if (p.n_cells > 0) {
+        // paper frame (D19): Omega = (0,1)^2 is n_cells^2 cells, Omega_int = (kappa_g, 1 - kappa_g)^2
+        if (p.elem != HELM_ELEM_Q1 || !(p.kappa_g >= 0.0) || !(2.0 * p.kappa_g < 1.0) || !(p.pml_c >= 0.0)) {
+            snprintf(err, errlen, "paper frame needs Q1, 0 <= kappa_g < 1/2 and pml_c >= 0");
+            return HELM_EINVAL;
+        }
+        G.frame = 1;
+        G.N = G.n_int = p.n_cells;
+        G.h = 1.0 / G.N;
+        G.ng = 0;
+        G.nf = G.N - 1;
+        G.lo_u = p.kappa_g / G.h;
+        G.hi_u = (double)G.N - G.lo_u;
+    } else {
+        // O1 / D2: n_int = round(ppw k / 2 pi) cells on (0,1), h = 1 / n_int, N = n_int + 2 n_g
+        if (p.ppw < 1 || p.n_pml_global < 1) {
+            snprintf(err, errlen, "invalid parameters (ppw, n_pml_global)");
+            return HELM_EINVAL;
+        }
+        G.n_int = round_half_up(p.ppw * p.k / (2.0 * M_PI));
+        if (G.n_int < 1) {
+            snprintf(err, errlen, "k * ppw too small: no interior cell");
+            return HELM_EINVAL;
+        }
+        G.h = 1.0 / G.n_int;
+        G.ng = p.n_pml_global;
+        G.N = G.n_int + 2 * G.ng;
+        G.nf = G.N - 1;
+        G.lo_u = G.ng;
+        G.hi_u = G.N - G.ng;
+    }
     // BJ configs[0]: delta = kappa = max(2, round(1.59 ln k)) cells unless given
     const int wdef = std::max(2, round_half_up(1.59 * log(p.k)));
     G.wo = p.n_ovlp < 0 ? wdef : p.n_ovlp;
@@ -241,8 +269,8 @@ struct helm_ctx {
 
     // constant interior stencil (rows with gamma = 1 on all six triangles) and its node range
     int cst[4] = {0, 0, 0, 0};
-    z2 c7[7] = {};
-    z2 lcS{}, lcSW{}, lcN{}, lcNE{};   // constant local couplings (apply)
+    z2 c7[9] = {};
+    z2 lcS{}, lcSW{}, lcN{}, lcNE{}, lcSE{}, lcNW{};   // constant local couplings (apply)
 
     StencilGeom geom_for(int xi0, int xj0, long long xstride) const
     {
@@ -259,7 +287,8 @@ struct helm_ctx {
         s.ci1 = cst[1];
         s.cj0 = cst[2];
         s.cj1 = cst[3];
-        for (int q = 0; q < 7; q++) s.c7[q] = c7[q];
+        s.ns = G.ns;
+        for (int q = 0; q < 9; q++) s.c7[q] = c7[q];
         return s;
     }
     StencilGeom owned_geom() const { return geom_for(G.i0, G.j0, G.i1 - G.i0); }
@@ -318,6 +347,12 @@ int build_layout(helm_ctx* ctx)
     g.ng = G.ng;
     g.lo3 = 3L * G.ng;
     g.hi3 = 3L * (G.N - G.ng);
+    g.elem = ctx->p.elem;
+    g.frame = G.frame;
+    g.lo_u = G.lo_u;
+    g.hi_u = G.hi_u;
+    g.pml_c = ctx->p.pml_c;
+    if (G.frame == 1) g.kappa = ctx->p.kappa_g;
     ctx->n_local = (long long)(G.i1 - G.i0) * (G.j1 - G.j0);
 
     long long fac = 0, stc = 0;
@@ -382,13 +417,14 @@ int build_layout(helm_ctx* ctx)
             d.jlo3 = 3 * int_lo[1];
             d.jhi3 = 3 * int_hi[1];
             d.flags = (has_lo[0] ? 1 : 0) | (has_hi[0] ? 2 : 0) | (has_lo[1] ? 4 : 0) | (has_hi[1] ? 8 : 0);
+            d.ns = G.ns;
             {
-                // constant-coupling node range: cells [max(a_j, n_g), min(b_j, N - n_g)) have local gamma = 1
-                // (inside the int box where g_j = g_i, and inside Omega_int where g_i = 0)
+                // constant-coupling node range: cells [max(a_j, ceil lo_u), min(b_j, floor hi_u)) have local
+                // gamma = 1 (inside the int box where g_j = g_i, and inside Omega_int where g_i = 0)
                 int c0[2], c1[2];
                 for (int ax = 0; ax < 2; ax++) {
-                    const int lo_cell = std::max(has_lo[ax] ? int_lo[ax] : 0, G.ng);
-                    const int hi_cell = std::min(has_hi[ax] ? int_hi[ax] : G.N, G.N - G.ng);
+                    const int lo_cell = std::max(has_lo[ax] ? int_lo[ax] : 0, (int)ceil(G.lo_u));
+                    const int hi_cell = std::min(has_hi[ax] ? int_hi[ax] : G.N, (int)floor(G.hi_u));
                     // nodes with both adjacent cells inside, and all neighbours free in Omega_j
                     c0[ax] = std::max(lo_cell + 1, full_lo[ax] + 2);
                     c1[ax] = std::min(hi_cell, full_hi[ax] - 1);
@@ -407,7 +443,7 @@ int build_layout(helm_ctx* ctx)
                 return set_err(ctx, HELM_ELAYOUT, "subdomain (%d,%d) reaches beyond the halo of rank %d", bx, by,
                                ctx->rank);
             fac += (long long)d.nb * d.m * d.m;
-            stc += (long long)d.nb * 7 * d.m;
+            stc += (long long)d.nb * G.ns * d.m;
             ctx->m_max = std::max(ctx->m_max, d.m);
             const long long n = (long long)d.m * d.nb;
             ctx->max_n = std::max(ctx->max_n, n);
@@ -416,17 +452,19 @@ int build_layout(helm_ctx* ctx)
             // algorithmic bytes of one apply of this subdomain
             const long long nblocks = d.nb + d.hi - d.lo;
             const long long owned = (long long)(d.ohi - d.olo + 1) * (d.hi - d.lo + 1);
-            // coupling vectors loaded per block step (two; four at the twist), except at constant-stencil nodes;
+            // coupling vectors loaded per block step (two, three for Q1; twice that at the twist), except at
+            // constant-stencil nodes;
             // the first step of each chain reads none (T: i = nb-1, B: i = 0)
             long long cpl = 0;
             auto loaded = [&](int i) { return (long long)d.m - ((i >= d.cy0 && i < d.cy1) ? (d.cx1 - d.cx0) : 0); };
+            const int cv = G.ns == 9 ? 3 : 2;                   // vectors per coupling matrix
             for (int i = 0; i < d.nb; i++) {
                 int uses = 0;
-                if (i > d.tw && i < d.nb - 1) uses += 2;        // T: U_i
-                if (i < d.tw && i > 0) uses += 2;               // B: L_i
-                if (i == d.tw) uses += (i > 0 ? 2 : 0) + (i < d.nb - 1 ? 2 : 0);   // Z: L and U
-                if (i < d.tw && i >= d.lo) uses += 2;           // D: U_i
-                if (i > d.tw && i <= d.hi) uses += 2;           // U: L_i
+                if (i > d.tw && i < d.nb - 1) uses += cv;       // T: U_i
+                if (i < d.tw && i > 0) uses += cv;              // B: L_i
+                if (i == d.tw) uses += (i > 0 ? cv : 0) + (i < d.nb - 1 ? cv : 0);   // Z: L and U
+                if (i < d.tw && i >= d.lo) uses += cv;          // D: U_i
+                if (i > d.tw && i <= d.hi) uses += cv;          // U: L_i
                 cpl += uses * loaded(i);
             }
             ctx->apply_bytes += 16 * (nblocks * d.m * d.m       // explicit inverse blocks streamed
@@ -564,6 +602,9 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     a.cSW = ctx->lcSW;
     a.cN = ctx->lcN;
     a.cNE = ctx->lcNE;
+    a.cSE = ctx->lcSE;
+    a.cNW = ctx->lcNW;
+    a.ns = ctx->G.ns;
     a.pou_buf = ctx->d_pou;
     a.delta = ctx->G.wo;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -951,7 +992,7 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     }
     // device buffers: global stencil, local stencils, descriptors
     const int nsub = (int)ctx->subs.size();
-    if ((rc = dalloc(ctx, &ctx->d_A7, 7 * (size_t)ctx->n_local)) || (rc = dalloc(ctx, &ctx->d_stc, ctx->n_stc)) ||
+    if ((rc = dalloc(ctx, &ctx->d_A7, ctx->G.ns * (size_t)ctx->n_local)) || (rc = dalloc(ctx, &ctx->d_stc, ctx->n_stc)) ||
         (rc = dalloc(ctx, &ctx->d_desc, nsub)) || (rc = dalloc(ctx, &ctx->d_order, nsub)) ||
         (rc = dalloc(ctx, &ctx->d_err, 4)) || (rc = dalloc(ctx, &ctx->d_sq, 2)))
         return rc;
@@ -976,18 +1017,20 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     CK(cudaMemcpyAsync(ctx->d_desc, ctx->subs.data(), sizeof(SubDesc) * nsub, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_order, order.data(), sizeof(int) * nsub, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(ctx->d_err, 0, 4 * sizeof(int), ctx->stream));
-    launch_assemble_global(ctx->geom, ctx->d_A7, ctx->G.i0, ctx->G.i1, ctx->G.j0, ctx->G.j1, ctx->stream);
+    launch_assemble_global(ctx->geom, ctx->d_A7, ctx->G.ns, ctx->G.i0, ctx->G.i1, ctx->G.j0, ctx->G.j1, ctx->stream);
     launch_assemble_local(ctx->geom, ctx->d_desc, nsub, ctx->d_stc, (int)ctx->max_n, ctx->stream);
     CK(cudaGetLastError());
     {
-        // constant interior stencil: nodes ng+1 .. N-ng-1 have gamma = 1 on all six triangles; copy the 7
-        // coefficients of one such owned row from A7 so the SpMV fast path is bitwise identical to A7
+        // constant interior stencil: nodes whose cells all lie in Omega_int (ceil lo_u + 1 .. floor hi_u - 1) have
+        // gamma = 1 everywhere around them; copy the coefficients of one such owned row from A so the SpMV fast
+        // path is bitwise identical to A
         const GridInfo& G = ctx->G;
-        const int a = std::max(G.i0, G.ng + 1), b = std::min(G.i1, G.N - G.ng);
-        const int c = std::max(G.j0, G.ng + 1), d = std::min(G.j1, G.N - G.ng);
+        const int clo = (int)ceil(G.lo_u) + 1, chi = (int)floor(G.hi_u);
+        const int a = std::max(G.i0, clo), b = std::min(G.i1, chi);
+        const int c = std::max(G.j0, clo), d = std::min(G.j1, chi);
         if (a < b && c < d) {
             const long long r = (long long)(a - G.i0) + (long long)(G.i1 - G.i0) * (c - G.j0);
-            for (int q = 0; q < 7; q++)
+            for (int q = 0; q < G.ns; q++)
                 CK(cudaMemcpyAsync(&ctx->c7[q], ctx->d_A7 + q * ctx->n_local + r, sizeof(z2), cudaMemcpyDeviceToHost,
                                    ctx->stream));
             CK(cudaStreamSynchronize(ctx->stream));
@@ -1000,10 +1043,10 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
         // has one (all such nodes are computed from gamma = 1 with exact arithmetic: identical bits)
         for (const SubDesc& sd : ctx->subs) {
             if (sd.cx0 >= sd.cx1 || sd.cy0 >= sd.cy1) continue;
-            const z2* row = ctx->d_stc + sd.stc_off + (long long)sd.cy0 * 7 * sd.m + sd.cx0;
-            z2* dst[4] = {&ctx->lcS, &ctx->lcSW, &ctx->lcN, &ctx->lcNE};
-            const int sl[4] = {SL_S, SL_SW, SL_N, SL_NE};
-            for (int q = 0; q < 4; q++)
+            const z2* row = ctx->d_stc + sd.stc_off + (long long)sd.cy0 * sd.ns * sd.m + sd.cx0;
+            z2* dst[6] = {&ctx->lcS, &ctx->lcSW, &ctx->lcN, &ctx->lcNE, &ctx->lcSE, &ctx->lcNW};
+            const int sl[6] = {SL_S, SL_SW, SL_N, SL_NE, SL_SE, SL_NW};
+            for (int q = 0; q < (sd.ns == 9 ? 6 : 4); q++)
                 CK(cudaMemcpyAsync(dst[q], row + sl[q] * sd.m, sizeof(z2), cudaMemcpyDeviceToHost, ctx->stream));
             CK(cudaStreamSynchronize(ctx->stream));
             break;
@@ -1064,7 +1107,8 @@ int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
     out->band_bytes = ctx->band_bytes + 16LL * ctx->n_local;
     // SpMV: x read + y write per row; rows off the constant interior stencil also read 7 coefficients
     const long long ncst = (long long)std::max(0, ctx->cst[1] - ctx->cst[0]) * std::max(0, ctx->cst[3] - ctx->cst[2]);
-    out->spmv_bytes = 16LL * 2 * ctx->n_local + 16LL * 7 * (ctx->n_local - ncst);
+    out->spmv_bytes = 16LL * 2 * ctx->n_local + 16LL * G.ns * (ctx->n_local - ncst);
+    out->stencil_slots = G.ns;
     return HELM_OK;
 }
 
@@ -1190,7 +1234,8 @@ int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int res
 int helm_export_stencil(helm_ctx* ctx, helm_z* out_dev)
 {
     if (!ctx || !out_dev) return set_err(ctx, HELM_EINVAL, "helm_export_stencil: bad arguments");
-    CK(cudaMemcpyAsync(out_dev, ctx->d_A7, sizeof(z2) * 7 * ctx->n_local, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(out_dev, ctx->d_A7, sizeof(z2) * ctx->G.ns * ctx->n_local, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
     return HELM_OK;
 }
 

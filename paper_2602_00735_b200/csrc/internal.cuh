@@ -51,6 +51,10 @@ struct Geom {
     int nf;                           // free nodes per side = N - 1
     int ng;                           // global PML cells per side
     long lo3, hi3;                    // Omega_int = nodes [n_g, N - n_g]  -> 3 n_g, 3 (N - n_g)
+    int elem;                         // HELM_ELEM_P1 / HELM_ELEM_Q1
+    int frame;                        // 0 BJ frame, 1 paper frame (Omega = (0,1)^2, PML inside; D19)
+    double lo_u, hi_u;                // Q1 path: Omega_int in cell units (node 0 at 0), ramps start there
+    double pml_c;                     // paper frame: g(t) = pml_c t^3
 };
 
 // One subdomain as seen by the local operator / factor / apply kernels.
@@ -71,7 +75,7 @@ struct SubDesc {
     int imp;        // impedance faces: bit0 x-lower, bit1 x-upper, bit2 y-lower, bit3 y-upper
     int s0x, s1x;   // block cells [s0, s1) per axis (linear-ramp partition of unity)
     int s0y, s1y;
-    int pad;
+    int ns;         // stencil slots per local row: 7 (P1) or 9 (Q1)
     long long fac_off;   // complex offset of block 0 of the explicit inverses (blocks m x m, column-major)
     long long stc_off;   // complex offset of the local stencil [nb][7][m]
     long long pou_off;   // ramp-PoU mode: offset of this subdomain's weighted solution [lo..hi][olo..ohi]
@@ -88,7 +92,7 @@ __host__ __device__ __forceinline__ double chi_ramp(int x, int s0, int s1, int d
     return 1.0;
 }
 
-enum { SL_C = 0, SL_E = 1, SL_W = 2, SL_N = 3, SL_S = 4, SL_NE = 5, SL_SW = 6 };
+enum { SL_C = 0, SL_E = 1, SL_W = 2, SL_N = 3, SL_S = 4, SL_NE = 5, SL_SW = 6, SL_NW = 7, SL_SE = 8 };
 
 #define HELM_CUDA_OK(expr)                                                                   \
     do {                                                                                     \
@@ -98,11 +102,12 @@ enum { SL_C = 0, SL_E = 1, SL_W = 2, SL_N = 3, SL_S = 4, SL_NE = 5, SL_SW = 6 };
     } while (0)
 
 // kernel launchers (defined in the .cu files)
-void launch_assemble_global(const Geom& g, z2* A7, int i0, int i1, int j0, int j1, cudaStream_t s);
+void launch_assemble_global(const Geom& g, z2* A, int ns, int i0, int i1, int j0, int j1, cudaStream_t s);
 void launch_assemble_local(const Geom& g, const SubDesc* d_desc, int nsub, z2* stencil, int max_n, cudaStream_t s);
 void launch_rhs(const Geom& g, int nsrc, const double* d_xy, const z2* d_amp, double sigma, z2* f_work, z2* b,
                 int i0, int i1, int j0, int j1, cudaStream_t s);
 int factor_smem_bytes(int m_max);
+constexpr int M_SMEM = 112;   // largest block the shared-memory factorisation holds; larger blocks use clusters
 void launch_factor(const SubDesc* d_desc, const SubDesc* h_desc, int nsub, int m_max, const z2* stencil, z2* dinv,
                    int* d_err, cudaStream_t s);
 
@@ -121,6 +126,8 @@ struct ApplyArgs {
     z2* scratch;            // per-CTA [max_rows][m_max]
     long long scratch_per_cta;
     z2 cS, cSW, cN, cNE;    // couplings of the constant interior stencil
+    z2 cSE, cNW;            // ... and the Q1 corner couplings
+    int ns;                 // local stencil slots (7 P1, 9 Q1)
     z2* pou_buf;            // ramp-PoU mode: weighted local solutions (else nullptr: owner write to out)
     int delta;              // overlap width (ramp half-width)
 };
@@ -129,7 +136,7 @@ void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, 
 int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
 
-// owned rows [i0, i0+nx) x [j0, j0+ny) of the 7-point operator; x read from a buffer with origin (xi0, xj0).
+// owned rows [i0, i0+nx) x [j0, j0+ny) of the 7- or 9-point operator; x read from a buffer with origin (xi0, xj0).
 // Rows whose node lies in [ci0, ci1) x [cj0, cj1) -- all six triangles inside Omega_int, gamma = 1 --
 // share one stencil c7 (copied from an assembled interior row, so bitwise equal to A7 there) and skip the
 // seven coefficient loads.
@@ -138,7 +145,8 @@ struct StencilGeom {
     int xi0, xj0;
     long long xstride;
     int ci0, ci1, cj0, cj1;
-    z2 c7[7];
+    int ns;                 // 7 (P1) or 9 (Q1) slots
+    z2 c7[9];
 };
 void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s);
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,

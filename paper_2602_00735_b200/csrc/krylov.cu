@@ -1,4 +1,4 @@
-// krylov.cu -- K5 SpMV (7-point P1 stencil) and the GMRES vector kernels (K6-K8): multi-dot, multi-axpy
+// krylov.cu -- K5 SpMV (7-point P1 / 9-point Q1 stencil) and the GMRES vector kernels (K6-K8): multi-dot, multi-axpy
 // with fused norm, normalisation, basis combination.  All reductions are deterministic: a fixed row
 // partition per CTA, warp-shuffle trees inside a CTA, and a single-CTA pass over the CTA partials in
 // index order (D15).  No floating-point atomics.
@@ -44,11 +44,13 @@ __device__ double block_sum(double v, double* sh)
     return s;
 }
 
-__constant__ int c_dx[7] = { 0, 1, -1, 0, 0, 1, -1 };
-__constant__ int c_dy[7] = { 0, 0, 0, 1, -1, 1, -1 };
+__constant__ int c_dx[9] = { 0, 1, -1, 0, 0, 1, -1, -1, 1 };
+__constant__ int c_dy[9] = { 0, 0, 0, 1, -1, 1, -1, 1, -1 };
 
-// Row r of the owned rectangle (x-fastest): y = sum_s A7[s][r] x(neighbour_s); x is read from a buffer
-// covering the owned rectangle plus whatever ghost frame the caller provides (origin xi0, xj0; stride).
+// Row r of the owned rectangle (x-fastest): y = sum_s A[s][r] x(neighbour_s), NS = 7 (P1) or 9 (Q1) slots; x is
+// read from a buffer covering the owned rectangle plus whatever ghost frame the caller provides (origin xi0,
+// xj0; stride).
+template <int NS>
 __device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* __restrict__ x, long long r,
                                           const StencilGeom& G)
 {
@@ -61,11 +63,11 @@ __device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* _
     if (i >= G.ci0 && i < G.ci1 && j >= G.cj0 && j < G.cj1) {   // constant interior stencil (all neighbours free)
         const z2* xc = x + (i - G.xi0) + G.xstride * (j - G.xj0);
 #pragma unroll
-        for (int s = 0; s < 7; s++) zfma(acc, G.c7[s], __ldg(xc + c_dx[s] + G.xstride * c_dy[s]));
+        for (int s = 0; s < NS; s++) zfma(acc, G.c7[s], __ldg(xc + c_dx[s] + G.xstride * c_dy[s]));
         return acc;
     }
 #pragma unroll
-    for (int s = 0; s < 7; s++) {
+    for (int s = 0; s < NS; s++) {
         const int qi = i + c_dx[s], qj = j + c_dy[s];
         if (qi >= 1 && qi <= G.nf && qj >= 1 && qj <= G.nf)
             zfma(acc, __ldg(A7 + s * n + r), __ldg(x + (qi - G.xi0) + G.xstride * (qj - G.xj0)));
@@ -74,6 +76,7 @@ __device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* _
 }
 
 // 2-D launch: blockIdx.y strides over rows j, x-threads over i (no 64-bit division per row)
+template <int NS>
 __global__ void __launch_bounds__(KT) k_spmv(const z2* __restrict__ A7, const z2* __restrict__ x, z2* __restrict__ y,
                                              StencilGeom G)
 {
@@ -81,11 +84,12 @@ __global__ void __launch_bounds__(KT) k_spmv(const z2* __restrict__ A7, const z2
     if (li >= G.nx) return;
     for (int lj = blockIdx.y; lj < G.ny; lj += gridDim.y) {
         const long long r = li + (long long)G.nx * lj;
-        y[r] = stencil_row(A7, x, r, G);
+        y[r] = stencil_row<NS>(A7, x, r, G);
     }
 }
 
 // r = b - A x, partial[blk] = ||r||^2 over the CTA's rows
+template <int NS>
 __global__ void __launch_bounds__(KT) k_residual(const z2* __restrict__ A7, const z2* __restrict__ x,
                                                  const z2* __restrict__ b, z2* __restrict__ r, StencilGeom G,
                                                  double* __restrict__ partial)
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(KT) k_residual(const z2* __restrict__ A7, cons
     chunk_of(n, r0, r1);
     double s = 0.0;
     for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
-        const z2 v = zsub(__ldg(b + e), stencil_row(A7, x, e, G));
+        const z2 v = zsub(__ldg(b + e), stencil_row<NS>(A7, x, e, G));
         r[e] = v;
         s += zabs2(v);
     }
@@ -345,12 +349,14 @@ void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStr
 {
     const int gx = (G.nx + KT - 1) / KT;
     const int gy = G.ny < 65535 ? G.ny : 65535;
-    k_spmv<<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
+    if (G.ns == 9) k_spmv<9><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
+    else k_spmv<7><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
 }
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s)
 {
-    k_residual<<<nblk, KT, 0, s>>>(A7, x, b, r, G, partial);
+    if (G.ns == 9) k_residual<9><<<nblk, KT, 0, s>>>(A7, x, b, r, G, partial);
+    else k_residual<7><<<nblk, KT, 0, s>>>(A7, x, b, r, G, partial);
 }
 void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,
                       int i0, int i1, int j0, int j1, cudaStream_t s)

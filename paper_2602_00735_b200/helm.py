@@ -26,7 +26,8 @@ HELM_OK, HELM_NOT_CONVERGED, HELM_BREAKDOWN = 0, 2, 3
 class Params(C.Structure):
     _fields_ = [("k", C.c_double), ("ppw", C.c_int), ("n_pml_global", C.c_int), ("sigma0", C.c_double),
                 ("nsub_x", C.c_int), ("nsub_y", C.c_int), ("n_ovlp", C.c_int), ("n_pml", C.c_int),
-                ("local_bc", C.c_int), ("gpu_grid_x", C.c_int), ("gpu_grid_y", C.c_int), ("pou", C.c_int)]
+                ("local_bc", C.c_int), ("gpu_grid_x", C.c_int), ("gpu_grid_y", C.c_int), ("pou", C.c_int),
+                ("elem", C.c_int), ("n_cells", C.c_int), ("kappa_g", C.c_double), ("pml_c", C.c_double)]
 
 
 class Layout(C.Structure):
@@ -35,7 +36,7 @@ class Layout(C.Structure):
                 ("owned_i0", C.c_int), ("owned_i1", C.c_int), ("owned_j0", C.c_int), ("owned_j1", C.c_int),
                 ("n_local", C.c_longlong), ("n_sub", C.c_int), ("n_sub_local", C.c_int), ("m_max", C.c_int),
                 ("local_unknowns", C.c_longlong), ("factor_bytes", C.c_longlong), ("apply_bytes", C.c_longlong),
-                ("band_bytes", C.c_longlong), ("spmv_bytes", C.c_longlong)]
+                ("band_bytes", C.c_longlong), ("spmv_bytes", C.c_longlong), ("stencil_slots", C.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -137,12 +138,25 @@ def _ptr(t) -> int:
 
 BC_DIRICHLET, BC_IMPEDANCE = 0, 1
 POU_OWNER, POU_RAMP = 0, 1
+ELEM_P1, ELEM_Q1 = 0, 1
 
 
 def make_params(k, nsub_x, nsub_y=None, ppw=10, n_pml_global=10, sigma0=5.0, n_ovlp=-1, n_pml=-1,
-                gpu_grid=(0, 0), local_bc=BC_DIRICHLET, pou=POU_OWNER) -> Params:
+                gpu_grid=(0, 0), local_bc=BC_DIRICHLET, pou=POU_OWNER, elem=ELEM_P1, n_cells=0, kappa_g=0.0,
+                pml_c=0.0) -> Params:
     return Params(float(k), ppw, n_pml_global, float(sigma0), nsub_x, nsub_y if nsub_y is not None else nsub_x,
-                  n_ovlp, n_pml, local_bc, gpu_grid[0], gpu_grid[1], pou)
+                  n_ovlp, n_pml, local_bc, gpu_grid[0], gpu_grid[1], pou, elem, n_cells, float(kappa_g),
+                  float(pml_c))
+
+
+def paper_params(k, nsub, pml, ovlp, n_cells=None, local_bc=BC_IMPEDANCE, pou=POU_RAMP, gpu_grid=(0, 0)) -> dict:
+    """Keyword arguments of Context for the paper's own experiment (D18-D22): Q1 on an
+    n x n grid of Omega = (0,1)^2 (n = 2k: "grid 600^2" at k = 300), kappa_g = 3 wavelengths, g(x) = 10 k x^3,
+    nsub^2 subdomains with `pml` / `ovlp` cells, RAS-PML-Imp and the linear-ramp PoU by default."""
+    import math
+    return dict(k=float(k), nsub_x=nsub, nsub_y=nsub, n_ovlp=ovlp, n_pml=pml, local_bc=local_bc, pou=pou,
+                elem=ELEM_Q1, n_cells=int(round(2 * k)) if n_cells is None else int(n_cells),
+                kappa_g=3.0 * 2.0 * math.pi / k, pml_c=10.0 * k, gpu_grid=gpu_grid)
 
 
 def plan_rank(params: Params, rank: int, nranks: int) -> dict:
@@ -180,13 +194,14 @@ class Context:
     def __init__(self, k: float, nsub_x: int, nsub_y: int | None = None, *, ppw: int = 10, n_pml_global: int = 10,
                  sigma0: float = 5.0, n_ovlp: int = -1, n_pml: int = -1, rank: int = 0, nranks: int = 1,
                  gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None, local_bc: int = BC_DIRICHLET,
-                 pou: int = POU_OWNER):
+                 pou: int = POU_OWNER, elem: int = ELEM_P1, n_cells: int = 0, kappa_g: float = 0.0,
+                 pml_c: float = 0.0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libhelm needs a CUDA device (no CPU fallback)")
         self.L = load()
         self.params = make_params(k, nsub_x, nsub_y, ppw, n_pml_global, sigma0, n_ovlp, n_pml, gpu_grid, local_bc,
-                                  pou)
+                                  pou, elem, n_cells, kappa_g, pml_c)
         self.rank, self.nranks = rank, nranks
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._h = C.c_void_p()
@@ -302,9 +317,10 @@ class Context:
 
     def export_stencil(self):
         import torch
-        out = torch.empty(7 * self.n, dtype=torch.complex128, device="cuda")
+        ns = self.layout.stencil_slots
+        out = torch.empty(ns * self.n, dtype=torch.complex128, device="cuda")
         self._check(self.L.helm_export_stencil(self._h, _ptr(out)))
-        return out.view(7, self.n)
+        return out.view(ns, self.n)
 
     def profile(self, on: bool = True):
         self._check(self.L.helm_profile_enable(self._h, int(on)))

@@ -174,7 +174,7 @@ def test_errors():
         ctx.precond_apply(torch.zeros(ctx.n, dtype=torch.complex128, device="cuda"))
     assert e.value.code == -7
     with pytest.raises(HelmError) as e:
-        Context(100.0, 1, 1)                      # one 178-node-wide block: above the 112 limit
+        Context(1600.0, 1, 1)                     # one 2565-node-wide block: above the 992 limit
     assert e.value.code == -1
 
 
