@@ -238,6 +238,8 @@ def run_ours(args):
         "setup_factor_s": setup_s,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_paper:
+        out["paper_table4"] = paper_table4(stream)
     if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, steps=1)
     if rank == 0:
@@ -245,6 +247,50 @@ def run_ours(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+# The paper's timed runs (Table 4: RAS-PML-Imp Richardson to rtol 1e-10, one processor per subdomain;
+# the paper names no hardware).  Context only: another machine, another discretisation code.
+PAPER_TABLE4 = {"t300": {"k": 300, "procs": 4, "iter": 7, "setup_s": 0.95, "solve_s": 0.27, "line": 322},
+                "t600": {"k": 600, "procs": 16, "iter": 14, "setup_s": 1.12, "solve_s": 0.68, "line": 323},
+                "t1200": {"k": 1200, "procs": 64, "iter": 31, "setup_s": 1.40, "solve_s": 1.87, "line": 324}}
+
+
+def paper_table4(stream, names=("t300", "t600")):
+    """The paper's own workload end to end on this GPU: setup (assembly) + factorisation, then Algorithm 1 to 1e-10
+    from u = 0, each timed with CUDA events on the library stream."""
+    import torch
+
+    from paper_2602_00735_b200 import Context
+    from paper_2602_00735_b200.helm import paper_params
+    from paper_2602_00735_b200.workloads import PAPER_CONFIGS, paper_source
+
+    rows = []
+    for name in names:
+        c = PAPER_CONFIGS[name]
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        ctx = Context(**paper_params(c.k, c.nsub, c.pml, c.ovlp, n_cells=c.n_cells, local_bc=c.local_bc),
+                      stream=stream)
+        ctx.factor()
+        ev[1].record(stream)
+        xy, amp, s = paper_source(c.k)
+        b = ctx.rhs(xy, amp, s)
+        ev[2].record(stream)
+        _, info, _ = ctx.richardson(b, rtol=c.rtol, maxit=c.maxit)
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        lay = ctx.layout
+        rows.append({"config": name, "k": c.k, "grid": c.n_cells, "subdomains": c.nsub ** 2, "pml": c.pml,
+                     "ovlp": c.ovlp, "m_max": lay.m_max, "factor_GB": round(lay.factor_bytes / 1e9, 2),
+                     "setup_factor_s": ev[0].elapsed_time(ev[1]) / 1e3, "solve_s": ev[2].elapsed_time(ev[3]) / 1e3,
+                     "iterations": info.iterations, "relres": info.relres,
+                     "paper": PAPER_TABLE4[name]})
+        ctx.close()
+        del ctx, b
+        torch.cuda.empty_cache()
+    return rows
 
 
 def applies_e2e(info, seconds):
@@ -351,6 +397,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-paper", action="store_true", help="skip the paper Table 4 comparison rows")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
