@@ -172,7 +172,7 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
         uint32_t k = 0;
         for (int w = blockIdx.x; w < a.nsub; w += gridDim.x) {
             const SubDesc d = a.desc[a.order[w]];
-            const int kc = slot_bytes / (d.m * (int)sizeof(z2));
+            const int kc = slot_bytes / (d.m * (int)sizeof(z2)) / 4 * 4;
             const int S = nsteps(d);
             for (int s = 0; s < S; s++) {
                 const Step st = step_of(d, s);
@@ -198,7 +198,7 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
         const SubDesc d = a.desc[a.order[w]];
         const int m = d.m;
         const bool act = t < m;
-        const int kc = slot_bytes / (m * (int)sizeof(z2));
+        const int kc = slot_bytes / (m * (int)sizeof(z2)) / 4 * 4;
         const int S = nsteps(d);
         Pre cur, nxt;
         prefetch(cur, d, step_of(d, 0), t, a, scr);
@@ -232,8 +232,10 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
                 rhs[t] = r;
             }
             consumer_bar(nct);
-            // ---- GEMV with the streamed block: acc = Dinv_i rhs
-            z2 acc0 = zmk(0, 0), acc1 = zmk(0, 0);
+            // ---- GEMV with the streamed block: acc = Dinv_i rhs.  Canonical order (shared with k_apply_split):
+            // four partial sums over the columns c = 0, 1, 2, 3 (mod 4), each in increasing c, then (s0+s1)+(s2+s3);
+            // kc is a multiple of 4, so a chunk-relative residue is the global one
+            z2 s0 = zmk(0, 0), s1 = zmk(0, 0), s2 = zmk(0, 0), s3 = zmk(0, 0);
             for (int c0 = 0; c0 < m; c0 += kc, k++) {
                 const int nc = min(kc, m - c0);
                 const uint32_t slot = k % NS, ph = (k / NS) & 1;
@@ -241,17 +243,21 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
                 const z2* col = reinterpret_cast<const z2*>(ring + (size_t)slot * slot_bytes);
                 if (act) {
                     int c = 0;
-#pragma unroll 4
-                    for (; c + 1 < nc; c += 2) {
-                        zfma(acc0, col[(size_t)c * m + t], rhs[c0 + c]);
-                        zfma(acc1, col[(size_t)(c + 1) * m + t], rhs[c0 + c + 1]);
+#pragma unroll 2
+                    for (; c + 3 < nc; c += 4) {
+                        zfma(s0, col[(size_t)c * m + t], rhs[c0 + c]);
+                        zfma(s1, col[(size_t)(c + 1) * m + t], rhs[c0 + c + 1]);
+                        zfma(s2, col[(size_t)(c + 2) * m + t], rhs[c0 + c + 2]);
+                        zfma(s3, col[(size_t)(c + 3) * m + t], rhs[c0 + c + 3]);
                     }
-                    if (c < nc) zfma(acc0, col[(size_t)c * m + t], rhs[c0 + c]);
+                    if (c < nc) zfma(s0, col[(size_t)c * m + t], rhs[c0 + c]);
+                    if (c + 1 < nc) zfma(s1, col[(size_t)(c + 1) * m + t], rhs[c0 + c + 1]);
+                    if (c + 2 < nc) zfma(s2, col[(size_t)(c + 2) * m + t], rhs[c0 + c + 2]);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
             }
-            const z2 acc = zadd(acc0, acc1);
+            const z2 acc = zadd(zadd(s0, s1), zadd(s2, s3));
             // ---- finish the step
             if (act) {
                 z2 x;
@@ -342,8 +348,8 @@ __global__ void k_pou_gather(const SubDesc* __restrict__ desc, const int* __rest
 
 int slot_bytes_for(int m_max)
 {
-    int kc = SLOT_TARGET / (m_max * (int)sizeof(z2));
-    if (kc < 1) kc = 1;
+    int kc = SLOT_TARGET / (m_max * (int)sizeof(z2)) / 4 * 4;   // whole groups of 4 columns (canonical GEMV order)
+    if (kc < 4) kc = 4;
     return kc * m_max * (int)sizeof(z2);
 }
 

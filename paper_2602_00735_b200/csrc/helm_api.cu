@@ -231,6 +231,8 @@ struct helm_ctx {
 
     // apply launch configuration
     int ap_block = 0, ap_smem = 0, ap_slot = 0, ap_grid = 0, ap_occ = 0;
+    // cluster-split apply (few large subdomains): G CTAs per chain, 2G per cluster; 0 = off
+    int sp_G = 0, sp_block = 0, sp_smem = 0, sp_slot = 0, sp_ncw = 0, sp_nss = 0;
 
     // ramp partition of unity: weighted local solutions + per-axis covering blocks
     long long pou_len = 0;
@@ -622,7 +624,16 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
         ctx->ev_free.pop_back();
         CK(cudaEventRecord(e0, ctx->stream));
     }
-    launch_apply(a, ctx->ap_grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->stream);
+    if (ctx->sp_G > 0) {
+        const int e = launch_apply_split(a, (int)ctx->subs.size(), ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
+                                         ctx->sp_ncw, ctx->m_max, ctx->sp_nss, ctx->stream);
+        if (e != 0) {
+            cudaGetLastError();   // the failed launch is reported here, not to the next caller
+            return set_err(ctx, HELM_ECUDA, "cluster apply launch: %s", cudaGetErrorString((cudaError_t)e));
+        }
+    } else {
+        launch_apply(a, ctx->ap_grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->stream);
+    }
     CK(cudaGetLastError());
     ctx->launches++;
     if (ctx->d_pou) {
@@ -1062,7 +1073,38 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     if (ctx->ap_occ < 1) return set_err(ctx, HELM_ECUDA, "apply kernel does not fit on an SM (smem %d)", ctx->ap_smem);
     ctx->ap_grid = std::min(nsub, nsm * ctx->ap_occ);
     ctx->nblk = nsm * 4;
-    if ((rc = dalloc(ctx, &ctx->d_scratch, (size_t)ctx->ap_grid * ctx->scratch_per_cta))) return rc;
+    // Fewer subdomains than SMs (the paper's regime): split every subdomain over a cluster of 2G CTAs (G per chain).
+    // Among the G <= 8 whose clusters are all resident at once, take the smallest that keeps >= 80 % of the SMs
+    // streaming (more G only adds exchange partners), else the largest; each CTA's ring takes the shared memory its
+    // share of an SM leaves.  HELM_SPLIT_G overrides (0 = off).
+    if (nsub < nsm) {
+        int gbest = 0, cbest = 1;
+        const char* env = getenv("HELM_SPLIT_G");
+        const int gforce = env ? atoi(env) : -1;
+        for (int G = 1; G <= 8; G++) {
+            if (gforce >= 0 && G != gforce) continue;
+            const int cps = (nsub * 2 * G + nsm - 1) / nsm;   // CTAs per SM if all are resident
+            int blk, sm, sl, ncw, nss;
+            if (split_configure(ctx->m_max, G, cps, &blk, &sm, &sl, &ncw, &nss)) continue;
+            if (gforce > 0 || max_split_clusters(G, blk, sm) >= nsub) {
+                gbest = G;
+                cbest = cps;
+                if (5 * nsub * 2 * G >= 4 * nsm) break;
+            }
+        }
+        if (gbest > 0 && !split_configure(ctx->m_max, gbest, cbest, &ctx->sp_block, &ctx->sp_smem, &ctx->sp_slot,
+                                          &ctx->sp_ncw, &ctx->sp_nss))
+            ctx->sp_G = gbest;
+        cudaGetLastError();
+    }
+    long long scr = (size_t)ctx->ap_grid * ctx->scratch_per_cta;
+    if (ctx->sp_G > 0) {
+        long long per = 0;
+        for (const SubDesc& sd : ctx->subs) per = std::max(per, (long long)(sd.hi - sd.lo + 1) * ((sd.m + ctx->sp_G - 1) / ctx->sp_G));
+        ctx->scratch_per_cta = per;
+        scr = (long long)nsub * 2 * ctx->sp_G * per;
+    }
+    if ((rc = dalloc(ctx, &ctx->d_scratch, (size_t)scr))) return rc;
     if (ctx->p.pou == HELM_POU_RAMP) {
         // per axis and node index: the (<= 2, ascending) blocks whose ramp chi is positive there
         const GridInfo& G = ctx->G;
@@ -1148,6 +1190,23 @@ int helm_factor(helm_ctx* ctx)
     launch_factor(ctx->d_desc, ctx->subs.data(), (int)ctx->subs.size(), ctx->m_max, ctx->d_stc, ctx->d_dinv,
                   ctx->d_err, ctx->stream);
     CK(cudaGetLastError());
+    if (ctx->sp_G > 1) {
+        // cluster-split apply: relay every inverse block slab-major (one contiguous panel per CTA of a chain)
+        std::vector<int2> blocks;
+        for (int j = 0; j < (int)ctx->subs.size(); j++)
+            for (int i = 0; i < ctx->subs[j].nb; i++) blocks.push_back(make_int2(j, i));
+        int2* d_blocks = nullptr;
+        z2* d_tmp = nullptr;
+        const int grid = 148;
+        const long long per = (long long)ctx->m_max * ctx->m_max;
+        if ((rc = dalloc(ctx, &d_blocks, blocks.size())) || (rc = dalloc(ctx, &d_tmp, (size_t)grid * per))) return rc;
+        CK(cudaMemcpyAsync(d_blocks, blocks.data(), sizeof(int2) * blocks.size(), cudaMemcpyHostToDevice, ctx->stream));
+        launch_relayout(ctx->d_desc, d_blocks, (int)blocks.size(), ctx->d_dinv, d_tmp, per, grid, ctx->sp_G, ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(d_blocks);
+        cudaFree(d_tmp);
+    }
     int herr[4];
     CK(cudaMemcpyAsync(herr, ctx->d_err, sizeof(herr), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "helm.h"
 
 // ---------------------------------------------------------------------------------------------------
@@ -134,6 +136,14 @@ struct ApplyArgs {
 void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int px, const z2* pou_buf, z2* z,
                        int i0, int i1, int j0, int j1, cudaStream_t s);
 int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
+// cluster-split apply for few large subdomains (apply_split.cu)
+int split_configure(int m_max, int G, int ctas_per_sm, int* block_threads, int* smem_bytes, int* slot_bytes, int* ncw,
+                    int* nslots);
+int max_split_clusters(int G, int block, int smem);
+int launch_apply_split(const ApplyArgs& a, int nsub, int G, int block, int smem, int slot_bytes, int ncw, int m_max,
+                       int nslots, cudaStream_t s);
+void launch_relayout(const SubDesc* desc, const int2* blocks, int nblocks, z2* dinv, z2* tmp, long long tmp_per_cta,
+                     int grid, int G, cudaStream_t s);
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
 
 // owned rows [i0, i0+nx) x [j0, j0+ny) of the 7- or 9-point operator; x read from a buffer with origin (xi0, xj0).
