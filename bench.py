@@ -208,6 +208,8 @@ def run_ours(args):
     hbm, peak_src = peaks()
     apply_avg_ms = apply_ms / max(apply_n, 1)
     achieved = lay["apply_bytes"] / (apply_avg_ms / 1e3) / 1e9
+    from paper_2602_00735_b200.helm import probe_read_bandwidth
+    read_peak = probe_read_bandwidth(8 << 30, 5)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k_apply_traffic.json")
     if os.path.exists(prof) and world == 1:
@@ -226,6 +228,7 @@ def run_ours(args):
                      "traffic": traffic, "kernel": "k_apply (fused restrict + twisted block solves + owner write)",
                      "algorithmic_bytes_per_launch": lay["apply_bytes"], "peak_source": peak_src,
                      "band_equivalent_GBps": lay["band_bytes"] / (apply_avg_ms / 1e3) / 1e9,
+                     "read_stream_probe_GBps": read_peak, "frac_of_read_probe": achieved / read_peak,
                      "apply_kernel_ms": apply_avg_ms, "apply_share_of_step": apply_ms / ms},
         "e2e": {"value": applies_e2e(einfo, e2e_s), "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                 "d2h_bytes_per_step": d2h / args.steps, "api": "helm_gmres_host (host b/x, copies inside)"},

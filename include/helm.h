@@ -211,6 +211,12 @@ int helm_nccl_unique_id(void* out128);
 int helm_precond_apply_ext(helm_ctx* ctx, const helm_z* ext_dev, helm_z* z_dev);
 int helm_matvec_ext(helm_ctx* ctx, const helm_z* ext1_dev, helm_z* y_dev);
 
+/* Measurement aid (not part of the method): read bandwidth of the bulk-copy streaming pattern k_apply uses, over a
+ * freshly allocated device buffer of `bytes` (>= 16 MiB, larger than L2 for a meaningful figure), `reps` timed passes
+ * on the legacy default stream.  Synchronous; *gbps = bytes * reps / time.  HELM_ENOMEM if the buffer cannot be
+ * allocated. */
+int helm_probe_read_bandwidth(long long bytes, int reps, double* gbps);
+
 const char* helm_last_error(const helm_ctx* ctx);
 void helm_destroy(helm_ctx* ctx);
 

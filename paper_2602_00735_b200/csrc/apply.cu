@@ -396,3 +396,84 @@ void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_by
     else if (cls == 1) k_apply<512><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
     else k_apply<1024><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
 }
+
+// ---------------------------------------------------------------------------------------------------------------------
+// Read-bandwidth probe (measurement aid for the roofline, not part of the method): the same persistent bulk-copy ring
+// as k_apply streaming a buffer HBM -> shared memory with no arithmetic, so bench.py can quote the attainable
+// read-stream bandwidth beside the measured copy (read + write) peak of MEASURED_PEAKS.json.
+namespace {
+__global__ void k_read_probe(const unsigned char* __restrict__ buf, long long bytes, int chunk, double* sink)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * chunk);
+    uint64_t* empty = full + NS;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < NS; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long nchunks = bytes / chunk;
+    if (tid == 32) {   // producer
+        uint32_t k = 0;
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, k++) {
+            const uint32_t slot = k % NS, ph = (k / NS) & 1;
+            mbar_wait(&empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&full[slot], (uint32_t)chunk);
+            bulk_g2s(smem + (size_t)slot * chunk, buf + c * chunk, (uint32_t)chunk, &full[slot]);
+        }
+    } else if (tid < 32) {   // consumer warp: touch one word per lane of every chunk
+        double acc = 0.0;
+        uint32_t k = 0;
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, k++) {
+            const uint32_t slot = k % NS, ph = (k / NS) & 1;
+            mbar_wait(&full[slot], ph);
+            acc += reinterpret_cast<const double*>(smem + (size_t)slot * chunk)[tid];
+            __syncwarp();
+            if (tid == 0) mbar_arrive(&empty[slot]);
+        }
+        if (acc == 12345.678) *sink = acc;   // keeps the reads live
+    }
+}
+}  // namespace
+
+extern "C" int helm_probe_read_bandwidth(long long bytes, int reps, double* gbps)
+{
+    if (bytes < (1 << 24) || reps < 1 || !gbps) return HELM_EINVAL;
+    const int chunk = 12288;
+    bytes = bytes / chunk * chunk;
+    unsigned char* buf = nullptr;
+    double* sink = nullptr;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return HELM_ENOMEM;
+    }
+    cudaMalloc(&sink, sizeof(double));
+    cudaMemset(buf, 0, bytes);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int smem = NS * chunk + 2 * NS * 8;
+    cudaFuncSetAttribute(k_read_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_read_probe<<<2 * nsm, 64, smem>>>(buf, bytes, chunk, sink);   // warm-up
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; r++) k_read_probe<<<2 * nsm, 64, smem>>>(buf, bytes, chunk, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    cudaFree(sink);
+    if (err != cudaSuccess) return HELM_ECUDA;
+    *gbps = (double)bytes * reps / (ms * 1e-3) / 1e9;
+    return HELM_OK;
+}
