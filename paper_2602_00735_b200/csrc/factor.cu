@@ -18,8 +18,57 @@
 namespace {
 
 constexpr int FT = 512;  // threads per factor CTA
+constexpr int GB = 32;   // Gauss-Jordan panel width
+constexpr int DLD = GB + 1;
 
+// acc -= a * b
+__device__ __forceinline__ void zfms(z2& acc, z2 a, z2 b)
+{
+    acc.x = fma(-a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(-a.x, b.y, acc.y);
+    acc.y = fma(-a.y, b.x, acc.y);
+}
+
+// D (kw x kw, row-major, stride DLD, kw <= 32) <- D^-1 by unpivoted in-place Gauss-Jordan, executed by the first
+// GJW warps of the CTA (lane c owns column c, warp w the rows r = w, w + GJW, ...; named barrier 2 over those warps
+// only).  A zero pivot is recorded as row kb + p.
 __host__ __device__ __forceinline__ int lds_of(int m) { return ((m + 7) / 8) * 8 + 1; }  // 16B-words, = 1 mod 8
+
+constexpr int GJW = 8;
+__device__ __forceinline__ void gj_bar() { asm volatile("bar.sync 2, %0;" ::"r"(GJW * 32) : "memory"); }
+
+__device__ void warp_gj(z2* D, int kw, int kb, int* bad)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int p = 0; p < kw; p++) {
+        const z2 pv = D[p * DLD + p];
+        const bool zero = pv.x == 0.0 && pv.y == 0.0;
+        if (zero && threadIdx.x == 0 && *bad < 0) *bad = kb + p;
+        const z2 inv = zero ? zmk(0, 0) : zinv(pv);
+        z2 rp = lane < kw ? D[p * DLD + lane] : zmk(0, 0);
+        if (lane != p) rp = zmul(rp, inv);                         // row p scaled (pivot column excluded)
+        gj_bar();                                                   // everyone has read row p before it changes
+        if (lane < kw && lane != p) {
+#pragma unroll 4
+            for (int r = w; r < kw; r += GJW)
+                if (r != p) zfms(D[r * DLD + lane], D[r * DLD + p], rp);   // column p is read, never written here
+        }
+        gj_bar();
+        if (w == 0 && lane < kw) {
+            if (lane != p) {
+                const z2 f = D[lane * DLD + p];
+                z2 v = zmk(0, 0);
+                zfms(v, f, inv);
+                D[lane * DLD + p] = v;                               // column p: -D[r][p] / pivot
+                D[p * DLD + lane] = rp;
+            } else {
+                D[p * DLD + p] = inv;
+            }
+        }
+        gj_bar();
+    }
+}
 
 // Couplings of block row i as m x m matrices (7-point P1: two diagonals; 9-point Q1: three):
 //   L_i[a][a] = S_i(a), L_i[a][a-1] = SW_i(a), L_i[a][a+1] = SE_i(a)          (A_{i,i-1})
@@ -109,9 +158,7 @@ __device__ __forceinline__ z2 schur_entry(const SubDesc& d, int i, int mode, con
 
 struct FactorSmem {
     z2* S;      // [m][lds] row-major
-    z2* fcol;   // [m]
-    int* perm;  // [m]
-    int* piv;   // [1]
+    z2* Dk;     // [GB][DLD] inverse of the current pivot block
 };
 
 // mode: 0 bottom chain block, 1 top chain block, 2 twist block
@@ -126,80 +173,112 @@ __device__ void build_block(const SubDesc& d, int i, int mode, const z2* __restr
     __syncthreads();
 }
 
-// In-place Gauss-Jordan inversion with partial row pivoting of S (m x m, row-major, stride ld).
-// Returns (through *err) the first zero pivot row.
-__device__ void gj_invert(int m, FactorSmem sm, int* bad_row)
+// In-place inversion of S (m x m, row-major, stride ld, shared memory) by blocked, unpivoted Gauss-Jordan with panels K
+// of GB columns (natural-order elimination: its pivots are the oracle's no-pivot band-LU pivots, D12):
+//   Dk = S[K,K]^-1 (one warp);  S[K,j] = Dk S[K,j] (j not in K);  S[i,j] -= S[i,K] S[K,j] (i, j not in K);
+//   S[i,K] = -S[i,K] Dk (i not in K);  S[K,K] = Dk.
+// The panel updates are computed into registers (<= RMAX results per thread) and written after a barrier, so they
+// work in place; the trailing update uses 2 x 2 register tiles (rows {ti, ti + hm}, columns {tj, tj + hn}).
+constexpr int RMAX = 8;   // register results per thread in the panel updates: m * GB <= RMAX * FT  (m <= 128)
+
+__device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
 {
     const int ld = lds_of(m);
     z2* S = sm.S;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int k = 0; k < m; k++) {
-        if (warp == 0) {
-            double best = -1.0;
-            int bi = k;
-            for (int r = k + lane; r < m; r += 32) {
-                const double v = zabs2(S[r * ld + k]);
-                if (v > best) { best = v; bi = r; }
+    z2* Dk = sm.Dk;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int hm = (m + 1) / 2;
+    for (int kb = 0; kb < m; kb += GB) {
+        const int kw = min(GB, m - kb);
+        if (tid < GJW * 32) {
+            for (int e = tid; e < kw * kw; e += GJW * 32) {
+                const int r = e / kw, c = e - r * kw;
+                Dk[r * DLD + c] = S[(kb + r) * ld + kb + c];
             }
-            for (int off = 16; off; off >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-            }
-            if (lane == 0) {
-                *sm.piv = bi;
-                sm.perm[k] = bi;
-                if (best == 0.0 && *bad_row < 0) *bad_row = k;
-            }
+            gj_bar();
+            warp_gj(Dk, kw, kb, bad_row);
         }
         __syncthreads();
-        const int p = *sm.piv;
-        if (p != k)
-            for (int c = tid; c < m; c += blockDim.x) {
-                const z2 t = S[k * ld + c];
-                S[k * ld + c] = S[p * ld + c];
-                S[p * ld + c] = t;
+        // ---- row panel: S[K, j] = Dk S[K, j], j not in K  (pairs (r, j), r fastest)
+        {
+            z2 res[RMAX];
+            const int np = kw * m;
+#pragma unroll
+            for (int u = 0; u < RMAX; u++) {
+                const int e = tid + u * nt;
+                if (e < np) {
+                    const int j = e / kw, r = e - j * kw;
+                    if (j < kb || j >= kb + kw) {
+                        z2 v = zmk(0, 0);
+                        for (int q = 0; q < kw; q++) zfma(v, Dk[r * DLD + q], S[(kb + q) * ld + j]);
+                        res[u] = v;
+                    }
+                }
             }
-        __syncthreads();
-        const z2 pv = S[k * ld + k];
-        const z2 inv = (zabs2(pv) > 0.0) ? zinv(pv) : zmk(0, 0);
-        // save column k (multipliers) and zero it; scale row k; pivot entry -> 1/pivot
-        for (int r = tid; r < m; r += blockDim.x) {
-            if (r != k) {
-                sm.fcol[r] = S[r * ld + k];
-                S[r * ld + k] = zmk(0, 0);
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < RMAX; u++) {
+                const int e = tid + u * nt;
+                if (e < np) {
+                    const int j = e / kw, r = e - j * kw;
+                    if (j < kb || j >= kb + kw) S[(kb + r) * ld + j] = res[u];
+                }
             }
+            __syncthreads();
         }
-        for (int c = tid; c < m; c += blockDim.x)
-            if (c != k) S[k * ld + c] = zmul(S[k * ld + c], inv);
-        __syncthreads();
-        if (tid == 0) S[k * ld + k] = inv;
-        __syncthreads();
-        // rank-1 update of every row but k
-        for (int e = tid; e < m * m; e += blockDim.x) {
-            const int r = e / m, c = e % m;
-            if (r == k) continue;
-            const z2 f = sm.fcol[r];
-            const z2 s = S[k * ld + c];
-            z2 v = S[r * ld + c];
-            v.x = fma(-f.x, s.x, v.x);
-            v.x = fma(f.y, s.y, v.x);
-            v.y = fma(-f.x, s.y, v.y);
-            v.y = fma(-f.y, s.x, v.y);
-            S[r * ld + c] = v;
+        // ---- trailing update, 2 x 2 register tiles
+        for (int e = tid; e < hm * hm; e += nt) {
+            const int ti = e / hm, tj = e - ti * hm;
+            const int i0 = ti, i1 = ti + hm, j0 = tj, j1 = tj + hm;
+            const bool ri0 = !(i0 >= kb && i0 < kb + kw), ri1 = i1 < m && !(i1 >= kb && i1 < kb + kw);
+            const bool cj0 = !(j0 >= kb && j0 < kb + kw), cj1 = j1 < m && !(j1 >= kb && j1 < kb + kw);
+            if (!((ri0 || ri1) && (cj0 || cj1))) continue;
+            z2 a00 = S[i0 * ld + j0], a01 = cj1 ? S[i0 * ld + j1] : zmk(0, 0);
+            z2 a10 = ri1 ? S[i1 * ld + j0] : zmk(0, 0), a11 = (ri1 && cj1) ? S[i1 * ld + j1] : zmk(0, 0);
+            const int i1s = i1 < m ? i1 : i0, j1s = j1 < m ? j1 : j0;
+            for (int q = 0; q < kw; q++) {
+                const z2 l0 = S[i0 * ld + kb + q], l1 = S[i1s * ld + kb + q];
+                const z2 u0 = S[(kb + q) * ld + j0], u1 = S[(kb + q) * ld + j1s];
+                zfms(a00, l0, u0);
+                zfms(a01, l0, u1);
+                zfms(a10, l1, u0);
+                zfms(a11, l1, u1);
+            }
+            if (ri0 && cj0) S[i0 * ld + j0] = a00;
+            if (ri0 && cj1) S[i0 * ld + j1] = a01;
+            if (ri1 && cj0) S[i1 * ld + j0] = a10;
+            if (ri1 && cj1) S[i1 * ld + j1] = a11;
         }
         __syncthreads();
-    }
-    // undo the row interchanges as column interchanges, last first
-    for (int k = m - 1; k >= 0; k--) {
-        const int p = sm.perm[k];
-        if (p != k)
-            for (int r = tid; r < m; r += blockDim.x) {
-                const z2 t = S[r * ld + k];
-                S[r * ld + k] = S[r * ld + p];
-                S[r * ld + p] = t;
+        // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K), S[K, K] = Dk  (pairs (i, c), i fastest)
+        {
+            z2 res[RMAX];
+            const int np = kw * m;
+#pragma unroll
+            for (int u = 0; u < RMAX; u++) {
+                const int e = tid + u * nt;
+                if (e < np) {
+                    const int c = e / m, i = e - c * m;
+                    if (i >= kb && i < kb + kw) {
+                        res[u] = Dk[(i - kb) * DLD + c];
+                    } else {
+                        z2 v = zmk(0, 0);
+                        for (int q = 0; q < kw; q++) zfms(v, S[i * ld + kb + q], Dk[q * DLD + c]);
+                        res[u] = v;
+                    }
+                }
             }
-        __syncthreads();
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < RMAX; u++) {
+                const int e = tid + u * nt;
+                if (e < np) {
+                    const int c = e / m, i = e - c * m;
+                    S[i * ld + kb + c] = res[u];
+                }
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -218,9 +297,7 @@ __device__ FactorSmem carve(unsigned char* base, int m)
 {
     FactorSmem sm;
     sm.S = reinterpret_cast<z2*>(base);
-    sm.fcol = sm.S + (size_t)m * lds_of(m);
-    sm.perm = reinterpret_cast<int*>(sm.fcol + m);
-    sm.piv = sm.perm + m;
+    sm.Dk = sm.S + (size_t)m * lds_of(m);
     return sm;
 }
 
@@ -247,14 +324,14 @@ __global__ void __launch_bounds__(FT) k_factor_chains(const SubDesc* __restrict_
     if (chain == 0) {
         for (int i = 0; i < d.tw; i++) {
             build_block(d, i, 0, stc, dinv, sm);
-            gj_invert(d.m, sm, &bad);
+            gj_blocked(d.m, sm, &bad);
             store_block(d, i, sm, dinv);
             report(err, bad, sub, i);
         }
     } else {
         for (int i = d.nb - 1; i > d.tw; i--) {
             build_block(d, i, 1, stc, dinv, sm);
-            gj_invert(d.m, sm, &bad);
+            gj_blocked(d.m, sm, &bad);
             store_block(d, i, sm, dinv);
             report(err, bad, sub, i);
         }
@@ -272,7 +349,7 @@ __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__
     if (threadIdx.x == 0) bad = -1;
     __syncthreads();
     build_block(d, d.tw, 2, stc, dinv, sm);
-    gj_invert(d.m, sm, &bad);
+    gj_blocked(d.m, sm, &bad);
     store_block(d, d.tw, sm, dinv);
     report(err, bad, sub, d.tw);
 }
@@ -289,13 +366,11 @@ __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__
 // Unpivoted elimination in natural order meets exactly the pivots of the oracle's no-pivot band LU (O7, D12), so it
 // breaks down only where the oracle does; a zero pivot is reported like the shared-memory path.
 // ------------------------------------------------------------------------------------------------------------------
-constexpr int BC = 8;      // CTAs per cluster (one cluster per chain)
+constexpr int BCMAX = 16;  // CTAs per cluster (one cluster per chain): 8, or 16 when there are few chains
 constexpr int BT = 256;    // threads per CTA
-constexpr int GB = 32;     // panel width
 constexpr int JT = 32;     // column tile of the trailing update
-constexpr int DLD = GB + 1;
 
-__host__ __device__ __forceinline__ int big_rows(int m) { return (m + BC - 1) / BC; }
+__host__ __device__ __forceinline__ int big_rows(int m, int bc) { return (m + bc - 1) / bc; }
 
 __device__ __forceinline__ void cluster_sync_all()
 {
@@ -310,69 +385,33 @@ __device__ __forceinline__ int cluster_rank()
     return (int)r;
 }
 
-// acc -= a * b
-__device__ __forceinline__ void zfms(z2& acc, z2 a, z2 b)
-{
-    acc.x = fma(-a.x, b.x, acc.x);
-    acc.x = fma(a.y, b.y, acc.x);
-    acc.y = fma(-a.x, b.y, acc.y);
-    acc.y = fma(-a.y, b.x, acc.y);
-}
-
-// Dk (kw x kw, row-major, stride DLD) <- Dk^-1 by unpivoted in-place Gauss-Jordan
-__device__ void small_gj(z2* Dk, int kw, int kb, int* bad)
-{
-    const int tid = threadIdx.x;
-    for (int p = 0; p < kw; p++) {
-        const z2 pv = Dk[p * DLD + p];
-        const bool zero = pv.x == 0.0 && pv.y == 0.0;
-        if (zero && tid == 0 && *bad < 0) *bad = kb + p;
-        const z2 inv = zero ? zmk(0, 0) : zinv(pv);
-        if (tid < kw && tid != p) Dk[p * DLD + tid] = zmul(Dk[p * DLD + tid], inv);   // scale row p
-        __syncthreads();
-        for (int e = tid; e < kw * kw; e += blockDim.x) {                          // rank-1 update off row / col p
-            const int r = e / kw, c = e - r * kw;
-            if (r == p || c == p) continue;
-            zfms(Dk[r * DLD + c], Dk[r * DLD + p], Dk[p * DLD + c]);
-        }
-        __syncthreads();
-        if (tid < kw && tid != p) {                                                 // column p
-            const z2 f = Dk[tid * DLD + p];
-            Dk[tid * DLD + p] = zmk(0, 0);
-            zfms(Dk[tid * DLD + p], f, inv);
-        }
-        if (tid == 0) Dk[p * DLD + p] = inv;
-        __syncthreads();
-    }
-}
-
-// one block of a chain, formed then inverted in place
+// one block of a chain, formed then inverted in place (column-major in its factor slot)
 __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restrict__ stc, z2* __restrict__ dinv, int rk,
-                          z2* Dk, z2* Aik, z2* AKj, int* bad)
+                          int bc, z2* Dk, z2* Aik, z2* AKj, int* bad)
 {
     const int m = d.m, tid = threadIdx.x;
     z2* A = dinv + d.fac_off + (long long)i * m * m;
-    {   // Schur complement, columns split over the cluster
-        const int c0 = (int)(((long long)m * rk) / BC), c1 = (int)(((long long)m * (rk + 1)) / BC);
-        for (long long e = (long long)c0 * m + tid; e < (long long)c1 * m; e += BT) {
-            const int b = (int)(e / m), a = (int)(e - (long long)b * m);
-            A[e] = schur_entry(d, i, mode, stc, dinv, a, b);
-        }
+    const int c0 = (int)(((long long)m * rk) / bc), c1 = (int)(((long long)m * (rk + 1)) / bc);
+    // Schur complement, columns split over the cluster
+    for (long long e = (long long)c0 * m + tid; e < (long long)c1 * m; e += BT) {
+        const int b = (int)(e / m), a = (int)(e - (long long)b * m);
+        A[e] = schur_entry(d, i, mode, stc, dinv, a, b);
     }
     cluster_sync_all();
-    const int R = big_rows(m), r0 = rk * R, r1 = min(m, r0 + R), nr = max(0, r1 - r0);
+    const int R = big_rows(m, bc), r0 = rk * R, r1 = min(m, r0 + R), nr = max(0, r1 - r0);
+    const int hr = (nr + 1) / 2;
     for (int kb = 0; kb < m; kb += GB) {
         const int kw = min(GB, m - kb);
-        // ---- Dk = A[K,K]^-1
+        // ---- Dk = A[K,K]^-1 (every CTA, one warp)
         for (int e = tid; e < kw * kw; e += BT) {
             const int c = e / kw, r = e - c * kw;
             Dk[r * DLD + c] = A[(long long)(kb + c) * m + kb + r];
         }
         __syncthreads();
-        small_gj(Dk, kw, kb, bad);
+        if (tid < GJW * 32) warp_gj(Dk, kw, kb, bad);
+        __syncthreads();
         // ---- row panel: A[K,j] = Dk A[K,j] for this CTA's columns (tiles of BT / GB columns)
         {
-            const int c0 = (int)(((long long)m * rk) / BC), c1 = (int)(((long long)m * (rk + 1)) / BC);
             const int per = BT / GB;
             for (int jt = c0; jt < c1; jt += per) {
                 const int jj = tid / GB, r = tid - jj * GB, j = jt + jj;
@@ -393,7 +432,8 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
             }
         }
         cluster_sync_all();
-        // ---- trailing update of this CTA's row slab [r0, r1)
+        // ---- trailing update of this CTA's row slab [r0, r1): A[i,K] staged in Aik, A[K, tile] in AKj;
+        //      2 x 2 register tiles: rows {ii, ii + hr}, columns {jj, jj + JT/2}
         for (int e = tid; e < nr * kw; e += BT) {
             const int q = e / nr, ii = e - q * nr;
             Aik[ii * DLD + q] = A[(long long)(kb + q) * m + r0 + ii];
@@ -406,20 +446,34 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
                 AKj[q * JT + jj] = A[(long long)(jt + jj) * m + kb + q];
             }
             __syncthreads();
-            for (int e = tid; e < nr * jw; e += BT) {
-                const int jj = e / nr, ii = e - jj * nr;
-                const int row = r0 + ii, j = jt + jj;
-                if (row >= kb && row < kb + kw) continue;
-                z2* dst = A + (long long)j * m + row;
-                z2 v;
-                if (j >= kb && j < kb + kw) {
-                    v = zmk(0, 0);
-                    for (int q = 0; q < kw; q++) zfms(v, Aik[ii * DLD + q], Dk[q * DLD + (j - kb)]);
-                } else {
-                    v = *dst;
-                    for (int q = 0; q < kw; q++) zfms(v, Aik[ii * DLD + q], AKj[q * JT + jj]);
+            for (int e = tid; e < hr * (JT / 2); e += BT) {
+                const int jj = e / hr, ii = e - jj * hr;
+                const int iA = ii, iB = ii + hr, jA = jj, jB = jj + JT / 2;
+                const int rowA = r0 + iA, rowB = r0 + iB, colA = jt + jA, colB = jt + jB;
+                const bool okA = iA < nr && !(rowA >= kb && rowA < kb + kw), okB = iB < nr && !(rowB >= kb && rowB < kb + kw);
+                const bool inA = jA < jw, inB = jB < jw;
+                if (!(okA || okB) || !(inA || inB)) continue;
+                const bool kA = colA >= kb && colA < kb + kw, kB = colB >= kb && colB < kb + kw;   // column panel
+                const int iAs = iA < nr ? iA : iB, iBs = iB < nr ? iB : iA;
+                z2 vAA = zmk(0, 0), vAB = zmk(0, 0), vBA = zmk(0, 0), vBB = zmk(0, 0);
+                if (okA && inA && !kA) vAA = A[(long long)colA * m + rowA];
+                if (okA && inB && !kB) vAB = A[(long long)colB * m + rowA];
+                if (okB && inA && !kA) vBA = A[(long long)colA * m + rowB];
+                if (okB && inB && !kB) vBB = A[(long long)colB * m + rowB];
+                for (int q = 0; q < kw; q++) {
+                    const z2 lA = Aik[iAs * DLD + q], lB = Aik[iBs * DLD + q];
+                    // trailing columns use the new row panel A[K, j]; panel columns use Dk (A[i,K] = -A[i,K] Dk)
+                    const z2 uA = kA ? Dk[q * DLD + (colA - kb)] : AKj[q * JT + jA];
+                    const z2 uB = kB ? Dk[q * DLD + (colB - kb)] : (inB ? AKj[q * JT + jB] : zmk(0, 0));
+                    zfms(vAA, lA, uA);
+                    zfms(vAB, lA, uB);
+                    zfms(vBA, lB, uA);
+                    zfms(vBB, lB, uB);
                 }
-                *dst = v;
+                if (okA && inA) A[(long long)colA * m + rowA] = vAA;
+                if (okA && inB) A[(long long)colB * m + rowA] = vAB;
+                if (okB && inA) A[(long long)colA * m + rowB] = vBA;
+                if (okB && inB) A[(long long)colB * m + rowB] = vBB;
             }
             __syncthreads();
         }
@@ -427,12 +481,12 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
     }
 }
 
-// blockIdx.x / BC = chain: mode 0 -> 2 * sub + (0 bottom | 1 top), mode 2 -> sub (twist block)
+// blockIdx.x / bc = chain: mode 0 -> 2 * sub + (0 bottom | 1 top), mode 2 -> sub (twist block)
 __global__ void __launch_bounds__(BT) k_factor_big(const SubDesc* __restrict__ desc, const z2* __restrict__ stc,
-                                                   z2* __restrict__ dinv, int* err, int mode)
+                                                   z2* __restrict__ dinv, int* err, int mode, int bc)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int rk = cluster_rank(), chain = blockIdx.x / BC;
+    const int rk = cluster_rank(), chain = blockIdx.x / bc;
     const int sub = mode == 0 ? chain >> 1 : chain;
     const SubDesc d = desc[sub];
     z2* Dk = reinterpret_cast<z2*>(smem);
@@ -442,41 +496,43 @@ __global__ void __launch_bounds__(BT) k_factor_big(const SubDesc* __restrict__ d
     if (threadIdx.x == 0) bad = -1;
     __syncthreads();
     if (mode == 2) {
-        big_block(d, d.tw, 2, stc, dinv, rk, Dk, Aik, AKj, &bad);
+        big_block(d, d.tw, 2, stc, dinv, rk, bc, Dk, Aik, AKj, &bad);
         report(err, bad, sub, d.tw);
     } else if ((chain & 1) == 0) {
         for (int i = 0; i < d.tw; i++) {
-            big_block(d, i, 0, stc, dinv, rk, Dk, Aik, AKj, &bad);
+            big_block(d, i, 0, stc, dinv, rk, bc, Dk, Aik, AKj, &bad);
             report(err, bad, sub, i);
         }
     } else {
         for (int i = d.nb - 1; i > d.tw; i--) {
-            big_block(d, i, 1, stc, dinv, rk, Dk, Aik, AKj, &bad);
+            big_block(d, i, 1, stc, dinv, rk, bc, Dk, Aik, AKj, &bad);
             report(err, bad, sub, i);
         }
     }
 }
 
-int big_smem_bytes(int m_max) { return (int)sizeof(z2) * (GB * DLD + GB * JT + big_rows(m_max) * DLD); }
+int big_smem_bytes(int m_max, int bc) { return (int)sizeof(z2) * (GB * DLD + GB * JT + big_rows(m_max, bc) * DLD); }
 
 }  // namespace
 
 int factor_smem_bytes(int m_max)
 {
-    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + m_max) + sizeof(int) * (m_max + 4));
+    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + GB * DLD));
 }
 
 void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, int m_max, const z2* stencil, z2* dinv,
                    int* d_err, cudaStream_t s)
 {
     if (m_max > M_SMEM) {
-        // clusters of BC CTAs: all chains, then all twist blocks
-        const int smem = big_smem_bytes(m_max);
+        // clusters of bc CTAs: all chains, then all twist blocks; 16-CTA clusters when 8-CTA ones leave SMs idle
+        const int bc = 2 * nsub * 8 < 148 ? BCMAX : 8;
+        const int smem = big_smem_bytes(m_max, bc);
         cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (bc > 8) cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = BC;
+        attr[0].val.clusterDim.x = bc;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.blockDim = dim3(BT);
@@ -484,10 +540,10 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
         cfg.stream = s;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        cfg.gridDim = dim3(2 * nsub * BC);
-        cudaLaunchKernelEx(&cfg, k_factor_big, d_desc, stencil, dinv, d_err, 0);
-        cfg.gridDim = dim3(nsub * BC);
-        cudaLaunchKernelEx(&cfg, k_factor_big, d_desc, stencil, dinv, d_err, 2);
+        cfg.gridDim = dim3(2 * nsub * bc);
+        cudaLaunchKernelEx(&cfg, k_factor_big, d_desc, stencil, dinv, d_err, 0, bc);
+        cfg.gridDim = dim3(nsub * bc);
+        cudaLaunchKernelEx(&cfg, k_factor_big, d_desc, stencil, dinv, d_err, 2, bc);
         return;
     }
     const int smem = factor_smem_bytes(m_max);
