@@ -174,7 +174,7 @@ __device__ void build_block(const SubDesc& d, int i, int mode, const z2* __restr
 }
 
 // In-place inversion of S (m x m, row-major, stride ld, shared memory) by blocked, unpivoted Gauss-Jordan with panels K
-// of GB columns (natural-order elimination: its pivots are the oracle's no-pivot band-LU pivots, D12):
+// of GB columns (unpivoted, D12; on the bottom chain the pivots are the oracle's no-pivot band-LU pivots):
 //   Dk = S[K,K]^-1 (one warp);  S[K,j] = Dk S[K,j] (j not in K);  S[i,j] -= S[i,K] S[K,j] (i, j not in K);
 //   S[i,K] = -S[i,K] Dk (i not in K);  S[K,K] = Dk.
 // The panel updates are computed into registers (<= RMAX results per thread) and written after a barrier, so they
@@ -363,8 +363,8 @@ __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__
 //   -- cluster barrier --
 //   A[i,j] -= A[i,K] A[K,j] (i, j not in K);  A[i,K] = -A[i,K] Dk (i not in K)   row slabs per CTA, A[i,K] staged
 //   -- cluster barrier --
-// Unpivoted elimination in natural order meets exactly the pivots of the oracle's no-pivot band LU (O7, D12), so it
-// breaks down only where the oracle does; a zero pivot is reported like the shared-memory path.
+// Unpivoted (D12): on the bottom chain the elimination order is the oracle's no-pivot band LU (O7), so the pivots are
+// the oracle's; a zero pivot is reported like the shared-memory path.
 // ------------------------------------------------------------------------------------------------------------------
 constexpr int BCMAX = 16;  // CTAs per cluster (one cluster per chain): 8, or 16 when there are few chains
 constexpr int BT = 256;    // threads per CTA
