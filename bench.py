@@ -206,6 +206,22 @@ def run_ours(args):
     d2h = 16 * n + sum(16 * (min(j % cfg.restart, cfg.restart - 1) + 2) for j in range(args.steps)) + 8 * (cycles + 1)
 
     hbm, peak_src = peaks()
+
+    # TTS roofline: bytes the solve must move at the kernels' algorithmic rates -- every Arnoldi step j
+    # (0-based within its cycle) moves apply + SpMV + CGS2 16 n (3 (j + 1) + 7) (multidot, fused axpy+dot, multiaxpy,
+    # scale); every cycle end adds the basis combination 16 n (m + 1), one apply, the update and a residual.
+    def tts_bytes(its, restarts):
+        n16 = 16 * ctx.n
+        tot, left = 0, its
+        for _ in range(restarts + 1):
+            m = min(cfg.restart, left)
+            for j in range(m):
+                tot += lay["apply_bytes"] + lay["spmv_bytes"] + n16 * (3 * (j + 1) + 7)
+            tot += n16 * (m + 1) + lay["apply_bytes"] + 3 * n16 + lay["spmv_bytes"] + n16
+            left -= m
+        return tot
+
+    tts_b = tts_bytes(tinfo.iterations, tinfo.restarts)
     apply_avg_ms = apply_ms / max(apply_n, 1)
     achieved = lay["apply_bytes"] / (apply_avg_ms / 1e3) / 1e9
     from paper_2602_00735_b200.helm import probe_read_bandwidth
@@ -237,7 +253,9 @@ def run_ours(args):
         "apply_only": {"ms": apply_only_ms, "applies_per_s": 1e3 / apply_only_ms,
                        "GBps": lay["apply_bytes"] / apply_only_ms / 1e6},
         "gmres_tts": {"seconds": tts_s, "iterations": tinfo.iterations, "restarts": tinfo.restarts,
-                      "relres_true": tinfo.relres_true, "status": tinfo.status, "rtol": cfg.rtol},
+                      "relres_true": tinfo.relres_true, "status": tinfo.status, "rtol": cfg.rtol,
+                      "algorithmic_bytes": tts_b, "roofline_s": tts_b / (hbm * 1e9),
+                      "roofline_frac": tts_b / (hbm * 1e9) / tts_s},
         "setup_factor_s": setup_s,
         "clocks": clk.summary(),
     }
