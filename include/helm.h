@@ -204,6 +204,14 @@ int helm_halo_schedule(const helm_params* params, int rank, int nranks, int widt
 /* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it); HELM_ENCCL without NCCL. */
 int helm_nccl_unique_id(void* out128);
 
+/* Test transport: rank `rank` of an in-process group `group` (>= 0) of `nranks` (2..16) contexts on ONE device, each
+ * driven by its own host thread and stream.  Every collective entry point (apply, matvec, gmres, richardson, the
+ * norms) then runs the full multi-rank code path -- ghost frames, the two-phase halo schedule, reductions -- with the
+ * NCCL calls replaced by device-to-device copies between the group's buffers ordered by host barriers (allreduce sums
+ * the ranks in rank order).  No kernel waits on another.  All ranks of a group must call the same functions in the
+ * same order from concurrent threads; helm_destroy leaves the group. */
+int helm_setup_loopback(const helm_params* params, int rank, int nranks, int group, void* cuda_stream, helm_ctx** out);
+
 /* Communication-free sharded entry points: the caller supplies the input already extended with ghosts.
  * ext_dev covers the plan's ext rectangle (apply) / the owned rectangle grown by one node toward every
  * neighbour (matvec), x-fastest.  Valid on every context, including nranks > 1 contexts created with

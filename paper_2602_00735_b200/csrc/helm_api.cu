@@ -9,6 +9,9 @@
 
 #include <algorithm>
 #include <complex>
+#include <condition_variable>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "internal.cuh"
@@ -202,6 +205,34 @@ int halo_schedule(const GridInfo& G, int width, helm_msg* out, int cap)
     return n;
 }
 
+// In-process loopback transport (helm_setup_loopback): the ranks of a group are contexts in one process, each driven
+// by its own host thread and stream on the same device.  Halo messages and allreduces go through device-to-device
+// copies between the contexts' buffers, ordered by host barriers -- no kernel ever waits on another.  It executes the
+// whole multi-rank code path (packing, schedules, ghost frames, reductions) except the NCCL calls themselves.
+struct LoopGroup {
+    int nranks = 0, members = 0;
+    std::vector<struct helm_ctx*> ctx;
+    std::vector<const double*> slot;   // buffer each rank contributes to the current allreduce
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long gen = 0;
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(mu);
+        const long g = gen;
+        if (++arrived == nranks) {
+            arrived = 0;
+            gen++;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+std::mutex g_loop_mu;
+std::map<int, LoopGroup*> g_loops;
+
 }  // namespace
 
 struct helm_ctx {
@@ -242,6 +273,9 @@ struct helm_ctx {
 
     // multi-rank: ghost-framed buffer (ext rectangle), pack / unpack buffers, communicator
     bool multi = false, has_comm = false;
+    LoopGroup* loop = nullptr;   // loopback transport (tests); nullptr with NCCL
+    int loop_id = -1;
+    double* d_loop_tmp = nullptr;
     z2* d_ext = nullptr;
     long long ext_stride = 0, n_ext = 0;
     z2* d_sendbuf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -515,10 +549,42 @@ int need_comm(helm_ctx* ctx)
 }
 
 // ---------------------------------------------------------------------------------------- collectives
+// loopback: after the phase's messages are packed, copy each peer's send buffer addressed to this rank into the
+// matching receive buffer (the peer's message index is recomputed from its own schedule)
+int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const int* idx, int k)
+{
+    LoopGroup* L = ctx->loop;
+    CK(cudaStreamSynchronize(ctx->stream));
+    L->barrier();   // every rank has packed this phase
+    for (int a = 0; a < k; a++) {
+        const helm_msg& m = msgs[idx[a]];
+        const helm_ctx* peer = L->ctx[m.peer];
+        helm_msg pm[4];
+        const int pn = halo_schedule(peer->G, W, pm, 4);
+        int pa = 0, found = -1, fq = -1;   // position among the peer's phase messages (= its send buffer), index in pm
+        for (int q = 0; q < pn; q++)
+            if (pm[q].phase == phase) {
+                if (pm[q].peer == ctx->rank) {
+                    found = pa;
+                    fq = q;
+                }
+                pa++;
+            }
+        if (found < 0) return set_err(ctx, HELM_ENCCL, "loopback: rank %d has no message for rank %d", m.peer, ctx->rank);
+        const size_t rcnt = (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+        const size_t scnt = (size_t)(pm[fq].send_i1 - pm[fq].send_i0) * (pm[fq].send_j1 - pm[fq].send_j0);
+        if (scnt != rcnt) return set_err(ctx, HELM_ENCCL, "loopback: message size mismatch %zu vs %zu", scnt, rcnt);
+        CK(cudaMemcpyAsync(ctx->d_recvbuf[a], peer->d_sendbuf[found], sizeof(z2) * rcnt, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    L->barrier();   // peers may refill their send buffers
+    return HELM_OK;
+}
+
 // halo exchange of width W on the ghost-framed buffer d_ext (ext rectangle layout)
 int exchange(helm_ctx* ctx, int W)
 {
-#ifdef HELM_HAVE_NCCL
     helm_msg msgs[4];
     const int nm = halo_schedule(ctx->G, W, msgs, 4);
     const GridInfo& G = ctx->G;
@@ -526,22 +592,31 @@ int exchange(helm_ctx* ctx, int W)
         int idx[4], k = 0;
         for (int q = 0; q < nm; q++)
             if (msgs[q].phase == phase) idx[k++] = q;
-        if (!k) continue;
+        if (!k && !ctx->loop) continue;   // (loopback ranks meet at every phase's barriers)
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
             launch_copy_rect(ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], m.send_i0, m.send_j0,
                              m.send_i1 - m.send_i0, m.send_i0, m.send_i1, m.send_j0, m.send_j1, ctx->stream);
             ctx->launches++;
         }
-        NK(ncclGroupStart());
-        for (int a = 0; a < k; a++) {
-            const helm_msg& m = msgs[idx[a]];
-            const size_t scnt = 2 * (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
-            const size_t rcnt = 2 * (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
-            NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
-            NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
+        if (ctx->loop) {
+            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k);
+            if (rc) return rc;
+        } else {
+#ifdef HELM_HAVE_NCCL
+            NK(ncclGroupStart());
+            for (int a = 0; a < k; a++) {
+                const helm_msg& m = msgs[idx[a]];
+                const size_t scnt = 2 * (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
+                const size_t rcnt = 2 * (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+                NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
+                NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
+            }
+            NK(ncclGroupEnd());
+#else
+            return set_err(ctx, HELM_ENCCL, "library built without NCCL");
+#endif
         }
-        NK(ncclGroupEnd());
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
             launch_copy_rect(ctx->d_recvbuf[a], m.recv_i0, m.recv_j0, m.recv_i1 - m.recv_i0, ctx->d_ext, G.e_i0,
@@ -550,16 +625,26 @@ int exchange(helm_ctx* ctx, int W)
         }
     }
     return HELM_OK;
-#else
-    (void)W;
-    return set_err(ctx, HELM_ENCCL, "library built without NCCL");
-#endif
 }
 
 // in-place sum over ranks of `count` doubles on the device
 int allreduce(helm_ctx* ctx, double* buf, size_t count)
 {
     if (!ctx->multi) return HELM_OK;
+    if (ctx->loop) {
+        // loopback: every rank sums all ranks' buffers in rank order (identical bits everywhere)
+        LoopGroup* L = ctx->loop;
+        if (count > 2 * NVMAX) return set_err(ctx, HELM_EINVAL, "loopback allreduce of %zu doubles", count);
+        CK(cudaStreamSynchronize(ctx->stream));
+        L->slot[ctx->rank] = buf;
+        L->barrier();
+        launch_sum_ranks(L->slot.data(), L->nranks, (int)count, ctx->d_loop_tmp, ctx->stream);
+        ctx->launches++;
+        CK(cudaStreamSynchronize(ctx->stream));
+        L->barrier();   // everyone has read everyone's contribution
+        CK(cudaMemcpyAsync(buf, ctx->d_loop_tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+        return HELM_OK;
+    }
 #ifdef HELM_HAVE_NCCL
     NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
     return HELM_OK;
@@ -977,8 +1062,8 @@ int helm_nccl_unique_id(void* out128)
 #endif
 }
 
-int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id, void* cuda_stream,
-               helm_ctx** out)
+static int setup_impl(const helm_params* params, int rank, int nranks, const void* nccl_unique_id, int loop_group,
+                      void* cuda_stream, helm_ctx** out)
 {
     if (!params || !out) return HELM_EINVAL;
     *out = nullptr;
@@ -991,7 +1076,25 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
     int rc = build_layout(ctx);
     if (rc) return rc;
     ctx->multi = nranks > 1;
-    if (ctx->multi && nccl_unique_id) {
+    if (ctx->multi && loop_group >= 0) {
+        std::lock_guard<std::mutex> lk(g_loop_mu);
+        LoopGroup*& L = g_loops[loop_group];
+        if (!L) {
+            L = new LoopGroup();
+            L->nranks = nranks;
+            L->ctx.assign(nranks, nullptr);
+            L->slot.assign(nranks, nullptr);
+        }
+        if (L->nranks != nranks || L->ctx[rank])
+            return set_err(ctx, HELM_EINVAL, "loopback group %d: rank %d of %d already taken or size mismatch", loop_group,
+                           rank, nranks);
+        L->ctx[rank] = ctx;
+        L->members++;
+        ctx->loop = L;
+        ctx->loop_id = loop_group;
+        ctx->has_comm = true;
+        if ((rc = dalloc(ctx, &ctx->d_loop_tmp, 2 * NVMAX))) return rc;
+    } else if (ctx->multi && nccl_unique_id) {
 #ifdef HELM_HAVE_NCCL
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof(id));
@@ -1325,6 +1428,18 @@ int helm_profile_read(helm_ctx* ctx, double* apply_ms, int* apply_launches, int*
     return HELM_OK;
 }
 
+int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id, void* cuda_stream,
+               helm_ctx** out)
+{
+    return setup_impl(params, rank, nranks, nccl_unique_id, -1, cuda_stream, out);
+}
+
+int helm_setup_loopback(const helm_params* params, int rank, int nranks, int group, void* cuda_stream, helm_ctx** out)
+{
+    if (group < 0 || nranks < 2 || nranks > 16) return HELM_EINVAL;
+    return setup_impl(params, rank, nranks, nullptr, group, cuda_stream, out);
+}
+
 const char* helm_last_error(const helm_ctx* ctx) { return ctx ? ctx->err : "null context"; }
 
 void helm_destroy(helm_ctx* ctx)
@@ -1335,6 +1450,16 @@ void helm_destroy(helm_ctx* ctx)
 #ifdef HELM_HAVE_NCCL
     if (ctx->comm) ncclCommDestroy(ctx->comm);
 #endif
+    if (ctx->loop) {
+        std::lock_guard<std::mutex> lk(g_loop_mu);
+        ctx->loop->ctx[ctx->rank] = nullptr;
+        if (--ctx->loop->members == 0) {
+            delete ctx->loop;
+            g_loops.erase(ctx->loop_id);
+        }
+        ctx->loop = nullptr;
+    }
+    if (ctx->d_loop_tmp) cudaFree(ctx->d_loop_tmp);
     void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
                     ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq,

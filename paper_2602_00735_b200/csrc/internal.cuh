@@ -178,4 +178,5 @@ void launch_scale_by_norm(const z2* w, const double* norm, z2* v, long long n, c
 void launch_combine(const z2* V, long long ldv, int nv, const z2* y, z2* t, long long n, cudaStream_t s);
 void launch_axpy(z2* x, const z2* z, long long n, cudaStream_t s);
 void launch_copy(z2* dst, const z2* src, long long n, cudaStream_t s);
+void launch_sum_ranks(const double* const* ptrs, int nranks, int count, double* out, cudaStream_t s);
 void launch_norm_partial(const z2* x, long long n, double* partial, int nblk, cudaStream_t s);

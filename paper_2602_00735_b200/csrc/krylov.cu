@@ -336,6 +336,17 @@ __global__ void __launch_bounds__(KT) k_norm_partial(const z2* __restrict__ x, l
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
+struct RankPtrs { const double* p[16]; };
+// out[i] = sum_r p[r][i] in rank order (loopback allreduce)
+__global__ void k_sum_ranks(RankPtrs ptrs, int nranks, int count, double* __restrict__ out)
+{
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < nranks; r++) s += ptrs.p[r][i];
+        out[i] = s;
+    }
+}
+
 int ew_grid(long long n)
 {
     long long b = (n + KT - 1) / KT;
@@ -406,6 +417,12 @@ void launch_combine(const z2* V, long long ldv, int nv, const z2* y, z2* t, long
     k_combine<<<ew_grid(n), KT, 0, s>>>(V, ldv, nv, y, t, n);
 }
 void launch_axpy(z2* x, const z2* z, long long n, cudaStream_t s) { k_axpy<<<ew_grid(n), KT, 0, s>>>(x, z, n); }
+void launch_sum_ranks(const double* const* ptrs, int nranks, int count, double* out, cudaStream_t s)
+{
+    RankPtrs rp{};
+    for (int r = 0; r < nranks && r < 16; r++) rp.p[r] = ptrs[r];
+    k_sum_ranks<<<1, 128, 0, s>>>(rp, nranks, count, out);
+}
 void launch_copy(z2* dst, const z2* src, long long n, cudaStream_t s) { k_copy<<<ew_grid(n), KT, 0, s>>>(dst, src, n); }
 void launch_norm_partial(const z2* x, long long n, double* partial, int nblk, cudaStream_t s)
 {

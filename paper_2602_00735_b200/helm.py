@@ -78,7 +78,7 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_precond_apply_host", "helm_gmres", "helm_gmres_host", "helm_export_stencil",
            "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy",
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
-           "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth"]
+           "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback"]
 
 
 def lib_path() -> str:
@@ -97,6 +97,7 @@ def load(build_if_missing: bool = True):
     L = C.CDLL(_build.LIB)
     vp, i, d = C.c_void_p, C.c_int, C.c_double
     L.helm_setup.argtypes = [C.POINTER(Params), i, i, vp, vp, C.POINTER(vp)]
+    L.helm_setup_loopback.argtypes = [C.POINTER(Params), i, i, i, vp, C.POINTER(vp)]
     L.helm_get_layout.argtypes = [vp, C.POINTER(Layout)]
     L.helm_rhs.argtypes = [vp, i, vp, vp, d, vp]
     L.helm_factor.argtypes = [vp]
@@ -206,7 +207,7 @@ class Context:
                  sigma0: float = 5.0, n_ovlp: int = -1, n_pml: int = -1, rank: int = 0, nranks: int = 1,
                  gpu_grid=(0, 0), stream=None, nccl_id: bytes | None = None, local_bc: int = BC_DIRICHLET,
                  pou: int = POU_OWNER, elem: int = ELEM_P1, n_cells: int = 0, kappa_g: float = 0.0,
-                 pml_c: float = 0.0):
+                 pml_c: float = 0.0, loopback_group: int | None = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libhelm needs a CUDA device (no CPU fallback)")
@@ -216,9 +217,13 @@ class Context:
         self.rank, self.nranks = rank, nranks
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        rc = self.L.helm_setup(C.byref(self.params), rank, nranks, idbuf, C.c_void_p(self.stream.cuda_stream),
-                               C.byref(self._h))
+        if loopback_group is not None:
+            rc = self.L.helm_setup_loopback(C.byref(self.params), rank, nranks, int(loopback_group),
+                                            C.c_void_p(self.stream.cuda_stream), C.byref(self._h))
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+            rc = self.L.helm_setup(C.byref(self.params), rank, nranks, idbuf, C.c_void_p(self.stream.cuda_stream),
+                                   C.byref(self._h))
         self._check(rc)
         self.layout = self._layout()
         self.n = self.layout.n_local

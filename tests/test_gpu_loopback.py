@@ -1,0 +1,120 @@
+"""The multi-rank code path executed on one GPU through libhelm's loopback transport (helm_setup_loopback): N rank
+contexts in one process, each driven by its own thread and stream, run the collective entry points -- the halo
+exchange of the apply input (width delta + kappa) and of the SpMV input (width 1, corners through the two-phase
+schedule), the CGS2 / norm allreduces of GMRES, the residual norms of Richardson -- with the NCCL calls replaced by
+device copies ordered by host barriers (no kernel waits on another).  Results must equal the single-rank run:
+apply and matvec bitwise (no cross-rank reduction), GMRES / Richardson iterations equal and solutions to 1e-8 (the
+inner products are summed in another order).  SURVEY 8(e).  -m gpu."""
+import itertools
+import threading
+
+import pytest
+
+from paper_2602_00735_b200.workloads import CONFIGS, paper_source, probe_vector, sources
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a B200", allow_module_level=True)
+
+from paper_2602_00735_b200 import Context  # noqa: E402
+from paper_2602_00735_b200.helm import BC_IMPEDANCE, POU_OWNER, paper_params  # noqa: E402
+
+_gid = itertools.count(100)
+
+
+def run_ranks(nranks, fn, timeout=300):
+    """fn(rank) in one thread per rank; returns the results in rank order, re-raises the first error."""
+    res, err = [None] * nranks, [None] * nranks
+
+    def body(r):
+        try:
+            res[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    if any(t.is_alive() for t in th):
+        pytest.fail("loopback ranks did not finish (deadlock?)")
+    for e in err:
+        if e is not None:
+            raise e
+    return res
+
+
+def owned(vec2d, pl):
+    return vec2d[pl["owned_j0"] - 1:pl["owned_j1"] - 1, pl["owned_i0"] - 1:pl["owned_i1"] - 1].contiguous().view(-1)
+
+
+def check_against_single_rank(kw, nranks, gg, b_of, restart=50, rtol=1e-6):
+    ref = Context(**kw)
+    ref.factor()
+    nf = ref.layout.N_cells - 1
+    v = torch.from_numpy(probe_vector(ref.n, 5)).cuda()
+    b = b_of(ref)
+    z_ref, y_ref = ref.precond_apply(v), ref.matvec(v)
+    x_ref, gi_ref, _ = ref.gmres(b, restart=restart, rtol=rtol)
+    xr_ref, ri_ref, _ = ref.richardson(b, rtol=rtol, maxit=200)
+    ref.close()
+    V, B = v.view(nf, nf), b.view(nf, nf)
+    gid = next(_gid)
+    torch.cuda.synchronize()
+
+    def rank(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c = Context(**{**kw, "gpu_grid": gg}, rank=r, nranks=nranks, stream=s, loopback_group=gid)
+            c.factor()
+            pl = c.plan
+            vl, bl = owned(V, pl), owned(B, pl)
+            z, y = c.precond_apply(vl), c.matvec(vl)
+            x, gi, _ = c.gmres(bl, restart=restart, rtol=rtol)
+            xr, ri, _ = c.richardson(bl, rtol=rtol, maxit=200)
+            s.synchronize()
+            out = dict(pl=pl, z=z.clone(), y=y.clone(), x=x.clone(), xr=xr.clone(), gits=gi.iterations,
+                       rits=ri.iterations, gstat=gi.status)
+            c.close()
+            return out
+
+    outs = run_ranks(nranks, rank)
+    Z, Y, X, XR = (torch.full_like(V, complex("nan")) for _ in range(4))
+    for o in outs:
+        pl = o["pl"]
+        sl = (slice(pl["owned_j0"] - 1, pl["owned_j1"] - 1), slice(pl["owned_i0"] - 1, pl["owned_i1"] - 1))
+        shape = (pl["owned_j1"] - pl["owned_j0"], pl["owned_i1"] - pl["owned_i0"])
+        Z[sl], Y[sl] = o["z"].view(shape), o["y"].view(shape)
+        X[sl], XR[sl] = o["x"].view(shape), o["xr"].view(shape)
+    assert torch.equal(Z.view(-1), z_ref) and torch.equal(Y.view(-1), y_ref)
+    assert all(o["gstat"] == 0 for o in outs)
+    assert len({o["gits"] for o in outs}) == 1 and abs(outs[0]["gits"] - gi_ref.iterations) <= 1
+    assert len({o["rits"] for o in outs}) == 1 and outs[0]["rits"] == ri_ref.iterations
+    rel = lambda a, b: float(torch.linalg.norm(a - b) / torch.linalg.norm(b))  # noqa: E731
+    assert rel(X.view(-1), x_ref) <= 1e-8 and rel(XR.view(-1), xr_ref) <= 1e-8
+
+
+def bj_rhs(name):
+    return lambda ctx: ctx.rhs(*sources(CONFIGS[name]))
+
+
+@pytest.mark.parametrize("name,nranks,gg", [("c1", 2, (2, 1)), ("c1", 4, (2, 2)), ("c2", 4, (2, 2)), ("c2", 8, (4, 2)),
+                                            ("c1", 3, (1, 3))])
+def test_loopback_bj(name, nranks, gg):
+    cfg = CONFIGS[name]
+    check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub), nranks, gg, bj_rhs(name))
+
+
+def test_loopback_impedance():
+    cfg = CONFIGS["c1"]
+    check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, local_bc=BC_IMPEDANCE), 2, (2, 1),
+                              bj_rhs("c1"))
+
+
+def test_loopback_paper_q1():
+    """Q1 (9-point SpMV: corner ghosts), cluster factorisation and cluster-split apply per rank."""
+    kw = paper_params(150.0, 4, 6, 3, pou=POU_OWNER)
+    check_against_single_rank(kw, 4, (2, 2), lambda ctx: ctx.rhs(*paper_source(150.0)), rtol=1e-10)
