@@ -225,7 +225,8 @@ def run_ours(args):
     apply_avg_ms = apply_ms / max(apply_n, 1)
     achieved = lay["apply_bytes"] / (apply_avg_ms / 1e3) / 1e9
     from paper_2602_00735_b200.helm import probe_read_bandwidth
-    read_peak = probe_read_bandwidth(8 << 30, 5)
+    read_peak = probe_read_bandwidth(8 << 30, 5, 0)          # chunks interleaved over the CTAs
+    read_streams = probe_read_bandwidth(16 << 30, 5, 1)      # one contiguous stream per CTA, like k_apply
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k_apply_traffic.json")
     if os.path.exists(prof) and world == 1:
@@ -245,6 +246,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": lay["apply_bytes"], "peak_source": peak_src,
                      "band_equivalent_GBps": lay["band_bytes"] / (apply_avg_ms / 1e3) / 1e9,
                      "read_stream_probe_GBps": read_peak, "frac_of_read_probe": achieved / read_peak,
+                     "read_streams_probe_GBps": read_streams, "frac_of_read_streams_probe": achieved / read_streams,
                      "apply_kernel_ms": apply_avg_ms, "apply_share_of_step": apply_ms / ms},
         "e2e": {"value": applies_e2e(einfo, e2e_s), "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                 "d2h_bytes_per_step": d2h / args.steps, "api": "helm_gmres_host (host b/x, copies inside)"},

@@ -224,6 +224,10 @@ int helm_matvec_ext(helm_ctx* ctx, const helm_z* ext1_dev, helm_z* y_dev);
  * on the legacy default stream.  Synchronous; *gbps = bytes * reps / time.  HELM_ENOMEM if the buffer cannot be
  * allocated. */
 int helm_probe_read_bandwidth(long long bytes, int reps, double* gbps);
+/* Same with an access-pattern mode: 0 (the call above) hands chunk c to CTA c mod grid, so all CTAs sweep one narrow
+ * address window together; 1 gives every CTA its own contiguous 1/grid of the buffer -- independent sequential
+ * streams, the pattern of the apply kernel (each CTA streams its own subdomains' factors). */
+int helm_probe_read_bandwidth_mode(long long bytes, int reps, int mode, double* gbps);
 
 const char* helm_last_error(const helm_ctx* ctx);
 void helm_destroy(helm_ctx* ctx);

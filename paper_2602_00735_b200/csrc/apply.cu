@@ -402,7 +402,9 @@ void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_by
 // as k_apply streaming a buffer HBM -> shared memory with no arithmetic, so bench.py can quote the attainable
 // read-stream bandwidth beside the measured copy (read + write) peak of MEASURED_PEAKS.json.
 namespace {
-__global__ void k_read_probe(const unsigned char* __restrict__ buf, long long bytes, int chunk, double* sink)
+// mode 0: chunk c goes to CTA c mod grid (all CTAs sweep one narrow address window together);
+// mode 1: CTA b streams its own contiguous 1/grid of the buffer (independent sequential streams, as k_apply does)
+__global__ void k_read_probe(const unsigned char* __restrict__ buf, long long bytes, int chunk, double* sink, int mode)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * chunk);
@@ -417,9 +419,13 @@ __global__ void k_read_probe(const unsigned char* __restrict__ buf, long long by
     }
     __syncthreads();
     const long long nchunks = bytes / chunk;
+    const long long per = (nchunks + gridDim.x - 1) / gridDim.x;
+    const long long c_begin = mode ? blockIdx.x * per : blockIdx.x;
+    const long long c_end = mode ? min(nchunks, c_begin + per) : nchunks;
+    const long long c_step = mode ? 1 : gridDim.x;
     if (tid == 32) {   // producer
         uint32_t k = 0;
-        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, k++) {
+        for (long long c = c_begin; c < c_end; c += c_step, k++) {
             const uint32_t slot = k % NS, ph = (k / NS) & 1;
             mbar_wait(&empty[slot], ph ^ 1);
             mbar_arrive_expect_tx(&full[slot], (uint32_t)chunk);
@@ -428,7 +434,7 @@ __global__ void k_read_probe(const unsigned char* __restrict__ buf, long long by
     } else if (tid < 32) {   // consumer warp: touch one word per lane of every chunk
         double acc = 0.0;
         uint32_t k = 0;
-        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, k++) {
+        for (long long c = c_begin; c < c_end; c += c_step, k++) {
             const uint32_t slot = k % NS, ph = (k / NS) & 1;
             mbar_wait(&full[slot], ph);
             acc += reinterpret_cast<const double*>(smem + (size_t)slot * chunk)[tid];
@@ -442,7 +448,12 @@ __global__ void k_read_probe(const unsigned char* __restrict__ buf, long long by
 
 extern "C" int helm_probe_read_bandwidth(long long bytes, int reps, double* gbps)
 {
-    if (bytes < (1 << 24) || reps < 1 || !gbps) return HELM_EINVAL;
+    return helm_probe_read_bandwidth_mode(bytes, reps, 0, gbps);
+}
+
+extern "C" int helm_probe_read_bandwidth_mode(long long bytes, int reps, int mode, double* gbps)
+{
+    if (bytes < (1 << 24) || reps < 1 || !gbps || mode < 0 || mode > 1) return HELM_EINVAL;
     const int chunk = 12288;
     bytes = bytes / chunk * chunk;
     unsigned char* buf = nullptr;
@@ -461,9 +472,9 @@ extern "C" int helm_probe_read_bandwidth(long long bytes, int reps, double* gbps
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    k_read_probe<<<2 * nsm, 64, smem>>>(buf, bytes, chunk, sink);   // warm-up
+    k_read_probe<<<2 * nsm, 64, smem>>>(buf, bytes, chunk, sink, mode);   // warm-up
     cudaEventRecord(e0);
-    for (int r = 0; r < reps; r++) k_read_probe<<<2 * nsm, 64, smem>>>(buf, bytes, chunk, sink);
+    for (int r = 0; r < reps; r++) k_read_probe<<<2 * nsm, 64, smem>>>(buf, bytes, chunk, sink, mode);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0.f;

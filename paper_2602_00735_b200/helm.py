@@ -78,7 +78,8 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_precond_apply_host", "helm_gmres", "helm_gmres_host", "helm_export_stencil",
            "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy",
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
-           "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback"]
+           "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
+           "helm_probe_read_bandwidth_mode"]
 
 
 def lib_path() -> str:
@@ -116,6 +117,7 @@ def load(build_if_missing: bool = True):
     L.helm_matvec_ext.argtypes = [vp, vp, vp]
     L.helm_richardson.argtypes = [vp, vp, vp, d, i, C.POINTER(RichardsonInfo)]
     L.helm_probe_read_bandwidth.argtypes = [C.c_longlong, i, C.POINTER(d)]
+    L.helm_probe_read_bandwidth_mode.argtypes = [C.c_longlong, i, i, C.POINTER(d)]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
     L.helm_destroy.argtypes = [vp]
@@ -181,11 +183,12 @@ def halo_schedule(params: Params, rank: int, nranks: int, width: int) -> list:
     return [msgs[q].as_dict() for q in range(n)]
 
 
-def probe_read_bandwidth(nbytes: int = 8 << 30, reps: int = 5) -> float:
-    """GB/s of libhelm's bulk-copy read stream over an nbytes device buffer (roofline context for bench.py)."""
+def probe_read_bandwidth(nbytes: int = 8 << 30, reps: int = 5, mode: int = 0) -> float:
+    """GB/s of libhelm's bulk-copy read stream over an nbytes device buffer (roofline context for bench.py);
+    mode 0 interleaved chunks, mode 1 one contiguous stream per CTA (the apply's pattern)."""
     L = load()
     g = C.c_double()
-    rc = L.helm_probe_read_bandwidth(int(nbytes), int(reps), C.byref(g))
+    rc = L.helm_probe_read_bandwidth_mode(int(nbytes), int(reps), int(mode), C.byref(g))
     if rc != 0:
         raise HelmError(rc, "helm_probe_read_bandwidth")
     return g.value
