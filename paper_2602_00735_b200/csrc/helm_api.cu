@@ -441,7 +441,10 @@ int build_layout(helm_ctx* ctx)
                 d.lo = std::max(own_lo[1], 1) - d.gy0;
                 d.hi = std::min(own_hi[1], G.N) - 1 - d.gy0;
             }
-            d.tw = (d.lo + d.hi) / 2;
+            // twist row: any row in [lo, hi] gives the same nb + hi - lo streamed blocks; this one
+            // balances the two chains' step counts (bottom: 2 tw - lo + 1, top: nb - 1 + hi - 2 tw + 1), which is the
+            // critical path when the chains run concurrently (k_apply_split)
+            d.tw = std::min(d.hi, std::max(d.lo, (d.nb - 1 + d.hi + d.lo + 2) / 4));
             d.s0x = own_lo[0];
             d.s1x = own_hi[0];
             d.s0y = own_lo[1];
