@@ -135,3 +135,44 @@ def test_two_phase_exchange_over_gloo(nranks):
     for pr in procs:
         pr.join(timeout=60)
     assert all(res[r] for r in range(nranks)), res
+
+
+@pytest.mark.parametrize("k,nsub,nranks", CASES)
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("W", [0, 1])
+def test_exact_communication_counts(k, nsub, nranks, bc, W):
+    """SURVEY 4.2 T3 (S:525 adapted): the elements a rank receives in one exchange equal the area of its ghost frame
+    exactly -- the two phases neither miss nor double-count a node (corners arrive once, in phase 1) -- and every
+    element sent is received."""
+    p = make_params(k, nsub, local_bc=bc)
+    sent = recv = 0
+    for r in range(nranks):
+        pl = plan_rank(p, r, nranks)
+        lo, hi = (pl["halo_lo"], pl["halo_hi"]) if W == 0 else (W, W)
+        nb = pl["nbr"]
+        fw = (pl["owned_i1"] - pl["owned_i0"]) + (lo if nb[0] >= 0 else 0) + (hi if nb[1] >= 0 else 0)
+        fh = (pl["owned_j1"] - pl["owned_j0"]) + (lo if nb[2] >= 0 else 0) + (hi if nb[3] >= 0 else 0)
+        frame = fw * fh - (pl["owned_i1"] - pl["owned_i0"]) * (pl["owned_j1"] - pl["owned_j0"])
+        msgs = halo_schedule(p, r, nranks, W)
+        got = sum((m["recv_i1"] - m["recv_i0"]) * (m["recv_j1"] - m["recv_j0"]) for m in msgs)
+        assert got == frame
+        recv += got
+        sent += sum((m["send_i1"] - m["send_i0"]) * (m["send_j1"] - m["send_j0"]) for m in msgs)
+    assert sent == recv
+
+
+@pytest.mark.parametrize("nranks,gg", [(2, (2, 1)), (4, (2, 2)), (8, (4, 2))])
+def test_paper_frame_plans(nranks, gg):
+    """The paper's Q1 frame (k = 600, grid 1200^2, 4 x 4 subdomains, pml 11 / ovlp 5, Imp): owned rectangles partition
+    the free nodes and the ghost frames are covered exactly."""
+    from paper_2602_00735_b200.helm import paper_params
+    kw = paper_params(600.0, 4, 11, 5, gpu_grid=gg)
+    p = make_params(kw["k"], 4, 4, n_ovlp=5, n_pml=11, gpu_grid=gg, local_bc=kw["local_bc"], pou=0, elem=kw["elem"],
+                    n_cells=kw["n_cells"], kappa_g=kw["kappa_g"], pml_c=kw["pml_c"])
+    nf = kw["n_cells"] - 1
+    cover = np.zeros((nf + 2, nf + 2), int)
+    for r in range(nranks):
+        pl = plan_rank(p, r, nranks)
+        cover[pl["owned_j0"]:pl["owned_j1"], pl["owned_i0"]:pl["owned_i1"]] += 1
+        assert pl["halo_lo"] == 5 + 11 - 1 + 1 and pl["halo_hi"] == 5 + 11 + 1   # Imp: face nodes are unknowns
+    assert np.all(cover[1:nf + 1, 1:nf + 1] == 1) and cover.sum() == nf * nf
