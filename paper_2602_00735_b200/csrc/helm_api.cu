@@ -14,7 +14,15 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
+
+// NVTX ranges (host-side, zero cost without a tool attached): setup, factor, apply, spmv, gmres, orth, comm
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 #ifdef HELM_HAVE_NCCL
 #include <nccl.h>
@@ -588,6 +596,7 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
 // halo exchange of width W on the ghost-framed buffer d_ext (ext rectangle layout)
 int exchange(helm_ctx* ctx, int W)
 {
+    NvtxRange nv_(W == 0 ? "helm.comm.halo_apply" : "helm.comm.halo_spmv");
     helm_msg msgs[4];
     const int nm = halo_schedule(ctx->G, W, msgs, 4);
     const GridInfo& G = ctx->G;
@@ -634,6 +643,7 @@ int exchange(helm_ctx* ctx, int W)
 int allreduce(helm_ctx* ctx, double* buf, size_t count)
 {
     if (!ctx->multi) return HELM_OK;
+    NvtxRange nv_("helm.comm.allreduce");
     if (ctx->loop) {
         // loopback: every rank sums all ranks' buffers in rank order (identical bits everywhere)
         LoopGroup* L = ctx->loop;
@@ -740,6 +750,7 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
 // z = B^-1 r for an owned input vector (exchanging the halo when sharded)
 int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
 {
+    NvtxRange nv_("helm.apply");
     int rc;
     if ((rc = need_comm(ctx))) return rc;
     if (!ctx->multi) return apply_raw(ctx, r, ctx->G.i0, ctx->G.j0, ctx->G.i1 - ctx->G.i0, z);
@@ -750,6 +761,7 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
 // y = A x for an owned input vector
 int spmv_impl(helm_ctx* ctx, const z2* x, z2* y)
 {
+    NvtxRange nv_("helm.spmv");
     int rc;
     if ((rc = need_comm(ctx))) return rc;
     if (!ctx->multi) {
@@ -815,6 +827,7 @@ int residual_host(helm_ctx* ctx, const z2* b, const z2* x, z2* r, double* out)
 // re-orthogonalisation pass (CGS2) on the device, Givens rotations on the host.
 int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int maxit, helm_gmres_info* info)
 {
+    NvtxRange nv_("helm.gmres");
     if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "gmres before helm_factor");
     if (restart < 1 || restart + 1 > NVMAX || maxit < 0)
         return set_err(ctx, HELM_EINVAL, "restart must be in [1, %d], maxit >= 0", NVMAX - 1);
@@ -866,6 +879,8 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             its++;
             // CGS2: h1 = V^H w; w -= V h1; h2 = V^H w; w -= V h2; H(:,j) = h1 + h2; H(j+1,j) = ||w||
             // (the first update and the second projection share one sweep over V: k_axpy_dot)
+            {
+            NvtxRange nv_o("helm.orth");
             launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
             launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h1, nullptr, nullptr, s);
             if ((rc = allreduce(ctx, (double*)ctx->d_h1, 2 * (size_t)(j + 1)))) return rc;
@@ -883,6 +898,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             if ((rc = finish_norm(ctx, ctx->d_Hcol + j + 1))) return rc;
             launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
             ctx->launches++;
+            }
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_Hcol, sizeof(z2) * (j + 2), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -959,6 +975,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
 // Algorithm 1: u <- u + B^-1 (b - A u)
 int richardson_impl(helm_ctx* ctx, const z2* b, z2* x, double rtol, int maxit, helm_richardson_info* info)
 {
+    NvtxRange nv_("helm.richardson");
     if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "richardson before helm_factor");
     if (maxit < 0) return set_err(ctx, HELM_EINVAL, "maxit >= 0");
     int rc;
@@ -1068,6 +1085,7 @@ int helm_nccl_unique_id(void* out128)
 static int setup_impl(const helm_params* params, int rank, int nranks, const void* nccl_unique_id, int loop_group,
                       void* cuda_stream, helm_ctx** out)
 {
+    NvtxRange nv_("helm.setup");
     if (!params || !out) return HELM_EINVAL;
     *out = nullptr;
     helm_ctx* ctx = new helm_ctx();
@@ -1288,6 +1306,7 @@ int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_h
 
 int helm_factor(helm_ctx* ctx)
 {
+    NvtxRange nv_("helm.factor");
     if (!ctx) return HELM_EINVAL;
     if (ctx->factored) return HELM_OK;
     int rc;
