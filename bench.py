@@ -263,6 +263,7 @@ def run_ours(args):
     }
     if world == 1 and not args.no_paper:
         out["paper_table4"] = paper_table4(stream)
+        out["gmres_tts_ramp_pou"] = ramp_pou_tts(cfg, stream, xy, amp, sig)
     if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, steps=1)
     if rank == 0:
@@ -314,6 +315,34 @@ def paper_table4(stream, names=("t300", "t600")):
         del ctx, b
         torch.cuda.empty_cache()
     return rows
+
+
+def ramp_pou_tts(cfg, stream, xy, amp, sig):
+    """The same GMRES(50) solve with the paper's linear-ramp partition of unity instead of the north_star's
+    owner write: reported beside the headline, not as it (one rank only)."""
+    import torch
+
+    from paper_2602_00735_b200 import Context
+    from paper_2602_00735_b200.helm import POU_RAMP
+
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub, pou=POU_RAMP, stream=stream)
+    ctx.factor()
+    ev[1].record(stream)
+    b = ctx.rhs(xy, amp, sig)
+    ev[2].record(stream)
+    _, info, _ = ctx.gmres(b, restart=cfg.restart, rtol=cfg.rtol, maxit=5000)
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    res = {"setup_factor_s": ev[0].elapsed_time(ev[1]) / 1e3, "seconds": ev[2].elapsed_time(ev[3]) / 1e3,
+           "iterations": info.iterations, "restarts": info.restarts, "relres_true": info.relres_true,
+           "apply_bytes": ctx.layout.apply_bytes}
+    ctx.close()
+    del ctx, b
+    torch.cuda.empty_cache()
+    return res
 
 
 def applies_e2e(info, seconds):
