@@ -1192,10 +1192,11 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // the one-CTA-per-subdomain kernel may not fit very wide blocks (its ring holds whole columns); that is only an
+    // error when the cluster-split kernel below does not take over
     apply_configure(ctx->m_max, &ctx->ap_block, &ctx->ap_smem, &ctx->ap_slot, &ctx->ap_occ);
-    CK(cudaGetLastError());
-    if (ctx->ap_occ < 1) return set_err(ctx, HELM_ECUDA, "apply kernel does not fit on an SM (smem %d)", ctx->ap_smem);
-    ctx->ap_grid = std::min(nsub, nsm * ctx->ap_occ);
+    if (cudaGetLastError() != cudaSuccess) ctx->ap_occ = 0;
+    ctx->ap_grid = std::min(nsub, nsm * std::max(ctx->ap_occ, 1));
     ctx->nblk = nsm * 4;
     // Fewer subdomains than SMs (the paper's regime): split every subdomain over a cluster of 2G CTAs (G per chain).
     // Among the G <= 8 whose clusters are all resident at once, take the smallest that keeps >= 80 % of the SMs
@@ -1221,6 +1222,8 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
             ctx->sp_G = gbest;
         cudaGetLastError();
     }
+    if (ctx->sp_G == 0 && ctx->ap_occ < 1)
+        return set_err(ctx, HELM_ECUDA, "apply kernel does not fit on an SM (smem %d)", ctx->ap_smem);
     long long scr = (size_t)ctx->ap_grid * ctx->scratch_per_cta;
     if (ctx->sp_G > 0) {
         long long per = 0;

@@ -188,3 +188,18 @@ def test_paper_sharded_apply_and_matvec_bitwise(nranks, gg):
     assert torch.equal(Z.view(-1), z_ref)
     assert torch.equal(Y.view(-1), y_ref)
     ref.close()
+
+
+def test_paper_wide_single_block_exact_inverse():
+    """One subdomain = Omega at k = 300 (grid 600^2): blocks 599 wide (19 Gauss-Jordan panels in the cluster
+    factorisation, large slabs in the cluster-split apply).  B^-1 = A^-1: A (B^-1 v) = v, and B^-1 is linear."""
+    ctx = Context(**paper_params(300.0, 1, 4, 2, n_cells=600))
+    assert ctx.layout.m_max == 599
+    ctx.factor()
+    v = torch.from_numpy(probe_vector(ctx.n, 8)).cuda()
+    u = torch.from_numpy(probe_vector(ctx.n, 9)).cuda()
+    z = ctx.precond_apply(v)
+    assert rel(ctx.matvec(z).cpu().numpy(), v.cpu().numpy()) <= 1e-10
+    zl = ctx.precond_apply(v + 2.5j * u)
+    assert rel(zl.cpu().numpy(), (z + 2.5j * ctx.precond_apply(u)).cpu().numpy()) <= 1e-12
+    ctx.close()
