@@ -17,6 +17,8 @@
 // serial block-row dependency chain.  Consumer thread t owns row t of every block: the GEMV reads column
 // c of the column-major block (consecutive lanes -> consecutive 16-byte words, conflict-free) and the
 // broadcast operand rhs[c].
+#include <mutex>
+
 #include "internal.cuh"
 
 namespace {
@@ -385,11 +387,15 @@ void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_by
 {
     // the dynamic-smem limit is a per-function attribute shared by every context in the process: raise it
     // whenever a context needs more than any earlier one
+    static std::mutex mu;
     static int smem_set[3] = {0, 0, 0};
     const int cls = block <= 256 ? 0 : (block <= 512 ? 1 : 2);
-    if (smem > smem_set[cls]) {
-        cudaFuncSetAttribute(apply_fn(block), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        smem_set[cls] = smem;
+    {
+        std::lock_guard<std::mutex> lk(mu);   // contexts may launch from concurrent threads (loopback ranks)
+        if (smem > smem_set[cls]) {
+            cudaFuncSetAttribute(apply_fn(block), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            smem_set[cls] = smem;
+        }
     }
     const int ncw = block / 32 - 1;
     if (cls == 0) k_apply<256><<<grid, block, smem, s>>>(a, ncw, slot_bytes);

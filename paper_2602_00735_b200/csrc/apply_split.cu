@@ -18,6 +18,8 @@
 // bulk-copies each step's input row b_i and coupling vectors into a double-buffered "aux" slot one step ahead, so
 // the per-step right-hand side is formed from shared memory only.  Per row the arithmetic is k_apply's up to the
 // split of the GEMV into two partial sums.
+#include <mutex>
+
 #include "internal.cuh"
 
 namespace {
@@ -377,8 +379,10 @@ const void* split_fn(int block) { return block <= 288 ? (const void*)k_apply_spl
 // the dynamic-smem limit is a per-function attribute shared by every context in the process: only ever raise it
 void ensure_split_smem(int block, int smem)
 {
+    static std::mutex mu;
     static int smem_set[2] = {0, 0};
     const int cls = block <= 288 ? 0 : 1;
+    std::lock_guard<std::mutex> lk(mu);   // contexts may launch from concurrent threads (loopback ranks)
     if (smem > smem_set[cls]) {
         cudaFuncSetAttribute(split_fn(block), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(split_fn(block), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -1290,21 +1290,25 @@ int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_h
     z2* d_amp = nullptr;
     z2* d_f = nullptr;
     const long long nfw = (long long)(G.i1 - G.i0 + 2) * (G.j1 - G.j0 + 2);
-    int rc;
-    if ((rc = dalloc(ctx, &d_xy, 2 * (size_t)std::max(nsrc, 1))) || (rc = dalloc(ctx, &d_amp, std::max(nsrc, 1))) ||
-        (rc = dalloc(ctx, &d_f, nfw)))
-        return rc;
-    if (nsrc > 0) {
-        CK(cudaMemcpyAsync(d_xy, xy_host, sizeof(double) * 2 * nsrc, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(d_amp, amp_host, sizeof(z2) * nsrc, cudaMemcpyHostToDevice, ctx->stream));
-    }
-    launch_rhs(ctx->geom, nsrc, d_xy, d_amp, sigma, d_f, (z2*)b_dev, G.i0, G.i1, G.j0, G.j1, ctx->stream);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_xy);
+    auto body = [&]() -> int {
+        int rc;
+        if ((rc = dalloc(ctx, &d_xy, 2 * (size_t)std::max(nsrc, 1))) || (rc = dalloc(ctx, &d_amp, std::max(nsrc, 1))) ||
+            (rc = dalloc(ctx, &d_f, nfw)))
+            return rc;
+        if (nsrc > 0) {
+            CK(cudaMemcpyAsync(d_xy, xy_host, sizeof(double) * 2 * nsrc, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync(d_amp, amp_host, sizeof(z2) * nsrc, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        launch_rhs(ctx->geom, nsrc, d_xy, d_amp, sigma, d_f, (z2*)b_dev, G.i0, G.i1, G.j0, G.j1, ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(ctx->stream));
+        return HELM_OK;
+    };
+    const int rc = body();
+    cudaFree(d_xy);   // temporaries are released on every path
     cudaFree(d_amp);
     cudaFree(d_f);
-    return HELM_OK;
+    return rc;
 }
 
 int helm_factor(helm_ctx* ctx)
@@ -1327,13 +1331,21 @@ int helm_factor(helm_ctx* ctx)
         z2* d_tmp = nullptr;
         const int grid = 148;
         const long long per = (long long)ctx->m_max * ctx->m_max;
-        if ((rc = dalloc(ctx, &d_blocks, blocks.size())) || (rc = dalloc(ctx, &d_tmp, (size_t)grid * per))) return rc;
-        CK(cudaMemcpyAsync(d_blocks, blocks.data(), sizeof(int2) * blocks.size(), cudaMemcpyHostToDevice, ctx->stream));
-        launch_relayout(ctx->d_desc, d_blocks, (int)blocks.size(), ctx->d_dinv, d_tmp, per, grid, ctx->sp_G, ctx->stream);
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(ctx->stream));
+        auto relay = [&]() -> int {
+            int rc2;
+            if ((rc2 = dalloc(ctx, &d_blocks, blocks.size())) || (rc2 = dalloc(ctx, &d_tmp, (size_t)grid * per))) return rc2;
+            CK(cudaMemcpyAsync(d_blocks, blocks.data(), sizeof(int2) * blocks.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+            launch_relayout(ctx->d_desc, d_blocks, (int)blocks.size(), ctx->d_dinv, d_tmp, per, grid, ctx->sp_G,
+                            ctx->stream);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(ctx->stream));
+            return HELM_OK;
+        };
+        rc = relay();
         cudaFree(d_blocks);
         cudaFree(d_tmp);
+        if (rc) return rc;
     }
     int herr[4];
     CK(cudaMemcpyAsync(herr, ctx->d_err, sizeof(herr), cudaMemcpyDeviceToHost, ctx->stream));
