@@ -27,16 +27,17 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def golden(k, solver, table=None):
+def golden(k, solver, table=None, variants=(0, 1)):
     out = []
     with open(GOLDEN) as f:
         for line in f:
             if line.startswith("#") or not line.strip():
                 continue
             t, ln, kk, grid, P, pml, ov, bc, sv, its, rr = line.split()
-            if float(kk) == k and sv == solver and (table is None or t == table):
+            if float(kk) == k and sv == solver and (table is None or t == table) and \
+                    {"drch": 0, "imp": 1, "rasimp": 2}[bc] in variants:
                 out.append(dict(table=t, grid=int(grid), nsub=int(P), pml=int(pml), ovlp=int(ov),
-                                bc=1 if bc == "imp" else 0, its=int(its)))
+                                bc={"drch": 0, "imp": 1, "rasimp": 2}[bc], its=int(its)))
     return out
 
 
@@ -203,3 +204,27 @@ def test_paper_wide_single_block_exact_inverse():
     zl = ctx.precond_apply(v + 2.5j * u)
     assert rel(zl.cpu().numpy(), (z + 2.5j * ctx.precond_apply(u)).cpu().numpy()) <= 1e-12
     ctx.close()
+
+
+def test_paper_claims_ras_pml_imp_vs_drch_vs_ras_imp():
+    """"RAS-PML-Imp exhibits superior performance over RAS-PML-Drch, particularly at high frequencies, while
+    RAS-Imp fails to converge at all for high k" (Table 1).  Richardson to 1e-10: Imp <= Drch at k = 300 / 600 / 1200;
+    RAS-Imp (no local PML, impedance on the subdomain faces) needs more iterations than both at k = 300 / 600 (printed
+    30 / 43; ours 29 / 48) and does not converge within the paper's 500 at k = 1200 (printed: stopped at 500, relres
+    0.016; ours: diverges, flagged once the residual exceeds 1e6)."""
+    its = {}
+    for k, P, pml, ov in [(300.0, 2, 8, 4), (600.0, 4, 11, 5), (1200.0, 8, 15, 6)]:
+        for variant, (bc, p_) in {"imp": (1, pml), "drch": (0, pml), "rasimp": (1, 0)}.items():
+            ctx = Context(**paper_params(k, P, p_, ov, n_cells=int(2 * k), local_bc=bc))
+            ctx.factor()
+            b = ctx.rhs(*paper_source(k))
+            _, info, _ = ctx.richardson(b, rtol=1e-10, maxit=500)
+            its[(k, variant)] = (info.iterations, info.status)
+            ctx.close()
+            torch.cuda.empty_cache()
+    for k in (300.0, 600.0, 1200.0):
+        assert its[(k, "imp")][1] == 0 and its[(k, "drch")][1] == 0
+        assert its[(k, "imp")][0] <= its[(k, "drch")][0]
+    for k in (300.0, 600.0):
+        assert its[(k, "rasimp")][1] == 0 and its[(k, "rasimp")][0] > its[(k, "drch")][0]
+    assert its[(1200.0, "rasimp")][1] != 0, its[(1200.0, "rasimp")]
