@@ -134,7 +134,7 @@ int helm_precond_apply(helm_ctx* ctx, const helm_z* r_dev, helm_z* z_dev);
 /* Same with host buffers: r_host -> device, apply, device -> z_host; synchronous (end-to-end path). */
 int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host);
 
-/* Right-preconditioned restarted GMRES(restart) on A (B^-1 u) = b, x = B^-1 u (D13):
+/* Right-preconditioned restarted GMRES(restart), 1 <= restart <= 63, on A (B^-1 u) = b, x = B^-1 u (D13):
  * x_dev in: initial guess, out: solution.  rtol on ||b - A x|| / ||b||; rtol <= 0 runs exactly maxit
  * iterations.  Synchronous.  Returns HELM_OK / HELM_NOT_CONVERGED / HELM_BREAKDOWN or an error. */
 int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, double rtol, int maxit,

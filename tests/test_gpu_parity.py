@@ -225,3 +225,27 @@ def test_c3_full_size_properties():
     r = b - ctx.matvec(x)
     assert float(torch.linalg.norm(r) / torch.linalg.norm(b)) <= cfg.rtol
     ctx.close()
+
+
+def test_gmres_initial_guess_and_restart_bounds():
+    """A nonzero initial guess x0 (the oracle's GMRES from the same x0: iterations +-1, x to 1e-6), short restarts
+    (GMRES(5) vs the oracle's GMRES(5)), the largest restart the ABI takes (63: 64 basis vectors) and the first it
+    refuses (64)."""
+    cfg = CONFIGS["c1"]
+    ctx, o = pair("c1")
+    o.factor()
+    b = o.rhs(*sources(cfg))
+    x0 = 0.3 * probe_vector(o.nfree, 77)
+    ref = orc_gmres(o.matvec, o.apply, b, restart=50, rtol=1e-6, x0=x0)
+    x, info, _ = ctx.gmres(to_dev(b), to_dev(x0.copy()), restart=50, rtol=1e-6)
+    assert info.status == 0 and abs(info.iterations - ref.iterations) <= 1
+    assert rel(to_np(x), ref.x) <= 1e-6
+    ref5 = orc_gmres(o.matvec, o.apply, b, restart=5, rtol=1e-6)
+    x5, info5, _ = ctx.gmres(to_dev(b), restart=5, rtol=1e-6)
+    assert info5.status == 0 and abs(info5.iterations - ref5.iterations) <= 1 and info5.restarts == ref5.restarts
+    assert rel(to_np(x5), ref5.x) <= 1e-6
+    _, info63, _ = ctx.gmres(to_dev(b), restart=63, rtol=1e-6)
+    assert info63.status == 0
+    with pytest.raises(HelmError) as e:
+        ctx.gmres(to_dev(b), restart=64, rtol=1e-6)
+    assert e.value.code == -1
