@@ -58,7 +58,9 @@ typedef struct {
     int local_bc;        /* HELM_BC_DIRICHLET or HELM_BC_IMPEDANCE */
     int gpu_grid_x, gpu_grid_y;   /* rank grid over the subdomain grid; product == nranks (0,0 => most square) */
     int pou;             /* HELM_POU_OWNER: restricted owner write (D10, the hot path); HELM_POU_RAMP: linear
-                            ramps across the overlaps, one rank only, blocks >= 2 delta cells */
+                            ramps across the overlaps, blocks >= 2 delta cells; on several ranks the sums over
+                            covering subdomains cross rank boundaries (additive reverse halo exchange), so ramp needs a
+                            communicator (NCCL or loopback), not a communication-free shard */
     /* The paper's own workload (D18-D22).  Zero-initialised fields give
      * the BASELINE.json problem above. */
     int elem;            /* HELM_ELEM_P1: P1 on the SW->NE split, 7-point stencil (D1); HELM_ELEM_Q1: bilinear

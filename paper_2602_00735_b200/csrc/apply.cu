@@ -321,30 +321,34 @@ const void* apply_fn(int block)
     return (const void*)k_apply<1024>;
 }
 
-// Ramp-PoU prolongation: z[g] = sum over the <= 2 x 2 subdomains whose chi is positive at
-// g of their weighted local solutions, summed in ascending subdomain index (deterministic).
-// candx / candy: per node index, the (up to) two blocks along that axis, -1 padded.
+// Ramp-PoU prolongation: out(g) = sum over the <= 2 x 2 subdomains whose chi is positive at g
+// of their weighted local solutions, summed in ascending subdomain index (deterministic).  Only subdomains of this
+// rank's block range [bx0, bx1) x [by0, by1) contribute (descriptors are indexed locally); on several ranks the rest
+// arrives through the additive reverse halo exchange.  candx / candy: per node index, the (up to) two blocks along
+// that axis, -1 padded.  Nodes [i0, i1) x [j0, j1) are written to out at origin (oi0, oj0), stride ostride.
 __global__ void k_pou_gather(const SubDesc* __restrict__ desc, const int* __restrict__ candx,
-                             const int* __restrict__ candy, int px, const z2* __restrict__ buf, z2* __restrict__ z,
+                             const int* __restrict__ candy, int bx0, int bx1, int by0, int by1,
+                             const z2* __restrict__ buf, z2* __restrict__ out, int oi0, int oj0, long long ostride,
                              int i0, int i1, int j0, int j1)
 {
     const int w = i1 - i0;
     const long long n = (long long)w * (j1 - j0);
+    const int lw = bx1 - bx0;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const int i = i0 + (int)(e % w), j = j0 + (int)(e / w);
         z2 acc = zmk(0, 0);
         for (int b = 0; b < 2; b++) {
             const int by = candy[2 * j + b];
-            if (by < 0) continue;
+            if (by < by0 || by >= by1) continue;   // -1 padding fails by < by0 as well
             for (int a = 0; a < 2; a++) {
                 const int bx = candx[2 * i + a];
-                if (bx < 0) continue;
-                const SubDesc d = desc[bx + px * by];
+                if (bx < bx0 || bx >= bx1) continue;
+                const SubDesc d = desc[(bx - bx0) + lw * (by - by0)];
                 const long long off = d.pou_off + (i - (d.gx0 + d.olo)) + (long long)(d.ohi - d.olo + 1) * (j - (d.gy0 + d.lo));
                 acc = zadd(acc, buf[off]);
             }
         }
-        z[e] = acc;
+        out[(i - oi0) + ostride * (j - oj0)] = acc;
     }
 }
 
@@ -374,13 +378,16 @@ int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_by
     return ncw;
 }
 
-void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int px, const z2* pou_buf, z2* z,
-                       int i0, int i1, int j0, int j1, cudaStream_t s)
+void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int bx0, int bx1, int by0, int by1,
+                       const z2* pou_buf, z2* out, int oi0, int oj0, long long ostride, int i0, int i1, int j0, int j1,
+                       cudaStream_t s)
 {
     const long long n = (long long)(i1 - i0) * (j1 - j0);
+    if (n <= 0) return;
     long long g = (n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    k_pou_gather<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(desc, candx, candy, px, pou_buf, z, i0, i1, j0, j1);
+    k_pou_gather<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(desc, candx, candy, bx0, bx1, by0, by1, pou_buf, out, oi0, oj0,
+                                                      ostride, i0, i1, j0, j1);
 }
 
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s)

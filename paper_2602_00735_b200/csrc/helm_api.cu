@@ -138,8 +138,8 @@ int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* 
         snprintf(err, errlen, "pou must be HELM_POU_OWNER or HELM_POU_RAMP");
         return HELM_EINVAL;
     }
-    if (p.pou == HELM_POU_RAMP && (nranks > 1 || G.wo < 1)) {
-        snprintf(err, errlen, "ramp PoU needs one rank and delta >= 1");
+    if (p.pou == HELM_POU_RAMP && G.wo < 1) {
+        snprintf(err, errlen, "ramp PoU needs delta >= 1");
         return HELM_EINVAL;
     }
     // rank grid: default = most square factorisation with gx >= gy
@@ -276,6 +276,7 @@ struct helm_ctx {
     // ramp partition of unity: weighted local solutions + per-axis covering blocks
     long long pou_len = 0;
     z2* d_pou = nullptr;
+    z2* d_cext = nullptr;   // multi-rank ramp PoU: weighted contributions on the ghost-framed rectangle
     int* d_candx = nullptr;
     int* d_candy = nullptr;
 
@@ -562,7 +563,7 @@ int need_comm(helm_ctx* ctx)
 // ---------------------------------------------------------------------------------------- collectives
 // loopback: after the phase's messages are packed, copy each peer's send buffer addressed to this rank into the
 // matching receive buffer (the peer's message index is recomputed from its own schedule)
-int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const int* idx, int k)
+int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const int* idx, int k, bool reverse)
 {
     LoopGroup* L = ctx->loop;
     CK(cudaStreamSynchronize(ctx->stream));
@@ -582,8 +583,12 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
                 pa++;
             }
         if (found < 0) return set_err(ctx, HELM_ENCCL, "loopback: rank %d has no message for rank %d", m.peer, ctx->rank);
-        const size_t rcnt = (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
-        const size_t scnt = (size_t)(pm[fq].send_i1 - pm[fq].send_i0) * (pm[fq].send_j1 - pm[fq].send_j0);
+        // forward: the peer packed its send rectangle into my receive rectangle; reverse: its receive rectangle (its
+        // ghost frame toward me) onto my send rectangle (my owned strip)
+        const size_t rcnt = reverse ? (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0)
+                                    : (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+        const size_t scnt = reverse ? (size_t)(pm[fq].recv_i1 - pm[fq].recv_i0) * (pm[fq].recv_j1 - pm[fq].recv_j0)
+                                    : (size_t)(pm[fq].send_i1 - pm[fq].send_i0) * (pm[fq].send_j1 - pm[fq].send_j0);
         if (scnt != rcnt) return set_err(ctx, HELM_ENCCL, "loopback: message size mismatch %zu vs %zu", scnt, rcnt);
         CK(cudaMemcpyAsync(ctx->d_recvbuf[a], peer->d_sendbuf[found], sizeof(z2) * rcnt, cudaMemcpyDeviceToDevice,
                            ctx->stream));
@@ -593,34 +598,41 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
     return HELM_OK;
 }
 
-// halo exchange of width W on the ghost-framed buffer d_ext (ext rectangle layout)
-int exchange(helm_ctx* ctx, int W)
+// halo exchange of width W on a ghost-framed buffer `buf` (ext rectangle layout).  Forward (reverse = false): the
+// owned strips travel to the neighbours' ghost frames, phase 0 (x) then phase 1 (y, carrying the corners).
+// Reverse (reverse = true, the ramp PoU's additive exchange): the ghost frames travel back and are ADDED onto the
+// neighbours' owned strips, phase 1 then phase 0, so corner contributions reach the diagonal rank in two hops.
+int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse)
 {
-    NvtxRange nv_(W == 0 ? "helm.comm.halo_apply" : "helm.comm.halo_spmv");
+    NvtxRange nv_(reverse ? "helm.comm.halo_add" : (W == 0 ? "helm.comm.halo_apply" : "helm.comm.halo_spmv"));
     helm_msg msgs[4];
     const int nm = halo_schedule(ctx->G, W, msgs, 4);
     const GridInfo& G = ctx->G;
-    for (int phase = 0; phase < 2; phase++) {
+    for (int ph = 0; ph < 2; ph++) {
+        const int phase = reverse ? 1 - ph : ph;
         int idx[4], k = 0;
         for (int q = 0; q < nm; q++)
             if (msgs[q].phase == phase) idx[k++] = q;
         if (!k && !ctx->loop) continue;   // (loopback ranks meet at every phase's barriers)
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
-            launch_copy_rect(ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], m.send_i0, m.send_j0,
-                             m.send_i1 - m.send_i0, m.send_i0, m.send_i1, m.send_j0, m.send_j1, ctx->stream);
+            const int i0 = reverse ? m.recv_i0 : m.send_i0, i1 = reverse ? m.recv_i1 : m.send_i1;
+            const int j0 = reverse ? m.recv_j0 : m.send_j0, j1 = reverse ? m.recv_j1 : m.send_j1;
+            launch_copy_rect(buf, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], i0, j0, i1 - i0, i0, i1, j0, j1,
+                             ctx->stream);
             ctx->launches++;
         }
         if (ctx->loop) {
-            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k);
+            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k, reverse);
             if (rc) return rc;
         } else {
 #ifdef HELM_HAVE_NCCL
             NK(ncclGroupStart());
             for (int a = 0; a < k; a++) {
                 const helm_msg& m = msgs[idx[a]];
-                const size_t scnt = 2 * (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
-                const size_t rcnt = 2 * (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+                const size_t sa = (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
+                const size_t ra = (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+                const size_t scnt = 2 * (reverse ? ra : sa), rcnt = 2 * (reverse ? sa : ra);
                 NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
                 NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
             }
@@ -631,13 +643,17 @@ int exchange(helm_ctx* ctx, int W)
         }
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
-            launch_copy_rect(ctx->d_recvbuf[a], m.recv_i0, m.recv_j0, m.recv_i1 - m.recv_i0, ctx->d_ext, G.e_i0,
-                             G.e_j0, ctx->ext_stride, m.recv_i0, m.recv_i1, m.recv_j0, m.recv_j1, ctx->stream);
+            const int i0 = reverse ? m.send_i0 : m.recv_i0, i1 = reverse ? m.send_i1 : m.recv_i1;
+            const int j0 = reverse ? m.send_j0 : m.recv_j0, j1 = reverse ? m.send_j1 : m.recv_j1;
+            launch_copy_rect(ctx->d_recvbuf[a], i0, j0, i1 - i0, buf, G.e_i0, G.e_j0, ctx->ext_stride, i0, i1, j0, j1,
+                             ctx->stream, reverse);
             ctx->launches++;
         }
     }
     return HELM_OK;
 }
+
+int exchange(helm_ctx* ctx, int W) { return exchange_buf(ctx, W, ctx->d_ext, false); }
 
 // in-place sum over ranks of `count` doubles on the device
 int allreduce(helm_ctx* ctx, double* buf, size_t count)
@@ -734,9 +750,10 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     }
     CK(cudaGetLastError());
     ctx->launches++;
-    if (ctx->d_pou) {
-        launch_pou_gather(ctx->d_desc, ctx->d_candx, ctx->d_candy, ctx->G.P[0], ctx->d_pou, z, ctx->G.i0, ctx->G.i1,
-                          ctx->G.j0, ctx->G.j1, ctx->stream);
+    if (ctx->d_pou && !ctx->multi) {
+        const GridInfo& G = ctx->G;
+        launch_pou_gather(ctx->d_desc, ctx->d_candx, ctx->d_candy, G.bx0, G.bx1, G.by0, G.by1, ctx->d_pou, z, G.i0,
+                          G.j0, G.i1 - G.i0, G.i0, G.i1, G.j0, G.j1, ctx->stream);
         CK(cudaGetLastError());
         ctx->launches++;
     }
@@ -755,7 +772,20 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
     if ((rc = need_comm(ctx))) return rc;
     if (!ctx->multi) return apply_raw(ctx, r, ctx->G.i0, ctx->G.j0, ctx->G.i1 - ctx->G.i0, z);
     if ((rc = fill_ext(ctx, r, 0))) return rc;
-    return apply_raw(ctx, ctx->d_ext, ctx->G.e_i0, ctx->G.e_j0, ctx->ext_stride, z);
+    if ((rc = apply_raw(ctx, ctx->d_ext, ctx->G.e_i0, ctx->G.e_j0, ctx->ext_stride, z))) return rc;
+    if (!ctx->d_pou) return HELM_OK;
+    // ramp PoU on several ranks: this rank's weighted contributions on its ghost-framed rectangle, the
+    // additive reverse exchange of the frames (width delta), then the owned part is the prolongation
+    const GridInfo& G = ctx->G;
+    launch_pou_gather(ctx->d_desc, ctx->d_candx, ctx->d_candy, G.bx0, G.bx1, G.by0, G.by1, ctx->d_pou, ctx->d_cext,
+                      G.e_i0, G.e_j0, ctx->ext_stride, G.e_i0, G.e_i1, G.e_j0, G.e_j1, ctx->stream);
+    ctx->launches++;
+    if ((rc = exchange_buf(ctx, G.wo, ctx->d_cext, true))) return rc;
+    launch_copy_rect(ctx->d_cext, G.e_i0, G.e_j0, ctx->ext_stride, z, G.i0, G.j0, G.i1 - G.i0, G.i0, G.i1, G.j0, G.j1,
+                     ctx->stream);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    return HELM_OK;
 }
 
 // y = A x for an owned input vector
@@ -1238,6 +1268,12 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
         if ((rc = dalloc(ctx, &ctx->d_pou, ctx->pou_len)) || (rc = dalloc(ctx, &ctx->d_candx, 2 * (G.N + 1))) ||
             (rc = dalloc(ctx, &ctx->d_candy, 2 * (G.N + 1))))
             return rc;
+        if (ctx->multi) {
+            // the sum over covering subdomains crosses rank boundaries: it needs the additive reverse exchange, so
+            // communication-free shards (the _ext entry points) cannot run the ramp PoU
+            if (!ctx->has_comm) return set_err(ctx, HELM_EINVAL, "ramp PoU on several ranks needs a communicator");
+            if ((rc = dalloc(ctx, &ctx->d_cext, ctx->n_ext))) return rc;
+        }
         for (int ax = 0; ax < 2; ax++) {
             std::vector<int> cand(2 * (G.N + 1), -1);
             for (int x = 0; x <= G.N; x++) {
@@ -1500,7 +1536,7 @@ void helm_destroy(helm_ctx* ctx)
     void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
                     ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq,
-                    ctx->d_pou, ctx->d_candx, ctx->d_candy};
+                    ctx->d_pou, ctx->d_candx, ctx->d_candy, ctx->d_cext};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int q = 0; q < 4; q++) {

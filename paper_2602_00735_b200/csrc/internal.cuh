@@ -133,8 +133,9 @@ struct ApplyArgs {
     z2* pou_buf;            // ramp-PoU mode: weighted local solutions (else nullptr: owner write to out)
     int delta;              // overlap width (ramp half-width)
 };
-void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int px, const z2* pou_buf, z2* z,
-                       int i0, int i1, int j0, int j1, cudaStream_t s);
+void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int bx0, int bx1, int by0, int by1,
+                       const z2* pou_buf, z2* out, int oi0, int oj0, long long ostride, int i0, int i1, int j0, int j1,
+                       cudaStream_t s);
 int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
 // cluster-split apply for few large subdomains (apply_split.cu)
 int split_configure(int m_max, int G, int ctas_per_sm, int* block_threads, int* smem_bytes, int* slot_bytes, int* ncw,
@@ -162,7 +163,7 @@ void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStr
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s);
 void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,
-                      int i0, int i1, int j0, int j1, cudaStream_t s);
+                      int i0, int i1, int j0, int j1, cudaStream_t s, bool add = false);
 void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t s);
 void launch_finish_norm(const double* sq, z2* out_slot, double* out_norm, cudaStream_t s);
 void launch_zadd(const z2* a, const z2* b, z2* out, int nv, cudaStream_t s);

@@ -110,15 +110,18 @@ __global__ void __launch_bounds__(KT) k_residual(const z2* __restrict__ A7, cons
 
 // dst(rect) = src(rect): strided 2-D copy between vectors with different origins / strides (halo pack,
 // unpack, owned -> ghost-framed buffer)
+// add: dst(rect) += src(rect) (unpack of the additive reverse exchange of the ramp PoU)
 __global__ void __launch_bounds__(KT) k_copy_rect(const z2* __restrict__ src, int si0, int sj0, long long sstride,
                                                   z2* __restrict__ dst, int di0, int dj0, long long dstride,
-                                                  int i0, int i1, int j0, int j1)
+                                                  int i0, int i1, int j0, int j1, int add)
 {
     const int w = i1 - i0;
     const long long n = (long long)w * (j1 - j0);
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const int i = i0 + (int)(e % w), j = j0 + (int)(e / w);
-        dst[(i - di0) + dstride * (j - dj0)] = src[(i - si0) + sstride * (j - sj0)];
+        z2* d = dst + (i - di0) + dstride * (j - dj0);
+        const z2 v = src[(i - si0) + sstride * (j - sj0)];
+        *d = add ? zadd(*d, v) : v;
     }
 }
 
@@ -370,11 +373,11 @@ void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const Stenci
     else k_residual<7><<<nblk, KT, 0, s>>>(A7, x, b, r, G, partial);
 }
 void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,
-                      int i0, int i1, int j0, int j1, cudaStream_t s)
+                      int i0, int i1, int j0, int j1, cudaStream_t s, bool add)
 {
     const long long n = (long long)(i1 - i0) * (j1 - j0);
     if (n <= 0) return;
-    k_copy_rect<<<ew_grid(n), KT, 0, s>>>(src, si0, sj0, sstride, dst, di0, dj0, dstride, i0, i1, j0, j1);
+    k_copy_rect<<<ew_grid(n), KT, 0, s>>>(src, si0, sj0, sstride, dst, di0, dj0, dstride, i0, i1, j0, j1, add ? 1 : 0);
 }
 void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t s)
 {

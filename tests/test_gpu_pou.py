@@ -44,9 +44,12 @@ def test_pou_apply_and_gmres_parity(name, nsub, bc):
     ctx.close()
 
 
-def test_pou_ramp_is_single_rank():
-    with pytest.raises(HelmError):
+def test_pou_ramp_needs_a_communicator_on_several_ranks():
+    """The ramp PoU sums over subdomains of neighbouring ranks (additive reverse exchange): communication-free shards
+    (no NCCL id, no loopback group) refuse it."""
+    with pytest.raises(HelmError) as e:
         Context(400.0, 16, 16, rank=0, nranks=2, pou=POU_RAMP)
+    assert e.value.code == -1
 
 
 def test_pou_c3_full_size_sampled():
