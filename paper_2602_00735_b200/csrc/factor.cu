@@ -30,6 +30,32 @@ __device__ __forceinline__ void zfms(z2& acc, z2 a, z2 b)
     acc.y = fma(-a.y, b.x, acc.y);
 }
 
+// FP64 tensor cores (DMMA, mma.sync m8n8k4): d += a b for one 8 x 8 x 4 real tile per warp.  Fragments: a = A[g][t],
+// b = B[t][g], c = (C[g][2t], C[g][2t+1]) with g = lane / 4, t = lane % 4.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Complex 8 x 8 tile update C -= A B over k in [0, kw) on the tensor cores, with A(r, q) = la(r, q), B(q, c) = lb(q, c)
+// supplied as accessors returning complex values (zero outside the matrix): Cr += (-Ar) Br + Ai Bi,
+// Ci += (-Ar) Bi + (-Ai) Br -- four real DMMAs per k-step of 4.
+template <class LA, class LB>
+__device__ __forceinline__ void ztile_fms(z2& c0, z2& c1, int kw, LA la, LB lb)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    for (int k = 0; k < kw; k += 4) {
+        const z2 a = k + t < kw ? la(g, k + t) : zmk(0, 0);
+        const z2 b = k + t < kw ? lb(k + t, g) : zmk(0, 0);
+        dmma(c0.x, c1.x, -a.x, b.x);
+        dmma(c0.x, c1.x, a.y, b.y);
+        dmma(c0.y, c1.y, -a.x, b.y);
+        dmma(c0.y, c1.y, -a.y, b.x);
+    }
+}
+
 // D (kw x kw, row-major, stride DLD, kw <= 32) <- D^-1 by unpivoted in-place Gauss-Jordan, executed by the first
 // GJW warps of the CTA (lane c owns column c, warp w the rows r = w, w + GJW, ...; named barrier 2 over those warps
 // only).  A zero pivot is recorded as row kb + p.
@@ -178,7 +204,7 @@ __device__ void build_block(const SubDesc& d, int i, int mode, const z2* __restr
 //   Dk = S[K,K]^-1 (one warp);  S[K,j] = Dk S[K,j] (j not in K);  S[i,j] -= S[i,K] S[K,j] (i, j not in K);
 //   S[i,K] = -S[i,K] Dk (i not in K);  S[K,K] = Dk.
 // The panel updates are computed into registers (<= RMAX results per thread) and written after a barrier, so they
-// work in place; the trailing update uses 2 x 2 register tiles (rows {ti, ti + hm}, columns {tj, tj + hn}).
+// work in place; the trailing update (a complex GEMM, 32 deep) runs on the FP64 tensor cores (DMMA), 8 x 8 tiles.
 constexpr int RMAX = 8;   // register results per thread in the panel updates: m * GB <= RMAX * FT  (m <= 128)
 
 __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
@@ -187,7 +213,6 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
     z2* S = sm.S;
     z2* Dk = sm.Dk;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int hm = (m + 1) / 2;
     for (int kb = 0; kb < m; kb += GB) {
         const int kw = min(GB, m - kb);
         if (tid < GJW * 32) {
@@ -226,28 +251,23 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
             }
             __syncthreads();
         }
-        // ---- trailing update, 2 x 2 register tiles
-        for (int e = tid; e < hm * hm; e += nt) {
-            const int ti = e / hm, tj = e - ti * hm;
-            const int i0 = ti, i1 = ti + hm, j0 = tj, j1 = tj + hm;
-            const bool ri0 = !(i0 >= kb && i0 < kb + kw), ri1 = i1 < m && !(i1 >= kb && i1 < kb + kw);
-            const bool cj0 = !(j0 >= kb && j0 < kb + kw), cj1 = j1 < m && !(j1 >= kb && j1 < kb + kw);
-            if (!((ri0 || ri1) && (cj0 || cj1))) continue;
-            z2 a00 = S[i0 * ld + j0], a01 = cj1 ? S[i0 * ld + j1] : zmk(0, 0);
-            z2 a10 = ri1 ? S[i1 * ld + j0] : zmk(0, 0), a11 = (ri1 && cj1) ? S[i1 * ld + j1] : zmk(0, 0);
-            const int i1s = i1 < m ? i1 : i0, j1s = j1 < m ? j1 : j0;
-            for (int q = 0; q < kw; q++) {
-                const z2 l0 = S[i0 * ld + kb + q], l1 = S[i1s * ld + kb + q];
-                const z2 u0 = S[(kb + q) * ld + j0], u1 = S[(kb + q) * ld + j1s];
-                zfms(a00, l0, u0);
-                zfms(a01, l0, u1);
-                zfms(a10, l1, u0);
-                zfms(a11, l1, u1);
+        // ---- trailing update S[i,j] -= S[i,K] S[K,j] on the FP64 tensor cores: one warp per 8 x 8 tile; tiles are
+        //      aligned to the 32-column panels, so the panel's rows and columns are skipped as whole tiles
+        {
+            const int mt = (m + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
+            for (int tile = tid >> 5; tile < mt * mt; tile += nt >> 5) {
+                const int i0 = (tile / mt) * 8, j0 = (tile % mt) * 8;
+                if ((i0 >= kb && i0 < kb + kw) || (j0 >= kb && j0 < kb + kw)) continue;
+                const int r = i0 + g, cA = j0 + 2 * t, cB = cA + 1;
+                z2 c0 = (r < m && cA < m) ? S[r * ld + cA] : zmk(0, 0);
+                z2 c1 = (r < m && cB < m) ? S[r * ld + cB] : zmk(0, 0);
+                ztile_fms(
+                    c0, c1, kw,
+                    [&](int rr, int q) { return i0 + rr < m ? S[(i0 + rr) * ld + kb + q] : zmk(0, 0); },
+                    [&](int q, int cc) { return j0 + cc < m ? S[(kb + q) * ld + j0 + cc] : zmk(0, 0); });
+                if (r < m && cA < m) S[r * ld + cA] = c0;
+                if (r < m && cB < m) S[r * ld + cB] = c1;
             }
-            if (ri0 && cj0) S[i0 * ld + j0] = a00;
-            if (ri0 && cj1) S[i0 * ld + j1] = a01;
-            if (ri1 && cj0) S[i1 * ld + j0] = a10;
-            if (ri1 && cj1) S[i1 * ld + j1] = a11;
         }
         __syncthreads();
         // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K), S[K, K] = Dk  (pairs (i, c), i fastest)
@@ -399,7 +419,6 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
     }
     cluster_sync_all();
     const int R = big_rows(m, bc), r0 = rk * R, r1 = min(m, r0 + R), nr = max(0, r1 - r0);
-    const int hr = (nr + 1) / 2;
     for (int kb = 0; kb < m; kb += GB) {
         const int kw = min(GB, m - kb);
         // ---- Dk = A[K,K]^-1 (every CTA, one warp)
@@ -432,48 +451,38 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
             }
         }
         cluster_sync_all();
-        // ---- trailing update of this CTA's row slab [r0, r1): A[i,K] staged in Aik, A[K, tile] in AKj;
-        //      2 x 2 register tiles: rows {ii, ii + hr}, columns {jj, jj + JT/2}
+        // ---- trailing update of this CTA's row slab [r0, r1): A[i,K] staged in Aik, A[K, tile] in AKj
         for (int e = tid; e < nr * kw; e += BT) {
             const int q = e / nr, ii = e - q * nr;
             Aik[ii * DLD + q] = A[(long long)(kb + q) * m + r0 + ii];
         }
         __syncthreads();
+        static_assert(JT == GB, "the panel's columns must form exactly one column tile");
+        const int nrt = (nr + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
         for (int jt = 0; jt < m; jt += JT) {
             const int jw = min(JT, m - jt);
-            for (int e = tid; e < jw * kw; e += BT) {
-                const int jj = e / kw, q = e - jj * kw;
-                AKj[q * JT + jj] = A[(long long)(jt + jj) * m + kb + q];
-            }
-            __syncthreads();
-            for (int e = tid; e < hr * (JT / 2); e += BT) {
-                const int jj = e / hr, ii = e - jj * hr;
-                const int iA = ii, iB = ii + hr, jA = jj, jB = jj + JT / 2;
-                const int rowA = r0 + iA, rowB = r0 + iB, colA = jt + jA, colB = jt + jB;
-                const bool okA = iA < nr && !(rowA >= kb && rowA < kb + kw), okB = iB < nr && !(rowB >= kb && rowB < kb + kw);
-                const bool inA = jA < jw, inB = jB < jw;
-                if (!(okA || okB) || !(inA || inB)) continue;
-                const bool kA = colA >= kb && colA < kb + kw, kB = colB >= kb && colB < kb + kw;   // column panel
-                const int iAs = iA < nr ? iA : iB, iBs = iB < nr ? iB : iA;
-                z2 vAA = zmk(0, 0), vAB = zmk(0, 0), vBA = zmk(0, 0), vBB = zmk(0, 0);
-                if (okA && inA && !kA) vAA = A[(long long)colA * m + rowA];
-                if (okA && inB && !kB) vAB = A[(long long)colB * m + rowA];
-                if (okB && inA && !kA) vBA = A[(long long)colA * m + rowB];
-                if (okB && inB && !kB) vBB = A[(long long)colB * m + rowB];
-                for (int q = 0; q < kw; q++) {
-                    const z2 lA = Aik[iAs * DLD + q], lB = Aik[iBs * DLD + q];
-                    // trailing columns use the new row panel A[K, j]; panel columns use Dk (A[i,K] = -A[i,K] Dk)
-                    const z2 uA = kA ? Dk[q * DLD + (colA - kb)] : AKj[q * JT + jA];
-                    const z2 uB = kB ? Dk[q * DLD + (colB - kb)] : (inB ? AKj[q * JT + jB] : zmk(0, 0));
-                    zfms(vAA, lA, uA);
-                    zfms(vAB, lA, uB);
-                    zfms(vBA, lB, uA);
-                    zfms(vBB, lB, uB);
+            const bool kcols = jt == kb;   // the column panel: A[i,K] = -A[i,K] Dk (a product with C = 0)
+            if (!kcols)
+                for (int e = tid; e < jw * kw; e += BT) {
+                    const int jj = e / kw, q = e - jj * kw;
+                    AKj[q * JT + jj] = A[(long long)(jt + jj) * m + kb + q];
                 }
-                if (okA && inA) A[(long long)colA * m + rowA] = vAA;
-                if (okA && inB) A[(long long)colB * m + rowA] = vAB;
-                if (okB && inA) A[(long long)colA * m + rowB] = vBA;
-                if (okB && inB) A[(long long)colB * m + rowB] = vBB;
+            __syncthreads();
+            // FP64 tensor cores: one warp per 8 x 8 tile of (slab rows) x (tile columns)
+            for (int tile = tid >> 5; tile < nrt * (JT / 8); tile += BT >> 5) {
+                const int i0 = (tile / (JT / 8)) * 8, j0 = (tile % (JT / 8)) * 8;
+                const int r = i0 + g, row = r0 + r, cA = j0 + 2 * t, cB = cA + 1;
+                const bool rok = r < nr && !(row >= kb && row < kb + kw);   // rows of the panel are final already
+                z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
+                if (!kcols && rok && cA < jw) c0 = A[(long long)(jt + cA) * m + row];
+                if (!kcols && rok && cB < jw) c1 = A[(long long)(jt + cB) * m + row];
+                ztile_fms(
+                    c0, c1, kw, [&](int rr, int q) { return i0 + rr < nr ? Aik[(i0 + rr) * DLD + q] : zmk(0, 0); },
+                    [&](int q, int cc) {
+                        return j0 + cc < jw ? (kcols ? Dk[q * DLD + j0 + cc] : AKj[q * JT + j0 + cc]) : zmk(0, 0);
+                    });
+                if (rok && cA < jw) A[(long long)(jt + cA) * m + row] = c0;
+                if (rok && cB < jw) A[(long long)(jt + cB) * m + row] = c1;
             }
             __syncthreads();
         }
