@@ -203,9 +203,8 @@ __device__ void build_block(const SubDesc& d, int i, int mode, const z2* __restr
 // of GB columns (unpivoted, D12; on the bottom chain the pivots are the oracle's no-pivot band-LU pivots):
 //   Dk = S[K,K]^-1 (one warp);  S[K,j] = Dk S[K,j] (j not in K);  S[i,j] -= S[i,K] S[K,j] (i, j not in K);
 //   S[i,K] = -S[i,K] Dk (i not in K);  S[K,K] = Dk.
-// The panel updates are computed into registers (<= RMAX results per thread) and written after a barrier, so they
-// work in place; the trailing update (a complex GEMM, 32 deep) runs on the FP64 tensor cores (DMMA), 8 x 8 tiles.
-constexpr int RMAX = 8;   // register results per thread in the panel updates: m * GB <= RMAX * FT  (m <= 128)
+// All three products (row panel, trailing update, column panel -- complex GEMMs, 32 deep) run on the FP64 tensor cores
+// (DMMA), one warp per 8 x 8 tile; a panel warp loads its whole operand strip before writing, so they work in place.
 
 __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
 {
@@ -224,29 +223,37 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
             warp_gj(Dk, kw, kb, bad_row);
         }
         __syncthreads();
-        // ---- row panel: S[K, j] = Dk S[K, j], j not in K  (pairs (r, j), r fastest)
+        // ---- row panel: S[K, j] = Dk S[K, j] (j not in K) on the tensor cores.  One warp owns an 8-column strip:
+        //      it loads the strip's old 32 x 8 block as B fragments first, then writes its four 8 x 8 row tiles, so
+        //      the update is in place without a second barrier
         {
-            z2 res[RMAX];
-            const int np = kw * m;
+            const int mt = (m + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
+            for (int strip = tid >> 5; strip < mt; strip += nt >> 5) {
+                const int j0 = strip * 8, col = j0 + g;
+                if (j0 >= kb && j0 < kb + kw) continue;
+                z2 bf[GB / 4];
 #pragma unroll
-            for (int u = 0; u < RMAX; u++) {
-                const int e = tid + u * nt;
-                if (e < np) {
-                    const int j = e / kw, r = e - j * kw;
-                    if (j < kb || j >= kb + kw) {
-                        z2 v = zmk(0, 0);
-                        for (int q = 0; q < kw; q++) zfma(v, Dk[r * DLD + q], S[(kb + q) * ld + j]);
-                        res[u] = v;
-                    }
+                for (int s4 = 0; s4 < GB / 4; s4++) {
+                    const int q = 4 * s4 + t;
+                    bf[s4] = (q < kw && col < m) ? S[(kb + q) * ld + col] : zmk(0, 0);
                 }
-            }
-            __syncthreads();
 #pragma unroll
-            for (int u = 0; u < RMAX; u++) {
-                const int e = tid + u * nt;
-                if (e < np) {
-                    const int j = e / kw, r = e - j * kw;
-                    if (j < kb || j >= kb + kw) S[(kb + r) * ld + j] = res[u];
+                for (int rt = 0; rt < GB / 8; rt++) {
+                    if (8 * rt >= kw) break;
+                    z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
+#pragma unroll
+                    for (int s4 = 0; s4 < GB / 4; s4++) {
+                        if (4 * s4 >= kw) break;
+                        const int r = 8 * rt + g, q = 4 * s4 + t;
+                        const z2 a = (r < kw && q < kw) ? Dk[r * DLD + q] : zmk(0, 0);
+                        dmma(c0.x, c1.x, a.x, bf[s4].x);    // C += A B
+                        dmma(c0.x, c1.x, -a.y, bf[s4].y);
+                        dmma(c0.y, c1.y, a.x, bf[s4].y);
+                        dmma(c0.y, c1.y, a.y, bf[s4].x);
+                    }
+                    const int r = 8 * rt + g, cA = j0 + 2 * t;
+                    if (r < kw && cA < m) S[(kb + r) * ld + cA] = c0;
+                    if (r < kw && cA + 1 < m) S[(kb + r) * ld + cA + 1] = c1;
                 }
             }
             __syncthreads();
@@ -270,32 +277,41 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
             }
         }
         __syncthreads();
-        // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K), S[K, K] = Dk  (pairs (i, c), i fastest)
+        // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K) on the tensor cores, one warp per 8-row strip (its old
+        //      8 x 32 block loaded as A fragments before it writes); S[K, K] = Dk
         {
-            z2 res[RMAX];
-            const int np = kw * m;
+            const int mt = (m + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
+            for (int strip = tid >> 5; strip < mt; strip += nt >> 5) {
+                const int i0 = strip * 8, row = i0 + g;
+                if (i0 >= kb && i0 < kb + kw) continue;
+                z2 af[GB / 4];
 #pragma unroll
-            for (int u = 0; u < RMAX; u++) {
-                const int e = tid + u * nt;
-                if (e < np) {
-                    const int c = e / m, i = e - c * m;
-                    if (i >= kb && i < kb + kw) {
-                        res[u] = Dk[(i - kb) * DLD + c];
-                    } else {
-                        z2 v = zmk(0, 0);
-                        for (int q = 0; q < kw; q++) zfms(v, S[i * ld + kb + q], Dk[q * DLD + c]);
-                        res[u] = v;
+                for (int s4 = 0; s4 < GB / 4; s4++) {
+                    const int q = 4 * s4 + t;
+                    af[s4] = (q < kw && row < m) ? S[row * ld + kb + q] : zmk(0, 0);
+                }
+#pragma unroll
+                for (int ct = 0; ct < GB / 8; ct++) {
+                    if (8 * ct >= kw) break;
+                    z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
+#pragma unroll
+                    for (int s4 = 0; s4 < GB / 4; s4++) {
+                        if (4 * s4 >= kw) break;
+                        const int q = 4 * s4 + t, c = 8 * ct + g;
+                        const z2 b = (q < kw && c < kw) ? Dk[q * DLD + c] : zmk(0, 0);
+                        dmma(c0.x, c1.x, -af[s4].x, b.x);   // C -= A B
+                        dmma(c0.x, c1.x, af[s4].y, b.y);
+                        dmma(c0.y, c1.y, -af[s4].x, b.y);
+                        dmma(c0.y, c1.y, -af[s4].y, b.x);
                     }
+                    const int cA = 8 * ct + 2 * t;
+                    if (row < m && cA < kw) S[row * ld + kb + cA] = c0;
+                    if (row < m && cA + 1 < kw) S[row * ld + kb + cA + 1] = c1;
                 }
             }
-            __syncthreads();
-#pragma unroll
-            for (int u = 0; u < RMAX; u++) {
-                const int e = tid + u * nt;
-                if (e < np) {
-                    const int c = e / m, i = e - c * m;
-                    S[i * ld + kb + c] = res[u];
-                }
+            for (int e = tid; e < kw * kw; e += nt) {
+                const int r = e / kw, c = e - r * kw;
+                S[(kb + r) * ld + kb + c] = Dk[r * DLD + c];
             }
             __syncthreads();
         }
