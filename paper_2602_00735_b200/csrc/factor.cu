@@ -445,25 +445,41 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
         __syncthreads();
         if (tid < GJW * 32) warp_gj(Dk, kw, kb, bad);
         __syncthreads();
-        // ---- row panel: A[K,j] = Dk A[K,j] for this CTA's columns (tiles of BT / GB columns)
+        // ---- row panel: A[K,j] = Dk A[K,j] for this CTA's columns on the tensor cores; one warp per 8-column strip
+        //      loads the strip's old 32 x 8 block as B fragments first, then writes its four row tiles (in place)
         {
-            const int per = BT / GB;
-            for (int jt = c0; jt < c1; jt += per) {
-                const int jj = tid / GB, r = tid - jj * GB, j = jt + jj;
-                const bool act = j < c1 && r < kw;
-                if (act) AKj[jj * GB + r] = A[(long long)j * m + kb + r];
-                __syncthreads();
-                if (act) {
-                    z2 v;
-                    if (j >= kb && j < kb + kw) {
-                        v = Dk[r * DLD + (j - kb)];
-                    } else {
-                        v = zmk(0, 0);
-                        for (int q = 0; q < kw; q++) zfma(v, Dk[r * DLD + q], AKj[jj * GB + q]);
-                    }
-                    A[(long long)j * m + kb + r] = v;
+            const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+            for (int j0 = c0 + (tid >> 5) * 8; j0 < c1; j0 += (BT >> 5) * 8) {
+                const int col = j0 + g;
+                z2 bf[GB / 4];
+#pragma unroll
+                for (int s4 = 0; s4 < GB / 4; s4++) {
+                    const int q = 4 * s4 + t;
+                    bf[s4] = (q < kw && col < c1) ? A[(long long)col * m + kb + q] : zmk(0, 0);
                 }
-                __syncthreads();
+#pragma unroll
+                for (int rt = 0; rt < GB / 8; rt++) {
+                    if (8 * rt >= kw) break;
+                    z2 v0 = zmk(0, 0), v1 = zmk(0, 0);
+#pragma unroll
+                    for (int s4 = 0; s4 < GB / 4; s4++) {
+                        if (4 * s4 >= kw) break;
+                        const int r = 8 * rt + g, q = 4 * s4 + t;
+                        const z2 a = (r < kw && q < kw) ? Dk[r * DLD + q] : zmk(0, 0);
+                        dmma(v0.x, v1.x, a.x, bf[s4].x);   // C += A B
+                        dmma(v0.x, v1.x, -a.y, bf[s4].y);
+                        dmma(v0.y, v1.y, a.x, bf[s4].y);
+                        dmma(v0.y, v1.y, a.y, bf[s4].x);
+                    }
+                    // outputs: row 8 rt + g of K, columns j0 + 2t, j0 + 2t + 1
+                    const int r = 8 * rt + g;
+                    for (int u = 0; u < 2; u++) {
+                        const int cc = j0 + 2 * t + u;
+                        if (r >= kw || cc >= c1) continue;
+                        const bool kcol = cc >= kb && cc < kb + kw;
+                        A[(long long)cc * m + kb + r] = kcol ? Dk[r * DLD + (cc - kb)] : (u ? v1 : v0);
+                    }
+                }
             }
         }
         cluster_sync_all();
