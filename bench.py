@@ -2,7 +2,8 @@
 
 A step is one right-preconditioned GMRES(50) Arnoldi iteration over the whole hot path:
 RAS-PML apply (restrict -> twisted block-tridiagonal local solves -> owner write), 7-point SpMV, CGS2
-orthogonalisation, Givens update on the host.  `value` = RAS-PML preconditioner applications per second
+orthogonalisation with the re-orthogonalisation delayed one step (DCGS2: two sweeps over the basis per step), Givens
+update on the host.  `value` = RAS-PML preconditioner applications per second
 (Arnoldi steps plus the cycle-end x-updates they trigger) over exactly K steps, all inputs resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
@@ -135,6 +136,9 @@ def run_ours(args):
     t0 = time.time()
     ctx = Context(cfg.k, cfg.nsub, cfg.nsub, rank=rank, nranks=world, stream=stream, nccl_id=nccl_id)
     ctx.factor()
+    if args.orth == "cgs2":
+        from paper_2602_00735_b200.helm import ORTH_CGS2
+        ctx.set_orthogonalisation(ORTH_CGS2)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     lay = ctx.layout.as_dict()
@@ -202,22 +206,32 @@ def run_ours(args):
     e2e_s = time.perf_counter() - t1
     n = ctx.n
     cycles = einfo.restarts + 1
-    h2d = 16 * n * 2 + 8 * cycles + 16 * args.steps          # b, x0; per-cycle beta; y coefficients
-    d2h = 16 * n + sum(16 * (min(j % cfg.restart, cfg.restart - 1) + 2) for j in range(args.steps)) + 8 * (cycles + 1)
+    h2d = 16 * n * 2 + 16 * args.steps                        # b, x0; y coefficients
+    if args.orth == "cgs2":
+        h2d += 8 * cycles                                       # per-cycle beta
+    if args.orth == "cgs2":   # one Hessenberg column per step
+        d2h = 16 * n + sum(16 * (min(j % cfg.restart, cfg.restart - 1) + 2) for j in range(args.steps)) + 8 * (cycles + 1)
+    else:   # DCGS2: the step record (2 x 64 + 2 complex) per step, the closed column per cycle
+        d2h = 16 * n + 16 * 130 * args.steps + 16 * (cfg.restart + 1) * cycles + 8 * (cycles + 1)
 
     hbm, peak_src = peaks()
 
-    # TTS roofline: bytes the solve must move at the kernels' algorithmic rates -- every Arnoldi step j
-    # (0-based within its cycle) moves apply + SpMV + CGS2 16 n (3 (j + 1) + 7) (multidot, fused axpy+dot, multiaxpy,
-    # scale); every cycle end adds the basis combination 16 n (m + 1), one apply, the update and a residual.
+    # TTS roofline: bytes the solve must move at the kernels' algorithmic rates (tts_bytes below).
     def tts_bytes(its, restarts):
+        """Algorithmic bytes of the whole solve: per Arnoldi step the apply, the SpMV and the orthogonalisation
+        sweeps (DCGS2: projection sweep over V_{j+1} and w, update sweep reading V_j, u_j, w and writing v_j,
+        u_{j+1}; CGS2: three sweeps over V_{j+1} plus w traffic); per cycle u_0 = r, the closing projection, the
+        combination V y, one apply, x += z and the true residual."""
         n16 = 16 * ctx.n
+        cgs2 = args.orth == "cgs2"
         tot, left = 0, its
         for _ in range(restarts + 1):
             m = min(cfg.restart, left)
             for j in range(m):
-                tot += lay["apply_bytes"] + lay["spmv_bytes"] + n16 * (3 * (j + 1) + 7)
-            tot += n16 * (m + 1) + lay["apply_bytes"] + 3 * n16 + lay["spmv_bytes"] + n16
+                orth = 3 * (j + 1) + 7 if cgs2 else 2 * (j + 1) + 4
+                tot += lay["apply_bytes"] + lay["spmv_bytes"] + n16 * orth
+            close = 0 if cgs2 else m + 1
+            tot += n16 * (2 + close + m + 1) + lay["apply_bytes"] + 3 * n16 + lay["spmv_bytes"] + n16
             left -= m
         return tot
 
@@ -238,7 +252,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {**workload_desc(cfg, lay), "parallelism": f"subdomain-sharded x{world}",
+        "config": {**workload_desc(cfg, lay), "parallelism": f"subdomain-sharded x{world}", "orth": args.orth,
                    "l2": "inputs larger than L2: %.1f GB of factor blocks streamed per apply vs 126 MB L2"
                          % (lay["apply_bytes"] / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -450,6 +464,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper Table 4 comparison rows")
+    ap.add_argument("--orth", default="dcgs2", choices=["dcgs2", "cgs2"],
+                    help="GMRES orthogonalisation (DESIGN.md 5.6); cgs2 = the undelayed form, for A/B")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -138,9 +138,22 @@ int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host)
 
 /* Right-preconditioned restarted GMRES(restart), 1 <= restart <= 63, on A (B^-1 u) = b, x = B^-1 u (D13):
  * x_dev in: initial guess, out: solution.  rtol on ||b - A x|| / ||b||; rtol <= 0 runs exactly maxit
- * iterations.  Synchronous.  Returns HELM_OK / HELM_NOT_CONVERGED / HELM_BREAKDOWN or an error. */
+ * iterations.  Synchronous.  Returns HELM_OK / HELM_NOT_CONVERGED / HELM_BREAKDOWN or an error.
+ * Orthogonalisation: classical Gram-Schmidt with one re-orthogonalisation pass (CGS2), by default with that pass
+ * delayed into the next step's projection sweep (DCGS2: two sweeps over the basis per step instead of
+ * three; the same vectors in exact arithmetic); helm_set_orthogonalisation selects the undelayed form. */
 int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, double rtol, int maxit,
                helm_gmres_info* info);
+
+enum { HELM_ORTH_DCGS2 = 0, HELM_ORTH_CGS2 = 1 };
+/* GMRES orthogonalisation of this context (default HELM_ORTH_DCGS2).  HELM_EINVAL for another mode.  Every rank of
+ * a multi-rank run must select the same mode. */
+int helm_set_orthogonalisation(helm_ctx* ctx, int mode);
+
+/* Copy the first nv vectors of the GMRES basis left by the last helm_gmres call (V slots 0 .. nv-1, each n_local
+ * values, x-fastest) to out_dev (nv * n_local values; device memory).  Diagnostic (orthogonality tests).
+ * HELM_ESTATE before any helm_gmres, HELM_EINVAL if nv exceeds the basis capacity (largest restart + 1 so far). */
+int helm_get_krylov_basis(helm_ctx* ctx, int nv, helm_z* out_dev);
 
 /* Same with host b / x (copied in and out inside the call). */
 int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int restart, double rtol, int maxit,

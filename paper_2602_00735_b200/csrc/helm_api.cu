@@ -304,7 +304,14 @@ struct helm_ctx {
     z2* d_zpart = nullptr;
     double* d_dpart = nullptr;
     int nblk = 148 * 4;
-    z2* h_pin = nullptr;   // pinned host staging for H columns / y (NVMAX complex)
+    z2* h_pin = nullptr;   // pinned host staging for y / norms (NVMAX complex)
+    z2* h_hc = nullptr;    // pinned host slots: Hessenberg columns (CGS2) / the DCGS2 step record
+    // DCGS2: device Hessenberg (NVMAX + 1) x NVMAX, reduced sweep sums, sweep-2 coefficients, step
+    // record for the host (final column j - 1, pending column j, nu_j, ||u_{j+1}||)
+    z2 *d_H = nullptr, *d_dots = nullptr, *d_ca = nullptr, *d_ce = nullptr, *d_hout = nullptr;
+    double* d_sc = nullptr;
+    bool orth_cgs2 = false;   // helm_set_orthogonalisation(HELM_ORTH_CGS2): the undelayed CGS2
+    cudaEvent_t ev_hc[2] = {nullptr, nullptr};
 
     // profiling of the apply kernel
     bool prof = false;
@@ -539,9 +546,16 @@ int ensure_krylov(helm_ctx* ctx, int restart)
             (rc = dalloc(ctx, &ctx->d_r, n)) || (rc = dalloc(ctx, &ctx->d_h1, NVMAX)) ||
             (rc = dalloc(ctx, &ctx->d_h2, NVMAX)) || (rc = dalloc(ctx, &ctx->d_Hcol, NVMAX)) ||
             (rc = dalloc(ctx, &ctx->d_y, NVMAX)) || (rc = dalloc(ctx, &ctx->d_norm, 4)) ||
-            (rc = dalloc(ctx, &ctx->d_zpart, (size_t)ctx->nblk * NVMAX)) || (rc = dalloc(ctx, &ctx->d_dpart, ctx->nblk)))
+            (rc = dalloc(ctx, &ctx->d_zpart, (size_t)ctx->nblk * 2 * NVMAX)) || (rc = dalloc(ctx, &ctx->d_dpart, ctx->nblk)) ||
+            (rc = dalloc(ctx, &ctx->d_H, (size_t)(NVMAX + 1) * NVMAX)) || (rc = dalloc(ctx, &ctx->d_dots, 2 * NVMAX)) ||
+            (rc = dalloc(ctx, &ctx->d_ca, NVMAX)) || (rc = dalloc(ctx, &ctx->d_ce, NVMAX)) ||
+            (rc = dalloc(ctx, &ctx->d_hout, 2 * NVMAX + 2)) || (rc = dalloc(ctx, &ctx->d_sc, 4)))
             return rc;
         CK(cudaMallocHost((void**)&ctx->h_pin, sizeof(z2) * NVMAX));
+        CK(cudaMallocHost((void**)&ctx->h_hc, sizeof(z2) * 2 * (2 * NVMAX + 2)));
+
+
+        for (auto& e : ctx->ev_hc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     if (restart + 1 > ctx->V_cap) {
         if (ctx->d_V) cudaFree(ctx->d_V);
@@ -854,7 +868,7 @@ int residual_host(helm_ctx* ctx, const z2* b, const z2* x, z2* r, double* out)
 }
 
 // Right-preconditioned restarted GMRES (O9 of DESIGN.md), classical Gram-Schmidt with one
-// re-orthogonalisation pass (CGS2) on the device, Givens rotations on the host.
+// re-orthogonalisation pass (CGS2) on the device, Givens rotations on the host one step behind the device.
 int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int maxit, helm_gmres_info* info)
 {
     NvtxRange nv_("helm.gmres");
@@ -892,77 +906,193 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
     int its = 0, cycles = 0;
     double est = beta / beta0;
     z2* V = ctx->d_V;
+    std::vector<cplx> Hraw((size_t)(m + 1) * m), gkeep(m + 1);
+    auto Rij = [&](int i, int j) -> cplx& { return Hraw[(size_t)i * m + j]; };
+    // Givens rotation of column jc from its unrotated copy (DCGS2 revisits a column once it is final)
+    auto rotate_col = [&](int jc) {
+        for (int i = 0; i <= jc + 1; i++) Hij(i, jc) = Rij(i, jc);
+        for (int i = 0; i < jc; i++) {
+            const cplx a = Hij(i, jc), c = Hij(i + 1, jc);
+            Hij(i, jc) = cs[i] * a + sn[i] * c;
+            Hij(i + 1, jc) = -std::conj(sn[i]) * a + cs[i] * c;
+        }
+        const cplx a = Hij(jc, jc), bb = Hij(jc + 1, jc);
+        if (a == cplx(0, 0)) {
+            cs[jc] = 0.0;
+            sn[jc] = 1.0;
+            Hij(jc, jc) = bb;
+        } else {
+            const double rho = sqrt(std::norm(a) + std::norm(bb));
+            const cplx ph = a / std::abs(a);
+            cs[jc] = std::abs(a) / rho;
+            sn[jc] = ph * std::conj(bb) / rho;
+            Hij(jc, jc) = ph * rho;
+        }
+        Hij(jc + 1, jc) = 0.0;
+        const cplx gs = gkeep[jc];
+        g[jc] = cs[jc] * gs;
+        g[jc + 1] = -std::conj(sn[jc]) * gs;
+        gkeep[jc + 1] = g[jc + 1];
+    };
     while (true) {
-        // v_0 = r / ||r||
-        memcpy(ctx->h_pin, &beta, sizeof(double));
-        CK(cudaMemcpyAsync(ctx->d_norm, ctx->h_pin, sizeof(double), cudaMemcpyHostToDevice, s));
-        launch_scale_by_norm(ctx->d_r, ctx->d_norm, V, n, s);
+        int jend = 0;
+        if (ctx->orth_cgs2) {
+            // v_0 = r / ||r||
+            memcpy(ctx->h_pin, &beta, sizeof(double));
+            CK(cudaMemcpyAsync(ctx->d_norm, ctx->h_pin, sizeof(double), cudaMemcpyHostToDevice, s));
+            launch_scale_by_norm(ctx->d_r, ctx->d_norm, V, n, s);
+            ctx->launches++;
+            std::fill(g.begin(), g.end(), cplx(0, 0));
+            g[0] = beta;
+            // (a one-step lookahead -- enqueueing step j + 1 before the host's Givens update of column j -- was
+            // measured: no gain at c3, one discarded apply per solve)
+            auto enqueue_step = [&](int j) -> int {
+                z2* vj = V + (long long)j * n;
+                int rc2;
+                if ((rc2 = apply_impl(ctx, vj, ctx->d_z))) return rc2;
+                inf->applies++;
+                if ((rc2 = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc2;
+                // CGS2: h1 = V^H w; w -= V h1; h2 = V^H w; w -= V h2; H(:,j) = h1 + h2; H(j+1,j) = ||w||
+                // (the first update and the second projection share one sweep over V: k_axpy_dot)
+                NvtxRange nv_o("helm.orth");
+                launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+                launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h1, nullptr, nullptr, s);
+                if ((rc2 = allreduce(ctx, (double*)ctx->d_h1, 2 * (size_t)(j + 1)))) return rc2;
+                launch_axpy_dot(V, n, j + 1, ctx->d_h1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+                if (!ctx->multi) {
+                    launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, ctx->d_Hcol, ctx->d_h1, s);
+                } else {
+                    launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, nullptr, nullptr, s);
+                    if ((rc2 = allreduce(ctx, (double*)ctx->d_h2, 2 * (size_t)(j + 1)))) return rc2;
+                    launch_zadd(ctx->d_h1, ctx->d_h2, ctx->d_Hcol, j + 1, s);
+                    ctx->launches++;
+                }
+                launch_multiaxpy(V, n, j + 1, ctx->d_h2, ctx->d_w, n, ctx->d_dpart, ctx->nblk, s);
+                ctx->launches += 5;   // multidot, axpy_dot, 2x reduce, multiaxpy
+                if ((rc2 = finish_norm(ctx, ctx->d_Hcol + j + 1))) return rc2;
+                launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
+                ctx->launches++;
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(ctx->h_hc + (j & 1) * NVMAX, ctx->d_Hcol, sizeof(z2) * (j + 2),
+                                   cudaMemcpyDeviceToHost, s));
+                CK(cudaEventRecord(ctx->ev_hc[j & 1], s));
+                return HELM_OK;
+            };
+            for (int j = 0; j < m; j++) {
+                if ((rc = enqueue_step(j))) return rc;
+                its++;
+                CK(cudaEventSynchronize(ctx->ev_hc[j & 1]));
+                const z2* hc = ctx->h_hc + (j & 1) * NVMAX;
+                for (int i = 0; i <= j + 1; i++) Hij(i, j) = cplx(hc[i].x, hc[i].y);
+                const double hn = Hij(j + 1, j).real();
+                if (!std::isfinite(hn)) {
+                    inf->iterations = its;
+                    inf->status = HELM_BREAKDOWN;
+                    return set_err(ctx, HELM_BREAKDOWN, "non-finite Arnoldi norm at iteration %d", its);
+                }
+                for (int i = 0; i < j; i++) {   // previous rotations
+                    const cplx a = Hij(i, j), c = Hij(i + 1, j);
+                    Hij(i, j) = cs[i] * a + sn[i] * c;
+                    Hij(i + 1, j) = -std::conj(sn[i]) * a + cs[i] * c;
+                }
+                const cplx a = Hij(j, j), bb = Hij(j + 1, j);   // new rotation
+                if (a == cplx(0, 0)) {
+                    cs[j] = 0.0;
+                    sn[j] = 1.0;
+                    Hij(j, j) = bb;
+                } else {
+                    const double rho = sqrt(std::norm(a) + std::norm(bb));
+                    const cplx ph = a / std::abs(a);
+                    cs[j] = std::abs(a) / rho;
+                    sn[j] = ph * std::conj(bb) / rho;
+                    Hij(j, j) = ph * rho;
+                }
+                Hij(j + 1, j) = 0.0;
+                g[j + 1] = -std::conj(sn[j]) * g[j];
+                g[j] = cs[j] * g[j];
+                est = std::abs(g[j + 1]) / beta0;
+                if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
+                jend = j + 1;
+                if ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || hn == 0.0 || its >= maxit) break;
+            }
+        } else {
+        // DCGS2: u_0 = r; step j applies the operator to the candidate u_j (V slot j), then one
+        // projection sweep and one update sweep over V; column j - 1 becomes final in step j, column j is used
+        // tentatively (its subdiagonal = ||u_{j+1}|| before re-orthogonalisation) for the convergence test and is
+        // closed with one extra projection sweep when the cycle ends.
+        launch_copy(V, ctx->d_r, n, s);
         ctx->launches++;
         std::fill(g.begin(), g.end(), cplx(0, 0));
-        g[0] = beta;
-        int jend = 0;
-        for (int j = 0; j < m; j++) {
-            z2* vj = V + (long long)j * n;
-            if ((rc = apply_impl(ctx, vj, ctx->d_z))) return rc;
+        constexpr int REC = 2 * NVMAX + 2;   // step record: final column j - 1, pending column j, nu_j, ||u_{j+1}||
+        auto enqueue_step = [&](int j) -> int {
+            z2* uj = V + (long long)j * n;
+            int rc2;
+            if ((rc2 = apply_impl(ctx, uj, ctx->d_z))) return rc2;
             inf->applies++;
-            if ((rc = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc;
-            its++;
-            // CGS2: h1 = V^H w; w -= V h1; h2 = V^H w; w -= V h2; H(:,j) = h1 + h2; H(j+1,j) = ||w||
-            // (the first update and the second projection share one sweep over V: k_axpy_dot)
-            {
+            if ((rc2 = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc2;
             NvtxRange nv_o("helm.orth");
-            launch_multidot(V, n, j + 1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
-            launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h1, nullptr, nullptr, s);
-            if ((rc = allreduce(ctx, (double*)ctx->d_h1, 2 * (size_t)(j + 1)))) return rc;
-            launch_axpy_dot(V, n, j + 1, ctx->d_h1, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
-            if (!ctx->multi) {
-                launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, ctx->d_Hcol, ctx->d_h1, s);
-            } else {
-                launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_h2, nullptr, nullptr, s);
-                if ((rc = allreduce(ctx, (double*)ctx->d_h2, 2 * (size_t)(j + 1)))) return rc;
-                launch_zadd(ctx->d_h1, ctx->d_h2, ctx->d_Hcol, j + 1, s);
-                ctx->launches++;
-            }
-            launch_multiaxpy(V, n, j + 1, ctx->d_h2, ctx->d_w, n, ctx->d_dpart, ctx->nblk, s);
-            ctx->launches += 5;   // multidot, axpy_dot, 2x reduce, multiaxpy
-            if ((rc = finish_norm(ctx, ctx->d_Hcol + j + 1))) return rc;
-            launch_scale_by_norm(ctx->d_w, ctx->d_norm, V + (long long)(j + 1) * n, n, s);
-            ctx->launches++;
-            }
+            launch_multidot2(V, n, j + 1, uj, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+            launch_reduce_z2(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_dots, s);
+            if ((rc2 = allreduce(ctx, (double*)ctx->d_dots, 2 * (size_t)(j + 1))) ||
+                (rc2 = allreduce(ctx, (double*)(ctx->d_dots + NVMAX), 2 * (size_t)(j + 1))))
+                return rc2;
+            launch_dcgs2_coef(ctx->d_dots, j, ctx->d_H, ctx->d_ca, ctx->d_ce, ctx->d_sc, ctx->d_hout, s);
+            launch_dcgs2_update(V, n, j, ctx->d_w, ctx->d_ca, ctx->d_ce, ctx->d_sc, n, ctx->d_dpart, ctx->nblk, s);
+            ctx->launches += 4;
+            if ((rc2 = finish_norm(ctx, ctx->d_hout + 2 * NVMAX + 1))) return rc2;
             CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_Hcol, sizeof(z2) * (j + 2), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            for (int i = 0; i <= j + 1; i++) Hij(i, j) = cplx(ctx->h_pin[i].x, ctx->h_pin[i].y);
-            const double hn = Hij(j + 1, j).real();
-            if (!std::isfinite(hn)) {
+            CK(cudaMemcpyAsync(ctx->h_hc, ctx->d_hout, sizeof(z2) * REC, cudaMemcpyDeviceToHost, s));
+            CK(cudaEventRecord(ctx->ev_hc[0], s));
+            return HELM_OK;
+        };
+        // (queueing step j + 1 before the host's update of step j -- step j + 1 needs only device data -- was
+        // measured at c3: 93.59 vs 93.56 applies/s, within noise, so the host waits for each step record)
+        for (int j = 0; j < m; j++) {
+            if ((rc = enqueue_step(j))) return rc;
+            its++;
+            CK(cudaEventSynchronize(ctx->ev_hc[0]));
+            const z2* hc = ctx->h_hc;
+            const double nu = hc[2 * NVMAX].x, un = hc[2 * NVMAX + 1].x;
+            if (!std::isfinite(nu) || !std::isfinite(un)) {
                 inf->iterations = its;
                 inf->status = HELM_BREAKDOWN;
                 return set_err(ctx, HELM_BREAKDOWN, "non-finite Arnoldi norm at iteration %d", its);
             }
-            for (int i = 0; i < j; i++) {   // previous rotations
-                const cplx a = Hij(i, j), c = Hij(i + 1, j);
-                Hij(i, j) = cs[i] * a + sn[i] * c;
-                Hij(i + 1, j) = -std::conj(sn[i]) * a + cs[i] * c;
-            }
-            const cplx a = Hij(j, j), bb = Hij(j + 1, j);   // new rotation
-            if (a == cplx(0, 0)) {
-                cs[j] = 0.0;
-                sn[j] = 1.0;
-                Hij(j, j) = bb;
+            if (j == 0) {
+                g[0] = gkeep[0] = nu;   // ||r|| from the same sweep that normalises v_0
             } else {
-                const double rho = sqrt(std::norm(a) + std::norm(bb));
-                const cplx ph = a / std::abs(a);
-                cs[j] = std::abs(a) / rho;
-                sn[j] = ph * std::conj(bb) / rho;
-                Hij(j, j) = ph * rho;
+                for (int i = 0; i <= j; i++) Rij(i, j - 1) = cplx(hc[i].x, hc[i].y);
+                rotate_col(j - 1);
+                est = std::abs(g[j]) / beta0;
+                if (inf->history && its - 2 < inf->history_cap) inf->history[its - 2] = est;
+                if (nu == 0.0) {   // invariant subspace found one column late: step j is discarded
+                    its--;
+                    jend = j;
+                    break;
+                }
             }
-            Hij(j + 1, j) = 0.0;
-            g[j + 1] = -std::conj(sn[j]) * g[j];
-            g[j] = cs[j] * g[j];
+            for (int i = 0; i <= j; i++) Rij(i, j) = cplx(hc[NVMAX + i].x, hc[NVMAX + i].y);
+            Rij(j + 1, j) = un;   // tentative
+            rotate_col(j);
             est = std::abs(g[j + 1]) / beta0;
             if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
             jend = j + 1;
-            if ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || hn == 0.0 || its >= maxit) break;
+            if ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || un == 0.0 || its >= maxit || j == m - 1) {
+                // close column j: re-orthogonalise u_{j+1} against V_{j+1}
+                launch_multidot(V, n, j + 2, V + (long long)(j + 1) * n, n, ctx->d_zpart, ctx->nblk, s);
+                launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 2, ctx->d_dots, nullptr, nullptr, s);
+                if ((rc = allreduce(ctx, (double*)ctx->d_dots, 2 * (size_t)(j + 2)))) return rc;
+                launch_dcgs2_close(ctx->d_dots, j, ctx->d_H, ctx->d_hout, s);
+                ctx->launches += 3;
+                CK(cudaMemcpyAsync(ctx->h_pin, ctx->d_hout, sizeof(z2) * (j + 2), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                for (int i = 0; i <= j + 1; i++) Rij(i, j) = cplx(ctx->h_pin[i].x, ctx->h_pin[i].y);
+                rotate_col(j);
+                est = std::abs(g[j + 1]) / beta0;
+                if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
+                break;
+            }
+        }
         }
         // H y = g (upper triangular), t = V y, x += B^-1 t
         for (int i = jend - 1; i >= 0; i--) {
@@ -1051,6 +1181,25 @@ int richardson_impl(helm_ctx* ctx, const z2* b, z2* x, double rtol, int maxit, h
 }  // namespace
 
 // ===================================================================================================== C ABI
+
+int helm_get_krylov_basis(helm_ctx* ctx, int nv, helm_z* out_dev)
+{
+    if (!ctx) return HELM_EINVAL;
+    if (!ctx->d_V) return set_err(ctx, HELM_ESTATE, "helm_get_krylov_basis before helm_gmres");
+    if (nv < 1 || nv > ctx->V_cap || !out_dev) return set_err(ctx, HELM_EINVAL, "helm_get_krylov_basis: nv %d", nv);
+    CK(cudaMemcpyAsync(out_dev, ctx->d_V, sizeof(z2) * ctx->n_local * nv, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HELM_OK;
+}
+
+int helm_set_orthogonalisation(helm_ctx* ctx, int mode)
+{
+    if (!ctx) return HELM_EINVAL;
+    if (mode != HELM_ORTH_DCGS2 && mode != HELM_ORTH_CGS2)
+        return set_err(ctx, HELM_EINVAL, "helm_set_orthogonalisation: mode %d", mode);
+    ctx->orth_cgs2 = mode == HELM_ORTH_CGS2;
+    return HELM_OK;
+}
 
 int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rtol, int maxit,
                     helm_richardson_info* info)
@@ -1536,7 +1685,8 @@ void helm_destroy(helm_ctx* ctx)
     void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
                     ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq,
-                    ctx->d_pou, ctx->d_candx, ctx->d_candy, ctx->d_cext};
+                    ctx->d_pou, ctx->d_candx, ctx->d_candy, ctx->d_cext, ctx->d_H, ctx->d_dots, ctx->d_ca,
+                    ctx->d_ce, ctx->d_hout, ctx->d_sc};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int q = 0; q < 4; q++) {
@@ -1544,6 +1694,9 @@ void helm_destroy(helm_ctx* ctx)
         if (ctx->d_recvbuf[q]) cudaFree(ctx->d_recvbuf[q]);
     }
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    if (ctx->h_hc) cudaFreeHost(ctx->h_hc);
+    for (auto e : ctx->ev_hc)
+        if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_free) cudaEventDestroy(e);
     for (auto& pr : ctx->ev_used) {
         cudaEventDestroy(pr.first);

@@ -174,6 +174,13 @@ void launch_axpy_dot(const z2* V, long long ldv, int nv, const z2* h, z2* w, lon
 void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, long long n, double* partial_norm,
                       int nblk, cudaStream_t s);
 void launch_reduce_z(const z2* partial, int nblk, int nv, z2* out, z2* out_plus, const z2* add, cudaStream_t s);
+void launch_multidot2(const z2* V, long long ldv, int nv, const z2* u, const z2* w, long long n, z2* partial, int nblk,
+                      cudaStream_t s);
+void launch_reduce_z2(const z2* partial, int nblk, int nv, z2* out, cudaStream_t s);
+void launch_dcgs2_coef(const z2* d, int j, z2* H, z2* ca, z2* ce, double* sc, z2* out, cudaStream_t s);
+void launch_dcgs2_close(const z2* d, int j, z2* H, z2* out, cudaStream_t s);
+void launch_dcgs2_update(z2* V, long long ldv, int j, const z2* w, const z2* ca, const z2* ce, const double* sc,
+                         long long n, double* partial, int nblk, cudaStream_t s);
 void launch_reduce_norm(const double* partial, int nblk, z2* out_slot, double* out_norm, cudaStream_t s);
 void launch_scale_by_norm(const z2* w, const double* norm, z2* v, long long n, cudaStream_t s);
 void launch_combine(const z2* V, long long ldv, int nv, const z2* y, z2* t, long long n, cudaStream_t s);

@@ -263,14 +263,194 @@ __global__ void __launch_bounds__(KT) k_multiaxpy(const z2* __restrict__ V, long
     }
 }
 
+// ---------------------------------------------------------------------------------------------------------------------
+// DCGS2: CGS2 with the re-orthogonalisation of v_j delayed into the projection sweep of step j + 1.
+// Step j holds V_j = [v_0 .. v_{j-1}] (final), the candidate u_j (V slot j, projected once) and w_j = A B^-1 u_j.
+//   sweep 1  (k_multidot2)  a = V_j^H u_j, alpha = u_j^H u_j, b = V_j^H w_j, c = u_j^H w_j          (reads V once)
+//   coeffs   (k_dcgs2_coef) nu = sqrt(alpha - |a|^2); column j-1 of H += a, H(j, j-1) = nu (final);
+//                           p = H(0:j, 0:j) a, q = nu a_{j-1}; column j of H (pending): h = (b - p) / nu,
+//                           h_jj = ((c - a^H b) / nu - q) / nu
+//   sweep 2  (k_dcgs2_update) v_j = (u_j - V_j a) / nu;  u_{j+1} = w_j / nu - (sigma / nu) u_j - V_j e,
+//                           sigma = q / nu + h_jj, e = p / nu + h - a sigma / nu                   (reads V once)
+// which is CGS2's v_j and u_{j+1} = A B^-1 v_j - V_{j+1} h in exact arithmetic (A B^-1 V_j = V_{j+1} H(0:j+1, 0:j)).
+
+// partial[blk][q] = sum_e conj(V_q[e]) u[e] (q < nv), partial[blk][NVMAX + q] = sum_e conj(V_q[e]) w[e]
+template <int R>
+__global__ void __launch_bounds__(KT) k_multidot2(const z2* __restrict__ V, long long ldv, int nv,
+                                                  const z2* __restrict__ u, const z2* __restrict__ w, long long n,
+                                                  z2* __restrict__ partial)
+{
+    __shared__ z2 acc[KT / 32][2 * NVMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int v = lane; v < 2 * NVMAX; v += 32) acc[warp][v] = zmk(0, 0);
+    __syncwarp();
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    for (long long base = r0; base < r1; base += (long long)KT * R) {
+        z2 uv[R], wv[R];
+        long long e[R];
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+            e[q] = base + q * KT + threadIdx.x;
+            uv[q] = e[q] < r1 ? __ldg(u + e[q]) : zmk(0, 0);
+            wv[q] = e[q] < r1 ? __ldg(w + e[q]) : zmk(0, 0);
+        }
+        for (int v = 0; v < nv; v++) {
+            const z2* Vv = V + v * ldv;
+            z2 su = zmk(0, 0), sw = zmk(0, 0);
+#pragma unroll
+            for (int q = 0; q < R; q++)
+                if (e[q] < r1) {
+                    const z2 x = __ldg(Vv + e[q]);
+                    zfma_conj(su, x, uv[q]);
+                    zfma_conj(sw, x, wv[q]);
+                }
+            su = warp_sum(su);
+            sw = warp_sum(sw);
+            if (lane == 0) {
+                acc[warp][v] = zadd(acc[warp][v], su);
+                acc[warp][NVMAX + v] = zadd(acc[warp][NVMAX + v], sw);
+            }
+        }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < 2 * NVMAX; v += blockDim.x) {
+        if ((v & (NVMAX - 1)) >= nv) continue;
+        z2 s = zmk(0, 0);
+        for (int q = 0; q < KT / 32; q++) s = zadd(s, acc[q][v]);
+        partial[(long long)blockIdx.x * 2 * NVMAX + v] = s;
+    }
+}
+
+// One warp.  d: the reduced sweep-1 sums (d[q] = V_q^H u_j, d[NVMAX + q] = V_q^H w_j, q <= j).  H: device Hessenberg,
+// column-major with leading dimension NVMAX + 1.  Writes the sweep-2 coefficients ca (= a / nu), ce (= e) and
+// sc = {1 / nu, sigma / nu}, and for the host: out[0 .. j] = final column j - 1 (rows 0 .. j), out[NVMAX .. NVMAX + j]
+// = pending column j, out[2 NVMAX] = (nu, 0).
+__global__ void k_dcgs2_coef(const z2* __restrict__ d, int j, z2* __restrict__ H, z2* __restrict__ ca,
+                             z2* __restrict__ ce, double* __restrict__ sc, z2* __restrict__ out)
+{
+    constexpr int LD = NVMAX + 1;
+    __shared__ z2 as[NVMAX];
+    const int lane = threadIdx.x;
+    double na = 0.0;
+    z2 ab = zmk(0, 0);
+    for (int i = lane; i < j; i += 32) {
+        const z2 a = d[i];
+        as[i] = a;
+        na += zabs2(a);
+        zfma_conj(ab, a, d[NVMAX + i]);
+    }
+    na = warp_sum(na);
+    ab = warp_sum(ab);
+    const double alpha = d[j].x;
+    const z2 c = d[NVMAX + j];
+    const double nu2 = alpha - na;
+    const double nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+    const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
+    if (j >= 1) {   // finish column j - 1
+        for (int i = lane; i < j; i += 32) H[(j - 1) * LD + i] = zadd(H[(j - 1) * LD + i], as[i]);
+        if (lane == 0) H[(j - 1) * LD + j] = zmk(nu, 0.0);
+    }
+    __syncwarp();
+    const z2 q = j >= 1 ? zscale(as[j - 1], nu) : zmk(0, 0);
+    const z2 hjj = zscale(zsub(zscale(zsub(c, ab), inv), q), inv);
+    const z2 sigma = zadd(zscale(q, inv), hjj);
+    const z2 sinv = zscale(sigma, inv);
+    for (int i = lane; i < j; i += 32) {
+        z2 p = zmk(0, 0);   // (H(0:j, 0:j) a)_i, columns k >= i - 1 only (Hessenberg), increasing k
+        for (int k = i > 0 ? i - 1 : 0; k < j; k++) zfma(p, H[k * LD + i], as[k]);
+        const z2 h = zscale(zsub(d[NVMAX + i], p), inv);
+        H[j * LD + i] = h;
+        out[NVMAX + i] = h;
+        const z2 e = zsub(zadd(zscale(p, inv), h), zmul(as[i], sinv));
+        ce[i] = e;
+        ca[i] = zscale(as[i], inv);
+    }
+    for (int i = lane; i <= j && j >= 1; i += 32) out[i] = H[(j - 1) * LD + i];
+    if (lane == 0) {
+        H[j * LD + j] = hjj;
+        out[NVMAX + j] = hjj;
+        out[2 * NVMAX] = zmk(nu, 0.0);
+        sc[0] = inv;
+        sc[1] = sigma.x * inv;
+        sc[2] = sigma.y * inv;
+    }
+}
+
+// Close column j with the re-orthogonalisation of u_{j+1} (cycle end): d[q] = V_q^H u_{j+1}, q <= j + 1.
+// H(0:j, j) += a, H(j+1, j) = nu; out[0 .. j+1] = the final column.
+__global__ void k_dcgs2_close(const z2* __restrict__ d, int j, z2* __restrict__ H, z2* __restrict__ out)
+{
+    constexpr int LD = NVMAX + 1;
+    const int lane = threadIdx.x;
+    double na = 0.0;
+    for (int i = lane; i <= j; i += 32) na += zabs2(d[i]);
+    na = warp_sum(na);
+    const double nu2 = d[j + 1].x - na;
+    const double nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+    for (int i = lane; i <= j; i += 32) {
+        const z2 h = zadd(H[j * LD + i], d[i]);
+        H[j * LD + i] = h;
+        out[i] = h;
+    }
+    if (lane == 0) {
+        H[j * LD + j + 1] = zmk(nu, 0.0);
+        out[j + 1] = zmk(nu, 0.0);
+    }
+}
+
+// Sweep 2: slot j <- v_j = u_j / nu - sum_q ca_q V_q;  slot j + 1 <- u_{j+1} = w / nu - (sigma / nu) u_j - sum_q ce_q V_q
+// (q < j); partial[blk] = ||u_{j+1}||^2 over the block.  V slot j is read and written by the same thread.
+__global__ void __launch_bounds__(KT) k_dcgs2_update(z2* V, long long ldv, int j, const z2* __restrict__ w,
+                                                     const z2* __restrict__ ca, const z2* __restrict__ ce,
+                                                     const double* __restrict__ sc, long long n,
+                                                     double* __restrict__ partial)
+{
+    __shared__ z2 cs[2 * NVMAX];
+    __shared__ double sh[KT / 32];
+    for (int v = threadIdx.x; v < j; v += blockDim.x) {
+        cs[v] = ca[v];
+        cs[NVMAX + v] = ce[v];
+    }
+    __syncthreads();
+    const double inv = sc[0];
+    const z2 sinv = zmk(sc[1], sc[2]);
+    z2* uj = V + j * ldv;
+    z2* un = uj + ldv;
+    long long r0, r1;
+    chunk_of(n, r0, r1);
+    double s = 0.0;
+    for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
+        const z2 u = uj[e];
+        z2 av = zmk(0, 0), ev = zmk(0, 0);
+        for (int v = 0; v < j; v++) {
+            const z2 x = __ldg(V + v * ldv + e);
+            zfma(av, cs[v], x);
+            zfma(ev, cs[NVMAX + v], x);
+        }
+        const z2 vj = zsub(zscale(u, inv), av);
+        z2 nx = zscale(__ldg(w + e), inv);
+        nx = zsub(nx, zmul(sinv, u));
+        nx = zsub(nx, ev);
+        uj[e] = vj;
+        un[e] = nx;
+        s += zabs2(nx);
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
 // out[v] = sum_blk partial[blk][v]; out_plus[v] = add[v] + out[v] (if given); one CTA, index order
 __global__ void k_reduce_z(const z2* __restrict__ partial, int nblk, int nv, z2* __restrict__ out,
-                           z2* __restrict__ out_plus, const z2* __restrict__ add)
+                           z2* __restrict__ out_plus, const z2* __restrict__ add, int stride, int off2)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int v = warp; v < nv; v += blockDim.x >> 5) {
+    // values v < nv, and (off2 > 0) the second group v + off2
+    const int nval = off2 ? 2 * nv : nv;
+    for (int q = warp; q < nval; q += blockDim.x >> 5) {
+        const int v = q < nv ? q : off2 + (q - nv);
         z2 s = zmk(0, 0);
-        for (int b = lane; b < nblk; b += 32) s = zadd(s, partial[(long long)b * NVMAX + v]);
+        for (int b = lane; b < nblk; b += 32) s = zadd(s, partial[(long long)b * stride + v]);
         s = warp_sum(s);
         if (lane == 0) {
             out[v] = s;
@@ -405,7 +585,29 @@ void launch_multiaxpy(const z2* V, long long ldv, int nv, const z2* h, z2* w, lo
 }
 void launch_reduce_z(const z2* partial, int nblk, int nv, z2* out, z2* out_plus, const z2* add, cudaStream_t s)
 {
-    k_reduce_z<<<1, 512, 0, s>>>(partial, nblk, nv, out, out_plus, add);
+    k_reduce_z<<<1, 512, 0, s>>>(partial, nblk, nv, out, out_plus, add, NVMAX, 0);
+}
+void launch_multidot2(const z2* V, long long ldv, int nv, const z2* u, const z2* w, long long n, z2* partial, int nblk,
+                      cudaStream_t s)
+{
+    k_multidot2<4><<<nblk, KT, 0, s>>>(V, ldv, nv, u, w, n, partial);
+}
+void launch_reduce_z2(const z2* partial, int nblk, int nv, z2* out, cudaStream_t s)
+{
+    k_reduce_z<<<1, 512, 0, s>>>(partial, nblk, nv, out, nullptr, nullptr, 2 * NVMAX, NVMAX);
+}
+void launch_dcgs2_coef(const z2* d, int j, z2* H, z2* ca, z2* ce, double* sc, z2* out, cudaStream_t s)
+{
+    k_dcgs2_coef<<<1, 32, 0, s>>>(d, j, H, ca, ce, sc, out);
+}
+void launch_dcgs2_close(const z2* d, int j, z2* H, z2* out, cudaStream_t s)
+{
+    k_dcgs2_close<<<1, 32, 0, s>>>(d, j, H, out);
+}
+void launch_dcgs2_update(z2* V, long long ldv, int j, const z2* w, const z2* ca, const z2* ce, const double* sc,
+                         long long n, double* partial, int nblk, cudaStream_t s)
+{
+    k_dcgs2_update<<<nblk, KT, 0, s>>>(V, ldv, j, w, ca, ce, sc, n, partial);
 }
 void launch_reduce_norm(const double* partial, int nblk, z2* out_slot, double* out_norm, cudaStream_t s)
 {

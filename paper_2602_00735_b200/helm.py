@@ -79,7 +79,8 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_profile_enable", "helm_profile_read", "helm_last_error", "helm_destroy",
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
            "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
-           "helm_probe_read_bandwidth_mode"]
+           "helm_probe_read_bandwidth_mode", "helm_set_orthogonalisation",
+           "helm_get_krylov_basis"]
 
 
 def lib_path() -> str:
@@ -107,6 +108,8 @@ def load(build_if_missing: bool = True):
     L.helm_precond_apply_host.argtypes = [vp, vp, vp]
     L.helm_gmres.argtypes = [vp, vp, vp, i, d, i, C.POINTER(GmresInfo)]
     L.helm_gmres_host.argtypes = [vp, vp, vp, i, d, i, C.POINTER(GmresInfo)]
+    L.helm_set_orthogonalisation.argtypes = [vp, i]
+    L.helm_get_krylov_basis.argtypes = [vp, i, vp]
     L.helm_export_stencil.argtypes = [vp, vp]
     L.helm_profile_enable.argtypes = [vp, i]
     L.helm_profile_read.argtypes = [vp, C.POINTER(d), C.POINTER(i), C.POINTER(i)]
@@ -143,6 +146,7 @@ def _ptr(t) -> int:
 BC_DIRICHLET, BC_IMPEDANCE = 0, 1
 POU_OWNER, POU_RAMP = 0, 1
 ELEM_P1, ELEM_Q1 = 0, 1
+ORTH_DCGS2, ORTH_CGS2 = 0, 1
 
 
 def make_params(k, nsub_x, nsub_y=None, ppw=10, n_pml_global=10, sigma0=5.0, n_ovlp=-1, n_pml=-1,
@@ -296,6 +300,17 @@ class Context:
     def precond_apply_host(self, r_host, z_host):
         self._check(self.L.helm_precond_apply_host(self._h, _ptr(r_host), _ptr(z_host)))
         return z_host
+
+    def set_orthogonalisation(self, mode: int):
+        """GMRES orthogonalisation: ORTH_DCGS2 (default, re-orthogonalisation delayed one step) or ORTH_CGS2."""
+        self._check(self.L.helm_set_orthogonalisation(self._h, int(mode)))
+
+    def krylov_basis(self, nv: int):
+        """The first nv GMRES basis vectors of the last gmres call, as an (nv, n) device tensor."""
+        import torch
+        out = torch.empty(nv, self.n, dtype=torch.complex128, device="cuda")
+        self._check(self.L.helm_get_krylov_basis(self._h, int(nv), _ptr(out)))
+        return out
 
     def gmres(self, b, x=None, restart: int = 50, rtol: float = 1e-6, maxit: int = 5000, history: bool = False):
         import numpy as np
