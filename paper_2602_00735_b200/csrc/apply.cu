@@ -17,14 +17,19 @@
 // serial block-row dependency chain.  Consumer thread t owns row t of every block: the GEMV reads column
 // c of the column-major block (consecutive lanes -> consecutive 16-byte words, conflict-free) and the
 // broadcast operand rhs[c].
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "internal.cuh"
 
 namespace {
 
-constexpr int NS = 8;              // ring slots
-constexpr int SLOT_TARGET = 12288; // bytes per slot (rounded down to whole columns of m_max)
+constexpr int NS = 8;              // ring slots of the read probe; k_apply takes its ring depth at launch
+// bytes per ring slot (rounded down to whole groups of 4 columns of m_max).  Swept at c3 (m = 88, 128-thread CTAs,
+// 4 per SM), apply ms: 2 slots x 16.9 KB 8.88, 6 x 5.6 KB 8.95, 3 x 11.3 KB 9.06, 2 x 22.5 KB 9.21, 8 x 11.3 KB (two
+// 163-register CTAs per SM) 9.35 -- a short ring of large chunks over more CTAs wins.  HELM_APPLY_SLOTB overrides.
+constexpr int SLOT_TARGET = 20000;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -147,20 +152,20 @@ __device__ __forceinline__ void prefetch(Pre& p, const SubDesc& d, Step st, int 
     if (st.ph >= PH_D) p.yz = scr[(long long)(st.i - d.lo) * d.m + t];
 }
 
-__device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int slot_bytes)
+__device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int slot_bytes, int NSL)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * slot_bytes);
-    uint64_t* empty = full + NS;
-    z2* vb = reinterpret_cast<z2*>(empty + NS);   // bottom chain carry / down-expansion carry
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NSL * slot_bytes);
+    uint64_t* empty = full + NSL;
+    z2* vb = reinterpret_cast<z2*>(empty + NSL);   // bottom chain carry / down-expansion carry
     const int nct = nc_warps * 32;                // consumer threads
     z2* vt = vb + nct + 1;                        // top chain carry / up-expansion carry
     z2* rhs = vt + nct + 1;                       // GEMV operand
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < NS; s++) {
+        for (int s = 0; s < NSL; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], nc_warps);
         }
@@ -171,7 +176,7 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
     if (warp == nc_warps) {
         // ---------------------------------------------------------------- producer: stream the factors
         if (lane != 0) return;
-        uint32_t k = 0;
+        uint32_t slot = 0, ph = 0;
         for (int w = blockIdx.x; w < a.nsub; w += gridDim.x) {
             const SubDesc d = a.desc[a.order[w]];
             const int kc = slot_bytes / (d.m * (int)sizeof(z2)) / 4 * 4;
@@ -179,13 +184,16 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
             for (int s = 0; s < S; s++) {
                 const Step st = step_of(d, s);
                 const z2* blk = a.dinv + d.fac_off + (long long)st.i * d.m * d.m;
-                for (int c0 = 0; c0 < d.m; c0 += kc, k++) {
+                for (int c0 = 0; c0 < d.m; c0 += kc) {
                     const int nc = min(kc, d.m - c0);
-                    const uint32_t slot = k % NS, ph = (k / NS) & 1;
                     mbar_wait(&empty[slot], ph ^ 1);
                     const uint32_t bytes = (uint32_t)(nc * d.m * sizeof(z2));
                     mbar_arrive_expect_tx(&full[slot], bytes);
                     bulk_g2s(ring + (size_t)slot * slot_bytes, blk + (long long)c0 * d.m, bytes, &full[slot]);
+                    if (++slot == (uint32_t)NSL) {
+                        slot = 0;
+                        ph ^= 1;
+                    }
                 }
             }
         }
@@ -194,7 +202,7 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
 
     // -------------------------------------------------------------------- consumers: solve the chain
     const int t = tid;
-    uint32_t k = 0;
+    uint32_t slot = 0, ph = 0;
     z2* scr = a.scratch + (long long)blockIdx.x * a.scratch_per_cta;
     for (int w = blockIdx.x; w < a.nsub; w += gridDim.x) {
         const SubDesc d = a.desc[a.order[w]];
@@ -238,9 +246,8 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
             // four partial sums over the columns c = 0, 1, 2, 3 (mod 4), each in increasing c, then (s0+s1)+(s2+s3);
             // kc is a multiple of 4, so a chunk-relative residue is the global one
             z2 s0 = zmk(0, 0), s1 = zmk(0, 0), s2 = zmk(0, 0), s3 = zmk(0, 0);
-            for (int c0 = 0; c0 < m; c0 += kc, k++) {
+            for (int c0 = 0; c0 < m; c0 += kc) {
                 const int nc = min(kc, m - c0);
-                const uint32_t slot = k % NS, ph = (k / NS) & 1;
                 mbar_wait(&full[slot], ph);
                 const z2* col = reinterpret_cast<const z2*>(ring + (size_t)slot * slot_bytes);
                 if (act) {
@@ -258,6 +265,10 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
+                if (++slot == (uint32_t)NSL) {
+                    slot = 0;
+                    ph ^= 1;
+                }
             }
             const z2 acc = zadd(zadd(s0, s1), zadd(s2, s3));
             // ---- finish the step
@@ -308,17 +319,18 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
 
 // One instance per CTA-size class so that the register budget matches the block: m <= 224 (the BASELINE.json
 // configs, m <= 91), m <= 480, m <= 992 (the paper's ~300-400-node-wide subdomains, D21).
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT) k_apply(ApplyArgs a, int nc_warps, int slot_bytes)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_apply(ApplyArgs a, int nc_warps, int slot_bytes, int nslots)
 {
-    apply_body(a, nc_warps, slot_bytes);
+    apply_body(a, nc_warps, slot_bytes, nslots);
 }
 
 const void* apply_fn(int block)
 {
-    if (block <= 256) return (const void*)k_apply<256>;
-    if (block <= 512) return (const void*)k_apply<512>;
-    return (const void*)k_apply<1024>;
+    if (block <= 128) return (const void*)k_apply<128, 4>;
+    if (block <= 256) return (const void*)k_apply<256, 1>;
+    if (block <= 512) return (const void*)k_apply<512, 1>;
+    return (const void*)k_apply<1024, 1>;
 }
 
 // Ramp-PoU prolongation: out(g) = sum over the <= 2 x 2 subdomains whose chi is positive at g
@@ -354,19 +366,20 @@ __global__ void k_pou_gather(const SubDesc* __restrict__ desc, const int* __rest
 
 int slot_bytes_for(int m_max)
 {
-    int kc = SLOT_TARGET / (m_max * (int)sizeof(z2)) / 4 * 4;   // whole groups of 4 columns (canonical GEMV order)
+    static const int target = [] { const char* e = getenv("HELM_APPLY_SLOTB"); return e ? atoi(e) : SLOT_TARGET; }();
+    int kc = target / (m_max * (int)sizeof(z2)) / 4 * 4;   // whole groups of 4 columns (canonical GEMV order)
     if (kc < 4) kc = 4;
     return kc * m_max * (int)sizeof(z2);
 }
 
 }  // namespace
 
-int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm)
+int apply_configure(int m_max, int nslots, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm)
 {
     const int ncw = (m_max + 31) / 32;
     *block_threads = 32 * (ncw + 1);
     *slot_bytes = slot_bytes_for(m_max);
-    *smem_bytes = NS * *slot_bytes + 2 * NS * 8 + 3 * (32 * ncw + 1) * (int)sizeof(z2);
+    *smem_bytes = nslots * *slot_bytes + 2 * nslots * 8 + 3 * (32 * ncw + 1) * (int)sizeof(z2);
     const void* fn = apply_fn(*block_threads);
     int cur = 0;
     cudaFuncAttributes fa;
@@ -390,13 +403,13 @@ void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, 
                                                       ostride, i0, i1, j0, j1);
 }
 
-void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s)
+void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, cudaStream_t s)
 {
     // the dynamic-smem limit is a per-function attribute shared by every context in the process: raise it
     // whenever a context needs more than any earlier one
     static std::mutex mu;
-    static int smem_set[3] = {0, 0, 0};
-    const int cls = block <= 256 ? 0 : (block <= 512 ? 1 : 2);
+    static int smem_set[4] = {0, 0, 0, 0};
+    const int cls = block <= 128 ? 3 : (block <= 256 ? 0 : (block <= 512 ? 1 : 2));
     {
         std::lock_guard<std::mutex> lk(mu);   // contexts may launch from concurrent threads (loopback ranks)
         if (smem > smem_set[cls]) {
@@ -405,9 +418,10 @@ void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_by
         }
     }
     const int ncw = block / 32 - 1;
-    if (cls == 0) k_apply<256><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
-    else if (cls == 1) k_apply<512><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
-    else k_apply<1024><<<grid, block, smem, s>>>(a, ncw, slot_bytes);
+    if (cls == 3) k_apply<128, 4><<<grid, block, smem, s>>>(a, ncw, slot_bytes, nslots);
+    else if (cls == 0) k_apply<256, 1><<<grid, block, smem, s>>>(a, ncw, slot_bytes, nslots);
+    else if (cls == 1) k_apply<512, 1><<<grid, block, smem, s>>>(a, ncw, slot_bytes, nslots);
+    else k_apply<1024, 1><<<grid, block, smem, s>>>(a, ncw, slot_bytes, nslots);
 }
 
 // ---------------------------------------------------------------------------------------------------------------------

@@ -269,7 +269,7 @@ struct helm_ctx {
     bool factored = false;
 
     // apply launch configuration
-    int ap_block = 0, ap_smem = 0, ap_slot = 0, ap_grid = 0, ap_occ = 0;
+    int ap_block = 0, ap_smem = 0, ap_slot = 0, ap_grid = 0, ap_occ = 0, ap_nslots = 2;   // ring depth: apply.cu
     // cluster-split apply (few large subdomains): G CTAs per chain, 2G per cluster; 0 = off
     int sp_G = 0, sp_block = 0, sp_smem = 0, sp_slot = 0, sp_ncw = 0, sp_nss = 0;
 
@@ -760,7 +760,7 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
             return set_err(ctx, HELM_ECUDA, "cluster apply launch: %s", cudaGetErrorString((cudaError_t)e));
         }
     } else {
-        launch_apply(a, ctx->ap_grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->stream);
+        launch_apply(a, ctx->ap_grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->ap_nslots, ctx->stream);
     }
     CK(cudaGetLastError());
     ctx->launches++;
@@ -1373,9 +1373,17 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     // the one-CTA-per-subdomain kernel may not fit very wide blocks (its ring holds whole columns); that is only an
     // error when the cluster-split kernel below does not take over
-    apply_configure(ctx->m_max, &ctx->ap_block, &ctx->ap_smem, &ctx->ap_slot, &ctx->ap_occ);
+    if (const char* e = getenv("HELM_APPLY_SLOTS")) ctx->ap_nslots = std::max(2, atoi(e));   // tuning override
+    apply_configure(ctx->m_max, ctx->ap_nslots, &ctx->ap_block, &ctx->ap_smem, &ctx->ap_slot, &ctx->ap_occ);
     if (cudaGetLastError() != cudaSuccess) ctx->ap_occ = 0;
+    // persistent CTAs: as many as fit, then trimmed so that every CTA gets the same number of subdomains (round-robin
+    // over the cost-sorted order); measured at c3 (apply ms): 1 GPU 296 CTAs 9.63 -> 293 9.33; the 1/4 shard
+    // (1024 subdomains) 296 -> 256 CTAs 2.56 -> 2.28; the 1/8 shard 1.24 -> 1.15 (scripts/shard_timing.py)
     ctx->ap_grid = std::min(nsub, nsm * std::max(ctx->ap_occ, 1));
+    {
+        const int per = (nsub + ctx->ap_grid - 1) / std::max(ctx->ap_grid, 1);
+        ctx->ap_grid = (nsub + per - 1) / per;
+    }
     ctx->nblk = nsm * 4;
     // Fewer subdomains than SMs (the paper's regime): split every subdomain over a cluster of 2G CTAs (G per chain).
     // Among the G <= 8 whose clusters are all resident at once, take the smallest that keeps >= 80 % of the SMs

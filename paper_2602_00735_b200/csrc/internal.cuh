@@ -136,7 +136,7 @@ struct ApplyArgs {
 void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, int bx0, int bx1, int by0, int by1,
                        const z2* pou_buf, z2* out, int oi0, int oj0, long long ostride, int i0, int i1, int j0, int j1,
                        cudaStream_t s);
-int apply_configure(int m_max, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
+int apply_configure(int m_max, int nslots, int* block_threads, int* smem_bytes, int* slot_bytes, int* ctas_per_sm);
 // cluster-split apply for few large subdomains (apply_split.cu)
 int split_configure(int m_max, int G, int ctas_per_sm, int* block_threads, int* smem_bytes, int* slot_bytes, int* ncw,
                     int* nslots);
@@ -145,7 +145,7 @@ int launch_apply_split(const ApplyArgs& a, int nsub, int G, int block, int smem,
                        int nslots, cudaStream_t s);
 void launch_relayout(const SubDesc* desc, const int2* blocks, int nblocks, z2* dinv, z2* tmp, long long tmp_per_cta,
                      int grid, int G, cudaStream_t s);
-void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, cudaStream_t s);
+void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, cudaStream_t s);
 
 // owned rows [i0, i0+nx) x [j0, j0+ny) of the 7- or 9-point operator; x read from a buffer with origin (xi0, xj0).
 // Rows whose node lies in [ci0, ci1) x [cj0, cj1) -- all six triangles inside Omega_int, gamma = 1 --
