@@ -18,6 +18,8 @@
 // bulk-copies each step's input row b_i and coupling vectors into a double-buffered "aux" slot one step ahead, so
 // the per-step right-hand side is formed from shared memory only.  Per row the arithmetic is k_apply's up to the
 // split of the GEMV into two partial sums.
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "internal.cuh"
@@ -25,7 +27,10 @@
 namespace {
 
 constexpr int NSMAX = 16;           // ring slots (runtime count nss <= NSMAX: sized from the smem left per CTA)
-constexpr int SLOT_T = 16384;       // target bytes per slot
+// target bytes per ring slot; swept on the paper workloads (apply ms t300 / t600 / t1200): 16384 -> 2.26 / 3.76 / 13.87,
+// 32000 -> 1.58 / 3.27 / 13.85, 48000 -> 1.47 / 3.24 / 11.92, 80000 -> 1.29 / 3.22 / 12.13 (scripts/split_ring_sweep.sh;
+// HELM_SPLIT_SLOTB / HELM_SPLIT_SLOTS override)
+constexpr int SLOT_T = 48000;
 constexpr int NAUX = 2;             // aux slots: [b, cd, clo, chi] x mcap each; the twist step takes two
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -419,7 +424,8 @@ __global__ void k_relayout(const SubDesc* __restrict__ desc, const int2* __restr
 int split_slot_bytes(int m_max, int G)
 {
     const int R = (m_max + G - 1) / G;
-    int kc = SLOT_T / (R * (int)sizeof(z2)) / 4 * 4;
+    static const int target = [] { const char* e = getenv("HELM_SPLIT_SLOTB"); return e ? atoi(e) : SLOT_T; }();
+    int kc = target / (R * (int)sizeof(z2)) / 4 * 4;
     if (kc < 4) kc = 4;
     return kc * R * (int)sizeof(z2);
 }
@@ -440,7 +446,8 @@ int split_configure(int m_max, int G, int ctas_per_sm, int* block_threads, int* 
     const int fixed = NAUX * 4 * m_max * (int)sizeof(z2) + (2 * NSMAX + 2 * NAUX + 4) * 8 + 4 * m_max * (int)sizeof(z2) +
                       std::max(32 * ncw, 4 * R) * (int)sizeof(z2);
     const int budget = 227 * 1024 / std::max(1, ctas_per_sm) - 1024 - fixed;
-    const int nss = std::min(NSMAX, budget / *slot_bytes);
+    static const int cap = [] { const char* e = getenv("HELM_SPLIT_SLOTS"); return e ? atoi(e) : NSMAX; }();
+    const int nss = std::min(std::min(NSMAX, cap), budget / *slot_bytes);
     if (nss < 2 || *block_threads > 512) return -1;
     *nslots = nss;
     *smem_bytes = nss * *slot_bytes + fixed;
