@@ -677,7 +677,7 @@ int allreduce(helm_ctx* ctx, double* buf, size_t count)
     if (ctx->loop) {
         // loopback: every rank sums all ranks' buffers in rank order (identical bits everywhere)
         LoopGroup* L = ctx->loop;
-        if (count > 2 * NVMAX) return set_err(ctx, HELM_EINVAL, "loopback allreduce of %zu doubles", count);
+        if (count > 4 * NVMAX) return set_err(ctx, HELM_EINVAL, "loopback allreduce of %zu doubles", count);
         CK(cudaStreamSynchronize(ctx->stream));
         L->slot[ctx->rank] = buf;
         L->barrier();
@@ -1033,9 +1033,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             NvtxRange nv_o("helm.orth");
             launch_multidot2(V, n, j + 1, uj, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
             launch_reduce_z2(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_dots, s);
-            if ((rc2 = allreduce(ctx, (double*)ctx->d_dots, 2 * (size_t)(j + 1))) ||
-                (rc2 = allreduce(ctx, (double*)(ctx->d_dots + NVMAX), 2 * (size_t)(j + 1))))
-                return rc2;
+            if ((rc2 = allreduce(ctx, (double*)ctx->d_dots, 4 * (size_t)(j + 1)))) return rc2;   // both groups
             launch_dcgs2_coef(ctx->d_dots, j, ctx->d_H, ctx->d_ca, ctx->d_ce, ctx->d_sc, ctx->d_hout, s);
             launch_dcgs2_update(V, n, j, ctx->d_w, ctx->d_ca, ctx->d_ce, ctx->d_sc, n, ctx->d_dpart, ctx->nblk, s);
             ctx->launches += 4;
@@ -1293,7 +1291,7 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
         ctx->loop = L;
         ctx->loop_id = loop_group;
         ctx->has_comm = true;
-        if ((rc = dalloc(ctx, &ctx->d_loop_tmp, 2 * NVMAX))) return rc;
+        if ((rc = dalloc(ctx, &ctx->d_loop_tmp, 4 * NVMAX))) return rc;
     } else if (ctx->multi && nccl_unique_id) {
 #ifdef HELM_HAVE_NCCL
         ncclUniqueId id;

@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(KT) k_multidot2(const z2* __restrict__ V, long
     }
 }
 
-// One warp.  d: the reduced sweep-1 sums (d[q] = V_q^H u_j, d[NVMAX + q] = V_q^H w_j, q <= j).  H: device Hessenberg,
+// One warp.  d: the reduced sweep-1 sums (d[q] = V_q^H u_j, d[j + 1 + q] = V_q^H w_j, q <= j; one allreduce).  H: device Hessenberg,
 // column-major with leading dimension NVMAX + 1.  Writes the sweep-2 coefficients ca (= a / nu), ce (= e) and
 // sc = {1 / nu, sigma / nu}, and for the host: out[0 .. j] = final column j - 1 (rows 0 .. j), out[NVMAX .. NVMAX + j]
 // = pending column j, out[2 NVMAX] = (nu, 0).
@@ -358,12 +358,12 @@ __global__ void k_dcgs2_coef(const z2* __restrict__ d, int j, z2* __restrict__ H
         const z2 a = d[i];
         as[i] = a;
         na += zabs2(a);
-        zfma_conj(ab, a, d[NVMAX + i]);
+        zfma_conj(ab, a, d[j + 1 + i]);
     }
     na = warp_sum(na);
     ab = warp_sum(ab);
     const double alpha = d[j].x;
-    const z2 c = d[NVMAX + j];
+    const z2 c = d[2 * j + 1];
     const double nu2 = alpha - na;
     const double nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
     const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
@@ -379,7 +379,7 @@ __global__ void k_dcgs2_coef(const z2* __restrict__ d, int j, z2* __restrict__ H
     for (int i = lane; i < j; i += 32) {
         z2 p = zmk(0, 0);   // (H(0:j, 0:j) a)_i, columns k >= i - 1 only (Hessenberg), increasing k
         for (int k = i > 0 ? i - 1 : 0; k < j; k++) zfma(p, H[k * LD + i], as[k]);
-        const z2 h = zscale(zsub(d[NVMAX + i], p), inv);
+        const z2 h = zscale(zsub(d[j + 1 + i], p), inv);
         H[j * LD + i] = h;
         out[NVMAX + i] = h;
         const z2 e = zsub(zadd(zscale(p, inv), h), zmul(as[i], sinv));
@@ -460,12 +460,12 @@ __global__ void __launch_bounds__(KT) k_dcgs2_update(z2* V, long long ldv, int j
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-// out[v] = sum_blk partial[blk][v]; out_plus[v] = add[v] + out[v] (if given); one CTA, index order
+// out[q] = sum_blk partial[blk][v]; out_plus[q] = add[q] + out[q] (if given); one CTA, index order.  Values
+// v = q < nv, and (off2 > 0) a second group v = off2 + (q - nv), packed behind the first: out[nv .. 2 nv).
 __global__ void k_reduce_z(const z2* __restrict__ partial, int nblk, int nv, z2* __restrict__ out,
                            z2* __restrict__ out_plus, const z2* __restrict__ add, int stride, int off2)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // values v < nv, and (off2 > 0) the second group v + off2
     const int nval = off2 ? 2 * nv : nv;
     for (int q = warp; q < nval; q += blockDim.x >> 5) {
         const int v = q < nv ? q : off2 + (q - nv);
@@ -473,8 +473,8 @@ __global__ void k_reduce_z(const z2* __restrict__ partial, int nblk, int nv, z2*
         for (int b = lane; b < nblk; b += 32) s = zadd(s, partial[(long long)b * stride + v]);
         s = warp_sum(s);
         if (lane == 0) {
-            out[v] = s;
-            if (out_plus) out_plus[v] = zadd(add[v], s);
+            out[q] = s;
+            if (out_plus) out_plus[q] = zadd(add[q], s);
         }
     }
 }
