@@ -47,7 +47,8 @@ def main():
     kw = paper_params(c.k, c.nsub, c.pml, c.ovlp, n_cells=c.n_cells)
     if args.drch:
         kw["local_bc"] = BC_DIRICHLET
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()   # dedicated library stream (NCCL on a non-default stream)
+    torch.cuda.set_stream(stream)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     if world > 1:
         dist.barrier()
