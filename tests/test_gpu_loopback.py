@@ -111,6 +111,13 @@ def test_loopback_bj(name, nranks, gg):
     check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub), nranks, gg, bj_rhs(name))
 
 
+def test_loopback_short_restart():
+    """GMRES(5) on 4 ranks: every cycle closes its last Hessenberg column with an extra projection sweep (DCGS2) whose
+    sums go through the allreduce too."""
+    cfg = CONFIGS["c1"]
+    check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub), 4, (2, 2), bj_rhs("c1"), restart=5)
+
+
 def test_loopback_impedance():
     cfg = CONFIGS["c1"]
     check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, local_bc=BC_IMPEDANCE), 2, (2, 1),
