@@ -316,28 +316,33 @@ def paper_table4(stream, names=("t300", "t600")):
     rows = []
     for name in names:
         c = PAPER_CONFIGS[name]
-        torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        ev[0].record(stream)
-        ctx = Context(**paper_params(c.k, c.nsub, c.pml, c.ovlp, n_cells=c.n_cells, local_bc=c.local_bc),
-                      stream=stream)
-        ctx.factor()
-        ev[1].record(stream)
-        xy, amp, s = paper_source(c.k)
-        b = ctx.rhs(xy, amp, s)
-        ev[2].record(stream)
-        _, info, _ = ctx.richardson(b, rtol=c.rtol, maxit=c.maxit)
-        ev[3].record(stream)
-        torch.cuda.synchronize()
-        lay = ctx.layout
-        rows.append({"config": name, "k": c.k, "grid": c.n_cells, "subdomains": c.nsub ** 2, "pml": c.pml,
-                     "ovlp": c.ovlp, "m_max": lay.m_max, "factor_GB": round(lay.factor_bytes / 1e9, 2),
-                     "setup_factor_s": ev[0].elapsed_time(ev[1]) / 1e3, "solve_s": ev[2].elapsed_time(ev[3]) / 1e3,
-                     "iterations": info.iterations, "relres": info.relres,
-                     "paper": PAPER_TABLE4[name]})
-        ctx.close()
-        del ctx, b
-        torch.cuda.empty_cache()
+        best = None
+        for _ in range(2):   # best of two: these runs last 0.1-0.3 s, where clock ramp-up and allocator noise show
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(stream)
+            ctx = Context(**paper_params(c.k, c.nsub, c.pml, c.ovlp, n_cells=c.n_cells, local_bc=c.local_bc),
+                          stream=stream)
+            ctx.factor()
+            ev[1].record(stream)
+            xy, amp, s = paper_source(c.k)
+            b = ctx.rhs(xy, amp, s)
+            ev[2].record(stream)
+            _, info, _ = ctx.richardson(b, rtol=c.rtol, maxit=c.maxit)
+            ev[3].record(stream)
+            torch.cuda.synchronize()
+            lay = ctx.layout
+            row = {"config": name, "k": c.k, "grid": c.n_cells, "subdomains": c.nsub ** 2, "pml": c.pml,
+                   "ovlp": c.ovlp, "m_max": lay.m_max, "factor_GB": round(lay.factor_bytes / 1e9, 2),
+                   "setup_factor_s": ev[0].elapsed_time(ev[1]) / 1e3, "solve_s": ev[2].elapsed_time(ev[3]) / 1e3,
+                   "iterations": info.iterations, "relres": info.relres, "timing": "best of 2 runs",
+                   "paper": PAPER_TABLE4[name]}
+            if best is None or row["setup_factor_s"] + row["solve_s"] < best["setup_factor_s"] + best["solve_s"]:
+                best = row
+            ctx.close()
+            del ctx, b
+            torch.cuda.empty_cache()
+        rows.append(best)
     return rows
 
 
