@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC]
+    cmd = [nvcc, *NVCC_FLAGS, *os.environ.get("HELM_NVCC_EXTRA", "").split(), "-I", INCLUDE, "-I", CSRC]
     nd = nccl_dirs()
     if nd:
         inc, lib = nd

@@ -96,6 +96,63 @@ __device__ void warp_gj(z2* D, int kw, int kb, int* bad)
     }
 }
 
+// The same inverse with the matrix in REGISTERS of the GJW = 8 warps: warp w holds rows w, w + 8, w + 16, w + 24 (lane
+// c = column c), so the pivot column reaches every row by a shuffle and only the scaled pivot row goes through shared
+// memory (a two-slot buffer, so one named barrier per pivot instead of three).  Per entry the arithmetic is
+// warp_gj's, in the same order:
+//   D[p][c] <- D[p][c] / D[p][p];  D[r][c] <- D[r][c] - D[r][p] D[p][c];  D[r][p] <- -D[r][p] / D[p][p];
+//   D[p][p] <- 1 / D[p][p]          (r != p, c != p).  A zero pivot is recorded as row kb + p.
+__device__ __forceinline__ z2 shfl_z(z2 v, int src)
+{
+    return zmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+__device__ void warp_gj8(z2* D, z2* rowbuf /* 2 x 32 */, int kw, int kb, int* bad)
+{
+    static_assert(GB == 4 * GJW, "four rows per warp");
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    z2 row[4];
+#pragma unroll
+    for (int s4 = 0; s4 < 4; s4++) {
+        const int r = w + GJW * s4;
+        row[s4] = (r < kw && lane < kw) ? D[r * DLD + lane] : zmk(0, 0);
+    }
+#pragma unroll
+    for (int p = 0; p < GB; p++) {
+        if (p >= kw) break;
+        z2* rb = rowbuf + (p & 1) * GB;
+        if (w == p % GJW) {   // owner of row p: scale it, publish it
+            const z2 pv = shfl_z(row[p / GJW], p);
+            const bool zero = pv.x == 0.0 && pv.y == 0.0;
+            if (zero && lane == 0 && *bad < 0) *bad = kb + p;
+            const double rd = zero ? 0.0 : 1.0 / (pv.x * pv.x + pv.y * pv.y);   // one division per pivot
+            const z2 inv = zmk(pv.x * rd, -pv.y * rd);
+            const z2 v = lane == p ? inv : zmul(row[p / GJW], inv);
+            row[p / GJW] = v;
+            rb[lane] = v;
+        }
+        gj_bar();
+        const z2 b = rb[lane], inv = rb[p];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; s4++) {
+            if (w + GJW * s4 == p) continue;
+            const z2 f = shfl_z(row[s4], p);   // D[r][p]
+            if (lane != p) {
+                zfms(row[s4], f, b);
+            } else {
+                z2 v = zmk(0, 0);
+                zfms(v, f, inv);
+                row[s4] = v;
+            }
+        }
+    }
+#pragma unroll
+    for (int s4 = 0; s4 < 4; s4++) {
+        const int r = w + GJW * s4;
+        if (r < kw && lane < kw) D[r * DLD + lane] = row[s4];
+    }
+}
+
 // Couplings of block row i as m x m matrices (7-point P1: two diagonals; 9-point Q1: three):
 //   L_i[a][a] = S_i(a), L_i[a][a-1] = SW_i(a), L_i[a][a+1] = SE_i(a)          (A_{i,i-1})
 //   U_i[a][a] = N_i(a), U_i[a][a+1] = NE_i(a), U_i[a][a-1] = NW_i(a)          (A_{i,i+1})
@@ -220,7 +277,7 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
                 Dk[r * DLD + c] = S[(kb + r) * ld + kb + c];
             }
             gj_bar();
-            warp_gj(Dk, kw, kb, bad_row);
+            warp_gj8(Dk, Dk + GB * DLD, kw, kb, bad_row);
         }
         __syncthreads();
         // ---- row panel: S[K, j] = Dk S[K, j] (j not in K) on the tensor cores.  One warp owns an 8-column strip:
@@ -404,9 +461,17 @@ __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__
 // ------------------------------------------------------------------------------------------------------------------
 constexpr int BCMAX = 16;  // CTAs per cluster (one cluster per chain): 8, or 16 when there are few chains
 constexpr int BT = 256;    // threads per CTA
-constexpr int JT = 32;     // column tile of the trailing update
+constexpr int CW = 128;    // columns of the row panel staged per chunk of the trailing update
 
 __host__ __device__ __forceinline__ int big_rows(int m, int bc) { return (m + bc - 1) / bc; }
+
+// 16-byte asynchronous global -> shared copy (LDGSTS): the staging loops issue all their loads before waiting
+__device__ __forceinline__ void cp_async16(z2* dst, const z2* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void cluster_sync_all()
 {
@@ -421,10 +486,26 @@ __device__ __forceinline__ int cluster_rank()
     return (int)r;
 }
 
+#ifdef HELM_FACTOR_PROF
+// development aid (-DHELM_FACTOR_PROF via HELM_NVCC_EXTRA): clock64 cycles per phase of big_block, printed by the
+// first CTA of the first cluster
+#define FPROF_N 8
+#define FPROF_T(k) do { const long long t_ = clock64(); if (prof) prof[k] += t_ - tprev; tprev = t_; } while (0)
+#else
+#define FPROF_T(k) do { } while (0)
+#endif
+
 // one block of a chain, formed then inverted in place (column-major in its factor slot)
 __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restrict__ stc, z2* __restrict__ dinv, int rk,
-                          int bc, z2* Dk, z2* Aik, z2* AKj, int* bad)
+                          int bc, z2* Dk, z2* Aik, z2* AK, int* bad
+#ifdef HELM_FACTOR_PROF
+                          , long long* prof
+#endif
+                          )
 {
+#ifdef HELM_FACTOR_PROF
+    long long tprev = clock64();
+#endif
     const int m = d.m, tid = threadIdx.x;
     z2* A = dinv + d.fac_off + (long long)i * m * m;
     const int c0 = (int)(((long long)m * rk) / bc), c1 = (int)(((long long)m * (rk + 1)) / bc);
@@ -433,7 +514,9 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
         const int b = (int)(e / m), a = (int)(e - (long long)b * m);
         A[e] = schur_entry(d, i, mode, stc, dinv, a, b);
     }
+    FPROF_T(0);
     cluster_sync_all();
+    FPROF_T(1);
     const int R = big_rows(m, bc), r0 = rk * R, r1 = min(m, r0 + R), nr = max(0, r1 - r0);
     for (int kb = 0; kb < m; kb += GB) {
         const int kw = min(GB, m - kb);
@@ -443,8 +526,10 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
             Dk[r * DLD + c] = A[(long long)(kb + c) * m + kb + r];
         }
         __syncthreads();
-        if (tid < GJW * 32) warp_gj(Dk, kw, kb, bad);
+        FPROF_T(2);
+        if (tid < GJW * 32) warp_gj8(Dk, Dk + GB * DLD, kw, kb, bad);
         __syncthreads();
+        FPROF_T(3);
         // ---- row panel: A[K,j] = Dk A[K,j] for this CTA's columns on the tensor cores; one warp per 8-column strip
         //      loads the strip's old 32 x 8 block as B fragments first, then writes its four row tiles (in place)
         {
@@ -482,48 +567,81 @@ __device__ void big_block(const SubDesc& d, int i, int mode, const z2* __restric
                 }
             }
         }
+        FPROF_T(4);
         cluster_sync_all();
-        // ---- trailing update of this CTA's row slab [r0, r1): A[i,K] staged in Aik, A[K, tile] in AKj
+        FPROF_T(1);
+        // ---- trailing update of this CTA's row slab [r0, r1): A[i,K] staged in Aik (once), the row panel A[K, :] in
+        //      chunks of CW columns in AK (the K columns stage Dk: A[i,K] = -A[i,K] Dk is the same product with C = 0).
+        //      A warp owns 8 slab rows x 32 columns: its A fragments are loaded once and feed four independent 8 x 8
+        //      accumulators (four DMMA chains in flight).
         for (int e = tid; e < nr * kw; e += BT) {
             const int q = e / nr, ii = e - q * nr;
-            Aik[ii * DLD + q] = A[(long long)(kb + q) * m + r0 + ii];
+            cp_async16(&Aik[ii * DLD + q], &A[(long long)(kb + q) * m + r0 + ii]);
         }
-        __syncthreads();
-        static_assert(JT == GB, "the panel's columns must form exactly one column tile");
         const int nrt = (nr + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
-        for (int jt = 0; jt < m; jt += JT) {
-            const int jw = min(JT, m - jt);
-            const bool kcols = jt == kb;   // the column panel: A[i,K] = -A[i,K] Dk (a product with C = 0)
-            if (!kcols)
-                for (int e = tid; e < jw * kw; e += BT) {
-                    const int jj = e / kw, q = e - jj * kw;
-                    AKj[q * JT + jj] = A[(long long)(jt + jj) * m + kb + q];
-                }
+        for (int cs = 0; cs < m; cs += CW) {
+            const int cw = min(CW, m - cs), ncg = (cw + 31) / 32;
+            for (int e = tid; e < cw * kw; e += BT) {
+                const int jj = e / kw, q = e - jj * kw, j = cs + jj;
+                if (j >= kb && j < kb + kw) AK[q * CW + jj] = Dk[q * DLD + (j - kb)];
+                else cp_async16(&AK[q * CW + jj], &A[(long long)j * m + kb + q]);
+            }
+            cp_async_wait_all();
             __syncthreads();
-            // FP64 tensor cores: one warp per 8 x 8 tile of (slab rows) x (tile columns)
-            for (int tile = tid >> 5; tile < nrt * (JT / 8); tile += BT >> 5) {
-                const int i0 = (tile / (JT / 8)) * 8, j0 = (tile % (JT / 8)) * 8;
-                const int r = i0 + g, row = r0 + r, cA = j0 + 2 * t, cB = cA + 1;
+            FPROF_T(5);
+            for (int u = tid >> 5; u < nrt * ncg; u += BT >> 5) {
+                const int i0 = (u / ncg) * 8, jg = (u % ncg) * 32;
+                const int r = i0 + g, row = r0 + r;
                 const bool rok = r < nr && !(row >= kb && row < kb + kw);   // rows of the panel are final already
-                z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
-                if (!kcols && rok && cA < jw) c0 = A[(long long)(jt + cA) * m + row];
-                if (!kcols && rok && cB < jw) c1 = A[(long long)(jt + cB) * m + row];
-                ztile_fms(
-                    c0, c1, kw, [&](int rr, int q) { return i0 + rr < nr ? Aik[(i0 + rr) * DLD + q] : zmk(0, 0); },
-                    [&](int q, int cc) {
-                        return j0 + cc < jw ? (kcols ? Dk[q * DLD + j0 + cc] : AKj[q * JT + j0 + cc]) : zmk(0, 0);
-                    });
-                if (rok && cA < jw) A[(long long)(jt + cA) * m + row] = c0;
-                if (rok && cB < jw) A[(long long)(jt + cB) * m + row] = c1;
+                z2 af[GB / 4];
+#pragma unroll
+                for (int s4 = 0; s4 < GB / 4; s4++) {
+                    const int q = 4 * s4 + t;
+                    af[s4] = (r < nr && q < kw) ? Aik[r * DLD + q] : zmk(0, 0);
+                }
+                z2 c0[4], c1[4];
+#pragma unroll
+                for (int ct = 0; ct < 4; ct++) {
+                    const int jA = jg + 8 * ct + 2 * t, jB = jA + 1;   // chunk-relative output columns
+                    const int gA = cs + jA, gB = cs + jB;
+                    const bool kA = gA >= kb && gA < kb + kw, kB = gB >= kb && gB < kb + kw;
+                    c0[ct] = (rok && jA < cw && !kA) ? A[(long long)gA * m + row] : zmk(0, 0);
+                    c1[ct] = (rok && jB < cw && !kB) ? A[(long long)gB * m + row] : zmk(0, 0);
+                }
+#pragma unroll
+                for (int s4 = 0; s4 < GB / 4; s4++) {
+                    if (4 * s4 >= kw) break;
+                    const z2 a = af[s4];
+                    const int q = 4 * s4 + t;
+#pragma unroll
+                    for (int ct = 0; ct < 4; ct++) {
+                        const int jj = jg + 8 * ct + g;
+                        const z2 b = (q < kw && jj < cw) ? AK[q * CW + jj] : zmk(0, 0);
+                        dmma(c0[ct].x, c1[ct].x, -a.x, b.x);   // C -= A B
+                        dmma(c0[ct].x, c1[ct].x, a.y, b.y);
+                        dmma(c0[ct].y, c1[ct].y, -a.x, b.y);
+                        dmma(c0[ct].y, c1[ct].y, -a.y, b.x);
+                    }
+                }
+                if (rok) {
+#pragma unroll
+                    for (int ct = 0; ct < 4; ct++) {
+                        const int jA = jg + 8 * ct + 2 * t, jB = jA + 1;
+                        if (jA < cw) A[(long long)(cs + jA) * m + row] = c0[ct];
+                        if (jB < cw) A[(long long)(cs + jB) * m + row] = c1[ct];
+                    }
+                }
             }
             __syncthreads();
+            FPROF_T(6);
         }
         cluster_sync_all();
+        FPROF_T(1);
     }
 }
 
 // blockIdx.x / bc = chain: mode 0 -> 2 * sub + (0 bottom | 1 top), mode 2 -> sub (twist block)
-__global__ void __launch_bounds__(BT) k_factor_big(const SubDesc* __restrict__ desc, const z2* __restrict__ stc,
+__global__ void __launch_bounds__(BT, 2) k_factor_big(const SubDesc* __restrict__ desc, const z2* __restrict__ stc,
                                                    z2* __restrict__ dinv, int* err, int mode, int bc)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -531,34 +649,47 @@ __global__ void __launch_bounds__(BT) k_factor_big(const SubDesc* __restrict__ d
     const int sub = mode == 0 ? chain >> 1 : chain;
     const SubDesc d = desc[sub];
     z2* Dk = reinterpret_cast<z2*>(smem);
-    z2* AKj = Dk + GB * DLD;
-    z2* Aik = AKj + GB * JT;
+    z2* AK = Dk + GB * DLD;
+    z2* Aik = AK + GB * CW;
     __shared__ int bad;
     if (threadIdx.x == 0) bad = -1;
     __syncthreads();
+#ifdef HELM_FACTOR_PROF
+    long long pr[FPROF_N] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long* prof = threadIdx.x == 0 ? pr : nullptr;
+#define PROFARG , prof
+#else
+#define PROFARG
+#endif
     if (mode == 2) {
-        big_block(d, d.tw, 2, stc, dinv, rk, bc, Dk, Aik, AKj, &bad);
+        big_block(d, d.tw, 2, stc, dinv, rk, bc, Dk, Aik, AK, &bad PROFARG);
         report(err, bad, sub, d.tw);
     } else if ((chain & 1) == 0) {
         for (int i = 0; i < d.tw; i++) {
-            big_block(d, i, 0, stc, dinv, rk, bc, Dk, Aik, AKj, &bad);
+            big_block(d, i, 0, stc, dinv, rk, bc, Dk, Aik, AK, &bad PROFARG);
             report(err, bad, sub, i);
         }
     } else {
         for (int i = d.nb - 1; i > d.tw; i--) {
-            big_block(d, i, 1, stc, dinv, rk, bc, Dk, Aik, AKj, &bad);
+            big_block(d, i, 1, stc, dinv, rk, bc, Dk, Aik, AK, &bad PROFARG);
             report(err, bad, sub, i);
         }
     }
+#ifdef HELM_FACTOR_PROF
+    if (threadIdx.x == 0 && blockIdx.x == 0 && mode == 0)
+        printf("FPROF schur %lld clusterbar %lld dkload %lld gj %lld rowpanel %lld akstage %lld tiles %lld\n", pr[0], pr[1],
+               pr[2], pr[3], pr[4], pr[5], pr[6]);
+#endif
 }
 
-int big_smem_bytes(int m_max, int bc) { return (int)sizeof(z2) * (GB * DLD + GB * JT + big_rows(m_max, bc) * DLD); }
+// Dk, AK (its first 2 x GB entries double as warp_gj8's pivot-row buffer: not live at the same time), Aik
+int big_smem_bytes(int m_max, int bc) { return (int)sizeof(z2) * (GB * DLD + GB * CW + big_rows(m_max, bc) * DLD); }
 
 }  // namespace
 
 int factor_smem_bytes(int m_max)
 {
-    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + GB * DLD));
+    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + GB * DLD + 2 * GB));   // S, Dk, pivot-row buffer
 }
 
 void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, int m_max, const z2* stencil, z2* dinv,
