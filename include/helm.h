@@ -91,6 +91,7 @@ typedef struct {
     long long band_bytes;     /* the same operator as band L+U factors + gather + write (SURVEY 8(d) B_apply) */
     long long spmv_bytes;     /* algorithmic bytes of one helm_matvec on this rank */
     int stencil_slots;        /* coefficients per row of A (helm_export_stencil): 7 (P1) or 9 (Q1) */
+    int overlap_interior;     /* multi-rank: subdomains applied while the halo is in flight (0: no overlap) */
 } helm_layout;
 
 typedef struct {

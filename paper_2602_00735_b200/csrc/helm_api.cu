@@ -310,7 +310,14 @@ struct helm_ctx {
     // record for the host (final column j - 1, pending column j, nu_j, ||u_{j+1}||)
     z2 *d_H = nullptr, *d_dots = nullptr, *d_ca = nullptr, *d_ce = nullptr, *d_hout = nullptr;
     double* d_sc = nullptr;
-    bool orth_cgs2 = false;   // helm_set_orthogonalisation(HELM_ORTH_CGS2): the undelayed CGS2
+    bool orth_cgs2 = false;
+    // multi-rank apply overlapped with its halo exchange: subdomains whose full box lies inside the
+    // owned rectangle run while the ghost frame is in flight; the rest run on the communication stream after it
+    bool overlap = false;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_ov[2] = {nullptr, nullptr};
+    int* d_order_ov = nullptr;   // interior subdomains (cost-sorted), then boundary subdomains (cost-sorted)
+    int n_int = 0, n_bnd = 0, grid_int = 0, grid_bnd = 0;   // helm_set_orthogonalisation(HELM_ORTH_CGS2): the undelayed CGS2
     cudaEvent_t ev_hc[2] = {nullptr, nullptr};
 
     // profiling of the apply kernel
@@ -577,10 +584,11 @@ int need_comm(helm_ctx* ctx)
 // ---------------------------------------------------------------------------------------- collectives
 // loopback: after the phase's messages are packed, copy each peer's send buffer addressed to this rank into the
 // matching receive buffer (the peer's message index is recomputed from its own schedule)
-int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const int* idx, int k, bool reverse)
+int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const int* idx, int k, bool reverse,
+                  cudaStream_t st)
 {
     LoopGroup* L = ctx->loop;
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(st));
     L->barrier();   // every rank has packed this phase
     for (int a = 0; a < k; a++) {
         const helm_msg& m = msgs[idx[a]];
@@ -605,9 +613,9 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
                                     : (size_t)(pm[fq].send_i1 - pm[fq].send_i0) * (pm[fq].send_j1 - pm[fq].send_j0);
         if (scnt != rcnt) return set_err(ctx, HELM_ENCCL, "loopback: message size mismatch %zu vs %zu", scnt, rcnt);
         CK(cudaMemcpyAsync(ctx->d_recvbuf[a], peer->d_sendbuf[found], sizeof(z2) * rcnt, cudaMemcpyDeviceToDevice,
-                           ctx->stream));
+                           st));
     }
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(st));
     L->barrier();   // peers may refill their send buffers
     return HELM_OK;
 }
@@ -616,7 +624,7 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
 // owned strips travel to the neighbours' ghost frames, phase 0 (x) then phase 1 (y, carrying the corners).
 // Reverse (reverse = true, the ramp PoU's additive exchange): the ghost frames travel back and are ADDED onto the
 // neighbours' owned strips, phase 1 then phase 0, so corner contributions reach the diagonal rank in two hops.
-int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse)
+int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse, cudaStream_t st)
 {
     NvtxRange nv_(reverse ? "helm.comm.halo_add" : (W == 0 ? "helm.comm.halo_apply" : "helm.comm.halo_spmv"));
     helm_msg msgs[4];
@@ -633,11 +641,11 @@ int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse)
             const int i0 = reverse ? m.recv_i0 : m.send_i0, i1 = reverse ? m.recv_i1 : m.send_i1;
             const int j0 = reverse ? m.recv_j0 : m.send_j0, j1 = reverse ? m.recv_j1 : m.send_j1;
             launch_copy_rect(buf, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], i0, j0, i1 - i0, i0, i1, j0, j1,
-                             ctx->stream);
+                             st);
             ctx->launches++;
         }
         if (ctx->loop) {
-            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k, reverse);
+            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k, reverse, st);
             if (rc) return rc;
         } else {
 #ifdef HELM_HAVE_NCCL
@@ -647,8 +655,8 @@ int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse)
                 const size_t sa = (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
                 const size_t ra = (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
                 const size_t scnt = 2 * (reverse ? ra : sa), rcnt = 2 * (reverse ? sa : ra);
-                NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
-                NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, ctx->stream));
+                NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, st));
+                NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, st));
             }
             NK(ncclGroupEnd());
 #else
@@ -660,14 +668,14 @@ int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse)
             const int i0 = reverse ? m.send_i0 : m.recv_i0, i1 = reverse ? m.send_i1 : m.recv_i1;
             const int j0 = reverse ? m.send_j0 : m.recv_j0, j1 = reverse ? m.send_j1 : m.recv_j1;
             launch_copy_rect(ctx->d_recvbuf[a], i0, j0, i1 - i0, buf, G.e_i0, G.e_j0, ctx->ext_stride, i0, i1, j0, j1,
-                             ctx->stream, reverse);
+                             st, reverse);
             ctx->launches++;
         }
     }
     return HELM_OK;
 }
 
-int exchange(helm_ctx* ctx, int W) { return exchange_buf(ctx, W, ctx->d_ext, false); }
+int exchange(helm_ctx* ctx, int W) { return exchange_buf(ctx, W, ctx->d_ext, false, ctx->stream); }
 
 // in-place sum over ranks of `count` doubles on the device
 int allreduce(helm_ctx* ctx, double* buf, size_t count)
@@ -709,9 +717,34 @@ int fill_ext(helm_ctx* ctx, const z2* v, int W)
 }
 
 // ------------------------------------------------------------------------------------------- operators
-int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z)
+// apply timing (helm_profile_enable): a pair of events on the library stream around each apply
+int prof_begin(helm_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1)
 {
-    if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
+    if (!ctx->prof) return HELM_OK;
+    if (ctx->ev_free.size() < 2) {
+        cudaEvent_t a0, a1;
+        CK(cudaEventCreate(&a0));
+        CK(cudaEventCreate(&a1));
+        ctx->ev_free.push_back(a0);
+        ctx->ev_free.push_back(a1);
+    }
+    *e1 = ctx->ev_free.back();
+    ctx->ev_free.pop_back();
+    *e0 = ctx->ev_free.back();
+    ctx->ev_free.pop_back();
+    CK(cudaEventRecord(*e0, ctx->stream));
+    return HELM_OK;
+}
+int prof_end(helm_ctx* ctx, cudaEvent_t e0, cudaEvent_t e1)
+{
+    if (!ctx->prof) return HELM_OK;
+    CK(cudaEventRecord(e1, ctx->stream));
+    ctx->ev_used.push_back({e0, e1});
+    return HELM_OK;
+}
+
+ApplyArgs apply_args(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z)
+{
     ApplyArgs a{};
     a.desc = ctx->d_desc;
     a.order = ctx->d_order;
@@ -737,21 +770,16 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     a.ns = ctx->G.ns;
     a.pou_buf = ctx->d_pou;
     a.delta = ctx->G.wo;
+    return a;
+}
+
+int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z)
+{
+    if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
+    const ApplyArgs a = apply_args(ctx, in, in_i0, in_j0, in_stride, z);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ctx->prof) {
-        if (ctx->ev_free.size() < 2) {
-            cudaEvent_t a0, a1;
-            CK(cudaEventCreate(&a0));
-            CK(cudaEventCreate(&a1));
-            ctx->ev_free.push_back(a0);
-            ctx->ev_free.push_back(a1);
-        }
-        e1 = ctx->ev_free.back();
-        ctx->ev_free.pop_back();
-        e0 = ctx->ev_free.back();
-        ctx->ev_free.pop_back();
-        CK(cudaEventRecord(e0, ctx->stream));
-    }
+    int rc;
+    if ((rc = prof_begin(ctx, &e0, &e1))) return rc;
     if (ctx->sp_G > 0) {
         const int e = launch_apply_split(a, (int)ctx->subs.size(), ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
                                          ctx->sp_ncw, ctx->m_max, ctx->sp_nss, ctx->stream);
@@ -771,11 +799,7 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
         CK(cudaGetLastError());
         ctx->launches++;
     }
-    if (ctx->prof) {
-        CK(cudaEventRecord(e1, ctx->stream));
-        ctx->ev_used.push_back({e0, e1});
-    }
-    return HELM_OK;
+    return prof_end(ctx, e0, e1);
 }
 
 // z = B^-1 r for an owned input vector (exchanging the halo when sharded)
@@ -785,8 +809,48 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
     int rc;
     if ((rc = need_comm(ctx))) return rc;
     if (!ctx->multi) return apply_raw(ctx, r, ctx->G.i0, ctx->G.j0, ctx->G.i1 - ctx->G.i0, z);
-    if ((rc = fill_ext(ctx, r, 0))) return rc;
-    if ((rc = apply_raw(ctx, ctx->d_ext, ctx->G.e_i0, ctx->G.e_j0, ctx->ext_stride, z))) return rc;
+    if (ctx->overlap) {
+        if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
+        const GridInfo& G = ctx->G;
+        launch_copy_rect(r, G.i0, G.j0, G.i1 - G.i0, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, G.i0, G.i1, G.j0,
+                         G.j1, ctx->stream);
+        CK(cudaEventRecord(ctx->ev_ov[0], ctx->stream));
+        cudaEvent_t e0 = nullptr, e1 = nullptr;   // timed: both parts and the exchange they hide
+        if ((rc = prof_begin(ctx, &e0, &e1))) return rc;
+        ApplyArgs a = apply_args(ctx, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, z);
+        auto part = [&](int grid, cudaStream_t st) -> int {
+            if (ctx->sp_G > 0) {
+                const int e = launch_apply_split(a, a.nsub, ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
+                                                 ctx->sp_ncw, ctx->m_max, ctx->sp_nss, st);
+                if (e != 0) {
+                    cudaGetLastError();
+                    return set_err(ctx, HELM_ECUDA, "cluster apply launch: %s", cudaGetErrorString((cudaError_t)e));
+                }
+            } else {
+                launch_apply(a, grid, ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->ap_nslots, st);
+            }
+            CK(cudaGetLastError());
+            return HELM_OK;
+        };
+        a.order = ctx->d_order_ov;   // interior subdomains: owned input only
+        a.nsub = ctx->n_int;
+        if ((rc = part(ctx->grid_int, ctx->stream))) return rc;
+        CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_ov[0], 0));
+        if ((rc = exchange_buf(ctx, 0, ctx->d_ext, false, ctx->cstream))) return rc;
+        a.order = ctx->d_order_ov + ctx->n_int;   // boundary subdomains, once the ghost frame is in
+        a.nsub = ctx->n_bnd;
+        // scratch slots after the interior launch's (plain: one per CTA; split: one per CTA of each cluster)
+        a.scratch = ctx->d_scratch + (ctx->sp_G > 0 ? (long long)ctx->n_int * 2 * ctx->sp_G : (long long)ctx->grid_int) *
+                                         ctx->scratch_per_cta;
+        if ((rc = part(ctx->grid_bnd, ctx->cstream))) return rc;
+        CK(cudaEventRecord(ctx->ev_ov[1], ctx->cstream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_ov[1], 0));
+        if ((rc = prof_end(ctx, e0, e1))) return rc;
+        ctx->launches += 3;
+    } else {
+        if ((rc = fill_ext(ctx, r, 0))) return rc;
+        if ((rc = apply_raw(ctx, ctx->d_ext, ctx->G.e_i0, ctx->G.e_j0, ctx->ext_stride, z))) return rc;
+    }
     if (!ctx->d_pou) return HELM_OK;
     // ramp PoU on several ranks: this rank's weighted contributions on its ghost-framed rectangle, the
     // additive reverse exchange of the frames (width delta), then the owned part is the prolongation
@@ -794,7 +858,7 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
     launch_pou_gather(ctx->d_desc, ctx->d_candx, ctx->d_candy, G.bx0, G.bx1, G.by0, G.by1, ctx->d_pou, ctx->d_cext,
                       G.e_i0, G.e_j0, ctx->ext_stride, G.e_i0, G.e_i1, G.e_j0, G.e_j1, ctx->stream);
     ctx->launches++;
-    if ((rc = exchange_buf(ctx, G.wo, ctx->d_cext, true))) return rc;
+    if ((rc = exchange_buf(ctx, G.wo, ctx->d_cext, true, ctx->stream))) return rc;
     launch_copy_rect(ctx->d_cext, G.e_i0, G.e_j0, ctx->ext_stride, z, G.i0, G.j0, G.i1 - G.i0, G.i0, G.i1, G.j0, G.j1,
                      ctx->stream);
     ctx->launches++;
@@ -1409,7 +1473,47 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     }
     if (ctx->sp_G == 0 && ctx->ap_occ < 1)
         return set_err(ctx, HELM_ECUDA, "apply kernel does not fit on an SM (smem %d)", ctx->ap_smem);
-    long long scr = (size_t)ctx->ap_grid * ctx->scratch_per_cta;
+    // overlap of the multi-rank apply with its halo exchange: split the subdomains into those whose full box lies in
+    // the owned rectangle (no ghost input) and the rest, and the persistent CTA slots in proportion to their bytes
+    const char* ovl = getenv("HELM_APPLY_OVERLAP");
+    if (ctx->multi && ctx->has_comm && !(ovl && ovl[0] == '0')) {
+        const GridInfo& G = ctx->G;
+        std::vector<int> oi, ob;
+        double ci = 0, cb = 0;
+        for (int w : order) {
+            const SubDesc& sd = ctx->subs[w];
+            const bool inside = sd.gx0 >= G.i0 && sd.gx0 + sd.m <= G.i1 && sd.gy0 >= G.j0 && sd.gy0 + sd.nb <= G.j1;
+            const double c = (double)(sd.nb + sd.hi - sd.lo) * sd.m * sd.m;
+            if (inside) {
+                oi.push_back(w);
+                ci += c;
+            } else {
+                ob.push_back(w);
+                cb += c;
+            }
+        }
+        const int S = nsm * std::max(ctx->ap_occ, 1);
+        if (!oi.empty() && !ob.empty() && S >= 2) {
+            int sb = (int)std::lround(S * cb / (ci + cb));
+            sb = std::max(1, std::min(S - 1, sb));
+            auto trim = [](int n, int slots) {
+                slots = std::max(1, std::min(slots, n));
+                const int per = (n + slots - 1) / slots;
+                return (n + per - 1) / per;
+            };
+            ctx->n_int = (int)oi.size();
+            ctx->n_bnd = (int)ob.size();
+            ctx->grid_int = trim(ctx->n_int, S - sb);
+            ctx->grid_bnd = trim(ctx->n_bnd, sb);
+            oi.insert(oi.end(), ob.begin(), ob.end());
+            if ((rc = dalloc(ctx, &ctx->d_order_ov, nsub))) return rc;
+            CK(cudaMemcpyAsync(ctx->d_order_ov, oi.data(), sizeof(int) * nsub, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+            for (auto& e : ctx->ev_ov) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->overlap = true;
+        }
+    }
+    long long scr = (size_t)std::max(ctx->ap_grid, ctx->grid_int + ctx->grid_bnd) * ctx->scratch_per_cta;
     if (ctx->sp_G > 0) {
         long long per = 0;
         for (const SubDesc& sd : ctx->subs) per = std::max(per, (long long)(sd.hi - sd.lo + 1) * ((sd.m + ctx->sp_G - 1) / ctx->sp_G));
@@ -1469,6 +1573,7 @@ int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
     const long long ncst = (long long)std::max(0, ctx->cst[1] - ctx->cst[0]) * std::max(0, ctx->cst[3] - ctx->cst[2]);
     out->spmv_bytes = 16LL * 2 * ctx->n_local + 16LL * G.ns * (ctx->n_local - ncst);
     out->stencil_slots = G.ns;
+    out->overlap_interior = ctx->overlap ? ctx->n_int : 0;
     return HELM_OK;
 }
 
@@ -1701,6 +1806,10 @@ void helm_destroy(helm_ctx* ctx)
     }
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     if (ctx->h_hc) cudaFreeHost(ctx->h_hc);
+    if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+    for (auto e : ctx->ev_ov)
+        if (e) cudaEventDestroy(e);
+    if (ctx->d_order_ov) cudaFree(ctx->d_order_ov);
     for (auto e : ctx->ev_hc)
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_free) cudaEventDestroy(e);

@@ -118,6 +118,20 @@ def test_loopback_short_restart():
     check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub), 4, (2, 2), bj_rhs("c1"), restart=5)
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_loopback_apply_overlap(overlap, monkeypatch):
+    """The apply overlapped with its halo exchange (interior subdomains on the library stream while the ghost frame
+    is exchanged and the boundary subdomains run on the communication stream) and the serial form: both bitwise equal
+    to one rank."""
+    monkeypatch.setenv("HELM_APPLY_OVERLAP", overlap)
+    cfg = CONFIGS["c2"]
+    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    probe = Context(**kw, rank=0, nranks=4, gpu_grid=(2, 2), loopback_group=next(_gid))
+    assert (probe.layout.overlap_interior > 0) == (overlap == "1")
+    probe.close()
+    check_against_single_rank(kw, 4, (2, 2), bj_rhs("c2"))
+
+
 def test_loopback_impedance():
     cfg = CONFIGS["c1"]
     check_against_single_rank(dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, local_bc=BC_IMPEDANCE), 2, (2, 1),
