@@ -311,6 +311,10 @@ struct helm_ctx {
     z2 *d_H = nullptr, *d_dots = nullptr, *d_ca = nullptr, *d_ce = nullptr, *d_hout = nullptr;
     double* d_sc = nullptr;
     bool orth_cgs2 = false;
+    // HELM_GMRES_PHASES=1 (development aid): CUDA events between the phases of every DCGS2 step, totals to stderr
+    bool phases = false;
+    cudaEvent_t ev_ph[8] = {};
+    double ph_ms[8] = {};
     // multi-rank apply overlapped with its halo exchange: subdomains whose full box lies inside the
     // owned rectangle run while the ghost frame is in flight; the rest run on the communication stream after it
     bool overlap = false;
@@ -560,6 +564,11 @@ int ensure_krylov(helm_ctx* ctx, int restart)
             return rc;
         CK(cudaMallocHost((void**)&ctx->h_pin, sizeof(z2) * NVMAX));
         CK(cudaMallocHost((void**)&ctx->h_hc, sizeof(z2) * 2 * (2 * NVMAX + 2)));
+        const char* ph = getenv("HELM_GMRES_PHASES");
+        if (ph && ph[0] == '1') {
+            ctx->phases = true;
+            for (auto& e : ctx->ev_ph) CK(cudaEventCreate(&e));
+        }
 
 
         for (auto& e : ctx->ev_hc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1088,31 +1097,54 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         ctx->launches++;
         std::fill(g.begin(), g.end(), cplx(0, 0));
         constexpr int REC = 2 * NVMAX + 2;   // step record: final column j - 1, pending column j, nu_j, ||u_{j+1}||
+        auto mark = [&](int k) { if (ctx->phases) cudaEventRecord(ctx->ev_ph[k], s); };
         auto enqueue_step = [&](int j) -> int {
             z2* uj = V + (long long)j * n;
             int rc2;
+            mark(0);
             if ((rc2 = apply_impl(ctx, uj, ctx->d_z))) return rc2;
             inf->applies++;
+            mark(1);
             if ((rc2 = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc2;
+            mark(2);
             NvtxRange nv_o("helm.orth");
             launch_multidot2(V, n, j + 1, uj, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
+            mark(3);
             launch_reduce_z2(ctx->d_zpart, ctx->nblk, j + 1, ctx->d_dots, s);
             if ((rc2 = allreduce(ctx, (double*)ctx->d_dots, 4 * (size_t)(j + 1)))) return rc2;   // both groups
             launch_dcgs2_coef(ctx->d_dots, j, ctx->d_H, ctx->d_ca, ctx->d_ce, ctx->d_sc, ctx->d_hout, s);
+            mark(4);
             launch_dcgs2_update(V, n, j, ctx->d_w, ctx->d_ca, ctx->d_ce, ctx->d_sc, n, ctx->d_dpart, ctx->nblk, s);
+            mark(5);
             ctx->launches += 4;
             if ((rc2 = finish_norm(ctx, ctx->d_hout + 2 * NVMAX + 1))) return rc2;
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(ctx->h_hc, ctx->d_hout, sizeof(z2) * REC, cudaMemcpyDeviceToHost, s));
+            mark(6);
             CK(cudaEventRecord(ctx->ev_hc[0], s));
             return HELM_OK;
         };
         // (queueing step j + 1 before the host's update of step j -- step j + 1 needs only device data -- was
         // measured at c3: 93.59 vs 93.56 applies/s, within noise, so the host waits for each step record)
         for (int j = 0; j < m; j++) {
+            if (ctx->phases && j > 0) {   // the previous step's end (mark 6, kept in slot 7) to this step's start
+                CK(cudaEventRecord(ctx->ev_ph[0], s));
+                CK(cudaEventSynchronize(ctx->ev_ph[0]));
+                float g = 0.f;
+                cudaEventElapsedTime(&g, ctx->ev_ph[7], ctx->ev_ph[0]);
+                ctx->ph_ms[7] += g;
+            }
             if ((rc = enqueue_step(j))) return rc;
             its++;
             CK(cudaEventSynchronize(ctx->ev_hc[0]));
+            if (ctx->phases) {
+                for (int k = 0; k < 6; k++) {
+                    float t = 0.f;
+                    cudaEventElapsedTime(&t, ctx->ev_ph[k], ctx->ev_ph[k + 1]);
+                    ctx->ph_ms[k] += t;
+                }
+                std::swap(ctx->ev_ph[6], ctx->ev_ph[7]);
+            }
             const z2* hc = ctx->h_hc;
             const double nu = hc[2 * NVMAX].x, un = hc[2 * NVMAX + 1].x;
             if (!std::isfinite(nu) || !std::isfinite(un)) {
@@ -1805,6 +1837,12 @@ void helm_destroy(helm_ctx* ctx)
         if (ctx->d_recvbuf[q]) cudaFree(ctx->d_recvbuf[q]);
     }
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    if (ctx->phases)
+        fprintf(stderr, "HELM_GMRES_PHASES ms: apply %.1f spmv %.1f multidot2 %.1f reduce+coef %.1f update %.1f "
+                        "norm+record %.1f gap(host) %.1f\n", ctx->ph_ms[0], ctx->ph_ms[1], ctx->ph_ms[2], ctx->ph_ms[3],
+                ctx->ph_ms[4], ctx->ph_ms[5], ctx->ph_ms[7]);
+    for (auto e : ctx->ev_ph)
+        if (e) cudaEventDestroy(e);
     if (ctx->h_hc) cudaFreeHost(ctx->h_hc);
     if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
     for (auto e : ctx->ev_ov)
