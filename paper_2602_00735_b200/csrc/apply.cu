@@ -98,8 +98,8 @@ struct Cp { z2 d, lo, hi; };
 // operands a consumer thread needs for one step, loaded one step ahead
 struct Pre {
     z2 b;         // restricted input b_i[t]      (T, B, Z)
-    Cp c;         // coupling: T, D -> U_i;  B, U, Z -> L_i
-    Cp c2;        // Z: U_i
+    Cp c;         // coupling: T, D -> U_i;  B, U, Z -> L_i  (the Z step's U_i is loaded when used: once per
+                  // subdomain, and keeping it here would spill the carried operands at every step)
     z2 yz;        // y_i / z_i from scratch       (D, U)
 };
 
@@ -144,7 +144,6 @@ __device__ __forceinline__ void prefetch(Pre& p, const SubDesc& d, Step st, int 
     if ((st.ph == PH_T && st.i == d.nb - 1) || (st.ph == PH_B && st.i == 0)) return;
     if (st.ph == PH_Z) {
         if (st.i > 0) p.c = load_lower(row, d.m, t, cst, a);
-        if (st.i < d.nb - 1) p.c2 = load_upper(row, d.m, t, cst, a);
         return;
     }
     if (st.ph == PH_T || st.ph == PH_D) p.c = load_upper(row, d.m, t, cst, a);
@@ -230,7 +229,11 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& a, int nc_warps, int
                 case PH_Z:
                     r = cur.b;
                     if (st.i > 0) cpl_apply(r, cur.c, vb, t, m, true);
-                    if (st.i < d.nb - 1) cpl_apply(r, cur.c2, vt, t, m, true);
+                    if (st.i < d.nb - 1) {
+                        const z2* row = a.stencil + d.stc_off + (long long)st.i * a.ns * d.m;
+                        const bool cst = t >= d.cx0 && t < d.cx1 && st.i >= d.cy0 && st.i < d.cy1;
+                        cpl_apply(r, load_upper(row, m, t, cst, a), vt, t, m, true);
+                    }
                     break;
                 case PH_D:   // U_i x_{i+1}
                     cpl_apply(r, cur.c, vb, t, m, false);
