@@ -1483,10 +1483,10 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     // Among the G <= 8 whose clusters are all resident at once, take the smallest that keeps >= 80 % of the SMs
     // streaming (more G only adds exchange partners), else the largest; each CTA's ring takes the shared memory its
     // share of an SM leaves.  HELM_SPLIT_G overrides (0 = off).
-    if (nsub < nsm) {
+    const char* env_g = getenv("HELM_SPLIT_G");
+    const int gforce = env_g ? atoi(env_g) : -1;
+    if (nsub < nsm || gforce > 0) {
         int gbest = 0, cbest = 1;
-        const char* env = getenv("HELM_SPLIT_G");
-        const int gforce = env ? atoi(env) : -1;
         for (int G = 1; G <= 8; G++) {
             if (gforce >= 0 && G != gforce) continue;
             const int cps = (nsub * 2 * G + nsm - 1) / nsm;   // CTAs per SM if all are resident
