@@ -12,9 +12,9 @@
 //   prolong    z[g] = x_i[t] for the owned nodes of block j only (restricted owner write, D10) -- no
 //              atomics, each global node written exactly once.
 // The dense m x m inverse blocks dominate the bytes.  They are streamed HBM -> shared
-// memory by one producer thread with cp.async.bulk (TMA bulk copies) into an NS-slot ring guarded by
-// mbarriers (full: complete_tx, empty: one arrive per consumer warp), so the stream runs ahead of the
-// serial block-row dependency chain.  Consumer thread t owns row t of every block: the GEMV reads column
+// memory by one producer thread with cp.async.bulk (TMA bulk copies) into a ring of `nslots` slots (2 by default,
+// ~17 KB each, with 4 CTAs per SM -- see SLOT_TARGET) guarded by mbarriers (full: complete_tx, empty: one arrive per
+// consumer warp), so the stream runs ahead of the serial block-row dependency chain.  Consumer thread t owns row t of every block: the GEMV reads column
 // c of the column-major block (consecutive lanes -> consecutive 16-byte words, conflict-free) and the
 // broadcast operand rhs[c].
 #include <stdlib.h>
