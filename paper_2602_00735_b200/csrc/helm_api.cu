@@ -1467,9 +1467,32 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     // the one-CTA-per-subdomain kernel may not fit very wide blocks (its ring holds whole columns); that is only an
     // error when the cluster-split kernel below does not take over
-    if (const char* e = getenv("HELM_APPLY_SLOTS")) ctx->ap_nslots = std::max(2, atoi(e));   // tuning override
     apply_configure(ctx->m_max, ctx->ap_nslots, &ctx->ap_block, &ctx->ap_smem, &ctx->ap_slot, &ctx->ap_occ);
     if (cudaGetLastError() != cudaSuccess) ctx->ap_occ = 0;
+    // Ring depth: two slots when every SM hosts as many CTAs as fit (many subdomains); with fewer subdomains than CTA
+    // slots each CTA may stream deeper -- take the deepest ring (<= 6 slots) that still leaves one CTA slot per SM to
+    // spare over the CTAs the subdomains need.  c2 (256 subdomains, ~2 CTAs/SM): 2 slots 0.617 ms, 3 0.522, 4 0.499,
+    // 6 0.518, 8 (one CTA/SM) 0.838.  HELM_APPLY_SLOTS overrides.
+    if (const char* e = getenv("HELM_APPLY_SLOTS")) {
+        ctx->ap_nslots = std::max(2, atoi(e));
+        apply_configure(ctx->m_max, ctx->ap_nslots, &ctx->ap_block, &ctx->ap_smem, &ctx->ap_slot, &ctx->ap_occ);
+        if (cudaGetLastError() != cudaSuccess) ctx->ap_occ = 0;
+    } else if (ctx->ap_occ > 0) {
+        const int cps = (std::min(nsub, nsm * ctx->ap_occ) + nsm - 1) / nsm;   // CTAs per SM the grid needs
+        for (int ns = 6; ns > 2; ns--) {
+            int blk, sm, sl, occ = 0;
+            apply_configure(ctx->m_max, ns, &blk, &sm, &sl, &occ);
+            if (cudaGetLastError() != cudaSuccess) continue;
+            if (occ >= cps + 1) {
+                ctx->ap_nslots = ns;
+                ctx->ap_block = blk;
+                ctx->ap_smem = sm;
+                ctx->ap_slot = sl;
+                ctx->ap_occ = occ;
+                break;
+            }
+        }
+    }
     // persistent CTAs: as many as fit, then trimmed so that every CTA gets the same number of subdomains (round-robin
     // over the cost-sorted order); measured at c3 (apply ms): 1 GPU 296 CTAs 9.63 -> 293 9.33; the 1/4 shard
     // (1024 subdomains) 296 -> 256 CTAs 2.56 -> 2.28; the 1/8 shard 1.24 -> 1.15 (scripts/shard_timing.py)
