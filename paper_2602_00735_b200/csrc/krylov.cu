@@ -561,8 +561,10 @@ int ew_grid(long long n)
 
 void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s)
 {
+    // each CTA walks several grid rows j (x rows j-1, j, j+1 stay in L1 between iterations) instead of one
     const int gx = (G.nx + KT - 1) / KT;
-    const int gy = G.ny < 65535 ? G.ny : 65535;
+    int gy = std::max(1, 148 * 64 / gx);
+    if (gy > G.ny) gy = G.ny;
     if (G.ns == 9) k_spmv<9><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
     else k_spmv<7><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
 }
