@@ -3,8 +3,9 @@
 A step is one right-preconditioned GMRES(50) Arnoldi iteration over the whole hot path:
 RAS-PML apply (restrict -> twisted block-tridiagonal local solves -> owner write), 7-point SpMV, CGS2
 orthogonalisation with the re-orthogonalisation delayed one step (DCGS2: two sweeps over the basis per step), Givens
-update on the host.  `value` = RAS-PML preconditioner applications per second
-(Arnoldi steps plus the cycle-end x-updates they trigger) over exactly K steps, all inputs resident in HBM.
+update on the host.  `value` = RAS-PML preconditioner applications per second over exactly K steps (one per
+Arnoldi step; a cycle's solution update reuses the steps' applies, so the timed region's cycle ends add only their
+vector work), all inputs resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
@@ -214,8 +215,8 @@ def run_ours(args):
         h2d += 8 * cycles                                       # per-cycle beta
     if args.orth == "cgs2":   # one Hessenberg column per step
         d2h = 16 * n + sum(16 * (min(j % cfg.restart, cfg.restart - 1) + 2) for j in range(args.steps)) + 8 * (cycles + 1)
-    else:   # DCGS2: the step record (2 x 64 + 2 complex) per step, the closed column per cycle
-        d2h = 16 * n + 16 * 130 * args.steps + 16 * (cfg.restart + 1) * cycles + 8 * (cycles + 1)
+    else:   # DCGS2: the step record (3 x 64 + 2 complex) per step, the closed column per cycle
+        d2h = 16 * n + 16 * 194 * args.steps + 16 * (cfg.restart + 1) * cycles + 8 * (cycles + 1)
 
     hbm, peak_src = peaks()
 
@@ -223,8 +224,9 @@ def run_ours(args):
     def tts_bytes(its, restarts):
         """Algorithmic bytes of the whole solve: per Arnoldi step the apply, the SpMV and the orthogonalisation
         sweeps (DCGS2: projection sweep over V_{j+1} and w, update sweep reading V_j, u_j, w and writing v_j,
-        u_{j+1}; CGS2: three sweeps over V_{j+1} plus w traffic); per cycle u_0 = r, the closing projection, the
-        combination V y, one apply, x += z and the true residual."""
+        u_{j+1}; CGS2: three sweeps over V_{j+1} plus w traffic); per cycle u_0 = r, then for DCGS2 the closing
+        projection and x += Z (R^-1 y) (no apply), for CGS2 the combination V y, one apply and x += z; then the
+        true residual."""
         n16 = 16 * ctx.n
         cgs2 = args.orth == "cgs2"
         tot, left = 0, its
@@ -233,8 +235,10 @@ def run_ours(args):
             for j in range(m):
                 orth = 3 * (j + 1) + 7 if cgs2 else 2 * (j + 1) + 4
                 tot += lay["apply_bytes"] + lay["spmv_bytes"] + n16 * orth
-            close = 0 if cgs2 else m + 1
-            tot += n16 * (2 + close + m + 1) + lay["apply_bytes"] + 3 * n16 + lay["spmv_bytes"] + n16
+            if cgs2:   # x += B^-1 (V y): combine, one apply, axpy; then the true residual
+                tot += n16 * (2 + m + 1) + lay["apply_bytes"] + 3 * n16 + lay["spmv_bytes"] + n16
+            else:      # closing projection, x += Z (R^-1 y): combine + axpy (no apply); then the true residual
+                tot += n16 * (2 + (m + 1) + (m + 1)) + 3 * n16 + lay["spmv_bytes"] + n16
             left -= m
         return tot
 

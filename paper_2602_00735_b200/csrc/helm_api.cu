@@ -309,6 +309,9 @@ struct helm_ctx {
     // DCGS2: device Hessenberg (NVMAX + 1) x NVMAX, reduced sweep sums, sweep-2 coefficients, step
     // record for the host (final column j - 1, pending column j, nu_j, ||u_{j+1}||)
     z2 *d_H = nullptr, *d_dots = nullptr, *d_ca = nullptr, *d_ce = nullptr, *d_hout = nullptr;
+    // B^-1 u_j of every step (DCGS2): x += B^-1 V y = Z (R^-1 y) at a cycle's end without another apply
+    z2* d_Z = nullptr;
+    int Z_cap = 0;
     double* d_sc = nullptr;
     bool orth_cgs2 = false;
     // HELM_GMRES_PHASES=1 (development aid): CUDA events between the phases of every DCGS2 step, totals to stderr
@@ -560,10 +563,10 @@ int ensure_krylov(helm_ctx* ctx, int restart)
             (rc = dalloc(ctx, &ctx->d_zpart, (size_t)ctx->nblk * 2 * NVMAX)) || (rc = dalloc(ctx, &ctx->d_dpart, ctx->nblk)) ||
             (rc = dalloc(ctx, &ctx->d_H, (size_t)(NVMAX + 1) * NVMAX)) || (rc = dalloc(ctx, &ctx->d_dots, 2 * NVMAX)) ||
             (rc = dalloc(ctx, &ctx->d_ca, NVMAX)) || (rc = dalloc(ctx, &ctx->d_ce, NVMAX)) ||
-            (rc = dalloc(ctx, &ctx->d_hout, 2 * NVMAX + 2)) || (rc = dalloc(ctx, &ctx->d_sc, 4)))
+            (rc = dalloc(ctx, &ctx->d_hout, 3 * NVMAX + 2)) || (rc = dalloc(ctx, &ctx->d_sc, 4)))
             return rc;
         CK(cudaMallocHost((void**)&ctx->h_pin, sizeof(z2) * NVMAX));
-        CK(cudaMallocHost((void**)&ctx->h_hc, sizeof(z2) * 2 * (2 * NVMAX + 2)));
+        CK(cudaMallocHost((void**)&ctx->h_hc, sizeof(z2) * 2 * (3 * NVMAX + 2)));
         const char* ph = getenv("HELM_GMRES_PHASES");
         if (ph && ph[0] == '1') {
             ctx->phases = true;
@@ -579,6 +582,13 @@ int ensure_krylov(helm_ctx* ctx, int restart)
         ctx->V_cap = 0;
         if ((rc = dalloc(ctx, &ctx->d_V, (size_t)(restart + 1) * n))) return rc;
         ctx->V_cap = restart + 1;
+    }
+    if (!ctx->orth_cgs2 && restart > ctx->Z_cap) {
+        if (ctx->d_Z) cudaFree(ctx->d_Z);
+        ctx->d_Z = nullptr;
+        ctx->Z_cap = 0;
+        if ((rc = dalloc(ctx, &ctx->d_Z, (size_t)restart * n))) return rc;
+        ctx->Z_cap = restart;
     }
     return HELM_OK;
 }
@@ -980,6 +990,8 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
     double est = beta / beta0;
     z2* V = ctx->d_V;
     std::vector<cplx> Hraw((size_t)(m + 1) * m), gkeep(m + 1);
+    std::vector<cplx> Rz((size_t)m * m);   // DCGS2: U = V R (u_j = nu_j v_j + V_j a^(j)), upper triangular
+    auto Rzi = [&](int i, int j) -> cplx& { return Rz[(size_t)i * m + j]; };
     auto Rij = [&](int i, int j) -> cplx& { return Hraw[(size_t)i * m + j]; };
     // Givens rotation of column jc from its unrotated copy (DCGS2 revisits a column once it is final)
     auto rotate_col = [&](int jc) {
@@ -1096,16 +1108,18 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         launch_copy(V, ctx->d_r, n, s);
         ctx->launches++;
         std::fill(g.begin(), g.end(), cplx(0, 0));
-        constexpr int REC = 2 * NVMAX + 2;   // step record: final column j - 1, pending column j, nu_j, ||u_{j+1}||
+        constexpr int REC = 3 * NVMAX + 2;   // step record: final column j - 1, pending column j, nu_j, ||u_{j+1}||,
+                                             // then a (column j of R)
         auto mark = [&](int k) { if (ctx->phases) cudaEventRecord(ctx->ev_ph[k], s); };
         auto enqueue_step = [&](int j) -> int {
             z2* uj = V + (long long)j * n;
             int rc2;
+            z2* zj = ctx->d_Z + (long long)j * n;   // B^-1 u_j, kept for the cycle's solution update
             mark(0);
-            if ((rc2 = apply_impl(ctx, uj, ctx->d_z))) return rc2;
+            if ((rc2 = apply_impl(ctx, uj, zj))) return rc2;
             inf->applies++;
             mark(1);
-            if ((rc2 = spmv_impl(ctx, ctx->d_z, ctx->d_w))) return rc2;
+            if ((rc2 = spmv_impl(ctx, zj, ctx->d_w))) return rc2;
             mark(2);
             NvtxRange nv_o("helm.orth");
             launch_multidot2(V, n, j + 1, uj, ctx->d_w, n, ctx->d_zpart, ctx->nblk, s);
@@ -1152,6 +1166,8 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
                 inf->status = HELM_BREAKDOWN;
                 return set_err(ctx, HELM_BREAKDOWN, "non-finite Arnoldi norm at iteration %d", its);
             }
+            Rzi(j, j) = nu;
+            for (int i = 0; i < j; i++) Rzi(i, j) = cplx(hc[2 * NVMAX + 2 + i].x, hc[2 * NVMAX + 2 + i].y);
             if (j == 0) {
                 g[0] = gkeep[0] = nu;   // ||r|| from the same sweep that normalises v_0
             } else {
@@ -1194,14 +1210,28 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             for (int c = i + 1; c < jend; c++) acc -= Hij(i, c) * y[c];
             y[i] = acc / Hij(i, i);
         }
-        for (int i = 0; i < jend; i++) ctx->h_pin[i] = zmk(y[i].real(), y[i].imag());
-        CK(cudaMemcpyAsync(ctx->d_y, ctx->h_pin, sizeof(z2) * jend, cudaMemcpyHostToDevice, s));
-        launch_combine(V, n, jend, ctx->d_y, ctx->d_t, n, s);
-        ctx->launches++;
-        if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
-        inf->applies++;
-        launch_axpy(x, ctx->d_z, n, s);
-        ctx->launches++;
+        if (!ctx->orth_cgs2) {
+            // B^-1 V y = B^-1 U R^-1 y = Z c with R c = y: the steps' preconditioned candidates, no extra apply
+            for (int i = jend - 1; i >= 0; i--) {
+                cplx acc = y[i];
+                for (int c = i + 1; c < jend; c++) acc -= Rzi(i, c) * y[c];
+                y[i] = acc / Rzi(i, i);
+            }
+            for (int i = 0; i < jend; i++) ctx->h_pin[i] = zmk(y[i].real(), y[i].imag());
+            CK(cudaMemcpyAsync(ctx->d_y, ctx->h_pin, sizeof(z2) * jend, cudaMemcpyHostToDevice, s));
+            launch_combine(ctx->d_Z, n, jend, ctx->d_y, ctx->d_t, n, s);
+            launch_axpy(x, ctx->d_t, n, s);
+            ctx->launches += 2;
+        } else {
+            for (int i = 0; i < jend; i++) ctx->h_pin[i] = zmk(y[i].real(), y[i].imag());
+            CK(cudaMemcpyAsync(ctx->d_y, ctx->h_pin, sizeof(z2) * jend, cudaMemcpyHostToDevice, s));
+            launch_combine(V, n, jend, ctx->d_y, ctx->d_t, n, s);
+            ctx->launches++;
+            if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
+            inf->applies++;
+            launch_axpy(x, ctx->d_z, n, s);
+            ctx->launches++;
+        }
         double rn;
         if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
         cycles++;
@@ -1852,7 +1882,7 @@ void helm_destroy(helm_ctx* ctx)
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
                     ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq,
                     ctx->d_pou, ctx->d_candx, ctx->d_candy, ctx->d_cext, ctx->d_H, ctx->d_dots, ctx->d_ca,
-                    ctx->d_ce, ctx->d_hout, ctx->d_sc};
+                    ctx->d_ce, ctx->d_hout, ctx->d_sc, ctx->d_Z};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int q = 0; q < 4; q++) {

@@ -371,6 +371,7 @@ __global__ void k_dcgs2_coef(const z2* __restrict__ d, int j, z2* __restrict__ H
         for (int i = lane; i < j; i += 32) H[(j - 1) * LD + i] = zadd(H[(j - 1) * LD + i], as[i]);
         if (lane == 0) H[(j - 1) * LD + j] = zmk(nu, 0.0);
     }
+    for (int i = lane; i < j; i += 32) out[2 * NVMAX + 2 + i] = as[i];   // u_j = nu v_j + V_j a: column j of R
     __syncwarp();
     const z2 q = j >= 1 ? zscale(as[j - 1], nu) : zmk(0, 0);
     const z2 hjj = zscale(zsub(zscale(zsub(c, ab), inv), q), inv);
