@@ -982,6 +982,14 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
     }
     double beta;
     if ((rc = residual_host(ctx, b, x, ctx->d_r, &beta))) return rc;
+    if (!std::isfinite(beta)) {
+        inf->status = HELM_BREAKDOWN;
+        return set_err(ctx, HELM_BREAKDOWN, "non-finite initial residual");
+    }
+    if (beta == 0.0 || (rtol > 0 && beta <= rtol * beta0)) {   // the initial guess already solves the system
+        inf->relres_est = inf->relres_true = beta / beta0;
+        return HELM_OK;
+    }
     const int m = restart;
     std::vector<cplx> H((size_t)(m + 1) * m), g(m + 1), sn(m), y(m);
     std::vector<double> cs(m);

@@ -244,8 +244,17 @@ def test_gmres_initial_guess_and_restart_bounds():
     x5, info5, _ = ctx.gmres(to_dev(b), restart=5, rtol=1e-6)
     assert info5.status == 0 and abs(info5.iterations - ref5.iterations) <= 1 and info5.restarts == ref5.restarts
     assert rel(to_np(x5), ref5.x) <= 1e-6
-    _, info63, _ = ctx.gmres(to_dev(b), restart=63, rtol=1e-6)
+    x63, info63, _ = ctx.gmres(to_dev(b), restart=63, rtol=1e-6)
     assert info63.status == 0
+    # an initial guess that already meets rtol returns at once (0 iterations, x unchanged); the exact zero residual
+    # (b = A x0 exactly, here b := A x63) too, with no division by a zero Krylov norm
+    xs = x63.clone()
+    again, info_a, _ = ctx.gmres(to_dev(b), xs, restart=50, rtol=1e-6)
+    assert info_a.status == 0 and info_a.iterations == 0 and torch.equal(again, x63)
+    bx = ctx.matvec(x63)
+    xz = x63.clone()
+    _, info_z, _ = ctx.gmres(bx, xz, restart=50, rtol=1e-12)
+    assert info_z.status == 0 and info_z.iterations == 0 and info_z.relres_true == 0.0 and torch.equal(xz, x63)
     with pytest.raises(HelmError) as e:
         ctx.gmres(to_dev(b), restart=64, rtol=1e-6)
     assert e.value.code == -1
