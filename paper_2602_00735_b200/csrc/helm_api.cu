@@ -1252,7 +1252,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             inf->status = HELM_BREAKDOWN;
             return set_err(ctx, HELM_BREAKDOWN, "non-finite residual");
         }
-        if (rtol > 0 && tr <= rtol) {
+        if (tr == 0.0 || (rtol > 0 && tr <= rtol)) {   // (an exactly zero residual ends the solve even at rtol = 0)
             inf->status = HELM_OK;
             return HELM_OK;
         }
