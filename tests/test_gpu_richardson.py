@@ -74,3 +74,31 @@ def test_gpu_iterates_keep_residual_on_interfaces():
     band = band.ravel()
     assert np.max(np.abs(r[~band])) <= 1e-12 * np.linalg.norm(b)
     assert np.max(np.abs(r[band])) > 1e-6 * np.linalg.norm(b)
+
+
+def test_error_propagation_identity():
+    """The iteration's error obeys e <- (I - B^-1 A) e: one Richardson step on b = A x* from u0 moves the
+    error x* - u to (I - B^-1 A)(x* - u0), computed independently from the apply and the matvec; and the error
+    operator annihilates nothing it should not -- two steps equal applying it twice."""
+    cfg = CONFIGS["c1"]
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub)
+    ctx.factor()
+    g = torch.Generator(device="cpu").manual_seed(11)
+    xs = torch.complex(torch.randn(ctx.n, generator=g, dtype=torch.float64),
+                       torch.randn(ctx.n, generator=g, dtype=torch.float64)).cuda()
+    u0 = 0.5 * torch.complex(torch.randn(ctx.n, generator=g, dtype=torch.float64),
+                             torch.randn(ctx.n, generator=g, dtype=torch.float64)).cuda()
+    b = ctx.matvec(xs)
+
+    def err_op(e):   # (I - B^-1 A) e
+        return e - ctx.precond_apply(ctx.matvec(e))
+
+    for steps in (1, 2):
+        u, info, _ = ctx.richardson(b, u0.clone(), rtol=0.0, maxit=steps)
+        assert info.iterations == steps
+        e = xs - u0
+        for _ in range(steps):
+            e = err_op(e)
+        got = xs - u
+        assert float(torch.linalg.norm(got - e) / torch.linalg.norm(e)) <= 1e-10
+    ctx.close()
