@@ -1606,6 +1606,14 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
             ctx->overlap = true;
         }
     }
+    if (const char* dbg = getenv("HELM_DEBUG_CONFIG"))   // diagnostic: the apply configuration this rank chose
+        if (dbg[0] == '1')
+            fprintf(stderr,
+                    "helm rank %d: %d subdomains, m_max %d; apply %s: grid %d block %d smem %d slot %d slots %d "
+                    "(occ %d); split G %d block %d smem %d slot %d slots %d; overlap %d (%d interior)\n",
+                    ctx->rank, nsub, ctx->m_max, ctx->sp_G > 0 ? "cluster-split" : "k_apply", ctx->ap_grid,
+                    ctx->ap_block, ctx->ap_smem, ctx->ap_slot, ctx->ap_nslots, ctx->ap_occ, ctx->sp_G, ctx->sp_block,
+                    ctx->sp_smem, ctx->sp_slot, ctx->sp_nss, (int)ctx->overlap, ctx->n_int);
     long long scr = (size_t)std::max(ctx->ap_grid, ctx->grid_int + ctx->grid_bnd) * ctx->scratch_per_cta;
     if (ctx->sp_G > 0) {
         long long per = 0;
