@@ -1,10 +1,10 @@
-"""SURVEY 8(d) "Reporting" for the BASELINE.json configs on one GPU, with the CPU oracle timed beside (a baseline,
-not the target).  Per config: setup and factorisation time, apply time (median of 20 after 3 warm-ups) as applies/s,
-algorithmic and band-equivalent GB/s against the measured copy peak, SpMV, GMRES(50) to 1e-6 (iterations,
-restarts, time) and its roofline fraction; the oracle's factorisation, apply (median of 3) and GMRES time for the
-configs it finishes in minutes.  Prints a markdown table (profiles/r01_configs.md).
+"""SURVEY 8(d) "Reporting" for the BASELINE.json configs on one GPU.  Per config: setup and factorisation time, apply
+time (median of 20 after 3 warm-ups) as applies/s, algorithmic and band-equivalent GB/s against the measured copy
+peak, SpMV, GMRES(50) to 1e-6 (iterations, restarts, time) and its roofline fraction.  Prints a markdown table
+(profiles/r01_configs.md).  The oracle's timings beside it come from bench.py's cpu_baseline leg
+(`python bench.py --config cX`, key cpu_baseline.full_oracle): only tests/, smoke() and that leg run the oracle.
 
-    python scripts/config_table.py c0 c1 c2 c3 [--oracle c0,c1,c2]
+    python scripts/config_table.py c0 c1 c2 c3
 """
 import json
 import os
@@ -80,53 +80,22 @@ def gpu_row(name):
     return row
 
 
-def oracle_row(name):
-    from oracle.oracle import Oracle, gmres
-    cfg = CONFIGS[name]
-    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
-    t = time.perf_counter()
-    o.factor()
-    fs = time.perf_counter() - t
-    v = probe_vector(o.nfree, int(cfg.k) + 1)
-    ts = []
-    for _ in range(3):
-        t = time.perf_counter()
-        o.apply(v)
-        ts.append(time.perf_counter() - t)
-    ap = statistics.median(ts)
-    b = o.rhs(*sources(cfg))
-    t = time.perf_counter()
-    res = gmres(o.matvec, o.apply, b, restart=cfg.restart, rtol=cfg.rtol)
-    tts = time.perf_counter() - t
-    o.close()
-    return dict(factor_s=fs, apply_s=ap, its=res.iterations, tts_s=tts)
-
-
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     names = args or ["c0", "c1", "c2", "c3"]
-    orc = []
-    for a in sys.argv[1:]:
-        if a.startswith("--oracle"):
-            orc = a.split("=", 1)[1].split(",") if "=" in a else ["c0", "c1", "c2"]
-    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
-    print(f"1 x {torch.cuda.get_device_name()}; copy peak {PEAK} GB/s (MEASURED_PEAKS.json); oracle on "
-          f"{os.environ['OMP_NUM_THREADS']} host threads\n")
+    print(f"1 x {torch.cuda.get_device_name()}; copy peak {PEAK} GB/s (MEASURED_PEAKS.json)\n")
     w = Context(CONFIGS["c0"].k, CONFIGS["c0"].nsub, CONFIGS["c0"].nsub)   # untimed: CUDA context and module loading
     w.factor()
     w.close()
     print("| cfg | unknowns | subdomains | factors GB | setup s | factor s | apply ms | applies/s | GB/s (frac) | "
-          "band-equiv. GB/s | SpMV ms | GMRES its / restarts | TTS s | TTS roofline frac | oracle factor s | "
-          "oracle apply s | oracle GMRES its / s |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+          "band-equiv. GB/s | SpMV ms | GMRES its / restarts | TTS s | TTS roofline frac |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for name in names:
         r = gpu_row(name)
-        o = oracle_row(name) if name in orc else None
-        ocol = (f"{o['factor_s']:.2f} | {o['apply_s']:.3f} | {o['its']} / {o['tts_s']:.1f}" if o else "— | — | —")
         print(f"| {name} | {r['unknowns']:,} | {r['subdomains']} | {r['factor_GB']:.2f} | {r['setup_s']:.3f} | "
               f"{r['factor_s']:.3f} | {r['apply_ms']:.3f} | {r['applies_per_s']:.1f} | {r['GBps']:.0f} "
               f"({r['GBps'] / PEAK:.2f}) | {r['band_GBps']:.0f} | {r['spmv_ms']:.3f} | {r['its']} / {r['restarts']} | "
-              f"{r['tts_s']:.3f} | {r['tts_roofline_frac']:.2f} | {ocol} |", flush=True)
+              f"{r['tts_s']:.3f} | {r['tts_roofline_frac']:.2f} |", flush=True)
 
 
 if __name__ == "__main__":
