@@ -8,6 +8,7 @@ inner products are summed in another order).  SURVEY 8(e).  -m gpu."""
 import itertools
 import threading
 
+import numpy as np
 import pytest
 
 from paper_2602_00735_b200.workloads import CONFIGS, paper_source, probe_vector, sources
@@ -158,3 +159,61 @@ def test_loopback_paper_q1_ramp():
     """The paper's own method (Q1, RAS-PML-Imp, linear ramps) across 4 ranks: the configuration Tables 1-4 run."""
     kw = paper_params(150.0, 4, 6, 3)
     check_against_single_rank(kw, 4, (2, 2), lambda ctx: ctx.rhs(*paper_source(150.0)), rtol=1e-10, bitwise=False)
+
+
+def _loop_draws(n=8, seed=77):
+    rng = np.random.default_rng(seed)
+    grids = [(2, 1), (1, 2), (2, 2), (3, 1), (2, 3), (4, 1)]
+    out = []
+    for _ in range(n):
+        gg = grids[int(rng.integers(0, len(grids)))]
+        out.append(dict(k=float(rng.choice([50, 80, 120])), nsub_x=int(rng.integers(gg[0], 9)),
+                        nsub_y=int(rng.integers(gg[1], 9)), gg=gg, local_bc=int(rng.integers(0, 2)),
+                        pou=int(rng.integers(0, 2))))
+    return out
+
+
+@pytest.mark.parametrize("d", _loop_draws(), ids=lambda d: "-".join(f"{a}{b}" for a, b in d.items()))
+def test_loopback_random_layouts(d):
+    """Seeded random layouts and rank grids: the sharded apply (overlapped with its halo) and matvec against one rank
+    -- bitwise for the owner write, to the order of the additions for the ramp PoU."""
+    kw = dict(k=d["k"], nsub_x=d["nsub_x"], nsub_y=d["nsub_y"], local_bc=d["local_bc"], pou=d["pou"])
+    gg = d["gg"]
+    nranks = gg[0] * gg[1]
+    if d["nsub_x"] < gg[0] or d["nsub_y"] < gg[1]:
+        pytest.skip("fewer subdomains than ranks along an axis")
+    ref = Context(**kw)
+    ref.factor()
+    nf = ref.layout.N_cells - 1
+    v = torch.from_numpy(probe_vector(ref.n, 12)).cuda()
+    z_ref, y_ref = ref.precond_apply(v), ref.matvec(v)
+    ref.close()
+    V = v.view(nf, nf)
+    gid = next(_gid)
+    torch.cuda.synchronize()
+
+    def rank(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c = Context(**kw, gpu_grid=gg, rank=r, nranks=nranks, stream=s, loopback_group=gid)
+            c.factor()
+            pl = c.plan
+            vl = owned(V, pl)
+            z, y = c.precond_apply(vl), c.matvec(vl)
+            s.synchronize()
+            out = dict(pl=pl, z=z.clone(), y=y.clone())
+            c.close()
+            return out
+
+    outs = run_ranks(nranks, rank)
+    Z, Y = torch.full_like(V, complex("nan")), torch.full_like(V, complex("nan"))
+    for o in outs:
+        pl = o["pl"]
+        sl = (slice(pl["owned_j0"] - 1, pl["owned_j1"] - 1), slice(pl["owned_i0"] - 1, pl["owned_i1"] - 1))
+        shape = (pl["owned_j1"] - pl["owned_j0"], pl["owned_i1"] - pl["owned_i0"])
+        Z[sl], Y[sl] = o["z"].view(shape), o["y"].view(shape)
+    assert torch.equal(Y.view(-1), y_ref)
+    if d["pou"] == 0:
+        assert torch.equal(Z.view(-1), z_ref)
+    else:
+        assert float(torch.linalg.norm(Z.view(-1) - z_ref) / torch.linalg.norm(z_ref)) <= 1e-13
