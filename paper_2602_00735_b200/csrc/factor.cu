@@ -13,6 +13,8 @@
 // adds a third diagonal to L_i (SE) and U_i (NW).
 #include <stdio.h>
 
+#include <stdlib.h>
+
 #include "internal.cuh"
 
 namespace {
@@ -697,7 +699,8 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
 {
     if (m_max > M_SMEM) {
         // clusters of bc CTAs: all chains, then all twist blocks; 16-CTA clusters when 8-CTA ones leave SMs idle
-        const int bc = 2 * nsub * 8 < 148 ? BCMAX : 8;
+        int bc = 2 * nsub * 8 < 148 ? BCMAX : 8;
+        if (const char* e = getenv("HELM_FACTOR_BC")) bc = atoi(e);   // tuning override (t1200: 4 0.83 s, 6 0.78, 8 0.86)
         const int smem = big_smem_bytes(m_max, bc);
         cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (bc > 8) cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
