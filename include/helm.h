@@ -142,7 +142,9 @@ int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host)
  * iterations.  Synchronous.  Returns HELM_OK / HELM_NOT_CONVERGED / HELM_BREAKDOWN or an error.
  * Orthogonalisation: classical Gram-Schmidt with one re-orthogonalisation pass (CGS2), by default with that pass
  * delayed into the next step's projection sweep (DCGS2: two sweeps over the basis per step instead of
- * three; the same vectors in exact arithmetic); helm_set_orthogonalisation selects the undelayed form. */
+ * three; the same vectors in exact arithmetic) and the cycle's solution update formed from the steps' own applies
+ * (x += Z R^-1 y: one apply per iteration, none per restart); helm_set_orthogonalisation selects the undelayed form.
+ * An initial guess that already meets rtol returns at once with 0 iterations.  info->applies counts applies. */
 int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, double rtol, int maxit,
                helm_gmres_info* info);
 
