@@ -123,6 +123,9 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl")
     cfg = CONFIGS[args.config]
+    if args.seed is not None:   # another draw of the same workload (sources; the probe vectors keep k + 1)
+        import dataclasses
+        cfg = dataclasses.replace(cfg, seed=args.seed)
     # a dedicated (non-default) stream for the library and everything timed around it; torch work issued below
     # (inputs, events, the barrier's NCCL collectives) is ordered on it as the current stream
     stream = torch.cuda.Stream()
@@ -487,6 +490,9 @@ def run_reference(args):
         return
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
     cfg = CONFIGS[args.config]
+    if args.seed is not None:   # another draw of the same workload (sources; the probe vectors keep k + 1)
+        import dataclasses
+        cfg = dataclasses.replace(cfg, seed=args.seed)
     step, desc = _oracle_step_model(cfg)
     for _ in range(args.warmup):
         step()
@@ -512,6 +518,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper Table 4 comparison rows")
+    ap.add_argument("--seed", type=int, default=None, help="source draw seed (default: the config's, = k)")
     ap.add_argument("--orth", default="dcgs2", choices=["dcgs2", "cgs2"],
                     help="GMRES orthogonalisation (DESIGN.md 5.6); cgs2 = the undelayed form, for A/B")
     args = ap.parse_args()
