@@ -1141,13 +1141,17 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             ctx->launches += 4;
             if ((rc2 = finish_norm(ctx, ctx->d_hout + 2 * NVMAX + 1))) return rc2;
             CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(ctx->h_hc, ctx->d_hout, sizeof(z2) * REC, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ctx->h_hc + (j & 1) * REC, ctx->d_hout, sizeof(z2) * REC, cudaMemcpyDeviceToHost, s));
             mark(6);
-            CK(cudaEventRecord(ctx->ev_hc[0], s));
+            CK(cudaEventRecord(ctx->ev_hc[j & 1], s));
             return HELM_OK;
         };
-        // (queueing step j + 1 before the host's update of step j -- step j + 1 needs only device data -- was
-        // measured at c3: 93.59 vs 93.56 applies/s, within noise, so the host waits for each step record)
+        // Several ranks: step j + 1 (it needs only device data) is queued before the host's update of step j, so the
+        // devices never wait for the host's turnaround; when step j turns out to be the cycle's last, step j + 1 is
+        // discarded and its record supplies the final column j.  One rank: the turnaround is 0.3 % of a c3 step
+        // (93.59 vs 93.56 applies/s with and without), not worth the discarded apply at convergence.
+        const bool lookahead = ctx->multi && !ctx->phases;
+        if (lookahead && (rc = enqueue_step(0))) return rc;
         for (int j = 0; j < m; j++) {
             if (ctx->phases && j > 0) {   // the previous step's end (mark 6, kept in slot 7) to this step's start
                 CK(cudaEventRecord(ctx->ev_ph[0], s));
@@ -1156,9 +1160,11 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
                 cudaEventElapsedTime(&g, ctx->ev_ph[7], ctx->ev_ph[0]);
                 ctx->ph_ms[7] += g;
             }
-            if ((rc = enqueue_step(j))) return rc;
+            const bool ahead = lookahead && j + 1 < m && its + 2 <= maxit;
+            if (!lookahead && (rc = enqueue_step(j))) return rc;
+            if (ahead && (rc = enqueue_step(j + 1))) return rc;
             its++;
-            CK(cudaEventSynchronize(ctx->ev_hc[0]));
+            CK(cudaEventSynchronize(ctx->ev_hc[j & 1]));
             if (ctx->phases) {
                 for (int k = 0; k < 6; k++) {
                     float t = 0.f;
@@ -1167,7 +1173,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
                 }
                 std::swap(ctx->ev_ph[6], ctx->ev_ph[7]);
             }
-            const z2* hc = ctx->h_hc;
+            const z2* hc = ctx->h_hc + (j & 1) * REC;
             const double nu = hc[2 * NVMAX].x, un = hc[2 * NVMAX + 1].x;
             if (!std::isfinite(nu) || !std::isfinite(un)) {
                 inf->iterations = its;
@@ -1196,6 +1202,15 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
             jend = j + 1;
             if ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || un == 0.0 || its >= maxit || j == m - 1) {
+                if (ahead) {   // the queued step j + 1 (discarded) has closed column j
+                    CK(cudaEventSynchronize(ctx->ev_hc[(j + 1) & 1]));
+                    const z2* h1 = ctx->h_hc + ((j + 1) & 1) * REC;
+                    for (int i = 0; i <= j + 1; i++) Rij(i, j) = cplx(h1[i].x, h1[i].y);
+                    rotate_col(j);
+                    est = std::abs(g[j + 1]) / beta0;
+                    if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
+                    break;
+                }
                 // close column j: re-orthogonalise u_{j+1} against V_{j+1}
                 launch_multidot(V, n, j + 2, V + (long long)(j + 1) * n, n, ctx->d_zpart, ctx->nblk, s);
                 launch_reduce_z(ctx->d_zpart, ctx->nblk, j + 2, ctx->d_dots, nullptr, nullptr, s);
