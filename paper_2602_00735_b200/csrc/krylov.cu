@@ -274,17 +274,19 @@ __global__ void __launch_bounds__(KT) k_multiaxpy(const z2* __restrict__ V, long
 //                           sigma = q / nu + h_jj, e = p / nu + h - a sigma / nu                   (reads V once)
 // which is CGS2's v_j and u_{j+1} = A B^-1 v_j - V_{j+1} h in exact arithmetic (A B^-1 V_j = V_{j+1} H(0:j+1, 0:j)).
 
-// partial[blk][q] = sum_e conj(V_q[e]) u[e] (q < nv), partial[blk][NVMAX + q] = sum_e conj(V_q[e]) w[e].
-// Basis vectors are taken VB at a time so that R * VB independent loads are in flight before the 2 * VB warp
-// reductions (which are independent of each other and pipeline).
-template <int R, int VB>
+// partial[blk][q] = sum_e conj(V_q[e]) u[e] (q < nv), partial[blk][NVMAX + q] = sum_e conj(V_q[e]) w[e], with a
+// transposing warp reduction: per batch of 8 basis vectors each lane holds 32 partial values
+// (8 vectors x {u, w} x {re, im}); five exchange-and-add levels (16 + 8 + 4 + 2 + 1 = 31 shuffles, instead of 5 per
+// value) leave lane L with the warp's sum of value L.  Fixed order: deterministic.
+template <int R>
 __global__ void __launch_bounds__(KT) k_multidot2(const z2* __restrict__ V, long long ldv, int nv,
-                                                  const z2* __restrict__ u, const z2* __restrict__ w, long long n,
-                                                  z2* __restrict__ partial)
+                                                   const z2* __restrict__ u, const z2* __restrict__ w, long long n,
+                                                   z2* __restrict__ partial)
 {
-    __shared__ z2 acc[KT / 32][2 * NVMAX];
+    constexpr int VB = 8;
+    __shared__ double acc[KT / 32][2 * NVMAX * 2];   // [warp][(v | NVMAX for w) * 2 + re/im]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int v = lane; v < 2 * NVMAX; v += 32) acc[warp][v] = zmk(0, 0);
+    for (int q = lane; q < 4 * NVMAX; q += 32) acc[warp][q] = 0.0;
     __syncwarp();
     long long r0, r1;
     chunk_of(n, r0, r1);
@@ -298,46 +300,44 @@ __global__ void __launch_bounds__(KT) k_multidot2(const z2* __restrict__ V, long
             wv[q] = e[q] < r1 ? __ldg(w + e[q]) : zmk(0, 0);
         }
         for (int v0 = 0; v0 < nv; v0 += VB) {
-            z2 x[VB][R];
-#pragma unroll
-            for (int b = 0; b < VB; b++)
-#pragma unroll
-                for (int q = 0; q < R; q++)
-                    x[b][q] = (v0 + b < nv && e[q] < r1) ? __ldg(V + (v0 + b) * ldv + e[q]) : zmk(0, 0);
-            z2 su[VB], sw[VB];
+            double t[32];
 #pragma unroll
             for (int b = 0; b < VB; b++) {
-                su[b] = zmk(0, 0);
-                sw[b] = zmk(0, 0);
+                z2 su = zmk(0, 0), sw = zmk(0, 0);
 #pragma unroll
                 for (int q = 0; q < R; q++) {
-                    zfma_conj(su[b], x[b][q], uv[q]);
-                    zfma_conj(sw[b], x[b][q], wv[q]);
+                    const z2 x = (v0 + b < nv && e[q] < r1) ? __ldg(V + (v0 + b) * ldv + e[q]) : zmk(0, 0);
+                    zfma_conj(su, x, uv[q]);
+                    zfma_conj(sw, x, wv[q]);
                 }
+                t[4 * b + 0] = su.x;
+                t[4 * b + 1] = su.y;
+                t[4 * b + 2] = sw.x;
+                t[4 * b + 3] = sw.y;
             }
 #pragma unroll
-            for (int off = 16; off; off >>= 1)
+            for (int o = 16; o; o >>= 1) {
+                const bool hi = lane & o;
 #pragma unroll
-                for (int b = 0; b < VB; b++) {
-                    su[b].x += __shfl_xor_sync(0xffffffffu, su[b].x, off);
-                    su[b].y += __shfl_xor_sync(0xffffffffu, su[b].y, off);
-                    sw[b].x += __shfl_xor_sync(0xffffffffu, sw[b].x, off);
-                    sw[b].y += __shfl_xor_sync(0xffffffffu, sw[b].y, off);
+                for (int k = 0; k < o; k++) {
+                    const double send = hi ? t[k] : t[k + o];
+                    const double keep = hi ? t[k + o] : t[k];
+                    t[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
-            if (lane == 0)
-#pragma unroll
-                for (int b = 0; b < VB; b++)
-                    if (v0 + b < nv) {
-                        acc[warp][v0 + b] = zadd(acc[warp][v0 + b], su[b]);
-                        acc[warp][NVMAX + v0 + b] = zadd(acc[warp][NVMAX + v0 + b], sw[b]);
-                    }
+            }
+            // lane L holds value L = 4 b + {0: Re u, 1: Im u, 2: Re w, 3: Im w}
+            const int b = lane >> 2, part = lane & 3;
+            if (v0 + b < nv) {
+                const int slot = ((part >> 1) ? NVMAX : 0) + v0 + b;
+                acc[warp][2 * slot + (part & 1)] += t[0];
+            }
         }
     }
     __syncthreads();
     for (int v = threadIdx.x; v < 2 * NVMAX; v += blockDim.x) {
         if ((v & (NVMAX - 1)) >= nv) continue;
         z2 s = zmk(0, 0);
-        for (int q = 0; q < KT / 32; q++) s = zadd(s, acc[q][v]);
+        for (int q = 0; q < KT / 32; q++) s = zadd(s, zmk(acc[q][2 * v], acc[q][2 * v + 1]));
         partial[(long long)blockIdx.x * 2 * NVMAX + v] = s;
     }
 }
@@ -613,9 +613,9 @@ void launch_reduce_z(const z2* partial, int nblk, int nv, z2* out, z2* out_plus,
 void launch_multidot2(const z2* V, long long ldv, int nv, const z2* u, const z2* w, long long n, z2* partial, int nblk,
                       cudaStream_t s)
 {
-    // R = 4 rows per thread, VB = 4 vectors per batch; measured at c3 (step ms): <4,4> 10.88, <4,1> 11.05,
-    // <2,4> 11.09, <2,2> 11.04, <1,4> 11.54
-    k_multidot2<4, 4><<<nblk, KT, 0, s>>>(V, ldv, nv, u, w, n, partial);
+    // c3, 105 steps (ms): transposing reduction R = 2 52.8, R = 4 54.8, R = 1 72.1; per-value shuffle trees with
+    // 4-vector batches (R = 4) 56.7
+    k_multidot2<2><<<nblk, KT, 0, s>>>(V, ldv, nv, u, w, n, partial);
 }
 void launch_reduce_z2(const z2* partial, int nblk, int nv, z2* out, cudaStream_t s)
 {
