@@ -441,14 +441,19 @@ __global__ void __launch_bounds__(KT) k_dcgs2_update(z2* V, long long ldv, int j
     long long r0, r1;
     chunk_of(n, r0, r1);
     double s = 0.0;
+    // the coefficients are read from shared memory ahead of each basis load and the loop is unrolled by 4, so four
+    // basis loads are in flight per thread (c3, 105 steps: 54.0 -> 49.5 ms; two rows per thread 53.2; the same loop
+    // with the shared-memory reads inside the FMAs 75 ms)
     for (long long e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
-        const z2 u = uj[e];
         z2 av = zmk(0, 0), ev = zmk(0, 0);
+#pragma unroll 4
         for (int v = 0; v < j; v++) {
+            const z2 ca_v = cs[v], ce_v = cs[NVMAX + v];
             const z2 x = __ldg(V + v * ldv + e);
-            zfma(av, cs[v], x);
-            zfma(ev, cs[NVMAX + v], x);
+            zfma(av, ca_v, x);
+            zfma(ev, ce_v, x);
         }
+        const z2 u = uj[e];
         const z2 vj = zsub(zscale(u, inv), av);
         z2 nx = zscale(__ldg(w + e), inv);
         nx = zsub(nx, zmul(sinv, u));
