@@ -24,18 +24,26 @@ def timed(fn, reps=10):
 
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+Ns = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 4, 8]
 cfg = CONFIGS[name]
-full = Context(cfg.k, cfg.nsub, cfg.nsub)
-full.factor()
-v = torch.randn(full.n, dtype=torch.complex128, device="cuda")
-t1 = timed(lambda: full.precond_apply(v))
-nf = full.layout.N_cells - 1
-V = v.view(nf, nf)
-full.close()
-del full
-torch.cuda.empty_cache()
-print(f"{name} N=1 apply {t1:.3f} ms", flush=True)
-for N in (2, 4, 8):
+if name == "c4":   # 198 GB of factors: no one-GPU reference; the shards alone (ideal = sum of shard bytes at the mean)
+    probe = Context(cfg.k, cfg.nsub, cfg.nsub, rank=0, nranks=Ns[0])
+    nf = probe.layout.N_cells - 1
+    probe.close()
+    V = torch.randn(nf * nf, dtype=torch.complex128, device="cuda").view(nf, nf)
+    t1 = None
+else:
+    full = Context(cfg.k, cfg.nsub, cfg.nsub)
+    full.factor()
+    v = torch.randn(full.n, dtype=torch.complex128, device="cuda")
+    t1 = timed(lambda: full.precond_apply(v))
+    nf = full.layout.N_cells - 1
+    V = v.view(nf, nf)
+    full.close()
+    del full
+    torch.cuda.empty_cache()
+    print(f"{name} N=1 apply {t1:.3f} ms", flush=True)
+for N in Ns:
     ts = []
     for r in range(N):
         c = Context(cfg.k, cfg.nsub, cfg.nsub, rank=r, nranks=N)
@@ -46,5 +54,6 @@ for N in (2, 4, 8):
         c.close()
         del c
         torch.cuda.empty_cache()
-    print(f"{name} N={N} shard apply ms: max {max(ts):.3f} mean {sum(ts) / N:.3f} ideal {t1 / N:.3f} "
-          f"-> balance efficiency {t1 / N / max(ts):.3f}  {['%.3f' % t for t in ts]}", flush=True)
+    ideal = t1 / N if t1 else sum(ts) / N
+    print(f"{name} N={N} shard apply ms: max {max(ts):.3f} mean {sum(ts) / N:.3f} ideal {ideal:.3f} "
+          f"-> balance efficiency {ideal / max(ts):.3f}  {['%.3f' % t for t in ts]}", flush=True)
