@@ -698,9 +698,32 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
                    int* d_err, cudaStream_t s)
 {
     if (m_max > M_SMEM) {
-        // clusters of bc CTAs: all chains, then all twist blocks; 16-CTA clusters when 8-CTA ones leave SMs idle
-        int bc = 2 * nsub * 8 < 148 ? BCMAX : 8;
-        if (const char* e = getenv("HELM_FACTOR_BC")) bc = atoi(e);   // tuning override (t1200: 4 0.83 s, 6 0.78, 8 0.86)
+        // clusters of bc CTAs: all chains, then all twist blocks; 16-CTA clusters when 8-CTA ones leave SMs idle.
+        // Otherwise 6 or 8 CTAs per chain, whichever the model (waves of resident CTAs) x (per-block cost ~ 29 + m/bc
+        // rows) says is shorter -- calibrated at k = 1200 (128 chains: bc 6 0.77 s, 8 0.86 s) and k = 600 (32 chains:
+        // bc 8 0.21 s, 6 0.23 s).  HELM_FACTOR_BC overrides.
+        int nsm = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        int bc = 2 * nsub * 8 < nsm ? BCMAX : 8;
+        if (bc == 8) {
+            double best = 1e300;
+            for (int cand : {8, 6}) {
+                const int sm = big_smem_bytes(m_max, cand);
+                cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+                int occ = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_big, BT, sm);
+                if (occ < 1) continue;
+                const long long slots = (long long)nsm * occ, ctas = 2LL * nsub * cand;
+                const double est = (double)((ctas + slots - 1) / slots) * (29.0 + (double)m_max / cand);
+                if (est < best) {
+                    best = est;
+                    bc = cand;
+                }
+            }
+            cudaGetLastError();
+        }
+        if (const char* e = getenv("HELM_FACTOR_BC")) bc = atoi(e);
         const int smem = big_smem_bytes(m_max, bc);
         cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (bc > 8) cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
