@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--solver", default="richardson", choices=["richardson", "gmres"])
     ap.add_argument("--drch", action="store_true")
+    ap.add_argument("--warmup", type=int, default=1, help="untimed warm-up on a small paper-type problem (0: off)")
     args = ap.parse_args()
 
     import torch
@@ -43,6 +44,12 @@ def main():
             buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, src=0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
+    if args.warmup:   # untimed: CUDA context, lazily loaded kernels and clocks, through the same code paths
+        for kw_, ns_ in ((60.0, 2), (100.0, 1)):
+            w = Context(**paper_params(kw_, ns_, 4, 2), rank=0, nranks=1)
+            w.factor()
+            w.richardson(w.rhs(*paper_source(kw_)), rtol=1e-6, maxit=3)
+            w.close()
     c = PAPER_CONFIGS[args.config]
     kw = paper_params(c.k, c.nsub, c.pml, c.ovlp, n_cells=c.n_cells)
     if args.drch:
