@@ -551,6 +551,8 @@ int build_layout(helm_ctx* ctx)
     return HELM_OK;
 }
 
+// work vectors, reduction buffers and pinned staging (restart = 0), plus a GMRES basis of restart + 1 vectors and
+// the DCGS2 Z basis (restart > 0).  helm_factor calls it with 0 so that a solve's timing holds no allocation.
 int ensure_krylov(helm_ctx* ctx, int restart)
 {
     int rc;
@@ -576,14 +578,14 @@ int ensure_krylov(helm_ctx* ctx, int restart)
 
         for (auto& e : ctx->ev_hc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    if (restart + 1 > ctx->V_cap) {
+    if (restart > 0 && restart + 1 > ctx->V_cap) {
         if (ctx->d_V) cudaFree(ctx->d_V);
         ctx->d_V = nullptr;
         ctx->V_cap = 0;
         if ((rc = dalloc(ctx, &ctx->d_V, (size_t)(restart + 1) * n))) return rc;
         ctx->V_cap = restart + 1;
     }
-    if (!ctx->orth_cgs2 && restart > ctx->Z_cap) {
+    if (restart > 0 && !ctx->orth_cgs2 && restart > ctx->Z_cap) {
         if (ctx->d_Z) cudaFree(ctx->d_Z);
         ctx->d_Z = nullptr;
         ctx->Z_cap = 0;
@@ -1287,7 +1289,7 @@ int richardson_impl(helm_ctx* ctx, const z2* b, z2* x, double rtol, int maxit, h
     if (maxit < 0) return set_err(ctx, HELM_EINVAL, "maxit >= 0");
     int rc;
     if ((rc = need_comm(ctx))) return rc;
-    if ((rc = ensure_krylov(ctx, 1))) return rc;
+    if ((rc = ensure_krylov(ctx, 0))) return rc;
     helm_richardson_info loc{};
     helm_richardson_info* inf = info ? info : &loc;
     inf->iterations = 0;
@@ -1764,6 +1766,7 @@ int helm_factor(helm_ctx* ctx)
     CK(cudaStreamSynchronize(ctx->stream));
     if (herr[0])
         return set_err(ctx, HELM_EZEROPIVOT, "zero pivot: subdomain %d, block %d, row %d", herr[1], herr[2], herr[3]);
+    if ((rc = ensure_krylov(ctx, 0))) return rc;   // the solvers' work buffers belong to setup, not to a solve
     ctx->factored = true;
     return HELM_OK;
 }
@@ -1808,7 +1811,7 @@ int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host)
 {
     if (!ctx || !r_host || !z_host) return set_err(ctx, HELM_EINVAL, "helm_precond_apply_host: bad arguments");
     int rc;
-    if ((rc = ensure_krylov(ctx, 1))) return rc;
+    if ((rc = ensure_krylov(ctx, 0))) return rc;
     const size_t bytes = sizeof(z2) * ctx->n_local;
     CK(cudaMemcpyAsync(ctx->d_t, r_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
