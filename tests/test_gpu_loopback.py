@@ -217,3 +217,49 @@ def test_loopback_random_layouts(d):
         assert torch.equal(Z.view(-1), z_ref)
     else:
         assert float(torch.linalg.norm(Z.view(-1) - z_ref) / torch.linalg.norm(z_ref)) <= 1e-13
+
+
+def test_loopback_c3_full_size_two_ranks():
+    """BASELINE.json's headline config at full size on two ranks (21 GB of factors each, both on this GPU): the
+    overlapped sharded apply bitwise equal to one rank on a probe vector, and GMRES(50) to 1e-6 -- DCGS2 with the
+    multi-rank lookahead, packed allreduces, the two-phase halos -- in the single-rank iteration count +-1."""
+    cfg = CONFIGS["c3"]
+    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    ref = Context(**kw)
+    ref.factor()
+    nf = ref.layout.N_cells - 1
+    v = torch.from_numpy(probe_vector(ref.n, 3)).cuda()
+    z_ref = ref.precond_apply(v)
+    b = ref.rhs(*sources(cfg))
+    _, gi_ref, _ = ref.gmres(b, restart=cfg.restart, rtol=cfg.rtol, maxit=1000)
+    ref.close()
+    del ref
+    torch.cuda.empty_cache()
+    V, B = v.view(nf, nf), b.view(nf, nf)
+    gid = next(_gid)
+    torch.cuda.synchronize()
+
+    def rank(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c = Context(**kw, gpu_grid=(2, 1), rank=r, nranks=2, stream=s, loopback_group=gid)
+            c.factor()
+            pl = c.plan
+            z = c.precond_apply(owned(V, pl))
+            _, gi, _ = c.gmres(owned(B, pl), restart=cfg.restart, rtol=cfg.rtol, maxit=1000)
+            s.synchronize()
+            out = dict(pl=pl, z=z.clone(), its=gi.iterations, status=gi.status, rr=gi.relres_true,
+                       ov=c.layout.overlap_interior)
+            c.close()
+            return out
+
+    outs = run_ranks(2, rank, timeout=900)
+    Z = torch.full_like(V, complex("nan"))
+    for o in outs:
+        pl = o["pl"]
+        sl = (slice(pl["owned_j0"] - 1, pl["owned_j1"] - 1), slice(pl["owned_i0"] - 1, pl["owned_i1"] - 1))
+        Z[sl] = o["z"].view(pl["owned_j1"] - pl["owned_j0"], pl["owned_i1"] - pl["owned_i0"])
+    assert torch.equal(Z.view(-1), z_ref)
+    assert all(o["ov"] > 0 for o in outs)   # the overlapped apply ran
+    assert all(o["status"] == 0 and o["rr"] <= cfg.rtol for o in outs)
+    assert outs[0]["its"] == outs[1]["its"] and abs(outs[0]["its"] - gi_ref.iterations) <= 1
