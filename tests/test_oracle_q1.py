@@ -278,3 +278,32 @@ def test_paper_frame_hankel_far_field_and_refinement():
     assert errs[0] < 0.1
     assert errs[0] / errs[1] > 3.3 and errs[1] / errs[2] > 3.3, errs
     assert errs[2] < 0.006
+
+
+@pytest.mark.parametrize("sub", [0, 1, 3])
+def test_q1_impedance_term_is_the_edge_mass(sub):
+    """RAS-PML-Imp with Q1: with the PML profile held fixed (g = c t^3, c not tied to k) the local matrix
+    is A_j(k) = K + k C + k^2 M exactly, and C = -i B with B the edge mass of the impedance faces -- for bilinear
+    elements the 1-D linear mass (h/6)[[2,1],[1,2]] per edge: real, symmetric, only on face nodes, row sums h for
+    nodes inside a face, positive diagonal.  Three wavenumbers recover B entrywise (Vandermonde)."""
+    def make(k):
+        h = 1.0 / 20
+        return Oracle(Problem(k=float(k), sigma0=0.0, h=h, nix=20, niy=20, ng=0, kappa=4 * h, px=2, py=2, novlp=2,
+                              npml=2, local_bc=1, pou=1, elem=1, frame=1, pml_c=300.0))
+    A1, A2, A3 = (make(k).local_matrix(sub) for k in (1.0, 2.0, 3.0))
+    Vi = np.linalg.inv(np.array([[1, 1, 1], [1, 2, 4], [1, 3, 9]], float))
+    C = Vi[1, 0] * A1 + Vi[1, 1] * A2 + Vi[1, 2] * A3
+    B = C / (-1j)
+    assert np.max(np.abs(B.imag)) < 1e-12 and np.allclose(B, B.T, atol=1e-14)
+    B = B.real
+    o = make(1.0)
+    h = o.prob.h
+    nz = np.abs(B) > 1e-13
+    rows = np.where(nz.any(axis=1))[0]
+    assert len(rows) > 0                                   # subdomain with impedance faces
+    # only node pairs on a common face edge: every nonzero is 2h/6 (diagonal, one edge), 4h/6 (two edges) or h/6
+    vals = np.unique(np.round(B[nz] / (h / 6), 9))
+    assert set(vals).issubset({1.0, 2.0, 4.0})
+    rs = B.sum(axis=1)[rows]
+    assert np.any(np.isclose(rs, h, rtol=1e-12))           # a node inside a face: two edges, (2+1+2+1) h/6 = h
+    assert np.all(np.diag(B)[rows] > 0)
