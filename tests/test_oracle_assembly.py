@@ -57,6 +57,46 @@ def test_rhs_mass_conservation():
     assert abs(b1.sum() - 1.0) < 1e-12 and np.max(np.abs(b1.imag)) == 0.0
 
 
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_rhs_is_consistent_mass_times_nodal_f(name):
+    """D14 / O5: b = M_ff f_I with the CONSISTENT P1 mass matrix, entrywise.  M is recovered from the assembly
+    itself: with sigma0 = 0, A(k') = K - k'^2 M, so M = (A(0) - A(k')) / k'^2 on the same mesh (k' h = 1); the
+    recovered M's interior rows are those of the closed-form stencil test above (h^2/2 centre, h^2/12 on the six
+    edge neighbours).  A lumped mass (or a dropped Gaussian, a wrong node coordinate, a swapped axis) fails this
+    at the 1e-12 level, which the sum rule above cannot see."""
+    cfg = CONFIGS[name]
+    P = problem_from_config(cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    o = Oracle(P)
+    xy, amp, sig = sources(cfg)
+    b = o.rhs(xy, amp, sig)
+    kp = 1.0 / P.h
+
+    def frame(kk):
+        return Oracle(Problem(k=kk, sigma0=0.0, h=P.h, nix=P.nix, niy=P.niy, ng=P.ng, kappa=P.kappa, px=1, py=1,
+                              novlp=P.novlp, npml=P.npml))
+
+    M = ((frame(0.0).matrix() - frame(kp).matrix()) / kp ** 2).tocsr()
+    nfx = o.nf[0]
+    idx = np.arange(o.nfree)
+    x = (idx % nfx + 1 - P.ng) * P.h
+    y = (idx // nfx + 1 - P.ng) * P.h
+    f = np.zeros(o.nfree, np.complex128)
+    for (xs, ys), a in zip(xy, amp):
+        f += a * np.exp(-((x - xs) ** 2 + (y - ys) ** 2) / (2 * sig * sig)) / (2 * math.pi * sig * sig)
+    ref = M @ f
+    assert np.max(np.abs(b - ref)) <= 1e-12 * np.max(np.abs(ref))
+    # the recovered M is the consistent one: interior row h^2/2 on the diagonal, h^2/12 on E/W/N/S/NE/SW
+    g = (P.ng + P.nix // 2 - 1) + nfx * (P.ng + P.nix // 2 - 1)
+    row = M.getrow(g).toarray().ravel()
+    h2 = P.h * P.h
+    assert abs(row[g] - h2 / 2) <= 1e-12 * h2
+    for d in (1, -1, nfx, -nfx, nfx + 1, -nfx - 1):
+        assert abs(row[g + d] - h2 / 12) <= 1e-12 * h2
+    assert abs(row.sum() - h2) <= 1e-12 * h2
+    # a lumped mass would give b = h^2 f at interior nodes: far from b
+    assert np.max(np.abs(b - h2 * f)) > 1e-4 * np.max(np.abs(ref))
+
+
 def _row_tris_in_box(s, gi, gj):
     """all six triangles around node (gi, gj) lie inside the int box"""
     return (s["int_lo"][0] <= gi - 1 and gi + 1 <= s["int_hi"][0]
