@@ -72,6 +72,9 @@ def lib():
         L.orc_factor.restype = C.c_int
         L.orc_factor.argtypes = [vp, ip, C.c_int, i64p]
         L.orc_release.argtypes = [vp]
+        L.orc_factor_dedup.restype = C.c_int
+        L.orc_factor_dedup.argtypes = [vp, i64p, ip]
+        L.orc_dedup_class.argtypes = [vp, C.c_int, ip]
         L.orc_chi1.restype = C.c_double
         L.orc_chi1.argtypes = [vp, C.c_int, C.c_int, C.c_int]
         L.orc_apply.restype = C.c_int
@@ -291,6 +294,25 @@ class Oracle:
         if rc != 0:
             raise OracleError(f"zero pivot: subdomain {-rc - 1}, row {zr.value}")
 
+    def factor_dedup(self) -> int:
+        """Dedup mode (SURVEY 8(d) memory fallback): factor one representative per bitwise-distinct A_j, after
+        asserting that every member is bitwise equal to its representative.  Returns the number of classes."""
+        zr = C.c_int64(-1)
+        nc = C.c_int(0)
+        rc = lib().orc_factor_dedup(self._h, C.byref(zr), C.byref(nc))
+        if rc != 0:
+            if -rc - 1 < self.nsub:
+                raise OracleError(f"zero pivot: subdomain {-rc - 1}, row {zr.value}")
+            raise OracleError(f"dedup: subdomain {-rc - 1 - self.nsub} is not bitwise equal to its representative")
+        self.nclasses = nc.value
+        return nc.value
+
+    def dedup_class(self, j: int):
+        """(class, representative, class size) of subdomain j after factor_dedup."""
+        o = (C.c_int * 3)()
+        lib().orc_dedup_class(self._h, j, o)
+        return o[0], o[1], o[2]
+
     def release(self):
         lib().orc_release(self._h)
 
@@ -369,6 +391,16 @@ class GmresResult:
     history: list
 
 
+def mgs(V, w: np.ndarray):
+    """O9 step 2, modified Gram-Schmidt against every vector of V in order: h_i = v_i^H w; w -= h_i v_i.
+    Returns (w, h)."""
+    h = np.zeros(len(V), np.complex128)
+    for i in range(len(V)):
+        h[i] = np.vdot(V[i], w)
+        w = w - h[i] * V[i]
+    return w, h
+
+
 def gmres(A, M, b: np.ndarray, restart: int = 50, rtol: float = 1e-6, maxit: int = 5000,
           x0: np.ndarray | None = None) -> GmresResult:
     """A, M: callables (vector -> vector).  Solves A M u = b, x = M u (right preconditioning)."""
@@ -393,9 +425,7 @@ def gmres(A, M, b: np.ndarray, restart: int = 50, rtol: float = 1e-6, maxit: int
         for j in range(m):
             w = A(M(V[j]))
             its += 1
-            for i in range(j + 1):                       # MGS
-                H[i, j] = np.vdot(V[i], w)
-                w = w - H[i, j] * V[i]
+            w, H[:j + 1, j] = mgs(V, w)
             hn = np.linalg.norm(w)
             H[j + 1, j] = hn
             if not np.isfinite(hn):

@@ -20,7 +20,10 @@
  * symmetry without PML, the g = 10 k t^3 profile closed forms / finite differences / local restarts, local rows =
  * global rows in the int box, Q1 FEM order 2, band LU vs zgesv, dense ramp-PoU RAS vs the apply, single subdomain
  * => exact inverse, unit mass of the smoothed delta, and the iteration counts printed in the paper's Tables 1 and 4
- * at k = 300 (tests/golden/paper_iterations.txt).  No function here is "parity unpinned".
+ * at k = 300 (tests/golden/paper_iterations.txt).  The right-hand side is pinned entrywise as b = M f_I with M the
+ * consistent mass recovered from the assembly (tests/test_oracle_assembly.py).  Dedup mode (orc_factor_dedup, SURVEY
+ * 8(d) memory fallback) is pinned by bitwise equality of its apply with the per-subdomain factorisation and by its
+ * own bitwise member == representative assertion.  No function here is "parity unpinned".
  */
 #include <complex.h>
 #include <math.h>
@@ -68,7 +71,18 @@ typedef struct {
     /* factor storage (band LU, O7) */
     zc *band;                   /* n x (2p+1), NULL until factored */
     int factored;
+    int shared;                 /* dedup mode: band belongs to a class (orc_ctx.cls), not to this subdomain */
 } orc_sub;
+
+/* dedup mode (SURVEY 8(d) "memory fallback"): one factored representative per distinct A_j */
+typedef struct {
+    uint64_t hash;
+    int mx, my;
+    int rep;                    /* representative subdomain (lowest index) */
+    int count;
+    zc *raw;                    /* the representative's assembled band (verification only, freed after) */
+    zc *band;                   /* its band LU factors, shared by every member */
+} orc_class;
 
 typedef struct {
     orc_params p;
@@ -81,6 +95,8 @@ typedef struct {
     int ns;          /* slots per global row: 7 (P1) or 9 (Q1) */
     double lo_u[2], hi_u[2];   /* Omega_int per axis in cell units (node 0 at 0): where the global ramps start */
     zc *A7;          /* global matrix, ns slots per free row (see slot_of) */
+    orc_class *cls;  /* dedup mode classes (NULL otherwise) */
+    int ncls;
 } orc_ctx;
 
 /* ------------------------------------------------------------------------------------------------
@@ -348,8 +364,10 @@ orc_ctx *orc_create(const orc_params *p, char *err, int errlen)
                 s->node0[ax] = s->full_lo[ax] + ((imp && s->has_lo[ax]) ? 0 : 1);
                 int last = s->full_hi[ax] - ((imp && s->has_hi[ax]) ? 0 : 1);
                 s->m[ax] = last - s->node0[ax] + 1;
-                if (s->full_lo[ax] < 0 || s->full_hi[ax] > c->N[ax]) {
-                    snprintf(err, errlen, "full box of subdomain (%d,%d) leaves Omega", jx, jy);
+                /* every local free node must be a global free node: an impedance face on dOmega (a block
+                   narrower than delta + kappa + 1 next to the boundary) would put node 0 or N into Omega_j */
+                if (s->full_lo[ax] < 0 || s->full_hi[ax] > c->N[ax] || s->node0[ax] < 1 || last > c->N[ax] - 1) {
+                    snprintf(err, errlen, "full box of subdomain (%d,%d) leaves Omega (or puts an impedance face on dOmega)", jx, jy);
                     free(c->sub); free(c->split[0]); free(c->split[1]); free(c); return NULL;
                 }
             }
@@ -357,10 +375,12 @@ orc_ctx *orc_create(const orc_params *p, char *err, int errlen)
     return c;
 }
 
+void orc_release(orc_ctx *c);
+
 void orc_destroy(orc_ctx *c)
 {
     if (!c) return;
-    for (int j = 0; j < c->nsub; j++) free(c->sub[j].band);
+    orc_release(c);
     free(c->sub);
     free(c->split[0]);
     free(c->split[1]);
@@ -684,7 +704,140 @@ int orc_factor(orc_ctx *c, const int *list, int nlist, int64_t *zero_row)
 /* drop factors (bench / memory control) */
 void orc_release(orc_ctx *c)
 {
-    for (int j = 0; j < c->nsub; j++) { free(c->sub[j].band); c->sub[j].band = NULL; c->sub[j].factored = 0; }
+    for (int j = 0; j < c->nsub; j++) {
+        if (!c->sub[j].shared) free(c->sub[j].band);
+        c->sub[j].band = NULL; c->sub[j].factored = 0; c->sub[j].shared = 0;
+    }
+    for (int q = 0; q < c->ncls; q++) { free(c->cls[q].band); free(c->cls[q].raw); }
+    free(c->cls);
+    c->cls = NULL;
+    c->ncls = 0;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Dedup mode (SURVEY 8(d) "memory fallback"; exact, oracle only).  Identical matrices have identical
+ * factors, so instead of storing one band LU per subdomain (86 GB at c3) the oracle
+ *   1. assembles every A_j (assemble_local, unchanged) and hashes its bytes (FNV-1a over 64-bit words,
+ *      together with m_x, m_y);
+ *   2. groups equal (hash, m_x, m_y) into classes, the lowest subdomain index being the representative;
+ *   3. factors each representative once (orc_band_lu, unchanged);
+ *   4. ASSERTS that every member's assembled band is bitwise equal to its representative's (memcmp): a
+ *      hash collision or a non-bitwise-equal pair fails loudly instead of sharing the wrong factors.
+ * The apply is unchanged (orc_band_solve per subdomain, on the shared factors).
+ * Returns 0 and *ncls; -(1 + j) with *zero_row on a zero pivot of representative j; or -(1 + nsub + j)
+ * when member j differs from its class representative.  Must be called on an unfactored context.
+ * ----------------------------------------------------------------------------------------------*/
+static uint64_t band_hash(const zc *band, size_t nz, int mx, int my)
+{
+    const uint64_t *w = (const uint64_t *)band;
+    uint64_t h = 1469598103934665603ULL;
+    h = (h ^ (uint64_t)mx) * 1099511628211ULL;
+    h = (h ^ (uint64_t)my) * 1099511628211ULL;
+    for (size_t i = 0; i < 2 * nz; i++) h = (h ^ w[i]) * 1099511628211ULL;
+    return h;
+}
+
+int orc_factor_dedup(orc_ctx *c, int64_t *zero_row, int *ncls_out)
+{
+    int ns = c->nsub;
+    uint64_t *hash = malloc(sizeof(uint64_t) * ns);
+    int *cls_of = malloc(sizeof(int) * ns);
+    orc_release(c);
+    /* 1. hash every assembled A_j */
+#pragma omp parallel
+    {
+        zc *buf = NULL;
+        size_t cap = 0;
+#pragma omp for schedule(dynamic, 1)
+        for (int j = 0; j < ns; j++) {
+            orc_sub *s = &c->sub[j];
+            int mx = s->m[0], my = s->m[1];
+            size_t nz = (size_t)mx * my * (2 * (mx + 1) + 1);
+            if (nz > cap) { free(buf); buf = malloc(sizeof(zc) * nz); cap = nz; }
+            assemble_local(c, j, buf);
+            hash[j] = band_hash(buf, nz, mx, my);
+        }
+        free(buf);
+    }
+    /* 2. classes in subdomain order (representative = first member) */
+    c->cls = calloc(ns, sizeof(orc_class));
+    c->ncls = 0;
+    for (int j = 0; j < ns; j++) {
+        int q;
+        for (q = 0; q < c->ncls; q++)
+            if (c->cls[q].hash == hash[j] && c->cls[q].mx == c->sub[j].m[0] && c->cls[q].my == c->sub[j].m[1]) break;
+        if (q == c->ncls) {
+            c->cls[q].hash = hash[j]; c->cls[q].mx = c->sub[j].m[0]; c->cls[q].my = c->sub[j].m[1];
+            c->cls[q].rep = j;
+            c->ncls++;
+        }
+        c->cls[q].count++;
+        cls_of[j] = q;
+    }
+    /* 3. factor each representative once */
+    int bad = -1;
+    int64_t badrow = -1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int q = 0; q < c->ncls; q++) {
+        orc_class *k = &c->cls[q];
+        int p = k->mx + 1;
+        int64_t n = (int64_t)k->mx * k->my;
+        size_t nz = (size_t)n * (2 * p + 1);
+        k->raw = malloc(sizeof(zc) * nz);
+        k->band = malloc(sizeof(zc) * nz);
+        assemble_local(c, k->rep, k->raw);
+        memcpy(k->band, k->raw, sizeof(zc) * nz);
+        int64_t zr = orc_band_lu(n, p, k->band);
+        if (zr >= 0) {
+#pragma omp critical
+            { if (bad < 0 || k->rep < bad) { bad = k->rep; badrow = zr; } }
+        }
+    }
+    /* 4. every member must equal its representative bitwise */
+    int differ = -1;
+    if (bad < 0) {
+#pragma omp parallel
+        {
+            zc *buf = NULL;
+            size_t cap = 0;
+#pragma omp for schedule(dynamic, 1)
+            for (int j = 0; j < ns; j++) {
+                orc_class *k = &c->cls[cls_of[j]];
+                if (k->rep == j) continue;
+                size_t nz = (size_t)k->mx * k->my * (2 * (k->mx + 1) + 1);
+                if (nz > cap) { free(buf); buf = malloc(sizeof(zc) * nz); cap = nz; }
+                assemble_local(c, j, buf);
+                if (memcmp(buf, k->raw, sizeof(zc) * nz) != 0) {
+#pragma omp critical
+                    { if (differ < 0 || j < differ) differ = j; }
+                }
+            }
+            free(buf);
+        }
+    }
+    for (int q = 0; q < c->ncls; q++) { free(c->cls[q].raw); c->cls[q].raw = NULL; }
+    if (bad < 0 && differ < 0)
+        for (int j = 0; j < ns; j++) {
+            c->sub[j].band = c->cls[cls_of[j]].band;
+            c->sub[j].shared = 1;
+            c->sub[j].factored = 1;
+        }
+    free(hash);
+    free(cls_of);
+    if (ncls_out) *ncls_out = c->ncls;
+    if (bad >= 0) { if (zero_row) *zero_row = badrow; orc_release(c); return -(1 + bad); }
+    if (differ >= 0) { orc_release(c); return -(1 + ns + differ); }
+    return 0;
+}
+
+/* class of subdomain j in dedup mode (-1 if not in dedup mode): out[0] = class, out[1] = representative,
+ * out[2] = class size */
+void orc_dedup_class(const orc_ctx *c, int j, int *out)
+{
+    out[0] = out[1] = out[2] = -1;
+    if (!c->cls || !c->sub[j].shared) return;
+    for (int q = 0; q < c->ncls; q++)
+        if (c->cls[q].band == c->sub[j].band) { out[0] = q; out[1] = c->cls[q].rep; out[2] = c->cls[q].count; return; }
 }
 
 /* ------------------------------------------------------------------------------------------------

@@ -204,3 +204,43 @@ def test_hankel_far_field_and_refinement():
     assert e[0] < 0.2
     assert e[0] / e[1] > 3.0 and e[1] / e[2] > 3.0, e
     assert e[2] < 0.02
+
+
+# ------------------------------------------------------------------------------------------ dedup mode
+@pytest.mark.parametrize("name,classes", [("c1", 9), ("c2", 9)])
+def test_dedup_apply_is_bitwise_the_per_subdomain_apply(name, classes):
+    """Memory fallback: factoring one representative per bitwise-distinct A_j is exact -- the apply is bitwise
+    the one with every subdomain factored separately.  Classes are {first, interior, last} per axis at c1/c2
+    (blocks 45/45/45/44 and 42/41x15: the interior sizes share one matrix because the int box and local PML
+    have the same widths; D5's integer-offset depth makes them bitwise equal)."""
+    cfg = CONFIGS[name]
+    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    assert o.factor_dedup() == classes
+    v = probe_vector(o.nfree, int(cfg.k) + 1)
+    z1 = o.apply(v)
+    reps = {o.dedup_class(j)[1] for j in range(o.nsub)}
+    assert len(reps) == classes and sum(o.dedup_class(r)[2] for r in reps) == o.nsub
+    o.release()
+    o.factor()
+    assert np.array_equal(z1, o.apply(v))
+
+
+def test_dedup_counts_one_class_per_distinct_matrix():
+    """With a single block per axis there is one class; with ramps/impedance (other matrices) the classes follow the
+    local matrices, and the member == representative assertion holds for every subdomain."""
+    o = Oracle(problem_from_config(20.0))
+    assert o.factor_dedup() == 1
+    o = Oracle(problem_from_config(100.0, nsub_x=4, nsub_y=4, local_bc=1))
+    assert o.factor_dedup() == 9
+    o = Oracle(problem_from_config(100.0, nsub_x=5, nsub_y=3))
+    assert o.factor_dedup() == 9
+
+
+def test_impedance_face_on_the_boundary_is_refused():
+    """with RAS-PML-Imp the full-box face nodes are local unknowns, so a block of exactly delta + kappa
+    cells next to dOmega would put the Dirichlet node 0 (or N) into Omega_j.  The oracle refuses that layout (the
+    Dirichlet variant of the same layout is valid)."""
+    k = 6 * math.pi          # n_int = 30, N = 50: ten blocks of 5 = delta + kappa cells
+    Oracle(problem_from_config(k, nsub_x=10, nsub_y=2, n_ovlp=2, n_pml=3, local_bc=0))
+    with pytest.raises(OracleError):
+        Oracle(problem_from_config(k, nsub_x=10, nsub_y=2, n_ovlp=2, n_pml=3, local_bc=1))
