@@ -98,7 +98,9 @@ typedef struct {
     int iterations;      /* Arnoldi steps (one A B^-1 product each) */
     int restarts;        /* completed cycles minus one */
     int status;          /* HELM_OK, HELM_NOT_CONVERGED, HELM_BREAKDOWN */
-    int applies;         /* preconditioner applications issued (iterations + one per cycle end) */
+    int applies;         /* preconditioner applications issued: DCGS2 (default) one per Arnoldi step, plus the
+                            discarded lookahead step at a cycle's end on several ranks; undelayed CGS2 one per
+                            step plus one per cycle end */
     double relres_est;   /* |g_{j+1}| / ||b|| of the last Givens step */
     double relres_true;  /* ||b - A x|| / ||b|| recomputed at the last cycle end */
     double* history;     /* caller-owned host buffer for relres_est per iteration, or NULL */
@@ -113,6 +115,13 @@ typedef struct {
  * cuda_stream: cudaStream_t or NULL (legacy default stream).  Allocates the operators. */
 int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl_unique_id,
                void* cuda_stream, helm_ctx** out);
+/* (nranks == 1 with a non-NULL nccl_unique_id runs the multi-rank code path over a one-rank NCCL communicator:
+ *  ghost-framed buffers and an NCCL allreduce of every inner product -- the NCCL data plane on one GPU.) */
+
+/* Which transport this context's collectives use, and the communicator's size and this rank's place in it as the
+ * transport reports them (ncclCommCount / ncclCommUserRank for NCCL).  Host only. */
+enum { HELM_TRANSPORT_NONE = 0, HELM_TRANSPORT_NCCL = 1, HELM_TRANSPORT_LOOPBACK = 2, HELM_TRANSPORT_SHARD = 3 };
+int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* comm_rank);
 
 /* Fill *out with the layout of this rank.  Synchronous, host only. */
 int helm_get_layout(const helm_ctx* ctx, helm_layout* out);

@@ -179,6 +179,24 @@ int compute_grid(const helm_params& p, int rank, int nranks, GridInfo& G, char* 
     G.nbr[1] = G.rx < gx - 1 ? rank + 1 : -1;
     G.nbr[2] = G.ry > 0 ? rank - gx : -1;
     G.nbr[3] = G.ry < gy - 1 ? rank + gx : -1;
+    // every rank's owned strip must be at least as wide as the ghost layers it sends: halo_hi owned layers to the
+    // lower neighbour and halo_lo to the upper one, never reaching past its own nodes (impedance makes the frame
+    // delta + kappa + 1 wide, one more than a block needs to be).  Checked for all ranks, so every rank
+    // accepts or refuses the same layout.
+    for (int ax = 0; ax < 2; ax++) {
+        const int g = ax ? gy : gx;
+        if (g < 2) continue;
+        const std::vector<int> sb = block_starts(G.P[ax], g);
+        for (int q = 0; q < g; q++) {
+            const int lo = std::max(G.st[ax][sb[q]], 1), hi = std::min(G.st[ax][sb[q + 1]], G.N);
+            const int need = std::max(q > 0 ? G.halo_hi : 0, q < g - 1 ? G.halo_lo : 0);
+            if (hi - lo < need) {
+                snprintf(err, errlen, "rank strip %d on axis %d owns %d nodes < the %d ghost layers it must send", q,
+                         ax, hi - lo, need);
+                return HELM_ELAYOUT;
+            }
+        }
+    }
     G.e_i0 = G.i0 - (G.nbr[0] >= 0 ? G.halo_lo : 0);
     G.e_i1 = G.i1 + (G.nbr[1] >= 0 ? G.halo_hi : 0);
     G.e_j0 = G.j0 - (G.nbr[2] >= 0 ? G.halo_lo : 0);
@@ -992,6 +1010,11 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         inf->relres_est = inf->relres_true = beta / beta0;
         return HELM_OK;
     }
+    if (maxit == 0) {   // no iteration allowed: x is the initial guess, not converged
+        inf->relres_est = inf->relres_true = beta / beta0;
+        inf->status = HELM_NOT_CONVERGED;
+        return HELM_NOT_CONVERGED;
+    }
     const int m = restart;
     std::vector<cplx> H((size_t)(m + 1) * m), g(m + 1), sn(m), y(m);
     std::vector<double> cs(m);
@@ -1424,7 +1447,9 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     *out = ctx;
     int rc = build_layout(ctx);
     if (rc) return rc;
-    ctx->multi = nranks > 1;
+    // nranks == 1 with an NCCL id: the multi-rank code path over a one-rank NCCL communicator (ghost-framed buffers,
+    // NCCL allreduce of every inner product) -- the NCCL data plane exercised on a single GPU
+    ctx->multi = nranks > 1 || (nranks == 1 && nccl_unique_id && loop_group < 0);
     if (ctx->multi && loop_group >= 0) {
         std::lock_guard<std::mutex> lk(g_loop_mu);
         LoopGroup*& L = g_loops[loop_group];
@@ -1666,6 +1691,32 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     return HELM_OK;
 }
 
+int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* comm_rank)
+{
+    if (!ctx) return HELM_EINVAL;
+    int t = HELM_TRANSPORT_NONE, n = 1, r = 0;
+    if (ctx->loop) {
+        t = HELM_TRANSPORT_LOOPBACK;
+        n = ctx->loop->nranks;
+        r = ctx->rank;
+    } else if (ctx->multi && !ctx->has_comm) {
+        t = HELM_TRANSPORT_SHARD;
+        n = ctx->nranks;
+        r = ctx->rank;
+    }
+#ifdef HELM_HAVE_NCCL
+    else if (ctx->comm) {
+        t = HELM_TRANSPORT_NCCL;
+        if (ncclCommCount(ctx->comm, &n) != ncclSuccess || ncclCommUserRank(ctx->comm, &r) != ncclSuccess)
+            return HELM_ENCCL;
+    }
+#endif
+    if (transport) *transport = t;
+    if (comm_nranks) *comm_nranks = n;
+    if (comm_rank) *comm_rank = r;
+    return HELM_OK;
+}
+
 int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
 {
     if (!ctx || !out) return HELM_EINVAL;
@@ -1765,7 +1816,8 @@ int helm_factor(helm_ctx* ctx)
     CK(cudaMemcpyAsync(herr, ctx->d_err, sizeof(herr), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (herr[0])
-        return set_err(ctx, HELM_EZEROPIVOT, "zero pivot: subdomain %d, block %d, row %d", herr[1], herr[2], herr[3]);
+        return set_err(ctx, HELM_EZEROPIVOT, "zero pivot (|pivot| < 1e-12 or not finite): subdomain %d, block %d, row %d",
+                       herr[1], herr[2], herr[3]);
     if ((rc = ensure_krylov(ctx, 0))) return rc;   // the solvers' work buffers belong to setup, not to a solve
     ctx->factored = true;
     return HELM_OK;

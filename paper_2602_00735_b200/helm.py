@@ -81,7 +81,7 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
            "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
            "helm_probe_read_bandwidth_mode", "helm_set_orthogonalisation",
-           "helm_get_krylov_basis"]
+           "helm_get_krylov_basis", "helm_comm_info"]
 
 
 def lib_path() -> str:
@@ -122,6 +122,7 @@ def load(build_if_missing: bool = True):
     L.helm_richardson.argtypes = [vp, vp, vp, d, i, C.POINTER(RichardsonInfo)]
     L.helm_probe_read_bandwidth.argtypes = [C.c_longlong, i, C.POINTER(d)]
     L.helm_probe_read_bandwidth_mode.argtypes = [C.c_longlong, i, i, C.POINTER(d)]
+    L.helm_comm_info.argtypes = [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
     L.helm_destroy.argtypes = [vp]
@@ -356,6 +357,14 @@ class Context:
         out = torch.empty(ns * self.n, dtype=torch.complex128, device="cuda")
         self._check(self.L.helm_export_stencil(self._h, _ptr(out)))
         return out.view(ns, self.n)
+
+    TRANSPORTS = {0: "none", 1: "nccl", 2: "loopback", 3: "shard"}
+
+    def comm_info(self) -> dict:
+        """{'transport': none|nccl|loopback|shard, 'nranks': ..., 'rank': ...} as the transport reports them."""
+        t, n, r = C.c_int(), C.c_int(), C.c_int()
+        self._check(self.L.helm_comm_info(self._h, C.byref(t), C.byref(n), C.byref(r)))
+        return {"transport": self.TRANSPORTS.get(t.value, str(t.value)), "nranks": n.value, "rank": r.value}
 
     def profile(self, on: bool = True):
         self._check(self.L.helm_profile_enable(self._h, int(on)))

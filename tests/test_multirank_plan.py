@@ -176,3 +176,34 @@ def test_paper_frame_plans(nranks, gg):
         cover[pl["owned_j0"]:pl["owned_j1"], pl["owned_i0"]:pl["owned_i1"]] += 1
         assert pl["halo_lo"] == 5 + 11 - 1 + 1 and pl["halo_hi"] == 5 + 11 + 1   # Imp: face nodes are unknowns
     assert np.all(cover[1:nf + 1, 1:nf + 1] == 1) and cover.sum() == nf * nf
+
+
+def test_narrow_rank_strips_are_refused():
+    """a rank sends halo_hi owned layers to its lower neighbour and halo_lo to its upper one, so its owned
+    strip must be at least that wide.  k = 6 pi (N = 50 cells), 10 x 2 subdomains of 5 = delta + kappa cells, one rank
+    per block column: with Dirichlet faces (halo 4 / 5; the edge ranks own 4 free nodes and send 4) the layout is
+    valid; with impedance faces (halo 5 / 6) it is refused on every rank, as the oracle refuses it
+    (tests/test_oracle_solvers.py).  Every accepted plan sends owned nodes only."""
+    from paper_2602_00735_b200.helm import HelmError
+    k = 6 * np.pi
+    pimp = make_params(k, 10, 2, n_ovlp=2, n_pml=3, local_bc=1, gpu_grid=(10, 1))
+    for r in range(10):
+        with pytest.raises(HelmError):
+            plan_rank(pimp, r, 10)
+    pdir = make_params(k, 10, 2, n_ovlp=2, n_pml=3, local_bc=0, gpu_grid=(10, 1))
+    for r in range(10):
+        pl = plan_rank(pdir, r, 10)
+        for m in halo_schedule(pdir, r, 10, 0):
+            if m["phase"] == 0:
+                assert pl["owned_i0"] <= m["send_i0"] and m["send_i1"] <= pl["owned_i1"]
+    # five rank columns of two blocks (10 owned nodes >= 6): accepted
+    pimp5 = make_params(k, 10, 2, n_ovlp=2, n_pml=3, local_bc=1, gpu_grid=(5, 1))
+    for r in range(5):
+        pl = plan_rank(pimp5, r, 5)
+        assert pl["owned_i1"] - pl["owned_i0"] >= pl["halo_hi"]
+    # every accepted plan sends only owned nodes (the schedule's send rectangles lie in the owned rectangle)
+    for r in range(5):
+        pl = plan_rank(pimp5, r, 5)
+        for m in halo_schedule(pimp5, r, 5, 0):
+            if m["phase"] == 0:
+                assert pl["owned_i0"] <= m["send_i0"] and m["send_i1"] <= pl["owned_i1"]
