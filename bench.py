@@ -1,16 +1,18 @@
 """bench.py -- RAS-PML hot path on B200 (driver contract: one JSON line on rank 0).
 
-A step is one right-preconditioned GMRES(50) Arnoldi iteration over the whole hot path:
-RAS-PML apply (restrict -> twisted block-tridiagonal local solves -> owner write), 7-point SpMV, CGS2
-orthogonalisation with the re-orthogonalisation delayed one step (DCGS2: two sweeps over the basis per step), Givens
-update on the host.  `value` = RAS-PML preconditioner applications per second over exactly K steps (one per
-Arnoldi step; a cycle's solution update reuses the steps' applies, so the timed region's cycle ends add only their
-vector work), all inputs resident in HBM.
+A step is one whole right-preconditioned GMRES(50) restart cycle over the hot path: 50 Arnoldi
+iterations, each one RAS-PML apply (restrict -> twisted block-tridiagonal local solves -> owner write), one 7-point
+SpMV and CGS2 orthogonalisation with the re-orthogonalisation delayed one step (DCGS2), Givens updates on the host,
+then the cycle end (closing projection, x += Z R^-1 y, true residual).  `value` = RAS-PML preconditioner applications
+(= Arnoldi iterations) per second over exactly K cycles, all inputs resident in HBM: a whole cycle, so the Krylov
+depth averages over 0..49 exactly as in a real solve (time to solution = cycles x cycle time).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
---impl reference times the CPU oracle (the only reference this paper has) on the box's host cores, on the
-same config / metric / unit, each step a bounded sample of the workload.
+--gpus N > 1 without torchrun's environment re-launches itself under torch.distributed.run (one rank per GPU).
+--impl reference times the CPU oracle (the only reference this paper has) on the box's host cores, on the same
+config / metric / unit: each step one full-size oracle Arnoldi step (apply over every subdomain, matvec, MGS) at
+depths spread evenly over a GMRES(50) cycle.
 """
 from __future__ import annotations
 
@@ -30,17 +32,17 @@ if ROOT not in sys.path:
 
 METRIC = "RAS-PML applies/s inside right-preconditioned GMRES(50) (1 apply + SpMV + CGS2 per Arnoldi step)"
 UNIT = "applies/s"
+STEP_DESC = ("one GMRES(50) restart cycle: 50 Arnoldi steps (RAS-PML apply + SpMV + orthogonalisation) + cycle end; "
+             "value = Arnoldi steps (one apply each) per second")
 
 
-def workload_desc(cfg, lay=None):
-    d = {"workload": f"{cfg.name}: k={cfg.k:g}, {cfg.nsub}x{cfg.nsub} subdomains, P1 10 ppw, GMRES({cfg.restart}), "
-                     f"seeded synthetic inputs (BASELINE.json configs[{list('01234').index(cfg.name[1])}])",
-         "k": cfg.k, "subdomains": cfg.nsub * cfg.nsub, "restart": cfg.restart, "nsrc": cfg.nsrc, "seed": cfg.seed}
-    if lay is not None:
-        d.update({"n_free": lay["n_free_global"], "cells_per_side": lay["N_cells"], "delta": lay["n_ovlp"],
-                  "kappa": lay["n_pml"], "local_unknowns": lay["local_unknowns"], "m_max": lay["m_max"],
-                  "factor_GB": round(lay["factor_bytes"] / 1e9, 3)})
-    return d
+def workload_desc(cfg, world: int):
+    """The workload, identical in both arms (no implementation or layout keys)."""
+    return {"workload": f"{cfg.name}: k={cfg.k:g}, {cfg.nsub}x{cfg.nsub} subdomains, P1 10 ppw, GMRES({cfg.restart}), "
+                        f"seeded synthetic inputs (BASELINE.json configs[{list('01234').index(cfg.name[1])}])",
+            "k": cfg.k, "subdomains": cfg.nsub * cfg.nsub, "restart": cfg.restart, "nsrc": cfg.nsrc, "seed": cfg.seed,
+            "rtol": cfg.rtol, "step": STEP_DESC, "parallelism": f"subdomain-sharded x{world}",
+            "l2": "inputs larger than L2: every apply streams all factor blocks (GBs at c2-c4) vs the 126 MB L2"}
 
 
 def peaks():
@@ -105,8 +107,36 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def nccl_init_lines(path_glob):
+    """NCCL INIT lines of this job (NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=INIT written to per-process files)."""
+    import glob
+    out = []
+    for f in sorted(glob.glob(path_glob)):
+        try:
+            with open(f) as fh:
+                for line in fh:
+                    if "Init COMPLETE" in line or "NVLS" in line or "nranks" in line:
+                        out.append(line.strip()[-200:])
+        except OSError:
+            pass
+    return out[:64]
+
+
 # ====================================================================================== our arm
 def run_ours(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # NCCL's own record of the communicators (rank 0 reports the INIT lines: N ranks, NVLS or not)
+    tag = os.environ.get("TORCHELASTIC_RUN_ID", str(os.getppid()))
+    nccl_log = f"/tmp/helm_nccl_{tag}"
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log + ".%h.%p.log")
+
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -114,11 +144,6 @@ def run_ours(args):
     from paper_2602_00735_b200 import Context
     from paper_2602_00735_b200.workloads import CONFIGS, sources
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl")
@@ -140,6 +165,27 @@ def run_ours(args):
         dist.broadcast(buf, src=0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather(v: float) -> list:
+        if world == 1:
+            return [v]
+        t = torch.zeros(world, device="cuda", dtype=torch.float64)
+        t[rank] = v
+        dist.all_reduce(t)
+        return t.cpu().tolist()
+
+    barrier()
     t0 = time.time()
     ctx = Context(cfg.k, cfg.nsub, cfg.nsub, rank=rank, nranks=world, stream=stream, nccl_id=nccl_id)
     ctx.factor()
@@ -147,41 +193,39 @@ def run_ours(args):
         from paper_2602_00735_b200.helm import ORTH_CGS2
         ctx.set_orthogonalisation(ORTH_CGS2)
     torch.cuda.synchronize()
-    setup_s = time.time() - t0
+    setup_s = max_over_ranks(time.time() - t0)
     lay = ctx.layout.as_dict()
+    comm = ctx.comm_info()
     xy, amp, sig = sources(cfg)
     b = ctx.rhs(xy, amp, sig)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---- warm-up: W Arnoldi steps
     x = torch.zeros_like(b)
-    ctx.gmres(b, x, restart=cfg.restart, rtol=0.0, maxit=max(args.warmup, 1))
-    # ---- timed: exactly K Arnoldi steps in one GMRES(50) call (rtol = 0: no early exit)
-    x.zero_()
+    R = cfg.restart
+
+    def cycles(k):
+        its = 0
+        for _ in range(k):
+            x.zero_()
+            _, inf, _ = ctx.gmres(b, x, restart=R, rtol=0.0, maxit=R)
+            its += inf.iterations
+        return its
+
+    # ---- warm-up: W cycles; timed: exactly K cycles (rtol = 0: no early exit), CUDA events on the library stream
+    cycles(args.warmup)
     ctx.profile(True)
     ctx.profile_read()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        _, info, _ = ctx.gmres(b, x, restart=cfg.restart, rtol=0.0, maxit=args.steps)
+        its = cycles(args.steps)
         ev1.record(stream)
         barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     apply_ms, apply_n, launches = ctx.profile_read()
     ctx.profile(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    applies = info.applies
-    value = applies / (ms / 1e3)
+    value = its / (ms / 1e3)
 
-    # ---- apply-only and SpMV-only rates (reported alongside; not the headline)
+    # ---- apply-only rate (reported alongside; not the headline)
     v = torch.randn(ctx.n, dtype=torch.complex128, device="cuda")
     z = torch.empty_like(v)
     for _ in range(3):
@@ -192,106 +236,123 @@ def run_ours(args):
         ctx.precond_apply(v, z)
     ev1.record(stream)
     barrier()
-    apply_only_ms = ev0.elapsed_time(ev1) / 10
+    apply_only_ms = max_over_ranks(ev0.elapsed_time(ev1) / 10)
 
     # ---- time to solution (rtol 1e-6), inputs resident
     x.zero_()
     barrier()
     ev0.record(stream)
-    _, tinfo, _ = ctx.gmres(b, x, restart=cfg.restart, rtol=cfg.rtol, maxit=5000)
+    _, tinfo, _ = ctx.gmres(b, x, restart=R, rtol=cfg.rtol, maxit=5000)
     ev1.record(stream)
     barrier()
-    tts_s = ev0.elapsed_time(ev1) / 1e3
+    tts_s = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
 
-    # ---- end to end through the C ABI with host buffers (pinned), K steps, copies inside
+    # ---- end to end through the C ABI with host buffers (pinned), K cycles, copies inside every call
     bh = b.cpu().pin_memory()
     xh = torch.zeros_like(bh).pin_memory()
-    ctx.gmres_host(bh.numpy(), xh.numpy(), restart=cfg.restart, rtol=0.0, maxit=max(args.warmup, 1))   # warm-up
-    xh.zero_()
+    xh_np = xh.numpy()
+    for _ in range(max(1, min(args.warmup, 2))):
+        xh.zero_()
+        ctx.gmres_host(bh.numpy(), xh_np, restart=R, rtol=0.0, maxit=R)   # warm-up (staging buffers on first use)
     barrier()
     t1 = time.perf_counter()
-    _, einfo = ctx.gmres_host(bh.numpy(), xh.numpy(), restart=cfg.restart, rtol=0.0, maxit=args.steps)
+    e_its = 0
+    for _ in range(args.steps):
+        xh.zero_()
+        _, einfo = ctx.gmres_host(bh.numpy(), xh_np, restart=R, rtol=0.0, maxit=R)
+        e_its += einfo.iterations
     barrier()
-    e2e_s = time.perf_counter() - t1
+    e2e_s = max_over_ranks(time.perf_counter() - t1)
     n = ctx.n
-    cycles = einfo.restarts + 1
-    h2d = 16 * n * 2 + 16 * args.steps                        # b, x0; y coefficients
+    h2d = 16 * n * 2 + 16 * R                                 # b, x0; the cycle's y coefficients
     if args.orth == "cgs2":
-        h2d += 8 * cycles                                       # per-cycle beta
-    if args.orth == "cgs2":   # one Hessenberg column per step
-        d2h = 16 * n + sum(16 * (min(j % cfg.restart, cfg.restart - 1) + 2) for j in range(args.steps)) + 8 * (cycles + 1)
-    else:   # DCGS2: the step record (3 x 64 + 2 complex) per step, the closed column per cycle
-        d2h = 16 * n + 16 * 194 * args.steps + 16 * (cfg.restart + 1) * cycles + 8 * (cycles + 1)
+        h2d += 8
+        d2h = 16 * n + sum(16 * (j + 2) for j in range(R)) + 8 * 2
+    else:   # DCGS2: the step record (3 x 64 + 2 complex) per step, the closed column, the norms
+        d2h = 16 * n + 16 * 194 * R + 16 * (R + 1) + 8 * 2
 
     hbm, peak_src = peaks()
 
-    # TTS roofline: bytes the solve must move at the kernels' algorithmic rates (tts_bytes below).
     def tts_bytes(its, restarts):
-        """Algorithmic bytes of the whole solve: per Arnoldi step the apply, the SpMV and the orthogonalisation
-        sweeps (DCGS2: projection sweep over V_{j+1} and w, update sweep reading V_j, u_j, w and writing v_j,
-        u_{j+1}; CGS2: three sweeps over V_{j+1} plus w traffic); per cycle u_0 = r, then for DCGS2 the closing
-        projection and x += Z (R^-1 y) (no apply), for CGS2 the combination V y, one apply and x += z; then the
-        true residual."""
+        """Algorithmic bytes of a solve: per Arnoldi step the apply, the SpMV and the orthogonalisation sweeps
+        (DCGS2: projection sweep over V_{j+1} and w, update sweep reading V_j, u_j, w and writing v_j, u_{j+1};
+        CGS2: three sweeps over V_{j+1} plus w traffic); per cycle u_0 = r, then for DCGS2 the closing projection and
+        x += Z (R^-1 y) (no apply), for CGS2 the combination V y, one apply and x += z; then the true residual."""
         n16 = 16 * ctx.n
         cgs2 = args.orth == "cgs2"
         tot, left = 0, its
         for _ in range(restarts + 1):
-            m = min(cfg.restart, left)
+            m = min(R, left)
             for j in range(m):
                 orth = 3 * (j + 1) + 7 if cgs2 else 2 * (j + 1) + 4
                 tot += lay["apply_bytes"] + lay["spmv_bytes"] + n16 * orth
-            if cgs2:   # x += B^-1 (V y): combine, one apply, axpy; then the true residual
+            if cgs2:
                 tot += n16 * (2 + m + 1) + lay["apply_bytes"] + 3 * n16 + lay["spmv_bytes"] + n16
-            else:      # closing projection, x += Z (R^-1 y): combine + axpy (no apply); then the true residual
+            else:
                 tot += n16 * (2 + (m + 1) + (m + 1)) + 3 * n16 + lay["spmv_bytes"] + n16
             left -= m
         return tot
 
     tts_b = tts_bytes(tinfo.iterations, tinfo.restarts)
+    cyc_b = tts_bytes(R, 0)
     apply_avg_ms = apply_ms / max(apply_n, 1)
-    achieved = lay["apply_bytes"] / (apply_avg_ms / 1e3) / 1e9
+    # per GPU: this rank's algorithmic apply bytes over its own mean apply time; the line reports the slowest rank
+    ach_r = gather(lay["apply_bytes"] / (apply_avg_ms / 1e3) / 1e9)
+    ms_r = gather(apply_avg_ms)
+    slow = max(range(world), key=lambda q: ms_r[q])
+    achieved = ach_r[slow]
     from paper_2602_00735_b200.helm import probe_read_bandwidth
     read_peak = probe_read_bandwidth(8 << 30, 5, 0)          # chunks interleaved over the CTAs
     read_streams = probe_read_bandwidth(16 << 30, 5, 1)      # one contiguous stream per CTA, like k_apply
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k_apply_traffic.json")
-    if os.path.exists(prof) and world == 1:
+    if os.path.exists(prof):
         with open(prof) as f:
             tj = json.load(f)
-        traffic = tj.get(cfg.name, {}).get("dram_bytes_per_launch")
+        key = cfg.name if world == 1 else f"{cfg.name}/{world}"
+        traffic = tj.get(key, {}).get("dram_bytes_per_launch")
+    launches_tot = int(sum(gather(float(launches))))
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {**workload_desc(cfg, lay), "parallelism": f"subdomain-sharded x{world}", "orth": args.orth,
-                   "l2": "inputs larger than L2: %.1f GB of factor blocks streamed per apply vs 126 MB L2"
-                         % (lay["apply_bytes"] / 1e9)},
+        "config": workload_desc(cfg, world),
+        "layout": {"n_free": lay["n_free_global"], "cells_per_side": lay["N_cells"], "delta": lay["n_ovlp"],
+                   "kappa": lay["n_pml"], "local_unknowns_rank0": lay["local_unknowns"], "m_max": lay["m_max"],
+                   "factor_GB_rank0": round(lay["factor_bytes"] / 1e9, 3),
+                   "apply_GB_rank0": round(lay["apply_bytes"] / 1e9, 3), "orth": args.orth},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "k_apply (fused restrict + twisted block solves + owner write)",
                      "algorithmic_bytes_per_launch": lay["apply_bytes"], "peak_source": peak_src,
+                     "per_gpu": world > 1, "slowest_rank": slow, "achieved_per_rank": ach_r,
                      "band_equivalent_GBps": lay["band_bytes"] / (apply_avg_ms / 1e3) / 1e9,
                      "read_stream_probe_GBps": read_peak, "frac_of_read_probe": achieved / read_peak,
                      "read_streams_probe_GBps": read_streams, "frac_of_read_streams_probe": achieved / read_streams,
-                     "apply_kernel_ms": apply_avg_ms, "apply_share_of_step": apply_ms / ms},
-        "e2e": {"value": applies_e2e(einfo, e2e_s), "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
-                "d2h_bytes_per_step": d2h / args.steps, "api": "helm_gmres_host (host b/x, copies inside)"},
-        "gpu_launches": launches,
-        "applies": applies, "iterations": info.iterations,
+                     "apply_kernel_ms": ms_r[slow], "apply_share_of_step": apply_ms / ms,
+                     "cycle_algorithmic_bytes": cyc_b, "cycle_frac": cyc_b / (hbm * 1e9) / (ms / args.steps / 1e3)},
+        "e2e": {"value": e_its / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "helm_gmres_host (host b/x, copies inside every call), one call per cycle"},
+        "gpu_launches": launches_tot,
+        "iterations": its, "applies": its,
         "apply_only": {"ms": apply_only_ms, "applies_per_s": 1e3 / apply_only_ms,
                        "GBps": lay["apply_bytes"] / apply_only_ms / 1e6},
         "gmres_tts": {"seconds": tts_s, "iterations": tinfo.iterations, "restarts": tinfo.restarts,
                       "relres_true": tinfo.relres_true, "status": tinfo.status, "rtol": cfg.rtol,
+                      "applies_per_s": tinfo.iterations / tts_s,
                       "algorithmic_bytes": tts_b, "roofline_s": tts_b / (hbm * 1e9),
                       "roofline_frac": tts_b / (hbm * 1e9) / tts_s},
         "setup_factor_s": setup_s,
+        "comm": comm,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_paper:
         out["paper_table4"] = paper_table4(stream)
         out["gmres_tts_ramp_pou"] = ramp_pou_tts(cfg, stream, xy, amp, sig)
-    if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg, steps=1)
+    if world > 1:
+        out["nccl_init"] = nccl_init_lines(nccl_log + ".*.log") if rank == 0 else []
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
@@ -383,63 +444,7 @@ def ramp_pou_tts(cfg, stream, xy, amp, sig):
     return res
 
 
-def applies_e2e(info, seconds):
-    return info.applies / seconds if seconds > 0 else None
-
-
 # ====================================================================================== oracle arm
-def _oracle_step_model(cfg):
-    """Set up the oracle on this config and return a callable timing one bounded-sample step."""
-    import numpy as np
-
-    from oracle.oracle import Oracle
-    from paper_2602_00735_b200.workloads import probe_vector
-
-    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
-    # stratified sample of subdomains: interior, edge and corner classes, at most 48
-    P = cfg.nsub
-    cand = sorted({0, P - 1, P * (P - 1), P * P - 1, 1, P, P * (P // 2) + P // 2, P * (P // 3) + (2 * P) // 3})
-    rng = np.random.default_rng(cfg.seed)
-    extra = rng.choice(P * P, size=min(48, P * P), replace=False).tolist()
-    sample = sorted(set(cand + extra))[:48] if P * P > 48 else list(range(P * P))
-
-    def cost(j):
-        s = o.subdomain(j)
-        mx, my = s["m"]
-        return mx * my * (mx + 1)          # band solve work ~ n * p
-
-    total = sum(cost(j) for j in range(o.nsub)) if o.nsub <= 20000 else None
-    scale = total / sum(cost(j) for j in sample)
-    t = time.perf_counter()
-    o.factor(sample)
-    factor_s = time.perf_counter() - t
-    v = probe_vector(o.nfree, int(cfg.k) + 1)
-    V = [v / np.linalg.norm(v)]
-    jdepth = cfg.restart // 2            # a cycle orthogonalises against ~restart/2 vectors on average
-    jsample = min(4, jdepth)             # time MGS against 4 of them, scale linearly
-    for i in range(jsample - 1):
-        w = probe_vector(o.nfree, 1000 + i)
-        V.append(w / np.linalg.norm(w))
-
-    def step():
-        t0 = time.perf_counter()
-        z = o.apply(V[0], subs=sample)
-        t1 = time.perf_counter()
-        w = o.matvec(z)
-        t2 = time.perf_counter()
-        for i in range(len(V)):               # MGS (O9)
-            h = np.vdot(V[i], w)
-            w = w - h * V[i]
-        np.linalg.norm(w)
-        t3 = time.perf_counter()
-        return (t1 - t0) * scale + (t2 - t1) + (t3 - t2) * jdepth / jsample
-
-    desc = (f"oracle GMRES step on {cfg.name}: band-LU RAS apply on {len(sample)} of {o.nsub} subdomains "
-            f"(scaled by band work x{scale:.1f}) + full matvec + MGS against {jsample} vectors scaled to {jdepth}; "
-            f"sample factor time {factor_s:.1f}s untimed")
-    return step, desc
-
-
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -447,40 +452,99 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(cfg, steps=1):
-    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
-    step, desc = _oracle_step_model(cfg)
-    ts = [step() for _ in range(max(1, steps))]
-    per = sum(ts) / len(ts)
-    out = {"value": 1.0 / per, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
-           "sample": desc, "seconds_per_step": per}
-    if cfg.name in ("c0", "c1", "c2"):   # small enough to time the whole oracle solve (SURVEY 8(d) reporting)
-        out["full_oracle"] = _oracle_full(cfg)
-    return out
+def host_info():
+    model, ram = "", None
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+        with open("/proc/meminfo") as f:
+            ram = round(int(f.readline().split()[1]) / 2 ** 20, 1)
+    except (OSError, ValueError, IndexError):
+        pass
+    return {"cores": cpu_threads(), "cpu_model": model, "ram_GiB": ram}
 
 
-def _oracle_full(cfg):
-    """The oracle on the whole workload: band-LU factorisation, apply (median of 3), MGS GMRES(50) to rtol."""
-    import statistics
+class OracleSteps:
+    """The oracle at the full size of the workload, as it stands: dedup-mode factorisation (SURVEY 8(d) memory
+    fallback: one band LU per bitwise-distinct A_j, exact), then full oracle Arnoldi steps -- w = A(B^-1 v) over every
+    subdomain and every row, MGS against the first j + 1 basis vectors (oracle.mgs, O9 step 2), ||w||."""
 
-    from oracle.oracle import Oracle, gmres
-    from paper_2602_00735_b200.workloads import probe_vector, sources
-    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
-    t = time.perf_counter()
-    o.factor()
-    fs = time.perf_counter() - t
-    v = probe_vector(o.nfree, int(cfg.k) + 1)
-    ts = []
-    for _ in range(3):
+    def __init__(self, cfg):
+        import numpy as np
+
+        from oracle.oracle import Oracle
+        from paper_2602_00735_b200.workloads import probe_vector
+        self.np = np
         t = time.perf_counter()
-        o.apply(v)
-        ts.append(time.perf_counter() - t)
-    b = o.rhs(*sources(cfg))
-    t = time.perf_counter()
-    res = gmres(o.matvec, o.apply, b, restart=cfg.restart, rtol=cfg.rtol)
-    tts = time.perf_counter() - t
-    o.close()
-    return {"factor_s": fs, "apply_s": statistics.median(ts), "gmres_iterations": res.iterations, "gmres_s": tts}
+        self.o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+        self.classes = self.o.factor_dedup()
+        self.factor_s = time.perf_counter() - t
+        n = self.o.nfree
+        # a basis of restart + 1 unit vectors (the MGS cost does not depend on their content)
+        self.V = []
+        for i in range(cfg.restart + 1):
+            v = probe_vector(n, 1000 + i)
+            self.V.append(v / np.linalg.norm(v))
+        self.o.matvec(self.V[0])                      # first call assembles the global stencil (untimed)
+
+    def step(self, j: int) -> float:
+        from oracle.oracle import mgs
+        t = time.perf_counter()
+        w = self.o.matvec(self.o.apply(self.V[j]))
+        w, _ = mgs(self.V[:j + 1], w)
+        self.np.linalg.norm(w)
+        return time.perf_counter() - t
+
+    def apply_s(self, reps: int = 3) -> float:
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            self.o.apply(self.V[0])
+            ts.append(time.perf_counter() - t)
+        return statistics.median(ts)
+
+
+def depths(k_steps: int, restart: int):
+    """Krylov depths of the reference arm's steps: spread evenly over one cycle (cycle-average cost)."""
+    return [min(restart - 1, int((s + 0.5) * restart / k_steps)) for s in range(k_steps)]
+
+
+def oracle_golden_timing(cfg):
+    """The full oracle GMRES(50) solve of this config as recorded by scripts/make_golden.py (oracle only, hours of
+    host time at c3/c4: run once and cached, keyed by config, seed and oracle source hash)."""
+    path = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_gmres.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        g = json.load(f)
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    try:
+        from make_golden import oracle_hash
+        cur = oracle_hash()
+    except Exception:
+        cur = None
+    t = g.get("oracle_timing", {})
+    return {"gmres_s": t.get("gmres_s"), "iterations": g.get("iterations"), "restarts": g.get("restarts"),
+            "maxit": g.get("maxit"), "status": g.get("status"), "seed": g.get("seed"),
+            "host": t.get("host"), "when": t.get("when"), "oracle_hash": g.get("oracle_hash"),
+            "oracle_hash_current": cur, "cached": True}
+
+
+def cpu_baseline(cfg):
+    """Rank 0, N = 1: the oracle timed on this box's host cores on a bounded sample -- ONE full-size oracle Arnoldi
+    step at the cycle-average depth (restart / 2) -- plus the full oracle's factorisation and apply (median of 3)
+    timed here and its whole GMRES solve from the cached golden record."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
+    st = OracleSteps(cfg)
+    j = cfg.restart // 2
+    sec = st.step(j)
+    return {"value": 1.0 / sec, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
+            "sample": f"one full-size oracle GMRES Arnoldi step on {cfg.name} at Krylov depth {j} (the cycle average): "
+                      f"band-LU RAS apply over all {st.o.nsub} subdomains (dedup mode, {st.classes} factor classes), "
+                      f"full matvec, MGS against {j + 1} vectors",
+            "seconds_per_step": sec, "host": host_info(),
+            "full_oracle": {"factor_dedup_s": st.factor_s, "classes": st.classes, "apply_s_median3": st.apply_s(),
+                            "gmres": oracle_golden_timing(cfg)}}
 
 
 def run_reference(args):
@@ -490,30 +554,48 @@ def run_reference(args):
         return
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
     cfg = CONFIGS[args.config]
-    if args.seed is not None:   # another draw of the same workload (sources; the probe vectors keep k + 1)
+    if args.seed is not None:
         import dataclasses
         cfg = dataclasses.replace(cfg, seed=args.seed)
-    step, desc = _oracle_step_model(cfg)
+    st = OracleSteps(cfg)
     for _ in range(args.warmup):
-        step()
-    ts = [step() for _ in range(args.steps)]
+        st.step(0)
+    ds = depths(args.steps, cfg.restart)
+    ts = [st.step(j) for j in ds]
     total = sum(ts)
     value = args.steps / total
+    cores = int(os.environ["OMP_NUM_THREADS"])
+    desc = (f"each step one full-size oracle GMRES Arnoldi step on {cfg.name} (band-LU RAS apply over all "
+            f"{st.o.nsub} subdomains in dedup mode, full matvec, MGS, norm) at Krylov depths spread evenly over a "
+            f"GMRES({cfg.restart}) cycle ({min(ds)}..{max(ds)}); warm-up steps at depth 0; setup "
+            f"{st.factor_s:.1f} s untimed")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": workload_desc(cfg),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
-                            "kind": "oracle", "sample": desc},
+           "config": workload_desc(cfg, args.gpus),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                            "host": host_info()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 without torchrun's environment: run this script under torch.distributed.run, one rank per GPU
+    (rendezvous on 127.0.0.1), and pass its output through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -526,6 +608,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     else:
         run_ours(args)
 

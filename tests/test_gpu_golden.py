@@ -1,0 +1,77 @@
+"""The headline config c3 (k = 1600, 6.58 M unknowns, 64 x 64 subdomains; BASELINE.json configs[3]) at FULL size,
+against the oracle: the whole assembled stencil and right-hand side element by element (oracle run live), and the
+GMRES(50) solve against the oracle-only golden record tests/golden/c3_gmres.json (scripts/make_golden.py: MGS GMRES
+on the dedup-mode oracle, written without libhelm) -- iterations +-1, the residual-estimate history to 1e-6 relative,
+||x|| and a seeded 64-row sketch S x to 1e-6 (north_star: "GPU solutions matching the oracle ... on all five
+configs"; GMRES P:240-242, B^-1 P:143-147, A P:58-62, b D14).  Launched exactly as bench.py times it (one rank,
+the persistent k_apply, DCGS2).  -m gpu."""
+import os
+
+import numpy as np
+import pytest
+
+from golden_util import as_complex, golden_path, load_golden, sketch_rel
+from oracle.oracle import Oracle
+from paper_2602_00735_b200.workloads import CONFIGS, sources
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a B200", allow_module_level=True)
+
+from paper_2602_00735_b200 import Context  # noqa: E402
+
+_C = {}
+
+
+def c3():
+    if "ctx" not in _C:
+        cfg = CONFIGS["c3"]
+        ctx = Context(cfg.k, cfg.nsub, cfg.nsub)
+        ctx.factor()
+        _C["ctx"] = ctx
+        _C["o"] = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    return _C["ctx"], _C["o"]
+
+
+def test_c3_stencil_full_vector():
+    """Every coefficient of the assembled 7-point operator (6.58 M rows x 7 slots) vs the oracle's assembly."""
+    ctx, o = c3()
+    A = ctx.export_stencil().cpu().numpy()          # [7][n]
+    R = o.stencil().T
+    assert A.shape == R.shape
+    assert np.max(np.abs(A - R)) <= 1e-13 * np.max(np.abs(R))
+
+
+def test_c3_rhs_full_vector():
+    """b = M f_I on every free node vs the oracle, and its sketch vs the golden record."""
+    ctx, o = c3()
+    cfg = CONFIGS["c3"]
+    xy, amp, sig = sources(cfg)
+    b = ctx.rhs(xy, amp, sig).cpu().numpy()
+    bo = o.rhs(xy, amp, sig)
+    assert np.max(np.abs(b - bo)) <= 1e-13 * np.max(np.abs(bo))
+    if os.path.exists(golden_path("c3")):
+        g = load_golden("c3")
+        assert abs(np.linalg.norm(b) - g["norm_b"]) <= 1e-13 * g["norm_b"]
+        assert sketch_rel(b, g, "sketch_b") <= 1e-13
+
+
+@pytest.mark.skipif(not os.path.exists(golden_path("c3")), reason="no c3 golden record")
+def test_c3_gmres_matches_the_oracle_golden():
+    ctx, _ = c3()
+    g = load_golden("c3")
+    cfg = CONFIGS["c3"]
+    assert g["seed"] == cfg.seed and g["restart"] == cfg.restart and g["rtol"] == cfg.rtol
+    b = ctx.rhs(*sources(cfg))
+    x, info, hist = ctx.gmres(b, restart=cfg.restart, rtol=cfg.rtol, maxit=g["maxit"], history=True)
+    assert info.status == g["status"] == 0
+    assert abs(info.iterations - g["iterations"]) <= 1
+    h_orc = np.asarray(g["history"])
+    n = min(len(hist), len(h_orc))
+    assert np.max(np.abs(hist[:n] - h_orc[:n]) / h_orc[:n]) <= 1e-6
+    assert info.relres_true <= cfg.rtol
+    xn = x.cpu().numpy()
+    assert abs(np.linalg.norm(xn) - g["norm_x"]) <= 1e-6 * g["norm_x"]
+    assert sketch_rel(xn, g) <= 1e-6
