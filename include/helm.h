@@ -256,6 +256,11 @@ int helm_probe_read_bandwidth(long long bytes, int reps, double* gbps);
  * streams, the pattern of the apply kernel (each CTA streams its own subdomains' factors). */
 int helm_probe_read_bandwidth_mode(long long bytes, int reps, int mode, double* gbps);
 
+/* Measurement aid (not part of the method): FP64 peak of this GPU, the roofline denominator of the setup factorisation.
+ * mode 0: tensor-core DMMA (mma.sync m8n8k4 f64) issue rate; mode 1: plain DFMA.  Synchronous; *tflops measured with
+ * CUDA events over one launch of independent chains on every SM. */
+int helm_probe_fp64_tflops(int mode, double* tflops);
+
 const char* helm_last_error(const helm_ctx* ctx);
 void helm_destroy(helm_ctx* ctx);
 

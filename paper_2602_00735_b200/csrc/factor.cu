@@ -8,7 +8,9 @@
 //   twist         Z = T_tw - L_tw P_{tw-1}^-1 U_{tw-1} - U_tw Q_{tw+1}^-1 L_{tw+1}
 // and store the explicit inverse of each block (P_i^-1, Z^-1, Q_i^-1) in block slot i, column-major.
 // Each inverse is formed by blocked Gauss-Jordan elimination WITHOUT pivoting (D12: the oracle's band LU is
-// unpivoted too); a zero, non-finite or tiny pivot (|pivot| < 1e-12, against O(1) stencil entries) raises
+// unpivoted too) with 8-column panels: the 8 x 8 pivot block inverted in one warp's registers (the serial part),
+// the row panel / trailing update / column panel on the FP64 tensor cores (DMMA), the next pivot block formed and
+// inverted by warp 0 while the other warps finish the trailing update (gj_panels8); a zero, non-finite or tiny pivot (|pivot| < 1e-12, against O(1) stencil entries) raises
 // HELM_EZEROPIVOT naming subdomain, block and row.
 // The two chains run in separate CTAs; a second launch forms the twist blocks.  Blocks wider than M_SMEM use
 // thread-block clusters and blocked Gauss-Jordan in global memory (k_factor_big).  The 9-point Q1 stencil (D18)
@@ -63,12 +65,18 @@ __device__ __forceinline__ void ztile_fms(z2& c0, z2& c1, int kw, LA la, LB lb)
 // D (kw x kw, row-major, stride DLD, kw <= 32) <- D^-1 by unpivoted in-place Gauss-Jordan, executed by the first
 // GJW warps of the CTA (lane c owns column c, warp w the rows r = w, w + GJW, ...; named barrier 2 over those warps
 // only).  A zero pivot is recorded as row kb + p.
-__host__ __device__ __forceinline__ int lds_of(int m) { return ((m + 7) / 8) * 8 + 1; }  // 16B-words, = 1 mod 8
+// Shared-memory layout of the block S being inverted: row stride ld = round_up(m, 8) + 4 16-B words (== 4 mod 8) and
+// the column swizzle c ^ (r & 2).  An LDS.128 is served 8 lanes at a time; with this layout the DMMA fragment loads of
+// both operands -- A (lanes: rows g in {2h, 2h+1}, columns t in 0..3) and B (rows t, columns g) -- hit 8 distinct 16-B
+// bank groups per quarter warp (with ld == 1 mod 8 both were 2-way conflicted: 5.3e9 excess wavefronts at c3, ncu).
+__host__ __device__ __forceinline__ int lds_of(int m) { return ((m + 7) / 8) * 8 + 4; }
+__device__ __forceinline__ int sx(int r, int c, int ld) { return r * ld + (c ^ (r & 2)); }
 
 constexpr int GJW = 8;
 // |pivot| < 1e-12 is reported as singular: the stencil entries of A_j are O(1e-3 .. 10) (P1/Q1 stiffness is
 // scale-free in 2D; |gamma|^-2 >= 1e-3 in every PML used here), so such a pivot means cond > 1e12
 constexpr double PIV_TINY2 = 1e-24;
+
 __device__ __forceinline__ void gj_bar() { asm volatile("bar.sync 2, %0;" ::"r"(GJW * 32) : "memory"); }
 
 __device__ void warp_gj(z2* D, int kw, int kb, int* bad)
@@ -160,58 +168,79 @@ __device__ void warp_gj8(z2* D, z2* rowbuf /* 2 x 32 */, int kw, int kb, int* ba
     }
 }
 
+// 8 x 8 inverse in the registers of ONE warp, in the DMMA accumulator layout (lane l holds row g = l / 4, columns
+// 2 (l % 4) and 2 (l % 4) + 1): unpivoted Gauss-Jordan (D12), the pivot and the pivot row reach the other lanes by
+// shuffles -- no shared memory, no barrier.  Rows / columns >= w8 must hold the identity.  A zero / tiny pivot is
+// recorded as row kbase + p.
+__device__ __forceinline__ void inv8_regs(z2& x0, z2& x1, int w8, int kbase, int* bad)
+{
+    const int lane = threadIdx.x & 31, r = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        const z2 mine = (p & 1) ? x1 : x0;
+        const z2 pv = shfl_z(mine, 4 * p + (p >> 1));          // D[p][p]
+        const z2 f = shfl_z(mine, (lane & ~3) + (p >> 1));     // D[r][p] of my row, before the update
+        const bool zero = !(pv.x * pv.x + pv.y * pv.y >= PIV_TINY2);
+        if (zero && p < w8 && lane == 0 && *bad < 0) *bad = kbase + p;
+        const double rd = zero ? 0.0 : 1.0 / (pv.x * pv.x + pv.y * pv.y);
+        const z2 inv = zmk(pv.x * rd, -pv.y * rd);
+        const z2 s0 = c0 == p ? inv : zmul(x0, inv), s1 = c1 == p ? inv : zmul(x1, inv);   // pivot row scaled
+        const z2 y0 = shfl_z(s0, 4 * p + t), y1 = shfl_z(s1, 4 * p + t);
+        if (r == p) {
+            x0 = s0;
+            x1 = s1;
+        } else {
+            const z2 b0 = c0 == p ? inv : y0, b1 = c1 == p ? inv : y1;
+            if (c0 == p) x0 = zmk(0, 0);                       // -D[r][p] / pivot
+            if (c1 == p) x1 = zmk(0, 0);
+            zfms(x0, f, b0);                                   // D[r][c] - D[r][p] D[p][c]
+            zfms(x1, f, b1);
+        }
+    }
+}
+
 // Couplings of block row i as m x m matrices (7-point P1: two diagonals; 9-point Q1: three):
 //   L_i[a][a] = S_i(a), L_i[a][a-1] = SW_i(a), L_i[a][a+1] = SE_i(a)          (A_{i,i-1})
 //   U_i[a][a] = N_i(a), U_i[a][a+1] = NE_i(a), U_i[a][a-1] = NW_i(a)          (A_{i,i+1})
 // Wl(c, d) reads W = the inverse stored column-major in global memory.
 struct Cpl { const z2 *d, *lo, *hi; };   // diagonal, sub-diagonal (entry [a][a-1]) and super ([a][a+1]) vectors
 
-// (L_i W U_{i-1})(a,b) = sum_c L[a][c] sum_d W[c][d] U[d][b];  U[d][b]: d = b N(b), d = b-1 NE(b-1), d = b+1 NW(b+1)
+// (L_i W U_{i-1})(a,b) = sum_c L[a][c] sum_d W[c][d] U[d][b];  U[d][b]: d = b N(b), d = b-1 NE(b-1), d = b+1 NW(b+1).
+// Branch-free: the three coefficients of each factor and the nine W entries (indices clamped into the block, their
+// coefficient zero when clamped) are loaded together, so the L2 round trips of one entry overlap instead of chaining
+// through data-dependent tests (ncu at c3: long-scoreboard stalls on these loads were 12 % of the kernel's samples).
+__device__ __forceinline__ z2 cpl3(const z2* __restrict__ W, int m, int a, int b, z2 l0, z2 l1, z2 l2, z2 u0, z2 u1,
+                                   z2 u2)
+{
+    const int cm = a > 0 ? a - 1 : a, cp = a + 1 < m ? a + 1 : a;
+    const int dm = b > 0 ? b - 1 : b, dp = b + 1 < m ? b + 1 : b;
+    const z2* w0 = W + (long long)dm * m;
+    const z2* w1 = W + (long long)b * m;
+    const z2* w2 = W + (long long)dp * m;
+    const z2 x00 = w0[cm], x01 = w1[cm], x02 = w2[cm];
+    const z2 x10 = w0[a], x11 = w1[a], x12 = w2[a];
+    const z2 x20 = w0[cp], x21 = w1[cp], x22 = w2[cp];
+    const z2 r0 = zadd(zadd(zmul(x00, u0), zmul(x01, u1)), zmul(x02, u2));
+    const z2 r1 = zadd(zadd(zmul(x10, u0), zmul(x11, u1)), zmul(x12, u2));
+    const z2 r2 = zadd(zadd(zmul(x20, u0), zmul(x21, u1)), zmul(x22, u2));
+    return zadd(zadd(zmul(l0, r0), zmul(l1, r1)), zmul(l2, r2));
+}
+
 __device__ __forceinline__ z2 term_below(const z2* __restrict__ W, int m, int a, int b, Cpl L, Cpl U)
 {
-    z2 ud[3];          // U[b-1][b], U[b][b], U[b+1][b]
-    ud[0] = (b > 0) ? U.hi[b - 1] : zmk(0, 0);
-    ud[1] = U.d[b];
-    ud[2] = (U.lo && b + 1 < m) ? U.lo[b + 1] : zmk(0, 0);
-    z2 acc = zmk(0, 0);
-    for (int dc = -1; dc <= 1; dc++) {
-        const int c = a + dc;
-        if (c < 0 || c >= m) continue;
-        const z2 l = dc == 0 ? L.d[a] : (dc < 0 ? L.lo[a] : (L.hi ? L.hi[a] : zmk(0, 0)));
-        if (l.x == 0.0 && l.y == 0.0) continue;
-        z2 r = zmk(0, 0);
-        for (int dd = -1; dd <= 1; dd++) {
-            const int d = b + dd;
-            if (d < 0 || d >= m) continue;
-            r = zadd(r, zmul(W[(long long)d * m + c], ud[dd + 1]));
-        }
-        acc = zadd(acc, zmul(l, r));
-    }
-    return acc;
+    const z2 zero = zmk(0, 0);
+    const z2 l0 = a > 0 ? L.lo[a] : zero, l1 = L.d[a], l2 = (L.hi && a + 1 < m) ? L.hi[a] : zero;
+    const z2 u0 = b > 0 ? U.hi[b - 1] : zero, u1 = U.d[b], u2 = (U.lo && b + 1 < m) ? U.lo[b + 1] : zero;
+    return cpl3(W, m, a, b, l0, l1, l2, u0, u1, u2);
 }
 
 // (U_i W L_{i+1})(a,b) = sum_c U[a][c] sum_d W[c][d] L[d][b];  L[d][b]: d = b S(b), d = b+1 SW(b+1), d = b-1 SE(b-1)
 __device__ __forceinline__ z2 term_above(const z2* __restrict__ W, int m, int a, int b, Cpl U, Cpl L)
 {
-    z2 ld[3];          // L[b-1][b], L[b][b], L[b+1][b]
-    ld[0] = (L.hi && b > 0) ? L.hi[b - 1] : zmk(0, 0);
-    ld[1] = L.d[b];
-    ld[2] = (b + 1 < m) ? L.lo[b + 1] : zmk(0, 0);
-    z2 acc = zmk(0, 0);
-    for (int dc = -1; dc <= 1; dc++) {
-        const int c = a + dc;
-        if (c < 0 || c >= m) continue;
-        const z2 u = dc == 0 ? U.d[a] : (dc > 0 ? U.hi[a] : (U.lo ? U.lo[a] : zmk(0, 0)));
-        if (u.x == 0.0 && u.y == 0.0) continue;
-        z2 r = zmk(0, 0);
-        for (int dd = -1; dd <= 1; dd++) {
-            const int d = b + dd;
-            if (d < 0 || d >= m) continue;
-            r = zadd(r, zmul(W[(long long)d * m + c], ld[dd + 1]));
-        }
-        acc = zadd(acc, zmul(u, r));
-    }
-    return acc;
+    const z2 zero = zmk(0, 0);
+    const z2 c0 = (U.lo && a > 0) ? U.lo[a] : zero, c1 = U.d[a], c2 = a + 1 < m ? U.hi[a] : zero;
+    const z2 d0 = (L.hi && b > 0) ? L.hi[b - 1] : zero, d1 = L.d[b], d2 = b + 1 < m ? L.lo[b + 1] : zero;
+    return cpl3(W, m, a, b, c0, c1, c2, d0, d1, d2);
 }
 
 __device__ __forceinline__ Cpl lower_of(const z2* row, int m, int ns)   // L of a block row
@@ -247,8 +276,9 @@ __device__ __forceinline__ z2 schur_entry(const SubDesc& d, int i, int mode, con
 }
 
 struct FactorSmem {
-    z2* S;      // [m][lds] row-major
-    z2* Dk;     // [GB][DLD] inverse of the current pivot block
+    z2* S;       // [m][lds] row-major, swizzled (sx)
+    z2* Dk[2];   // pivot-block inverses: [GB][DLD] (32-wide path) / the current and the next 8 x 8 (8-wide path)
+    z2* rowbuf;  // [2][GB] warp_gj8's pivot-row buffer
 };
 
 // mode: 0 bottom chain block, 1 top chain block, 2 twist block
@@ -256,129 +286,232 @@ __device__ void build_block(const SubDesc& d, int i, int mode, const z2* __restr
                             FactorSmem sm)
 {
     const int m = d.m, ld = lds_of(m);
+    // consecutive threads take consecutive ROWS a: the column-major W entries W[d m + c], c = a - 1 .. a + 1, and the
+    // coupling vectors L.*[a] / U.*[a] are then coalesced (with b fastest every W load of a warp touched 32 lines --
+    // the build took a third of the factorisation)
+#pragma unroll 2
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int a = e / m, b = e % m;
-        sm.S[a * ld + b] = schur_entry(d, i, mode, stc, dinv, a, b);
+        const int b = e / m, a = e - b * m;
+        sm.S[sx(a, b, ld)] = schur_entry(d, i, mode, stc, dinv, a, b);
     }
     __syncthreads();
 }
 
 // In-place inversion of S (m x m, row-major, stride ld, shared memory) by blocked, unpivoted Gauss-Jordan with panels K
 // of GB columns (unpivoted, D12; on the bottom chain the pivots are the oracle's no-pivot band-LU pivots):
-//   Dk = S[K,K]^-1 (one warp);  S[K,j] = Dk S[K,j] (j not in K);  S[i,j] -= S[i,K] S[K,j] (i, j not in K);
+//   Dk = S[K,K]^-1 (8 warps);  S[K,j] = Dk S[K,j] (j not in K);  S[i,j] -= S[i,K] S[K,j] (i, j not in K);
 //   S[i,K] = -S[i,K] Dk (i not in K);  S[K,K] = Dk.
 // All three products (row panel, trailing update, column panel -- complex GEMMs, 32 deep) run on the FP64 tensor cores
 // (DMMA), one warp per 8 x 8 tile; a panel warp loads its whole operand strip before writing, so they work in place.
 
-__device__ void gj_blocked(int m, FactorSmem sm, int* bad_row)
+// one warp: S[K,j] = Dk S[K,j] for the 8-column strip j0.. (B fragments loaded before the row tiles are written)
+__device__ __forceinline__ void row_strip(z2* S, int ld, int m, int kb, int kw, const z2* Dk, int j0)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, col = j0 + g;
+    z2 bf[GB / 4];
+#pragma unroll
+    for (int s4 = 0; s4 < GB / 4; s4++) {
+        const int q = 4 * s4 + t;
+        bf[s4] = (q < kw && col < m) ? S[sx(kb + q, col, ld)] : zmk(0, 0);
+    }
+#pragma unroll
+    for (int rt = 0; rt < GB / 8; rt++) {
+        if (8 * rt >= kw) break;
+        z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
+#pragma unroll
+        for (int s4 = 0; s4 < GB / 4; s4++) {
+            if (4 * s4 >= kw) break;
+            const int r = 8 * rt + g, q = 4 * s4 + t;
+            const z2 a = (r < kw && q < kw) ? Dk[r * DLD + q] : zmk(0, 0);
+            dmma(c0.x, c1.x, a.x, bf[s4].x);    // C += A B
+            dmma(c0.x, c1.x, -a.y, bf[s4].y);
+            dmma(c0.y, c1.y, a.x, bf[s4].y);
+            dmma(c0.y, c1.y, a.y, bf[s4].x);
+        }
+        const int r = 8 * rt + g, cA = j0 + 2 * t;
+        if (r < kw && cA < m) S[sx(kb + r, cA, ld)] = c0;
+        if (r < kw && cA + 1 < m) S[sx(kb + r, cA + 1, ld)] = c1;
+    }
+}
+
+// one warp: trailing tile S[i0.., j0..] -= S[i0.., K] S[K, j0..]
+__device__ __forceinline__ void trail_tile(z2* S, int ld, int m, int kb, int kw, int i0, int j0)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int r = i0 + g, cA = j0 + 2 * t, cB = cA + 1;
+    z2 c0 = (r < m && cA < m) ? S[sx(r, cA, ld)] : zmk(0, 0);
+    z2 c1 = (r < m && cB < m) ? S[sx(r, cB, ld)] : zmk(0, 0);
+    ztile_fms(
+        c0, c1, kw, [&](int rr, int q) { return i0 + rr < m ? S[sx(i0 + rr, kb + q, ld)] : zmk(0, 0); },
+        [&](int q, int cc) { return j0 + cc < m ? S[sx(kb + q, j0 + cc, ld)] : zmk(0, 0); });
+    if (r < m && cA < m) S[sx(r, cA, ld)] = c0;
+    if (r < m && cB < m) S[sx(r, cB, ld)] = c1;
+}
+
+// one warp: S[i, K] = -S[i, K] Dk for the 8-row strip i0.. (A fragments loaded before it writes)
+__device__ __forceinline__ void col_strip(z2* S, int ld, int m, int kb, int kw, const z2* Dk, int i0)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, row = i0 + g;
+    z2 af[GB / 4];
+#pragma unroll
+    for (int s4 = 0; s4 < GB / 4; s4++) {
+        const int q = 4 * s4 + t;
+        af[s4] = (q < kw && row < m) ? S[sx(row, kb + q, ld)] : zmk(0, 0);
+    }
+#pragma unroll
+    for (int ct = 0; ct < GB / 8; ct++) {
+        if (8 * ct >= kw) break;
+        z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
+#pragma unroll
+        for (int s4 = 0; s4 < GB / 4; s4++) {
+            if (4 * s4 >= kw) break;
+            const int q = 4 * s4 + t, c = 8 * ct + g;
+            const z2 b = (q < kw && c < kw) ? Dk[q * DLD + c] : zmk(0, 0);
+            dmma(c0.x, c1.x, -af[s4].x, b.x);   // C -= A B
+            dmma(c0.x, c1.x, af[s4].y, b.y);
+            dmma(c0.y, c1.y, -af[s4].x, b.y);
+            dmma(c0.y, c1.y, -af[s4].y, b.x);
+        }
+        const int cA = 8 * ct + 2 * t;
+        if (row < m && cA < kw) S[sx(row, kb + cA, ld)] = c0;
+        if (row < m && cA + 1 < kw) S[sx(row, kb + cA + 1, ld)] = c1;
+    }
+}
+
+// warps 0 .. GJW-1: Dk = S[K,K]^-1 (K = kb .. kb + kw - 1)
+__device__ __forceinline__ void pivot_inverse(const z2* S, int ld, z2* Dk, z2* rowbuf, int kb, int kw, int* bad_row)
+{
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kw * kw; e += GJW * 32) {
+        const int r = e / kw, c = e - r * kw;
+        Dk[r * DLD + c] = S[sx(kb + r, kb + c, ld)];
+    }
+    gj_bar();
+    warp_gj8(Dk, rowbuf, kw, kb, bad_row);
+}
+
+#ifdef HELM_FACTOR_PROF
+#define CPROF(k) do { if (cpr) { const long long t_ = clock64(); cpr[k] += t_ - *ctp; *ctp = t_; } } while (0)
+#define CPROF_ARGS , long long* cpr, long long* ctp
+#define CPROF_PASS , cpr, ctp
+#else
+#define CPROF(k) do { } while (0)
+#define CPROF_ARGS
+#define CPROF_PASS
+#endif
+
+// Panels of 32 columns (the former default; HELM_FACTOR_PANEL=32 keeps it for A/B): the pivot inverse is warp_gj8,
+// one 256-thread barrier per pivot.
+__device__ void gj_blocked(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
 {
     const int ld = lds_of(m);
     z2* S = sm.S;
-    z2* Dk = sm.Dk;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x, nw = blockDim.x >> 5, w = tid >> 5, mt = (m + 7) / 8;
+    const z2* Dk = sm.Dk[0];
     for (int kb = 0; kb < m; kb += GB) {
         const int kw = min(GB, m - kb);
-        if (tid < GJW * 32) {
-            for (int e = tid; e < kw * kw; e += GJW * 32) {
-                const int r = e / kw, c = e - r * kw;
-                Dk[r * DLD + c] = S[(kb + r) * ld + kb + c];
-            }
-            gj_bar();
-            warp_gj8(Dk, Dk + GB * DLD, kw, kb, bad_row);
+        if (tid < GJW * 32) pivot_inverse(S, ld, sm.Dk[0], sm.rowbuf, kb, kw, bad_row);
+        __syncthreads();
+        CPROF(1);
+        // ---- row panel: S[K, j] = Dk S[K, j] (j not in K), one warp per 8-column strip
+        for (int strip = w; strip < mt; strip += nw) {
+            const int j0 = strip * 8;
+            if (j0 >= kb && j0 < kb + kw) continue;
+            row_strip(S, ld, m, kb, kw, Dk, j0);
         }
         __syncthreads();
-        // ---- row panel: S[K, j] = Dk S[K, j] (j not in K) on the tensor cores.  One warp owns an 8-column strip:
-        //      it loads the strip's old 32 x 8 block as B fragments first, then writes its four 8 x 8 row tiles, so
-        //      the update is in place without a second barrier
-        {
-            const int mt = (m + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
-            for (int strip = tid >> 5; strip < mt; strip += nt >> 5) {
-                const int j0 = strip * 8, col = j0 + g;
-                if (j0 >= kb && j0 < kb + kw) continue;
-                z2 bf[GB / 4];
-#pragma unroll
-                for (int s4 = 0; s4 < GB / 4; s4++) {
-                    const int q = 4 * s4 + t;
-                    bf[s4] = (q < kw && col < m) ? S[(kb + q) * ld + col] : zmk(0, 0);
-                }
-#pragma unroll
-                for (int rt = 0; rt < GB / 8; rt++) {
-                    if (8 * rt >= kw) break;
-                    z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
-#pragma unroll
-                    for (int s4 = 0; s4 < GB / 4; s4++) {
-                        if (4 * s4 >= kw) break;
-                        const int r = 8 * rt + g, q = 4 * s4 + t;
-                        const z2 a = (r < kw && q < kw) ? Dk[r * DLD + q] : zmk(0, 0);
-                        dmma(c0.x, c1.x, a.x, bf[s4].x);    // C += A B
-                        dmma(c0.x, c1.x, -a.y, bf[s4].y);
-                        dmma(c0.y, c1.y, a.x, bf[s4].y);
-                        dmma(c0.y, c1.y, a.y, bf[s4].x);
-                    }
-                    const int r = 8 * rt + g, cA = j0 + 2 * t;
-                    if (r < kw && cA < m) S[(kb + r) * ld + cA] = c0;
-                    if (r < kw && cA + 1 < m) S[(kb + r) * ld + cA + 1] = c1;
-                }
-            }
-            __syncthreads();
+        CPROF(2);
+        // ---- trailing update S[i,j] -= S[i,K] S[K,j]: tiles aligned to the 32-column panels, so the panel's rows
+        //      and columns are skipped as whole tiles
+        for (int tile = w; tile < mt * mt; tile += nw) {
+            const int i0 = (tile / mt) * 8, j0 = (tile % mt) * 8;
+            if ((i0 >= kb && i0 < kb + kw) || (j0 >= kb && j0 < kb + kw)) continue;
+            trail_tile(S, ld, m, kb, kw, i0, j0);
         }
-        // ---- trailing update S[i,j] -= S[i,K] S[K,j] on the FP64 tensor cores: one warp per 8 x 8 tile; tiles are
-        //      aligned to the 32-column panels, so the panel's rows and columns are skipped as whole tiles
+        __syncthreads();
+        CPROF(4);
+        // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K), one warp per 8-row strip; S[K, K] = Dk
+        for (int strip = w; strip < mt; strip += nw) {
+            const int i0 = strip * 8;
+            if (i0 >= kb && i0 < kb + kw) continue;
+            col_strip(S, ld, m, kb, kw, Dk, i0);
+        }
+        for (int e = tid; e < kw * kw; e += blockDim.x) {
+            const int r = e / kw, c = e - r * kw;
+            S[sx(kb + r, kb + c, ld)] = Dk[r * DLD + c];
+        }
+        __syncthreads();
+        CPROF(5);
+    }
+}
+
+// Panels of 8 columns (P8): the same blocked Gauss-Jordan with GB = 8.  The pivot inverse is the serial part of any
+// blocked Gauss-Jordan (m pivots per block); with 8-wide panels it runs in ONE warp's registers (inv8_regs: no
+// barrier per pivot), and warp 0 forms the NEXT panel's pivot tile (its trailing update, in the accumulator layout
+// inv8_regs takes) and inverts it while warps 1.. finish the trailing update: three CTA barriers per 8 pivots instead
+// of one 256-thread barrier per pivot.  The DMMA work (row panel, trailing update, column panel) is the same m^3.
+__device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
+{
+    const int ld = lds_of(m);
+    z2* S = sm.S;
+    const int tid = threadIdx.x, nw = blockDim.x >> 5, w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int mt = (m + 7) / 8;
+    int cur = 0;
+    if (w == 0) {   // P_0 = S[0:8, 0:8]^-1
+        const int w8 = min(8, m);
+        z2 x0 = (g < w8 && 2 * t < w8) ? S[sx(g, 2 * t, ld)] : zmk(g == 2 * t ? 1.0 : 0.0, 0.0);
+        z2 x1 = (g < w8 && 2 * t + 1 < w8) ? S[sx(g, 2 * t + 1, ld)] : zmk(g == 2 * t + 1 ? 1.0 : 0.0, 0.0);
+        inv8_regs(x0, x1, w8, 0, bad_row);
+        sm.Dk[0][g * DLD + 2 * t] = x0;
+        sm.Dk[0][g * DLD + 2 * t + 1] = x1;
+    }
+    __syncthreads();
+    CPROF(1);
+    for (int kb = 0; kb < m; kb += 8) {
+        const int kw = min(8, m - kb);
+        const z2* Dk = cur ? sm.Dk[1] : sm.Dk[0];
+        // ---- row panel: S[K, j] = Dk S[K, j] (j not in K), one 8 x 8 tile per warp
+        for (int strip = w; strip < mt; strip += nw)
+            if (strip * 8 != kb) row_strip(S, ld, m, kb, kw, Dk, strip * 8);
+        __syncthreads();
+        CPROF(2);
+        // ---- trailing update; warp 0 first forms and inverts the next pivot tile
+        const int nk = kb + 8;
+        if (w == 0 && nk < m) {
+            const int w8 = min(8, m - nk);
+            z2 c0 = (g < w8 && 2 * t < w8) ? S[sx(nk + g, nk + 2 * t, ld)] : zmk(0, 0);
+            z2 c1 = (g < w8 && 2 * t + 1 < w8) ? S[sx(nk + g, nk + 2 * t + 1, ld)] : zmk(0, 0);
+            ztile_fms(
+                c0, c1, kw, [&](int rr, int q) { return nk + rr < m ? S[sx(nk + rr, kb + q, ld)] : zmk(0, 0); },
+                [&](int q, int cc) { return nk + cc < m ? S[sx(kb + q, nk + cc, ld)] : zmk(0, 0); });
+            if (!(g < w8 && 2 * t < w8)) c0 = zmk(g == 2 * t ? 1.0 : 0.0, 0.0);          // identity padding
+            if (!(g < w8 && 2 * t + 1 < w8)) c1 = zmk(g == 2 * t + 1 ? 1.0 : 0.0, 0.0);
+            inv8_regs(c0, c1, w8, nk, bad_row);
+            z2* Dn = cur ? sm.Dk[0] : sm.Dk[1];
+            Dn[g * DLD + 2 * t] = c0;
+            Dn[g * DLD + 2 * t + 1] = c1;
+        }
         {
-            const int mt = (m + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
-            for (int tile = tid >> 5; tile < mt * mt; tile += nt >> 5) {
+            const int w0 = nk < m ? 1 : 0;   // warp 0 is busy with the next pivot
+            for (int tile = w - w0; tile < mt * mt; tile += nw - w0) {
+                if (tile < 0) break;
                 const int i0 = (tile / mt) * 8, j0 = (tile % mt) * 8;
-                if ((i0 >= kb && i0 < kb + kw) || (j0 >= kb && j0 < kb + kw)) continue;
-                const int r = i0 + g, cA = j0 + 2 * t, cB = cA + 1;
-                z2 c0 = (r < m && cA < m) ? S[r * ld + cA] : zmk(0, 0);
-                z2 c1 = (r < m && cB < m) ? S[r * ld + cB] : zmk(0, 0);
-                ztile_fms(
-                    c0, c1, kw,
-                    [&](int rr, int q) { return i0 + rr < m ? S[(i0 + rr) * ld + kb + q] : zmk(0, 0); },
-                    [&](int q, int cc) { return j0 + cc < m ? S[(kb + q) * ld + j0 + cc] : zmk(0, 0); });
-                if (r < m && cA < m) S[r * ld + cA] = c0;
-                if (r < m && cB < m) S[r * ld + cB] = c1;
+                if (i0 == kb || j0 == kb || (i0 == nk && j0 == nk)) continue;
+                trail_tile(S, ld, m, kb, kw, i0, j0);
             }
         }
         __syncthreads();
-        // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K) on the tensor cores, one warp per 8-row strip (its old
-        //      8 x 32 block loaded as A fragments before it writes); S[K, K] = Dk
-        {
-            const int mt = (m + 7) / 8, lane = tid & 31, g = lane >> 2, t = lane & 3;
-            for (int strip = tid >> 5; strip < mt; strip += nt >> 5) {
-                const int i0 = strip * 8, row = i0 + g;
-                if (i0 >= kb && i0 < kb + kw) continue;
-                z2 af[GB / 4];
-#pragma unroll
-                for (int s4 = 0; s4 < GB / 4; s4++) {
-                    const int q = 4 * s4 + t;
-                    af[s4] = (q < kw && row < m) ? S[row * ld + kb + q] : zmk(0, 0);
-                }
-#pragma unroll
-                for (int ct = 0; ct < GB / 8; ct++) {
-                    if (8 * ct >= kw) break;
-                    z2 c0 = zmk(0, 0), c1 = zmk(0, 0);
-#pragma unroll
-                    for (int s4 = 0; s4 < GB / 4; s4++) {
-                        if (4 * s4 >= kw) break;
-                        const int q = 4 * s4 + t, c = 8 * ct + g;
-                        const z2 b = (q < kw && c < kw) ? Dk[q * DLD + c] : zmk(0, 0);
-                        dmma(c0.x, c1.x, -af[s4].x, b.x);   // C -= A B
-                        dmma(c0.x, c1.x, af[s4].y, b.y);
-                        dmma(c0.y, c1.y, -af[s4].x, b.y);
-                        dmma(c0.y, c1.y, -af[s4].y, b.x);
-                    }
-                    const int cA = 8 * ct + 2 * t;
-                    if (row < m && cA < kw) S[row * ld + kb + cA] = c0;
-                    if (row < m && cA + 1 < kw) S[row * ld + kb + cA + 1] = c1;
-                }
-            }
-            for (int e = tid; e < kw * kw; e += nt) {
-                const int r = e / kw, c = e - r * kw;
-                S[(kb + r) * ld + kb + c] = Dk[r * DLD + c];
-            }
-            __syncthreads();
+        CPROF(4);
+        // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K); S[K, K] = Dk
+        for (int strip = w; strip < mt; strip += nw)
+            if (strip * 8 != kb) col_strip(S, ld, m, kb, kw, Dk, strip * 8);
+        if (tid < 64) {
+            const int r = tid >> 3, c = tid & 7;
+            if (r < kw && c < kw) S[sx(kb + r, kb + c, ld)] = Dk[r * DLD + c];
         }
+        __syncthreads();
+        CPROF(5);
+        cur ^= 1;
     }
 }
 
@@ -388,16 +521,20 @@ __device__ void store_block(const SubDesc& d, int i, FactorSmem sm, z2* __restri
     z2* out = dinv + d.fac_off + (long long)i * m * m;
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
         const int c = e / m, r = e % m;   // column-major: coalesced stores
-        out[e] = sm.S[r * ld + c];
+        out[e] = sm.S[sx(r, c, ld)];
     }
     __syncthreads();
 }
 
+// S, then Dk[0] (GB x DLD: the 32-wide path's pivot inverse; the 8-wide path uses its first 8 rows), Dk[1] (8 x DLD:
+// the 8-wide path's next pivot inverse), the pivot-row buffer (2 x GB)
 __device__ FactorSmem carve(unsigned char* base, int m)
 {
     FactorSmem sm;
     sm.S = reinterpret_cast<z2*>(base);
-    sm.Dk = sm.S + (size_t)m * lds_of(m);
+    sm.Dk[0] = sm.S + (size_t)m * lds_of(m);
+    sm.Dk[1] = sm.Dk[0] + GB * DLD;
+    sm.rowbuf = sm.Dk[1] + 8 * DLD;
     return sm;
 }
 
@@ -411,6 +548,7 @@ __device__ void report(int* err, int bad_row, int sub, int block)
 }
 
 // blockIdx.x = 2 * sub + chain (0 bottom: i = 0 .. tw-1, 1 top: i = nb-1 .. tw+1)
+template <bool P8>
 __global__ void __launch_bounds__(FT) k_factor_chains(const SubDesc* __restrict__ desc, const z2* __restrict__ stc,
                                                       z2* __restrict__ dinv, int* err)
 {
@@ -421,23 +559,34 @@ __global__ void __launch_bounds__(FT) k_factor_chains(const SubDesc* __restrict_
     __shared__ int bad;
     if (threadIdx.x == 0) bad = -1;
     __syncthreads();
-    if (chain == 0) {
-        for (int i = 0; i < d.tw; i++) {
-            build_block(d, i, 0, stc, dinv, sm);
-            gj_blocked(d.m, sm, &bad);
-            store_block(d, i, sm, dinv);
-            report(err, bad, sub, i);
-        }
-    } else {
-        for (int i = d.nb - 1; i > d.tw; i--) {
-            build_block(d, i, 1, stc, dinv, sm);
-            gj_blocked(d.m, sm, &bad);
-            store_block(d, i, sm, dinv);
-            report(err, bad, sub, i);
-        }
+#ifdef HELM_FACTOR_PROF
+    // development aid (-DHELM_FACTOR_PROF): clock64 cycles per phase as thread 0 sees them (waits included), printed
+    // by CTA 0: build, pivot inverse (alone), row panel, -, trailing (+ the 8-wide path's next pivot inverse), column
+    // panel, store
+    long long prl[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tnow = clock64();
+    long long* cpr = threadIdx.x == 0 ? prl : nullptr;
+    long long* ctp = &tnow;
+#endif
+    const int i0 = chain == 0 ? 0 : d.nb - 1, i1 = chain == 0 ? d.tw : d.tw, step = chain == 0 ? 1 : -1;
+    for (int i = i0; i != i1; i += step) {
+        build_block(d, i, chain, stc, dinv, sm);
+        CPROF(0);
+        if (P8)
+            gj_panels8(d.m, sm, &bad CPROF_PASS);
+        else
+            gj_blocked(d.m, sm, &bad CPROF_PASS);
+        store_block(d, i, sm, dinv);
+        CPROF(6);
+        report(err, bad, sub, i);
     }
+#ifdef HELM_FACTOR_PROF
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        printf("CPROF m %d blocks %d build %lld pinv %lld row %lld nextpiv %lld trail %lld col %lld store %lld\n", d.m,
+               d.tw, prl[0], prl[1], prl[2], prl[3], prl[4], prl[5], prl[6]);
+#endif
 }
 
+template <bool P8>
 __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__ desc, const z2* __restrict__ stc,
                                                      z2* __restrict__ dinv, int* err)
 {
@@ -449,7 +598,14 @@ __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__
     if (threadIdx.x == 0) bad = -1;
     __syncthreads();
     build_block(d, d.tw, 2, stc, dinv, sm);
-    gj_blocked(d.m, sm, &bad);
+#ifdef HELM_FACTOR_PROF
+    long long* cpr = nullptr;
+    long long* ctp = nullptr;
+#endif
+    if (P8)
+        gj_panels8(d.m, sm, &bad CPROF_PASS);
+    else
+        gj_blocked(d.m, sm, &bad CPROF_PASS);
     store_block(d, d.tw, sm, dinv);
     report(err, bad, sub, d.tw);
 }
@@ -696,7 +852,14 @@ int big_smem_bytes(int m_max, int bc) { return (int)sizeof(z2) * (GB * DLD + GB 
 
 int factor_smem_bytes(int m_max)
 {
-    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + GB * DLD + 2 * GB));   // S, Dk, pivot-row buffer
+    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + GB * DLD + 8 * DLD + 2 * GB));
+}
+
+// 8-wide panels with the register-resident pivot inverse (gj_panels8) unless HELM_FACTOR_PANEL=32
+bool factor_panels8()
+{
+    const char* e = getenv("HELM_FACTOR_PANEL");
+    return !(e && atoi(e) == 32);
 }
 
 void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, int m_max, const z2* stencil, z2* dinv,
@@ -750,8 +913,78 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
         return;
     }
     const int smem = factor_smem_bytes(m_max);
-    cudaFuncSetAttribute(k_factor_chains, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_factor_twist, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_factor_chains<<<2 * nsub, FT, smem, s>>>(d_desc, stencil, dinv, d_err);
-    k_factor_twist<<<nsub, FT, smem, s>>>(d_desc, stencil, dinv, d_err);
+    auto go = [&](auto kc, auto kt) {
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kc<<<2 * nsub, FT, smem, s>>>(d_desc, stencil, dinv, d_err);
+        kt<<<nsub, FT, smem, s>>>(d_desc, stencil, dinv, d_err);
+    };
+    if (factor_panels8())
+        go(k_factor_chains<true>, k_factor_twist<true>);
+    else
+        go(k_factor_chains<false>, k_factor_twist<false>);
+}
+
+// ------------------------------------------------------------------------------------------------------------------
+// Measurement aid: FP64 peak of this GPU (the factorisation's roofline denominator; MEASURED_PEAKS.json holds only
+// HBM and bf16).  mode 0: DMMA (mma.sync m8n8k4 f64, 8 independent accumulator tiles per warp); mode 1: DFMA
+// (8 independent FMA chains per thread).  Grid = SMs x 4 CTAs of 256 threads, `iters` loop trips, timed with events.
+// ------------------------------------------------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(256) k_fp64_probe(int mode, int iters, double* sink)
+{
+    const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * blockIdx.x;
+    double c[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) c[q] = 1e-3 * q;
+    if (mode == 0) {
+        for (int it = 0; it < iters; it++) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) dmma(c[2 * q], c[2 * q + 1], a, b);
+        }
+    } else {
+        for (int it = 0; it < iters; it++) {
+#pragma unroll
+            for (int q = 0; q < 16; q++) c[q] = fma(a, c[q], b);
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int q = 0; q < 16; q++) s += c[q];
+    if (s == 1234.5678) *sink = s;   // keeps the chains live
+}
+}  // namespace
+
+extern "C" int helm_probe_fp64_tflops(int mode, double* tflops)
+{
+    if (!tflops || mode < 0 || mode > 1) return HELM_EINVAL;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    double* sink = nullptr;
+    if (cudaMalloc(&sink, sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return HELM_ENOMEM;
+    }
+    const int grid = 4 * nsm, block = 256, iters = mode == 0 ? 4096 : 8192;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fp64_probe<<<grid, block>>>(mode, iters / 8, sink);   // warm-up
+    cudaEventRecord(e0);
+    k_fp64_probe<<<grid, block>>>(mode, iters, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (err != cudaSuccess) return HELM_ECUDA;
+    // DMMA: 8 tiles x 8x8x4 MACs per warp per trip; DFMA: 16 FMAs per thread per trip
+    const double flops = mode == 0 ? 2.0 * 8 * 256 * (double)iters * (grid * block / 32)
+                                   : 2.0 * 16 * (double)iters * grid * block;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return HELM_OK;
 }

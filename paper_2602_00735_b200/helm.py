@@ -81,7 +81,7 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
            "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
            "helm_probe_read_bandwidth_mode", "helm_set_orthogonalisation",
-           "helm_get_krylov_basis", "helm_comm_info"]
+           "helm_get_krylov_basis", "helm_comm_info", "helm_probe_fp64_tflops"]
 
 
 def lib_path() -> str:
@@ -122,6 +122,7 @@ def load(build_if_missing: bool = True):
     L.helm_richardson.argtypes = [vp, vp, vp, d, i, C.POINTER(RichardsonInfo)]
     L.helm_probe_read_bandwidth.argtypes = [C.c_longlong, i, C.POINTER(d)]
     L.helm_probe_read_bandwidth_mode.argtypes = [C.c_longlong, i, i, C.POINTER(d)]
+    L.helm_probe_fp64_tflops.argtypes = [i, C.POINTER(d)]
     L.helm_comm_info.argtypes = [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
@@ -197,6 +198,16 @@ def probe_read_bandwidth(nbytes: int = 8 << 30, reps: int = 5, mode: int = 0) ->
     rc = L.helm_probe_read_bandwidth_mode(int(nbytes), int(reps), int(mode), C.byref(g))
     if rc != 0:
         raise HelmError(rc, "helm_probe_read_bandwidth")
+    return g.value
+
+
+def probe_fp64_tflops(mode: int = 0) -> float:
+    """Measured FP64 TFLOP/s of this GPU: mode 0 tensor-core DMMA, mode 1 DFMA (roofline context for the factorisation)."""
+    L = load()
+    g = C.c_double()
+    rc = L.helm_probe_fp64_tflops(int(mode), C.byref(g))
+    if rc != 0:
+        raise HelmError(rc, "helm_probe_fp64_tflops")
     return g.value
 
 

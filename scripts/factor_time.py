@@ -1,0 +1,31 @@
+"""Factorisation time (CUDA events around helm_factor, best of 3 contexts) per config; HELM_FACTOR_LOOKAHEAD=0/1
+selects the pivot-inverse lookahead.  python scripts/factor_time.py c2 c3"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2602_00735_b200 import Context  # noqa: E402
+from paper_2602_00735_b200.workloads import CONFIGS  # noqa: E402
+
+for name in sys.argv[1:] or ["c3"]:
+    c = CONFIGS[name]
+    for look, panel in (("1", "8"), ("0", "32")):
+        os.environ["HELM_FACTOR_LOOKAHEAD"] = look
+        os.environ["HELM_FACTOR_PANEL"] = panel
+        best = None
+        for _ in range(3):
+            ctx = Context(c.k, c.nsub, c.nsub)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            ctx.factor()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None else min(best, t)
+            ctx.close()
+            del ctx
+            torch.cuda.empty_cache()
+        print(f"{name} panel={panel} lookahead={look} factor {best:.4f} s", flush=True)

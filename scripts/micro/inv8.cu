@@ -1,0 +1,94 @@
+// Latency of the register-resident 8x8 complex Gauss-Jordan inverse (one warp), variants:
+//   0: pivot row scaled by 1/p then broadcast (factor.cu inv8_regs)
+//   1: unscaled pivot row broadcast, multiplier l = D[r][p] / p per row
+//   2: as 1 with rcp.approx.ftz.f64 + two Newton steps for 1/|p|^2
+#include <cstdio>
+typedef double2 z2;
+__device__ __forceinline__ z2 zmk(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ z2 zmul(z2 a, z2 b) { return zmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ void zfms(z2& acc, z2 a, z2 b)
+{
+    acc.x = fma(-a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(-a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ z2 shfl_z(z2 v, int src) { return zmk(__shfl_sync(~0u, v.x, src), __shfl_sync(~0u, v.y, src)); }
+__device__ __forceinline__ double rcp_fast(double d)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0); r = fma(r, e, r);
+    e = fma(-d, r, 1.0); r = fma(r, e, r);
+    return r;
+}
+template <int V>
+__device__ __forceinline__ void inv8(z2& x0, z2& x1)
+{
+    const int lane = threadIdx.x & 31, r = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        const z2 mine = (p & 1) ? x1 : x0;
+        const z2 pv = shfl_z(mine, 4 * p + (p >> 1));
+        const z2 f = shfl_z(mine, (lane & ~3) + (p >> 1));
+        const double n2 = pv.x * pv.x + pv.y * pv.y;
+        const double rd = V == 2 ? rcp_fast(n2) : 1.0 / n2;
+        const z2 inv = zmk(pv.x * rd, -pv.y * rd);
+        if (V == 0) {
+            const z2 s0 = c0 == p ? inv : zmul(x0, inv), s1 = c1 == p ? inv : zmul(x1, inv);
+            const z2 y0 = shfl_z(s0, 4 * p + t), y1 = shfl_z(s1, 4 * p + t);
+            if (r == p) { x0 = s0; x1 = s1; }
+            else {
+                const z2 b0 = c0 == p ? inv : y0, b1 = c1 == p ? inv : y1;
+                if (c0 == p) x0 = zmk(0, 0);
+                if (c1 == p) x1 = zmk(0, 0);
+                zfms(x0, f, b0); zfms(x1, f, b1);
+            }
+        } else {
+            const z2 y0 = shfl_z(x0, 4 * p + t), y1 = shfl_z(x1, 4 * p + t);   // unscaled pivot row
+            const z2 l = zmul(f, inv);                                         // D[r][p] / pivot
+            if (r == p) {
+                x0 = c0 == p ? inv : zmul(x0, inv);
+                x1 = c1 == p ? inv : zmul(x1, inv);
+            } else {
+                if (c0 == p) { x0 = zmk(-l.x, -l.y); } else zfms(x0, l, y0);
+                if (c1 == p) { x1 = zmk(-l.x, -l.y); } else zfms(x1, l, y1);
+            }
+        }
+    }
+}
+template <int V>
+__global__ void k(z2* io, long long* cyc, int reps)
+{
+    const int lane = threadIdx.x, r = lane >> 2, t = lane & 3;
+    z2 a0 = io[r * 8 + 2 * t], a1 = io[r * 8 + 2 * t + 1];
+    z2 x0 = a0, x1 = a1;
+    long long t0 = clock64();
+    for (int i = 0; i < reps; i++) {
+        x0 = a0; x1 = a1;
+        x0.x += 1e-300 * i;
+        inv8<V>(x0, x1);
+        a0.y += 1e-300 * x0.x;   // keep a dependency between reps
+    }
+    long long t1 = clock64();
+    if (lane == 0) cyc[V] = (t1 - t0) / reps;
+    io[64 * (V + 1) + r * 8 + 2 * t] = x0;
+    io[64 * (V + 1) + r * 8 + 2 * t + 1] = x1;
+}
+int main()
+{
+    z2* io;
+    long long* c;
+    cudaMallocManaged(&io, 64 * 4 * sizeof(z2));
+    cudaMallocManaged(&c, 4 * 8);
+    for (int i = 0; i < 64; i++) io[i] = make_double2((i % 9 == 0 ? 4.0 : 0.0) + 0.1 * ((i * 37) % 11) / 11.0, 0.05 * ((i * 13) % 7));
+    for (int it = 0; it < 2; it++) {
+        k<0><<<1, 32>>>(io, c, 1000); k<1><<<1, 32>>>(io, c, 1000); k<2><<<1, 32>>>(io, c, 1000);
+        cudaDeviceSynchronize();
+    }
+    double d1 = 0, d2 = 0;
+    for (int i = 0; i < 64; i++) {
+        d1 = fmax(d1, fabs(io[128 + i].x - io[64 + i].x) + fabs(io[128 + i].y - io[64 + i].y));
+        d2 = fmax(d2, fabs(io[192 + i].x - io[64 + i].x) + fabs(io[192 + i].y - io[64 + i].y));
+    }
+    printf("inv8 cycles: v0 %lld v1 %lld v2 %lld | max diff v1 %.2e v2 %.2e\n", c[0], c[1], c[2], d1, d2);
+    return 0;
+}
