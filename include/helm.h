@@ -184,6 +184,26 @@ typedef struct {
 int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rtol, int maxit,
                     helm_richardson_info* info);
 
+/* Practical improvement (i) of the paper (section 3): "the right-hand side of (local-ras-discrete) is
+ * nonzero only in overlapping regions, and thus the communication of the local residuals can be restricted to these
+ * regions".  With the owner partition of unity (the default, D10) helm_richardson restricts the residual of every step
+ * after the first to the interface band -- node indices s_p - 1, s_p of every interior block boundary, per axis; outside
+ * it the residual is rounding noise (pinned on the oracle) and is set to exactly 0 -- and on several ranks the apply's
+ * halo exchange carries only the band part of the ghost frame.  on = 1 (default with the owner PoU) / 0 (Algorithm 1
+ * with the full residual).  HELM_EINVAL for on = 1 with the ramp PoU (its residual fills the whole overlap). */
+int helm_set_residual_band(helm_ctx* ctx, int on);
+
+/* Complex elements sent / received and messages posted by this context's halo exchanges since the last reset
+ * (out3[0..2]); reset != 0 zeroes them after reading.  Host only. */
+int helm_comm_counters(helm_ctx* ctx, int reset, long long* out3);
+
+/* Host logic, no GPU: this rank's apply-frame halo volume in complex elements -- out4 = {sent full, sent band, received
+ * full, received band} (band = the section 3(i) restriction) -- and the band sub-rectangles (i0, i1, j0, j1 per
+ * rectangle, node indices, canonical packing order) of message `msg` of helm_halo_schedule(width 0), side 0 = its
+ * send rectangle, 1 = its receive rectangle; returns the rectangle count (at most cap written). */
+int helm_halo_band_counts(const helm_params* params, int rank, int nranks, long long* out4);
+int helm_halo_band_rects(const helm_params* params, int rank, int nranks, int msg, int side, int* out, int cap);
+
 /* Parity export: the global operator as S slot arrays [S][n_local], S = helm_layout.stencil_slots (slot order
  * centre, E, W, N, S, NE, SW, and for Q1 NW, SE; a slot pointing at a Dirichlet node is 0).  out_dev: S * n_local
  * values. */

@@ -231,6 +231,59 @@ int halo_schedule(const GridInfo& G, int width, helm_msg* out, int cap)
     return n;
 }
 
+// Section 3(i): "the right-hand side of eq. (local-ras-discrete) is nonzero only in overlapping regions, and
+// thus the communication of the local residuals can be restricted to these regions".  With the restricted owner write
+// the residual b - A u after a RAS step vanishes at every node whose stencil stays inside its own block (a_j = a there
+// and the local solve satisfied the equation), i.e. outside the interface band: node indices s_p - 1 and s_p of every
+// interior block boundary s_p, per axis (tests/test_oracle_richardson.py pins this on the oracle).
+std::vector<unsigned char> band_flags(const GridInfo& G, int ax)
+{
+    std::vector<unsigned char> f(G.N + 1, 0);
+    for (int p = 1; p < G.P[ax]; p++) {
+        const int b = G.st[ax][p];
+        if (b - 1 >= 0) f[b - 1] = 1;
+        if (b <= G.N) f[b] = 1;
+    }
+    return f;
+}
+
+// Canonical decomposition of the band nodes of the rectangle [i0,i1) x [j0,j1) into disjoint sub-rectangles: row
+// ranges in increasing j -- a run of band rows is one full-width rectangle, a run of other rows contributes its runs of
+// band columns in increasing i.  Sender and receiver of a message decompose the same global rectangle, so their packing
+// orders agree.
+void band_rects(const std::vector<unsigned char>& bx, const std::vector<unsigned char>& by, int i0, int i1, int j0,
+                int j1, std::vector<int4>& out)
+{
+    int j = j0;
+    while (j < j1) {
+        int je = j;
+        const unsigned char t = by[j];
+        while (je < j1 && by[je] == t) je++;
+        if (t) {
+            out.push_back(make_int4(i0, i1, j, je));
+        } else {
+            for (int i = i0; i < i1;) {
+                if (!bx[i]) {
+                    i++;
+                    continue;
+                }
+                int ie = i;
+                while (ie < i1 && bx[ie]) ie++;
+                out.push_back(make_int4(i, ie, j, je));
+                i = ie;
+            }
+        }
+        j = je;
+    }
+}
+
+long long rects_area(const std::vector<int4>& r)
+{
+    long long a = 0;
+    for (const int4& q : r) a += (long long)(q.y - q.x) * (q.w - q.z);
+    return a;
+}
+
 // In-process loopback transport (helm_setup_loopback): the ranks of a group are contexts in one process, each driven
 // by its own host thread and stream on the same device.  Halo messages and allreduces go through device-to-device
 // copies between the contexts' buffers, ordered by host barriers -- no kernel ever waits on another.  It executes the
@@ -312,6 +365,18 @@ struct helm_ctx {
 #ifdef HELM_HAVE_NCCL
     ncclComm_t comm = nullptr;
 #endif
+    // Section 3(i): band flags per node index, the band sub-rectangles of every apply-frame message (by schedule
+    // index), and element counters of the halo traffic (helm_comm_counters)
+    bool res_band = false;     // Richardson restricts its residual to the interface band (owner PoU only)
+    bool band_xchg = false;    // the current apply exchanges only the band part of its ghost frame
+    unsigned char *d_bandx = nullptr, *d_bandy = nullptr;
+    struct BandMsg {
+        int4* d_rects = nullptr;
+        long long* d_off = nullptr;
+        int n = 0;
+        long long total = 0, max_area = 0;
+    } band_send[4], band_recv[4];
+    long long xc_sent = 0, xc_recv = 0, xc_msgs = 0;
 
     // Krylov workspace
     z2* d_V = nullptr;
@@ -624,7 +689,7 @@ int need_comm(helm_ctx* ctx)
 // loopback: after the phase's messages are packed, copy each peer's send buffer addressed to this rank into the
 // matching receive buffer (the peer's message index is recomputed from its own schedule)
 int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const int* idx, int k, bool reverse,
-                  cudaStream_t st)
+                  bool band, cudaStream_t st)
 {
     LoopGroup* L = ctx->loop;
     CK(cudaStreamSynchronize(st));
@@ -646,10 +711,14 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
         if (found < 0) return set_err(ctx, HELM_ENCCL, "loopback: rank %d has no message for rank %d", m.peer, ctx->rank);
         // forward: the peer packed its send rectangle into my receive rectangle; reverse: its receive rectangle (its
         // ghost frame toward me) onto my send rectangle (my owned strip)
-        const size_t rcnt = reverse ? (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0)
-                                    : (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
-        const size_t scnt = reverse ? (size_t)(pm[fq].recv_i1 - pm[fq].recv_i0) * (pm[fq].recv_j1 - pm[fq].recv_j0)
-                                    : (size_t)(pm[fq].send_i1 - pm[fq].send_i0) * (pm[fq].send_j1 - pm[fq].send_j0);
+        size_t rcnt = reverse ? (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0)
+                              : (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+        size_t scnt = reverse ? (size_t)(pm[fq].recv_i1 - pm[fq].recv_i0) * (pm[fq].recv_j1 - pm[fq].recv_j0)
+                              : (size_t)(pm[fq].send_i1 - pm[fq].send_i0) * (pm[fq].send_j1 - pm[fq].send_j0);
+        if (band) {   // band parts only (section 3(i)): my decomposition of the receive rectangle, the peer's of its send
+            rcnt = (size_t)ctx->band_recv[idx[a]].total;
+            scnt = (size_t)peer->band_send[fq].total;
+        }
         if (scnt != rcnt) return set_err(ctx, HELM_ENCCL, "loopback: message size mismatch %zu vs %zu", scnt, rcnt);
         CK(cudaMemcpyAsync(ctx->d_recvbuf[a], peer->d_sendbuf[found], sizeof(z2) * rcnt, cudaMemcpyDeviceToDevice,
                            st));
@@ -669,33 +738,46 @@ int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse, cudaStream_t st)
     helm_msg msgs[4];
     const int nm = halo_schedule(ctx->G, W, msgs, 4);
     const GridInfo& G = ctx->G;
+    // section 3(i): only the interface-band part of the apply frame (the caller zeroed the rest of the frame)
+    const bool band = ctx->band_xchg && W == 0 && !reverse;
     for (int ph = 0; ph < 2; ph++) {
         const int phase = reverse ? 1 - ph : ph;
         int idx[4], k = 0;
         for (int q = 0; q < nm; q++)
             if (msgs[q].phase == phase) idx[k++] = q;
         if (!k && !ctx->loop) continue;   // (loopback ranks meet at every phase's barriers)
+        size_t scnt[4], rcnt[4];
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
-            const int i0 = reverse ? m.recv_i0 : m.send_i0, i1 = reverse ? m.recv_i1 : m.send_i1;
-            const int j0 = reverse ? m.recv_j0 : m.send_j0, j1 = reverse ? m.recv_j1 : m.send_j1;
-            launch_copy_rect(buf, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], i0, j0, i1 - i0, i0, i1, j0, j1,
-                             st);
+            const size_t sa = (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
+            const size_t ra = (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+            scnt[a] = band ? (size_t)ctx->band_send[idx[a]].total : (reverse ? ra : sa);
+            rcnt[a] = band ? (size_t)ctx->band_recv[idx[a]].total : (reverse ? sa : ra);
+            if (band) {
+                const auto& bm = ctx->band_send[idx[a]];
+                launch_pack_rects(buf, G.e_i0, G.e_j0, ctx->ext_stride, bm.d_rects, bm.d_off, bm.n, bm.max_area,
+                                  ctx->d_sendbuf[a], false, st);
+            } else {
+                const int i0 = reverse ? m.recv_i0 : m.send_i0, i1 = reverse ? m.recv_i1 : m.send_i1;
+                const int j0 = reverse ? m.recv_j0 : m.send_j0, j1 = reverse ? m.recv_j1 : m.send_j1;
+                launch_copy_rect(buf, G.e_i0, G.e_j0, ctx->ext_stride, ctx->d_sendbuf[a], i0, j0, i1 - i0, i0, i1, j0,
+                                 j1, st);
+            }
             ctx->launches++;
+            ctx->xc_sent += (long long)scnt[a];
+            ctx->xc_recv += (long long)rcnt[a];
+            ctx->xc_msgs++;
         }
         if (ctx->loop) {
-            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k, reverse, st);
+            int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k, reverse, band, st);
             if (rc) return rc;
         } else {
 #ifdef HELM_HAVE_NCCL
             NK(ncclGroupStart());
             for (int a = 0; a < k; a++) {
                 const helm_msg& m = msgs[idx[a]];
-                const size_t sa = (size_t)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
-                const size_t ra = (size_t)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
-                const size_t scnt = 2 * (reverse ? ra : sa), rcnt = 2 * (reverse ? sa : ra);
-                NK(ncclSend(ctx->d_sendbuf[a], scnt, ncclDouble, m.peer, ctx->comm, st));
-                NK(ncclRecv(ctx->d_recvbuf[a], rcnt, ncclDouble, m.peer, ctx->comm, st));
+                NK(ncclSend(ctx->d_sendbuf[a], 2 * scnt[a], ncclDouble, m.peer, ctx->comm, st));
+                NK(ncclRecv(ctx->d_recvbuf[a], 2 * rcnt[a], ncclDouble, m.peer, ctx->comm, st));
             }
             NK(ncclGroupEnd());
 #else
@@ -704,10 +786,16 @@ int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse, cudaStream_t st)
         }
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
-            const int i0 = reverse ? m.send_i0 : m.recv_i0, i1 = reverse ? m.send_i1 : m.recv_i1;
-            const int j0 = reverse ? m.send_j0 : m.recv_j0, j1 = reverse ? m.send_j1 : m.recv_j1;
-            launch_copy_rect(ctx->d_recvbuf[a], i0, j0, i1 - i0, buf, G.e_i0, G.e_j0, ctx->ext_stride, i0, i1, j0, j1,
-                             st, reverse);
+            if (band) {
+                const auto& bm = ctx->band_recv[idx[a]];
+                launch_pack_rects(buf, G.e_i0, G.e_j0, ctx->ext_stride, bm.d_rects, bm.d_off, bm.n, bm.max_area,
+                                  ctx->d_recvbuf[a], true, st);
+            } else {
+                const int i0 = reverse ? m.send_i0 : m.recv_i0, i1 = reverse ? m.send_i1 : m.recv_i1;
+                const int j0 = reverse ? m.send_j0 : m.recv_j0, j1 = reverse ? m.send_j1 : m.recv_j1;
+                launch_copy_rect(ctx->d_recvbuf[a], i0, j0, i1 - i0, buf, G.e_i0, G.e_j0, ctx->ext_stride, i0, i1, j0,
+                                 j1, st, reverse);
+            }
             ctx->launches++;
         }
     }
@@ -749,6 +837,8 @@ int allreduce(helm_ctx* ctx, double* buf, size_t count)
 int fill_ext(helm_ctx* ctx, const z2* v, int W)
 {
     const GridInfo& G = ctx->G;
+    if (ctx->band_xchg && W == 0)   // the frame's non-band nodes are zero, not last exchange's values
+        CK(cudaMemsetAsync(ctx->d_ext, 0, sizeof(z2) * ctx->n_ext, ctx->stream));
     launch_copy_rect(v, G.i0, G.j0, G.i1 - G.i0, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, G.i0, G.i1, G.j0, G.j1,
                      ctx->stream);
     ctx->launches++;
@@ -851,6 +941,7 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
     if (ctx->overlap) {
         if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
         const GridInfo& G = ctx->G;
+        if (ctx->band_xchg) CK(cudaMemsetAsync(ctx->d_ext, 0, sizeof(z2) * ctx->n_ext, ctx->stream));
         launch_copy_rect(r, G.i0, G.j0, G.i1 - G.i0, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, G.i0, G.i1, G.j0,
                          G.j1, ctx->stream);
         CK(cudaEventRecord(ctx->ev_ov[0], ctx->stream));
@@ -1329,8 +1420,19 @@ int richardson_impl(helm_ctx* ctx, const z2* b, z2* x, double rtol, int maxit, h
     if ((rc = residual_host(ctx, b, x, ctx->d_r, &rn))) return rc;
     double rel = rn / beta0;
     int its = 0;
+    // section 3(i): after a RAS step the residual lives on the interface band; restrict it there exactly
+    // (the rest is rounding noise) and exchange only the band part of the apply's ghost frame
+    const bool band = ctx->res_band && ctx->p.pou == HELM_POU_OWNER;
     while (rel > rtol && its < maxit) {
-        if ((rc = apply_impl(ctx, ctx->d_r, ctx->d_z))) return rc;   // sum_j chi_j c_j
+        if (band && its > 0) {
+            const GridInfo& G = ctx->G;
+            launch_band_mask(ctx->d_r, G.i0, G.i1, G.j0, G.j1, ctx->d_bandx, ctx->d_bandy, ctx->stream);
+            ctx->launches++;
+            ctx->band_xchg = ctx->multi;
+        }
+        rc = apply_impl(ctx, ctx->d_r, ctx->d_z);   // sum_j chi_j c_j
+        ctx->band_xchg = false;
+        if (rc) return rc;
         launch_axpy(x, ctx->d_z, ctx->n_local, ctx->stream);
         ctx->launches++;
         its++;
@@ -1494,6 +1596,44 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
         for (int q = 0; q < 4; q++)
             if ((rc = dalloc(ctx, &ctx->d_sendbuf[q], ctx->msg_cap)) || (rc = dalloc(ctx, &ctx->d_recvbuf[q], ctx->msg_cap)))
                 return rc;
+    }
+    {
+        // section 3(i): band flags, and the band sub-rectangles of every apply-frame message (send and receive side)
+        const GridInfo& G = ctx->G;
+        const std::vector<unsigned char> bx = band_flags(G, 0), by = band_flags(G, 1);
+        if ((rc = dalloc(ctx, &ctx->d_bandx, G.N + 1)) || (rc = dalloc(ctx, &ctx->d_bandy, G.N + 1))) return rc;
+        CK(cudaMemcpyAsync(ctx->d_bandx, bx.data(), G.N + 1, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->d_bandy, by.data(), G.N + 1, cudaMemcpyHostToDevice, ctx->stream));
+        ctx->res_band = ctx->p.pou == HELM_POU_OWNER;
+        if (ctx->multi && ctx->has_comm) {
+            helm_msg msgs[4];
+            const int nm = halo_schedule(G, 0, msgs, 4);
+            for (int q = 0; q < nm; q++)
+                for (int side = 0; side < 2; side++) {
+                    const helm_msg& m = msgs[q];
+                    std::vector<int4> rects;
+                    if (side == 0) band_rects(bx, by, m.send_i0, m.send_i1, m.send_j0, m.send_j1, rects);
+                    else band_rects(bx, by, m.recv_i0, m.recv_i1, m.recv_j0, m.recv_j1, rects);
+                    auto& bm = side == 0 ? ctx->band_send[q] : ctx->band_recv[q];
+                    std::vector<long long> off(rects.size() + 1, 0);
+                    for (size_t r = 0; r < rects.size(); r++) {
+                        const long long a = (long long)(rects[r].y - rects[r].x) * (rects[r].w - rects[r].z);
+                        off[r + 1] = off[r] + a;
+                        bm.max_area = std::max(bm.max_area, a);
+                    }
+                    bm.n = (int)rects.size();
+                    bm.total = off.back();
+                    if (bm.n > 0) {
+                        if ((rc = dalloc(ctx, &bm.d_rects, bm.n)) || (rc = dalloc(ctx, &bm.d_off, bm.n + 1))) return rc;
+                        CK(cudaMemcpyAsync(bm.d_rects, rects.data(), sizeof(int4) * bm.n, cudaMemcpyHostToDevice,
+                                           ctx->stream));
+                        CK(cudaMemcpyAsync(bm.d_off, off.data(), sizeof(long long) * (bm.n + 1), cudaMemcpyHostToDevice,
+                                           ctx->stream));
+                    }
+                }
+            CK(cudaStreamSynchronize(ctx->stream));   // the host vectors die here
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     // processing order: most expensive first (static round-robin over persistent CTAs)
     std::vector<int> order(nsub);
@@ -1715,6 +1855,76 @@ int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* c
     if (comm_nranks) *comm_nranks = n;
     if (comm_rank) *comm_rank = r;
     return HELM_OK;
+}
+
+int helm_set_residual_band(helm_ctx* ctx, int on)
+{
+    if (!ctx || on < 0 || on > 1) return set_err(ctx, HELM_EINVAL, "helm_set_residual_band: on must be 0 or 1");
+    if (on && ctx->p.pou != HELM_POU_OWNER)
+        return set_err(ctx, HELM_EINVAL, "the residual band (section 3(i)) needs the owner partition of unity");
+    ctx->res_band = on == 1;
+    return HELM_OK;
+}
+
+int helm_comm_counters(helm_ctx* ctx, int reset, long long* out3)
+{
+    if (!ctx || !out3) return HELM_EINVAL;
+    out3[0] = ctx->xc_sent;
+    out3[1] = ctx->xc_recv;
+    out3[2] = ctx->xc_msgs;
+    if (reset) ctx->xc_sent = ctx->xc_recv = ctx->xc_msgs = 0;
+    return HELM_OK;
+}
+
+int helm_halo_band_counts(const helm_params* params, int rank, int nranks, long long* out4)
+{
+    if (!params || !out4) return HELM_EINVAL;
+    GridInfo G;
+    char err[256];
+    int rc = compute_grid(*params, rank, nranks, G, err, sizeof(err));
+    if (rc) return rc;
+    const std::vector<unsigned char> bx = band_flags(G, 0), by = band_flags(G, 1);
+    helm_msg msgs[4];
+    const int nm = halo_schedule(G, 0, msgs, 4);
+    long long sf = 0, sb = 0, rf = 0, rb = 0;
+    for (int q = 0; q < nm; q++) {
+        const helm_msg& m = msgs[q];
+        std::vector<int4> rs, rr;
+        band_rects(bx, by, m.send_i0, m.send_i1, m.send_j0, m.send_j1, rs);
+        band_rects(bx, by, m.recv_i0, m.recv_i1, m.recv_j0, m.recv_j1, rr);
+        sf += (long long)(m.send_i1 - m.send_i0) * (m.send_j1 - m.send_j0);
+        rf += (long long)(m.recv_i1 - m.recv_i0) * (m.recv_j1 - m.recv_j0);
+        sb += rects_area(rs);
+        rb += rects_area(rr);
+    }
+    out4[0] = sf;
+    out4[1] = sb;
+    out4[2] = rf;
+    out4[3] = rb;
+    return HELM_OK;
+}
+
+int helm_halo_band_rects(const helm_params* params, int rank, int nranks, int msg, int side, int* out, int cap)
+{
+    if (!params || msg < 0 || msg >= 4 || side < 0 || side > 1) return HELM_EINVAL;
+    GridInfo G;
+    char err[256];
+    int rc = compute_grid(*params, rank, nranks, G, err, sizeof(err));
+    if (rc) return rc;
+    helm_msg msgs[4];
+    const int nm = halo_schedule(G, 0, msgs, 4);
+    if (msg >= nm) return HELM_EINVAL;
+    const helm_msg& m = msgs[msg];
+    std::vector<int4> r;
+    if (side == 0) band_rects(band_flags(G, 0), band_flags(G, 1), m.send_i0, m.send_i1, m.send_j0, m.send_j1, r);
+    else band_rects(band_flags(G, 0), band_flags(G, 1), m.recv_i0, m.recv_i1, m.recv_j0, m.recv_j1, r);
+    for (int q = 0; q < (int)r.size() && q < cap; q++) {
+        out[4 * q] = r[q].x;
+        out[4 * q + 1] = r[q].y;
+        out[4 * q + 2] = r[q].z;
+        out[4 * q + 3] = r[q].w;
+    }
+    return (int)r.size();
 }
 
 int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
@@ -1974,7 +2184,13 @@ void helm_destroy(helm_ctx* ctx)
     for (int q = 0; q < 4; q++) {
         if (ctx->d_sendbuf[q]) cudaFree(ctx->d_sendbuf[q]);
         if (ctx->d_recvbuf[q]) cudaFree(ctx->d_recvbuf[q]);
+        for (auto* bm : {&ctx->band_send[q], &ctx->band_recv[q]}) {
+            if (bm->d_rects) cudaFree(bm->d_rects);
+            if (bm->d_off) cudaFree(bm->d_off);
+        }
     }
+    if (ctx->d_bandx) cudaFree(ctx->d_bandx);
+    if (ctx->d_bandy) cudaFree(ctx->d_bandy);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     if (ctx->phases)
         fprintf(stderr, "HELM_GMRES_PHASES ms: apply %.1f spmv %.1f multidot2 %.1f reduce+coef %.1f update %.1f "

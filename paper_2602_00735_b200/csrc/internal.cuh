@@ -165,6 +165,10 @@ void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const Stenci
 void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,
                       int i0, int i1, int j0, int j1, cudaStream_t s, bool add = false);
 void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t s);
+void launch_band_mask(z2* v, int i0, int i1, int j0, int j1, const unsigned char* bx, const unsigned char* by,
+                      cudaStream_t s);
+void launch_pack_rects(z2* ext, int e_i0, int e_j0, long long stride, const int4* rects, const long long* off,
+                       int nrects, long long max_area, z2* buf, bool unpack, cudaStream_t s);
 void launch_finish_norm(const double* sq, z2* out_slot, double* out_norm, cudaStream_t s);
 void launch_zadd(const z2* a, const z2* b, z2* out, int nv, cudaStream_t s);
 void launch_multidot(const z2* V, long long ldv, int nv, const z2* w, long long n, z2* partial, int nblk,

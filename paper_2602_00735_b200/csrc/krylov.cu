@@ -2,6 +2,8 @@
 // with fused norm, normalisation, basis combination.  All reductions are deterministic: a fixed row
 // partition per CTA, warp-shuffle trees inside a CTA, and a single-CTA pass over the CTA partials in
 // index order (D15).  No floating-point atomics.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace {
@@ -122,6 +124,39 @@ __global__ void __launch_bounds__(KT) k_copy_rect(const z2* __restrict__ src, in
         z2* d = dst + (i - di0) + dstride * (j - dj0);
         const z2 v = src[(i - si0) + sstride * (j - sj0)];
         *d = add ? zadd(*d, v) : v;
+    }
+}
+
+// Section 3(i): the interface band.  bx[i] / by[j] flag the node indices whose stencil crosses a block
+// boundary along that axis (i = s_p - 1, s_p).  k_band_mask zeroes every entry of the owned vector outside the band;
+// k_pack_rects moves the band part of a ghost-framed buffer through a contiguous message buffer, rectangle by
+// rectangle (a canonical decomposition of the message rectangle into band sub-rectangles, offsets = prefix areas).
+__global__ void __launch_bounds__(KT) k_band_mask(z2* __restrict__ v, int i0, int i1, int j0, int j1,
+                                                 const unsigned char* __restrict__ bx, const unsigned char* __restrict__ by)
+{
+    const int w = i1 - i0;
+    const long long n = (long long)w * (j1 - j0);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int i = i0 + (int)(e % w), j = j0 + (int)(e / w);
+        if (!bx[i] && !by[j]) v[e] = zmk(0, 0);
+    }
+}
+
+__global__ void __launch_bounds__(KT) k_pack_rects(z2* __restrict__ ext, int e_i0, int e_j0, long long stride,
+                                                  const int4* __restrict__ rects, const long long* __restrict__ off,
+                                                  z2* __restrict__ buf, int unpack)
+{
+    const int4 r = rects[blockIdx.y];
+    const int w = r.y - r.x;
+    const long long n = (long long)w * (r.w - r.z);
+    z2* b = buf + off[blockIdx.y];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int i = r.x + (int)(e % w), j = r.z + (int)(e / w);
+        z2* x = ext + (i - e_i0) + stride * (j - e_j0);
+        if (unpack)
+            *x = b[e];
+        else
+            b[e] = *x;
     }
 }
 
@@ -586,6 +621,20 @@ void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* ds
     const long long n = (long long)(i1 - i0) * (j1 - j0);
     if (n <= 0) return;
     k_copy_rect<<<ew_grid(n), KT, 0, s>>>(src, si0, sj0, sstride, dst, di0, dj0, dstride, i0, i1, j0, j1, add ? 1 : 0);
+}
+void launch_band_mask(z2* v, int i0, int i1, int j0, int j1, const unsigned char* bx, const unsigned char* by,
+                      cudaStream_t s)
+{
+    const long long n = (long long)(i1 - i0) * (j1 - j0);
+    if (n <= 0) return;
+    k_band_mask<<<ew_grid(n), KT, 0, s>>>(v, i0, i1, j0, j1, bx, by);
+}
+void launch_pack_rects(z2* ext, int e_i0, int e_j0, long long stride, const int4* rects, const long long* off,
+                       int nrects, long long max_area, z2* buf, bool unpack, cudaStream_t s)
+{
+    if (nrects <= 0 || max_area <= 0) return;
+    const int gx = (int)std::min<long long>((max_area + KT - 1) / KT, 64);
+    k_pack_rects<<<dim3(gx, nrects), KT, 0, s>>>(ext, e_i0, e_j0, stride, rects, off, buf, unpack ? 1 : 0);
 }
 void launch_reduce_sq(const double* partial, int nblk, double* sq, cudaStream_t s)
 {

@@ -81,7 +81,8 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_plan_rank", "helm_halo_schedule", "helm_nccl_unique_id", "helm_precond_apply_ext",
            "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
            "helm_probe_read_bandwidth_mode", "helm_set_orthogonalisation",
-           "helm_get_krylov_basis", "helm_comm_info", "helm_probe_fp64_tflops"]
+           "helm_get_krylov_basis", "helm_comm_info", "helm_probe_fp64_tflops", "helm_set_residual_band",
+           "helm_comm_counters", "helm_halo_band_counts", "helm_halo_band_rects"]
 
 
 def lib_path() -> str:
@@ -123,6 +124,10 @@ def load(build_if_missing: bool = True):
     L.helm_probe_read_bandwidth.argtypes = [C.c_longlong, i, C.POINTER(d)]
     L.helm_probe_read_bandwidth_mode.argtypes = [C.c_longlong, i, i, C.POINTER(d)]
     L.helm_probe_fp64_tflops.argtypes = [i, C.POINTER(d)]
+    L.helm_set_residual_band.argtypes = [vp, i]
+    L.helm_comm_counters.argtypes = [vp, i, C.POINTER(C.c_longlong)]
+    L.helm_halo_band_counts.argtypes = [C.POINTER(Params), i, i, C.POINTER(C.c_longlong)]
+    L.helm_halo_band_rects.argtypes = [C.POINTER(Params), i, i, i, i, C.POINTER(i), i]
     L.helm_comm_info.argtypes = [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
@@ -188,6 +193,27 @@ def halo_schedule(params: Params, rank: int, nranks: int, width: int) -> list:
     if n < 0:
         raise HelmError(n, "helm_halo_schedule")
     return [msgs[q].as_dict() for q in range(n)]
+
+
+def halo_band_counts(params: Params, rank: int, nranks: int) -> dict:
+    """This rank's apply-frame halo volume (complex elements): full and section 3(i) band, sent and received."""
+    L = load()
+    out = (C.c_longlong * 4)()
+    rc = L.helm_halo_band_counts(C.byref(params), rank, nranks, out)
+    if rc != 0:
+        raise HelmError(rc, "helm_halo_band_counts")
+    return {"sent_full": out[0], "sent_band": out[1], "recv_full": out[2], "recv_band": out[3]}
+
+
+def halo_band_rects(params: Params, rank: int, nranks: int, msg: int, side: int) -> list:
+    """Band sub-rectangles (i0, i1, j0, j1) of apply-frame message `msg` (side 0 send, 1 receive), packing order."""
+    L = load()
+    cap = 4096
+    buf = (C.c_int * (4 * cap))()
+    n = L.helm_halo_band_rects(C.byref(params), rank, nranks, msg, side, buf, cap)
+    if n < 0:
+        raise HelmError(n, "helm_halo_band_rects")
+    return [tuple(buf[4 * q:4 * q + 4]) for q in range(min(n, cap))]
 
 
 def probe_read_bandwidth(nbytes: int = 8 << 30, reps: int = 5, mode: int = 0) -> float:
@@ -368,6 +394,15 @@ class Context:
         out = torch.empty(ns * self.n, dtype=torch.complex128, device="cuda")
         self._check(self.L.helm_export_stencil(self._h, _ptr(out)))
         return out.view(ns, self.n)
+
+    def set_residual_band(self, on: bool):
+        """Section 3(i) residual restriction + band-only halo in helm_richardson (default on, owner PoU)."""
+        self._check(self.L.helm_set_residual_band(self._h, int(bool(on))))
+
+    def comm_counters(self, reset: bool = False) -> dict:
+        out = (C.c_longlong * 3)()
+        self._check(self.L.helm_comm_counters(self._h, int(bool(reset)), out))
+        return {"sent": out[0], "recv": out[1], "msgs": out[2]}
 
     TRANSPORTS = {0: "none", 1: "nccl", 2: "loopback", 3: "shard"}
 

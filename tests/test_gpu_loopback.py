@@ -322,3 +322,74 @@ def test_loopback_c3_full_size(gg):
         g = load_golden("c3")
         assert abs(outs[0]["its"] - g["iterations"]) <= 1
         assert sketch_rel(X.view(-1).cpu().numpy(), g) <= 1e-6
+
+
+@pytest.mark.parametrize("name,nranks,gg", [("c1", 4, (2, 2)), ("c2", 8, (4, 2))])
+def test_loopback_richardson_residual_band(name, nranks, gg):
+    """Section 3(i): Richardson restricting its residual to the interface band and exchanging only the band
+    part of the apply's ghost frame.  Exact counts: every apply after the first receives exactly the band area of the
+    ghost frame (helm_halo_band_counts), the first one the full frame, each residual the width-1 frame.  The solution
+    is bitwise the single-rank band run's, the iteration count the oracle's full-residual Algorithm 1's, x within 1e-8
+    of it; the full-frame run (band off) agrees to the same tolerance."""
+    from oracle.oracle import richardson as orc_rich
+    from paper_2602_00735_b200.helm import halo_band_counts, halo_schedule, make_params
+    cfg = CONFIGS[name]
+    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    ref = Context(**kw)
+    ref.factor()
+    nf = ref.layout.N_cells - 1
+    b = ref.rhs(*sources(cfg))
+    x1, i1, _ = ref.richardson(b, rtol=cfg.rtol, maxit=300)
+    ref.set_residual_band(False)
+    x1f, i1f, _ = ref.richardson(b, rtol=cfg.rtol, maxit=300)
+    ref.close()
+    B = b.view(nf, nf)
+    p = make_params(cfg.k, cfg.nsub, gpu_grid=gg)
+    gid = next(_gid)
+    torch.cuda.synchronize()
+
+    def rank(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c = Context(**kw, gpu_grid=gg, rank=r, nranks=nranks, stream=s, loopback_group=gid)
+            c.factor()
+            pl = c.plan
+            bl = owned(B, pl)
+            c.comm_counters(reset=True)
+            x, inf, _ = c.richardson(bl, rtol=cfg.rtol, maxit=300)
+            cnt = c.comm_counters(reset=True)
+            c.set_residual_band(False)
+            xf, inff, _ = c.richardson(bl, rtol=cfg.rtol, maxit=300)
+            cntf = c.comm_counters(reset=True)
+            s.synchronize()
+            out = dict(pl=pl, x=x.clone(), xf=xf.clone(), its=inf.iterations, itsf=inff.iterations, cnt=cnt,
+                       cntf=cntf)
+            c.close()
+            return out
+
+    outs = run_ranks(nranks, rank)
+    X = torch.full_like(B, complex("nan"))
+    XF = torch.full_like(B, complex("nan"))
+    for q, o in enumerate(outs):
+        pl = o["pl"]
+        sl = (slice(pl["owned_j0"] - 1, pl["owned_j1"] - 1), slice(pl["owned_i0"] - 1, pl["owned_i1"] - 1))
+        shape = (pl["owned_j1"] - pl["owned_j0"], pl["owned_i1"] - pl["owned_i0"])
+        X[sl], XF[sl] = o["x"].view(shape), o["xf"].view(shape)
+        its = o["its"]
+        hb = halo_band_counts(p, q, nranks)
+        w1 = sum((m["recv_i1"] - m["recv_i0"]) * (m["recv_j1"] - m["recv_j0"]) for m in halo_schedule(p, q, nranks, 1))
+        # norm(b) has no exchange; residuals: initial + one per step (width 1); applies: first full, then band
+        assert o["cnt"]["recv"] == hb["recv_full"] + (its - 1) * hb["recv_band"] + (its + 1) * w1, (q, o["cnt"], hb)
+        assert o["cntf"]["recv"] == o["itsf"] * hb["recv_full"] + (o["itsf"] + 1) * w1
+        assert hb["recv_band"] < hb["recv_full"]
+    assert len({o["its"] for o in outs}) == 1 and abs(outs[0]["its"] - i1.iterations) <= 1   # (norms summed in
+    if outs[0]["its"] == i1.iterations:                                                        # another order)
+        assert torch.equal(X.view(-1), x1)                 # bitwise the single-rank band run
+    rel = lambda a, c: float(torch.linalg.norm(a - c) / torch.linalg.norm(c))  # noqa: E731
+    assert rel(XF.view(-1), x1f) <= 1e-8 and rel(X.view(-1), XF.view(-1)) <= 1e-8
+    o = oracle_for(kw)
+    o.factor()
+    bn = b.cpu().numpy()
+    ro = orc_rich(o.matvec, o.apply, bn, rtol=cfg.rtol, maxit=300)
+    assert abs(outs[0]["its"] - ro.iterations) <= 1 and i1f.iterations == ro.iterations
+    assert np.linalg.norm(X.view(-1).cpu().numpy() - ro.x) <= 1e-8 * np.linalg.norm(ro.x)

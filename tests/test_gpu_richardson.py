@@ -102,3 +102,29 @@ def test_error_propagation_identity():
         got = xs - u
         assert float(torch.linalg.norm(got - e) / torch.linalg.norm(e)) <= 1e-10
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+def test_residual_band_single_rank(name):
+    """Section 3(i) on one rank: restricting the residual to the interface band after the first step
+    changes Algorithm 1 only at the rounding level (the residual outside the band is rounding noise): same iteration
+    count as the full residual and as the oracle, solutions within 1e-10 of each other and 1e-8 of the oracle's."""
+    from oracle.oracle import Oracle, richardson as orc_rich
+    from paper_2602_00735_b200 import Context
+    from paper_2602_00735_b200.workloads import CONFIGS, sources
+    cfg = CONFIGS[name]
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub)
+    ctx.factor()
+    b = ctx.rhs(*sources(cfg))
+    xb, ib, _ = ctx.richardson(b, rtol=cfg.rtol, maxit=300)
+    ctx.set_residual_band(False)
+    xf, i_f, _ = ctx.richardson(b, rtol=cfg.rtol, maxit=300)
+    assert ib.status == 0 and i_f.status == 0 and ib.iterations == i_f.iterations
+    xbn, xfn = xb.cpu().numpy(), xf.cpu().numpy()
+    assert np.linalg.norm(xbn - xfn) <= 1e-10 * np.linalg.norm(xfn)
+    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    o.factor()
+    ro = orc_rich(o.matvec, o.apply, b.cpu().numpy(), rtol=cfg.rtol, maxit=300)
+    assert ro.iterations == ib.iterations
+    assert np.linalg.norm(xbn - ro.x) <= 1e-8 * np.linalg.norm(ro.x)
+    ctx.close()

@@ -207,3 +207,128 @@ def test_narrow_rank_strips_are_refused():
         for m in halo_schedule(pimp5, r, 5, 0):
             if m["phase"] == 0:
                 assert pl["owned_i0"] <= m["send_i0"] and m["send_i1"] <= pl["owned_i1"]
+
+
+# ------------------------------------------------------------------------------------------ section 3(i) band halo
+def _band_sets(o):
+    """Independent of libhelm: node indices whose stencil crosses a block boundary, per axis, from the oracle's
+    ownership ranges (tests/test_oracle_richardson.py pins that the residual lives there)."""
+    out = []
+    for ax in (0, 1):
+        starts = sorted({o.subdomain(j)["own_lo"][ax] for j in range(o.nsub)})
+        out.append({v for s in starts[1:] for v in (s - 1, s)})
+    return out
+
+
+@pytest.mark.parametrize("k,nsub,nranks", CASES)
+def test_band_halo_counts_equal_the_band_area(k, nsub, nranks):
+    """Section 3(i): on the band exchange a rank receives exactly the band nodes of its ghost frame (ext rectangle minus
+    owned rectangle, corners included), and everything sent is received."""
+    from paper_2602_00735_b200.helm import halo_band_counts
+    p = make_params(k, nsub)
+    o = Oracle.from_config(k=k, nsub_x=nsub, nsub_y=nsub)
+    bx, by = _band_sets(o)
+    tot_s = tot_r = full_r = 0
+    for r in range(nranks):
+        pl = plan_rank(p, r, nranks)
+        c = halo_band_counts(p, r, nranks)
+        area = 0
+        for j in range(pl["ext_j0"], pl["ext_j1"]):
+            for i in range(pl["ext_i0"], pl["ext_i1"]):
+                own = pl["owned_i0"] <= i < pl["owned_i1"] and pl["owned_j0"] <= j < pl["owned_j1"]
+                if not own and (i in bx or j in by):
+                    area += 1
+        assert c["recv_band"] == area, (r, c, area)
+        assert c["recv_full"] == (pl["ext_i1"] - pl["ext_i0"]) * (pl["ext_j1"] - pl["ext_j0"]) - \
+            (pl["owned_i1"] - pl["owned_i0"]) * (pl["owned_j1"] - pl["owned_j0"])
+        tot_s += c["sent_band"]
+        tot_r += c["recv_band"]
+        full_r += c["recv_full"]
+    assert tot_s == tot_r
+    if nranks > 1:
+        assert 0 < tot_r < full_r
+
+
+@pytest.mark.parametrize("k,nsub,nranks", [(100.0, 4, 4), (400.0, 16, 8), (100.0, 5, 3)])
+def test_band_rects_pair_up(k, nsub, nranks):
+    """The sender's packing order (band sub-rectangles of its send rectangle) is the receiver's unpacking order."""
+    from paper_2602_00735_b200.helm import halo_band_rects
+    p = make_params(k, nsub)
+    sched = {r: halo_schedule(p, r, nranks, 0) for r in range(nranks)}
+    for r, msgs in sched.items():
+        for q, m in enumerate(msgs):
+            back = [t for t, x in enumerate(sched[m["peer"]]) if x["peer"] == r and x["phase"] == m["phase"]]
+            assert len(back) == 1
+            assert halo_band_rects(p, r, nranks, q, 0) == halo_band_rects(p, m["peer"], nranks, back[0], 1)
+
+
+def _band_exchange_worker(rank, nranks, port, k, nsub, result_q):
+    """The band exchange executed over gloo: every rank packs the band sub-rectangles of its send rectangles (libhelm's
+    canonical order) from a synthetic global field, the peers unpack into a zeroed frame; afterwards the frame holds
+    the global value at every band node and 0 elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_00735_b200.helm import halo_band_rects
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    try:
+        p = make_params(k, nsub)
+        pl = plan_rank(p, rank, nranks)
+        o = Oracle.from_config(k=k, nsub_x=nsub, nsub_y=nsub)
+        bx, by = _band_sets(o)
+        nf = o.nf[0]
+        gid = lambda i, j: float((i - 1) + nf * (j - 1) + 1)   # noqa: E731
+        e_i0, e_j0 = pl["ext_i0"], pl["ext_j0"]
+        buf = torch.zeros((pl["ext_j1"] - e_j0, pl["ext_i1"] - e_i0), dtype=torch.float64)
+        for j in range(pl["owned_j0"], pl["owned_j1"]):
+            for i in range(pl["owned_i0"], pl["owned_i1"]):
+                buf[j - e_j0, i - e_i0] = gid(i, j) if (i in bx or j in by) else 0.0   # the masked residual
+        msgs = halo_schedule(p, rank, nranks, 0)
+        for phase in (0, 1):
+            ops, recvs = [], []
+            for q, m in enumerate(msgs):
+                if m["phase"] != phase:
+                    continue
+                srects = halo_band_rects(p, rank, nranks, q, 0)
+                send = torch.cat([buf[j0 - e_j0:j1 - e_j0, i0 - e_i0:i1 - e_i0].reshape(-1)
+                                  for i0, i1, j0, j1 in srects]) if srects else torch.zeros(0, dtype=torch.float64)
+                rrects = halo_band_rects(p, rank, nranks, q, 1)
+                recv = torch.empty(sum((i1 - i0) * (j1 - j0) for i0, i1, j0, j1 in rrects), dtype=torch.float64)
+                ops.append(dist.P2POp(dist.isend, send.contiguous(), m["peer"]))
+                ops.append(dist.P2POp(dist.irecv, recv, m["peer"]))
+                recvs.append((rrects, recv))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            for rrects, recv in recvs:
+                off = 0
+                for i0, i1, j0, j1 in rrects:
+                    n = (i1 - i0) * (j1 - j0)
+                    buf[j0 - e_j0:j1 - e_j0, i0 - e_i0:i1 - e_i0] = recv[off:off + n].view(j1 - j0, i1 - i0)
+                    off += n
+        ok = True
+        for j in range(pl["ext_j0"], pl["ext_j1"]):
+            for i in range(pl["ext_i0"], pl["ext_i1"]):
+                want = gid(i, j) if (i in bx or j in by) else 0.0
+                if buf[j - e_j0, i - e_i0].item() != want:
+                    ok = False
+        result_q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks,nsub", [(2, 4), (4, 5)])
+def test_band_exchange_over_gloo(nranks, nsub):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_exchange_worker, args=(r, nranks, port, 100.0, nsub, q)) for r in range(nranks)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=240) for _ in range(nranks))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(res[r] for r in range(nranks)), res
