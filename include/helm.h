@@ -123,6 +123,12 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
 enum { HELM_TRANSPORT_NONE = 0, HELM_TRANSPORT_NCCL = 1, HELM_TRANSPORT_LOOPBACK = 2, HELM_TRANSPORT_SHARD = 3 };
 int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* comm_rank);
 
+/* Test aid: the NCCL transport of the halo exchange (the grouped ncclSend / ncclRecv every exchange phase posts) run on
+ * this context's communicator with every rank sending nmsg (1..4) messages of nelem - q complex elements to ITSELF --
+ * the same function exchange phases call, executable on a single GPU.  *mismatches = received elements that differ
+ * from what was sent (0 on success).  HELM_ENCCL without a communicator. */
+int helm_nccl_selftest(helm_ctx* ctx, long long nelem, int nmsg, long long* mismatches);
+
 /* Fill *out with the layout of this rank.  Synchronous, host only. */
 int helm_get_layout(const helm_ctx* ctx, helm_layout* out);
 
@@ -193,9 +199,9 @@ int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rt
  * with the full residual).  HELM_EINVAL for on = 1 with the ramp PoU (its residual fills the whole overlap). */
 int helm_set_residual_band(helm_ctx* ctx, int on);
 
-/* Complex elements sent / received and messages posted by this context's halo exchanges since the last reset
- * (out3[0..2]); reset != 0 zeroes them after reading.  Host only. */
-int helm_comm_counters(helm_ctx* ctx, int reset, long long* out3);
+/* Traffic of this context's collectives since the last reset: out4 = {complex elements sent and received by halo
+ * exchanges, halo messages posted, allreduces issued}; reset != 0 zeroes them after reading.  Host only. */
+int helm_comm_counters(helm_ctx* ctx, int reset, long long* out4);
 
 /* Host logic, no GPU: this rank's apply-frame halo volume in complex elements -- out4 = {sent full, sent band, received
  * full, received band} (band = the section 3(i) restriction) -- and the band sub-rectangles (i0, i1, j0, j1 per

@@ -376,7 +376,7 @@ struct helm_ctx {
         int n = 0;
         long long total = 0, max_area = 0;
     } band_send[4], band_recv[4];
-    long long xc_sent = 0, xc_recv = 0, xc_msgs = 0;
+    long long xc_sent = 0, xc_recv = 0, xc_msgs = 0, xc_allreduce = 0;
 
     // Krylov workspace
     z2* d_V = nullptr;
@@ -728,6 +728,26 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
     return HELM_OK;
 }
 
+// The NCCL transport of one exchange phase: k grouped send/receive pairs of complex128 buffers (counts in complex
+// elements) with the given peers, on stream st.
+int nccl_sendrecv(helm_ctx* ctx, int k, const int* peers, z2* const* sendbuf, const size_t* scnt, z2* const* recvbuf,
+                  const size_t* rcnt, cudaStream_t st)
+{
+#ifdef HELM_HAVE_NCCL
+    if (!ctx->comm) return set_err(ctx, HELM_ENCCL, "no NCCL communicator");
+    NK(ncclGroupStart());
+    for (int a = 0; a < k; a++) {
+        NK(ncclSend(sendbuf[a], 2 * scnt[a], ncclDouble, peers[a], ctx->comm, st));
+        NK(ncclRecv(recvbuf[a], 2 * rcnt[a], ncclDouble, peers[a], ctx->comm, st));
+    }
+    NK(ncclGroupEnd());
+    return HELM_OK;
+#else
+    (void)k; (void)peers; (void)sendbuf; (void)scnt; (void)recvbuf; (void)rcnt; (void)st;
+    return set_err(ctx, HELM_ENCCL, "library built without NCCL");
+#endif
+}
+
 // halo exchange of width W on a ghost-framed buffer `buf` (ext rectangle layout).  Forward (reverse = false): the
 // owned strips travel to the neighbours' ghost frames, phase 0 (x) then phase 1 (y, carrying the corners).
 // Reverse (reverse = true, the ramp PoU's additive exchange): the ghost frames travel back and are ADDED onto the
@@ -772,17 +792,10 @@ int exchange_buf(helm_ctx* ctx, int W, z2* buf, bool reverse, cudaStream_t st)
             int rc = loop_sendrecv(ctx, W, phase, msgs, idx, k, reverse, band, st);
             if (rc) return rc;
         } else {
-#ifdef HELM_HAVE_NCCL
-            NK(ncclGroupStart());
-            for (int a = 0; a < k; a++) {
-                const helm_msg& m = msgs[idx[a]];
-                NK(ncclSend(ctx->d_sendbuf[a], 2 * scnt[a], ncclDouble, m.peer, ctx->comm, st));
-                NK(ncclRecv(ctx->d_recvbuf[a], 2 * rcnt[a], ncclDouble, m.peer, ctx->comm, st));
-            }
-            NK(ncclGroupEnd());
-#else
-            return set_err(ctx, HELM_ENCCL, "library built without NCCL");
-#endif
+            int peers[4];
+            for (int a = 0; a < k; a++) peers[a] = msgs[idx[a]].peer;
+            int rc = nccl_sendrecv(ctx, k, peers, ctx->d_sendbuf, scnt, ctx->d_recvbuf, rcnt, st);
+            if (rc) return rc;
         }
         for (int a = 0; a < k; a++) {
             const helm_msg& m = msgs[idx[a]];
@@ -808,6 +821,7 @@ int exchange(helm_ctx* ctx, int W) { return exchange_buf(ctx, W, ctx->d_ext, fal
 int allreduce(helm_ctx* ctx, double* buf, size_t count)
 {
     if (!ctx->multi) return HELM_OK;
+    ctx->xc_allreduce++;
     NvtxRange nv_("helm.comm.allreduce");
     if (ctx->loop) {
         // loopback: every rank sums all ranks' buffers in rank order (identical bits everywhere)
@@ -1004,6 +1018,21 @@ int spmv_impl(helm_ctx* ctx, const z2* x, z2* y)
     if ((rc = need_comm(ctx))) return rc;
     if (!ctx->multi) {
         launch_spmv(ctx->d_A7, x, y, ctx->owned_geom(), ctx->stream);
+    } else if (ctx->overlap) {
+        // rows whose stencil stays in the owned rectangle run while the width-1 frame is exchanged on the communication
+        // stream; the frame rows follow (each row computes exactly what the serial form does: bitwise equal)
+        const GridInfo& G = ctx->G;
+        const int a0 = G.nbr[0] >= 0, a1 = G.nbr[1] >= 0, b0 = G.nbr[2] >= 0, b1 = G.nbr[3] >= 0;
+        launch_copy_rect(x, G.i0, G.j0, G.i1 - G.i0, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, G.i0, G.i1, G.j0,
+                         G.j1, ctx->stream);
+        CK(cudaEventRecord(ctx->ev_ov[0], ctx->stream));
+        launch_spmv(ctx->d_A7, ctx->d_ext, y, ctx->ext_geom(), ctx->stream, a0, a1, b0, b1);
+        CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_ov[0], 0));
+        if ((rc = exchange_buf(ctx, 1, ctx->d_ext, false, ctx->cstream))) return rc;
+        CK(cudaEventRecord(ctx->ev_ov[1], ctx->cstream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_ov[1], 0));
+        launch_spmv_frame(ctx->d_A7, ctx->d_ext, y, ctx->ext_geom(), a0, a1, b0, b1, ctx->stream);
+        ctx->launches += 2;
     } else {
         if ((rc = fill_ext(ctx, x, 1))) return rc;
         launch_spmv(ctx->d_A7, ctx->d_ext, y, ctx->ext_geom(), ctx->stream);
@@ -1235,6 +1264,15 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         constexpr int REC = 3 * NVMAX + 2;   // step record: final column j - 1, pending column j, nu_j, ||u_{j+1}||,
                                              // then a (column j of R)
         auto mark = [&](int k) { if (ctx->phases) cudaEventRecord(ctx->ev_ph[k], s); };
+        // Several ranks: step j + 1 (it needs only device data) is queued before the host's update of step j, so the
+        // devices never wait for the host's turnaround.  One rank: the turnaround is 0.3 % of a c3 step (93.59 vs
+        // 93.56 applies/s with and without), not worth a discarded apply at convergence.
+        const bool lookahead = ctx->multi && !ctx->phases;
+        // folded norm (several ranks, HELM_GMRES_FOLD=0 disables): one collective per Arnoldi step -- the convergence
+        // test uses column j - 1 once step j's record has made it final, one step later than the tentative test; the
+        // price is one more discarded step at convergence
+        const char* fenv = getenv("HELM_GMRES_FOLD");
+        const bool lookahead_folded = lookahead && !(fenv && fenv[0] == '0');
         auto enqueue_step = [&](int j) -> int {
             z2* uj = V + (long long)j * n;
             int rc2;
@@ -1255,18 +1293,18 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
             launch_dcgs2_update(V, n, j, ctx->d_w, ctx->d_ca, ctx->d_ce, ctx->d_sc, n, ctx->d_dpart, ctx->nblk, s);
             mark(5);
             ctx->launches += 4;
-            if ((rc2 = finish_norm(ctx, ctx->d_hout + 2 * NVMAX + 1))) return rc2;
+            // ||u_{j+1}|| feeds only the host's tentative convergence test.  On several ranks (lookahead) it costs a
+            // collective of its own; the next step's projection sweep computes alpha_{j+1} = ||u_{j+1}||^2 inside the
+            // one packed allreduce anyway, so the host tests the FINAL column instead and this norm is not formed.
+            if (!lookahead_folded && (rc2 = finish_norm(ctx, ctx->d_hout + 2 * NVMAX + 1))) return rc2;
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(ctx->h_hc + (j & 1) * REC, ctx->d_hout, sizeof(z2) * REC, cudaMemcpyDeviceToHost, s));
             mark(6);
             CK(cudaEventRecord(ctx->ev_hc[j & 1], s));
             return HELM_OK;
         };
-        // Several ranks: step j + 1 (it needs only device data) is queued before the host's update of step j, so the
-        // devices never wait for the host's turnaround; when step j turns out to be the cycle's last, step j + 1 is
-        // discarded and its record supplies the final column j.  One rank: the turnaround is 0.3 % of a c3 step
-        // (93.59 vs 93.56 applies/s with and without), not worth the discarded apply at convergence.
-        const bool lookahead = ctx->multi && !ctx->phases;
+        // (lookahead: when step j turns out to be the cycle's last, step j + 1 is discarded and its record supplies the
+        // final column j)
         if (lookahead && (rc = enqueue_step(0))) return rc;
         for (int j = 0; j < m; j++) {
             if (ctx->phases && j > 0) {   // the previous step's end (mark 6, kept in slot 7) to this step's start
@@ -1290,7 +1328,7 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
                 std::swap(ctx->ev_ph[6], ctx->ev_ph[7]);
             }
             const z2* hc = ctx->h_hc + (j & 1) * REC;
-            const double nu = hc[2 * NVMAX].x, un = hc[2 * NVMAX + 1].x;
+            const double nu = hc[2 * NVMAX].x, un = lookahead_folded ? 1.0 : hc[2 * NVMAX + 1].x;
             if (!std::isfinite(nu) || !std::isfinite(un)) {
                 inf->iterations = its;
                 inf->status = HELM_BREAKDOWN;
@@ -1310,14 +1348,23 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
                     jend = j;
                     break;
                 }
+                if (lookahead_folded && rtol > 0 && std::abs(g[j]) <= rtol * beta0) {
+                    // folded norm: the final column j - 1 meets rtol -> steps j (and j + 1 if queued) are discarded
+                    its--;
+                    jend = j;
+                    break;
+                }
             }
             for (int i = 0; i <= j; i++) Rij(i, j) = cplx(hc[NVMAX + i].x, hc[NVMAX + i].y);
-            Rij(j + 1, j) = un;   // tentative
-            rotate_col(j);
-            est = std::abs(g[j + 1]) / beta0;
-            if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
             jend = j + 1;
-            if ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || un == 0.0 || its >= maxit || j == m - 1) {
+            if (!lookahead_folded) {
+                Rij(j + 1, j) = un;   // tentative
+                rotate_col(j);
+                est = std::abs(g[j + 1]) / beta0;
+                if (inf->history && its - 1 < inf->history_cap) inf->history[its - 1] = est;
+            }
+            const bool done_tent = !lookahead_folded && ((rtol > 0 && std::abs(g[j + 1]) <= rtol * beta0) || un == 0.0);
+            if (done_tent || its >= maxit || j == m - 1) {
                 if (ahead) {   // the queued step j + 1 (discarded) has closed column j
                     CK(cudaEventSynchronize(ctx->ev_hc[(j + 1) & 1]));
                     const z2* h1 = ctx->h_hc + ((j + 1) & 1) * REC;
@@ -1857,6 +1904,43 @@ int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* c
     return HELM_OK;
 }
 
+int helm_nccl_selftest(helm_ctx* ctx, long long nelem, int nmsg, long long* mismatches)
+{
+    if (!ctx || nelem < 1 || nmsg < 1 || nmsg > 4 || !mismatches) return HELM_EINVAL;
+    z2 *sb[4] = {}, *rb[4] = {};
+    size_t cnt[4];
+    int peers[4];
+    int rc = HELM_OK;
+    std::vector<z2> h((size_t)nelem), g((size_t)nelem);
+    *mismatches = 0;
+    for (int a = 0; a < nmsg && !rc; a++) {
+        cnt[a] = (size_t)nelem - a;   // distinct sizes per message
+        peers[a] = ctx->rank;         // send-to-self: every rank of the communicator runs the same code path
+        if ((rc = dalloc(ctx, &sb[a], nelem)) || (rc = dalloc(ctx, &rb[a], nelem))) break;
+        for (long long e = 0; e < nelem; e++) h[e] = zmk(1000.0 * a + e, -0.5 * e);
+        if (cudaMemcpyAsync(sb[a], h.data(), sizeof(z2) * nelem, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+            cudaMemsetAsync(rb[a], 0, sizeof(z2) * nelem, ctx->stream) != cudaSuccess)
+            rc = set_err(ctx, HELM_ECUDA, "selftest staging");
+    }
+    if (!rc) rc = nccl_sendrecv(ctx, nmsg, peers, sb, cnt, rb, cnt, ctx->stream);
+    for (int a = 0; a < nmsg && !rc; a++) {
+        if (cudaMemcpyAsync(g.data(), rb[a], sizeof(z2) * nelem, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+            rc = set_err(ctx, HELM_ECUDA, "selftest readback");
+            break;
+        }
+        for (long long e = 0; e < nelem; e++) {
+            const z2 want = e < (long long)cnt[a] ? zmk(1000.0 * a + e, -0.5 * e) : zmk(0, 0);
+            if (g[e].x != want.x || g[e].y != want.y) (*mismatches)++;
+        }
+    }
+    for (int a = 0; a < 4; a++) {
+        if (sb[a]) cudaFree(sb[a]);
+        if (rb[a]) cudaFree(rb[a]);
+    }
+    return rc;
+}
+
 int helm_set_residual_band(helm_ctx* ctx, int on)
 {
     if (!ctx || on < 0 || on > 1) return set_err(ctx, HELM_EINVAL, "helm_set_residual_band: on must be 0 or 1");
@@ -1866,13 +1950,14 @@ int helm_set_residual_band(helm_ctx* ctx, int on)
     return HELM_OK;
 }
 
-int helm_comm_counters(helm_ctx* ctx, int reset, long long* out3)
+int helm_comm_counters(helm_ctx* ctx, int reset, long long* out4)
 {
-    if (!ctx || !out3) return HELM_EINVAL;
-    out3[0] = ctx->xc_sent;
-    out3[1] = ctx->xc_recv;
-    out3[2] = ctx->xc_msgs;
-    if (reset) ctx->xc_sent = ctx->xc_recv = ctx->xc_msgs = 0;
+    if (!ctx || !out4) return HELM_EINVAL;
+    out4[0] = ctx->xc_sent;
+    out4[1] = ctx->xc_recv;
+    out4[2] = ctx->xc_msgs;
+    out4[3] = ctx->xc_allreduce;
+    if (reset) ctx->xc_sent = ctx->xc_recv = ctx->xc_msgs = ctx->xc_allreduce = 0;
     return HELM_OK;
 }
 

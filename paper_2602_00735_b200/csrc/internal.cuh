@@ -159,7 +159,10 @@ struct StencilGeom {
     int ns;                 // 7 (P1) or 9 (Q1) slots
     z2 c7[9];
 };
-void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s);
+void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s, int a0 = 0, int a1 = 0,
+                 int b0 = 0, int b1 = 0);
+void launch_spmv_frame(const z2* A7, const z2* x, z2* y, const StencilGeom& G, int a0, int a1, int b0, int b1,
+                       cudaStream_t s);
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s);
 void launch_copy_rect(const z2* src, int si0, int sj0, long long sstride, z2* dst, int di0, int dj0, long long dstride,

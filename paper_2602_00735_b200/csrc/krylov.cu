@@ -80,11 +80,37 @@ __device__ __forceinline__ z2 stencil_row(const z2* __restrict__ A7, const z2* _
 // 2-D launch: blockIdx.y strides over rows j, x-threads over i (no 64-bit division per row)
 template <int NS>
 __global__ void __launch_bounds__(KT) k_spmv(const z2* __restrict__ A7, const z2* __restrict__ x, z2* __restrict__ y,
-                                             StencilGeom G)
+                                             StencilGeom G, int a0, int a1, int b0, int b1)
 {
-    const int li = blockIdx.x * blockDim.x + threadIdx.x;
-    if (li >= G.nx) return;
-    for (int lj = blockIdx.y; lj < G.ny; lj += gridDim.y) {
+    // rows li in [a0, nx - a1), lj in [b0, ny - b1) of the owned rectangle (all of it: a0 = a1 = b0 = b1 = 0)
+    const int li = a0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= G.nx - a1) return;
+    for (int lj = b0 + blockIdx.y; lj < G.ny - b1; lj += gridDim.y) {
+        const long long r = li + (long long)G.nx * lj;
+        y[r] = stencil_row<NS>(A7, x, r, G);
+    }
+}
+
+// the complement: the frame of width a0 / a1 / b0 / b1 around that interior (the rows whose stencil reads ghost nodes)
+template <int NS>
+__global__ void __launch_bounds__(KT) k_spmv_frame(const z2* __restrict__ A7, const z2* __restrict__ x,
+                                                   z2* __restrict__ y, StencilGeom G, int a0, int a1, int b0, int b1)
+{
+    const long long nrow = (long long)(b0 + b1) * G.nx;            // bottom and top rows, full width
+    const int hin = G.ny - b0 - b1;                                   // rows of the side columns
+    const long long n = nrow + (long long)(a0 + a1) * max(hin, 0);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        int li, lj;
+        if (e < nrow) {
+            const int q = (int)(e / G.nx);
+            li = (int)(e - (long long)q * G.nx);
+            lj = q < b0 ? q : G.ny - b1 + (q - b0);
+        } else {
+            const long long f = e - nrow;
+            const int c = (int)(f / hin);
+            lj = b0 + (int)(f - (long long)c * hin);
+            li = c < a0 ? c : G.nx - a1 + (c - a0);
+        }
         const long long r = li + (long long)G.nx * lj;
         y[r] = stencil_row<NS>(A7, x, r, G);
     }
@@ -600,14 +626,25 @@ int ew_grid(long long n)
 
 }  // namespace
 
-void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s)
+void launch_spmv(const z2* A7, const z2* x, z2* y, const StencilGeom& G, cudaStream_t s, int a0, int a1, int b0,
+                 int b1)
 {
     // each CTA walks several grid rows j (x rows j-1, j, j+1 stay in L1 between iterations) instead of one
-    const int gx = (G.nx + KT - 1) / KT;
+    const int nx = G.nx - a0 - a1, ny = G.ny - b0 - b1;
+    if (nx <= 0 || ny <= 0) return;
+    const int gx = (nx + KT - 1) / KT;
     int gy = std::max(1, 148 * 64 / gx);
-    if (gy > G.ny) gy = G.ny;
-    if (G.ns == 9) k_spmv<9><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
-    else k_spmv<7><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G);
+    if (gy > ny) gy = ny;
+    if (G.ns == 9) k_spmv<9><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G, a0, a1, b0, b1);
+    else k_spmv<7><<<dim3(gx, gy), KT, 0, s>>>(A7, x, y, G, a0, a1, b0, b1);
+}
+void launch_spmv_frame(const z2* A7, const z2* x, z2* y, const StencilGeom& G, int a0, int a1, int b0, int b1,
+                       cudaStream_t s)
+{
+    const long long n = (long long)(b0 + b1) * G.nx + (long long)(a0 + a1) * std::max(G.ny - b0 - b1, 0);
+    if (n <= 0) return;
+    if (G.ns == 9) k_spmv_frame<9><<<ew_grid(n), KT, 0, s>>>(A7, x, y, G, a0, a1, b0, b1);
+    else k_spmv_frame<7><<<ew_grid(n), KT, 0, s>>>(A7, x, y, G, a0, a1, b0, b1);
 }
 void launch_residual(const z2* A7, const z2* x, const z2* b, z2* r, const StencilGeom& G, double* partial, int nblk,
                      cudaStream_t s)

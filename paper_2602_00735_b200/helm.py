@@ -82,7 +82,7 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
            "helm_probe_read_bandwidth_mode", "helm_set_orthogonalisation",
            "helm_get_krylov_basis", "helm_comm_info", "helm_probe_fp64_tflops", "helm_set_residual_band",
-           "helm_comm_counters", "helm_halo_band_counts", "helm_halo_band_rects"]
+           "helm_comm_counters", "helm_halo_band_counts", "helm_halo_band_rects", "helm_nccl_selftest"]
 
 
 def lib_path() -> str:
@@ -125,6 +125,7 @@ def load(build_if_missing: bool = True):
     L.helm_probe_read_bandwidth_mode.argtypes = [C.c_longlong, i, i, C.POINTER(d)]
     L.helm_probe_fp64_tflops.argtypes = [i, C.POINTER(d)]
     L.helm_set_residual_band.argtypes = [vp, i]
+    L.helm_nccl_selftest.argtypes = [vp, C.c_longlong, i, C.POINTER(C.c_longlong)]
     L.helm_comm_counters.argtypes = [vp, i, C.POINTER(C.c_longlong)]
     L.helm_halo_band_counts.argtypes = [C.POINTER(Params), i, i, C.POINTER(C.c_longlong)]
     L.helm_halo_band_rects.argtypes = [C.POINTER(Params), i, i, i, i, C.POINTER(i), i]
@@ -399,10 +400,16 @@ class Context:
         """Section 3(i) residual restriction + band-only halo in helm_richardson (default on, owner PoU)."""
         self._check(self.L.helm_set_residual_band(self._h, int(bool(on))))
 
+    def nccl_selftest(self, nelem: int, nmsg: int = 2) -> int:
+        """Grouped ncclSend/ncclRecv of the halo transport, every rank to itself; returns the mismatch count."""
+        mm = C.c_longlong()
+        self._check(self.L.helm_nccl_selftest(self._h, int(nelem), int(nmsg), C.byref(mm)))
+        return mm.value
+
     def comm_counters(self, reset: bool = False) -> dict:
-        out = (C.c_longlong * 3)()
+        out = (C.c_longlong * 4)()
         self._check(self.L.helm_comm_counters(self._h, int(bool(reset)), out))
-        return {"sent": out[0], "recv": out[1], "msgs": out[2]}
+        return {"sent": out[0], "recv": out[1], "msgs": out[2], "allreduces": out[3]}
 
     TRANSPORTS = {0: "none", 1: "nccl", 2: "loopback", 3: "shard"}
 

@@ -393,3 +393,55 @@ def test_loopback_richardson_residual_band(name, nranks, gg):
     ro = orc_rich(o.matvec, o.apply, bn, rtol=cfg.rtol, maxit=300)
     assert abs(outs[0]["its"] - ro.iterations) <= 1 and i1f.iterations == ro.iterations
     assert np.linalg.norm(X.view(-1).cpu().numpy() - ro.x) <= 1e-8 * np.linalg.norm(ro.x)
+
+
+@pytest.mark.parametrize("fold", ["1", "0"])
+def test_loopback_gmres_collectives_per_step(fold, monkeypatch):
+    """Several ranks: with the folded norm (default) an Arnoldi step issues ONE allreduce (the packed projection sums);
+    unfolded, two (plus the norm).  Both give the single-rank iteration count +-1 and its solution to 1e-8, and the
+    oracle's count +-1; the SpMV of every step overlaps its width-1 halo with the interior rows (bitwise: matvec
+    equals one rank in test_loopback_bj)."""
+    monkeypatch.setenv("HELM_GMRES_FOLD", fold)
+    cfg = CONFIGS["c2"]
+    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    ref = Context(**kw)
+    ref.factor()
+    nf = ref.layout.N_cells - 1
+    b = ref.rhs(*sources(cfg))
+    x_ref, gi_ref, _ = ref.gmres(b, restart=cfg.restart, rtol=cfg.rtol)
+    ref.close()
+    B = b.view(nf, nf)
+    gid = next(_gid)
+    torch.cuda.synchronize()
+
+    def rank(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c = Context(**kw, gpu_grid=(2, 2), rank=r, nranks=4, stream=s, loopback_group=gid)
+            c.factor()
+            pl = c.plan
+            c.comm_counters(reset=True)
+            x, gi, _ = c.gmres(owned(B, pl), restart=cfg.restart, rtol=cfg.rtol)
+            cnt = c.comm_counters(reset=True)
+            s.synchronize()
+            out = dict(pl=pl, x=x.clone(), its=gi.iterations, applies=gi.applies, restarts=gi.restarts, cnt=cnt)
+            c.close()
+            return out
+
+    outs = run_ranks(4, rank)
+    X = torch.full_like(B, complex("nan"))
+    for o in outs:
+        pl = o["pl"]
+        X[pl["owned_j0"] - 1:pl["owned_j1"] - 1, pl["owned_i0"] - 1:pl["owned_i1"] - 1] = o["x"].view(
+            pl["owned_j1"] - pl["owned_j0"], pl["owned_i1"] - pl["owned_i0"])
+    its = outs[0]["its"]
+    assert abs(its - gi_ref.iterations) <= 1
+    tol = 1e-8 if its == gi_ref.iterations else 1e-6
+    assert float(torch.linalg.norm(X.view(-1) - x_ref) / torch.linalg.norm(x_ref)) <= tol
+    steps = outs[0]["applies"]                      # Arnoldi steps issued, discarded lookahead steps included
+    cycles = outs[0]["restarts"] + 1
+    # per step: the packed projection allreduce (+ the norm unfolded); per cycle: ||b||, ||r|| (residual), closing
+    # projection; once: ||b|| for beta0
+    per_step = 1 if fold == "1" else 2
+    ar = outs[0]["cnt"]["allreduces"]
+    assert steps * per_step <= ar <= steps * per_step + 3 * cycles + 2, (ar, steps, cycles)

@@ -66,6 +66,22 @@ def test_one_rank_nccl_communicator(name):
     nc.close()
 
 
+def test_nccl_send_recv_transport_on_one_gpu():
+    """The grouped ncclSend/ncclRecv transport every halo phase posts (nccl_sendrecv), run on a one-rank communicator
+    with messages to itself: four messages of distinct sizes arrive intact (the send-to-self path is local -- no kernel
+    waits on another process)."""
+    nc = Context(100.0, 4, 4, nccl_id=nccl_unique_id())
+    assert nc.comm_info()["transport"] == "nccl"
+    assert nc.nccl_selftest(50_000, 4) == 0
+    assert nc.nccl_selftest(7, 1) == 0
+    plain = Context(100.0, 4, 4)
+    from paper_2602_00735_b200 import HelmError
+    with pytest.raises(HelmError):
+        plain.nccl_selftest(10, 1)
+    nc.close()
+    plain.close()
+
+
 # ------------------------------------------------------------------------------------------------- N GPUs
 def spawn(nranks, kw, gg, job):
     import torch.multiprocessing as mp
