@@ -188,12 +188,16 @@ def run_ours(args):
     barrier()
     t0 = time.time()
     ctx = Context(cfg.k, cfg.nsub, cfg.nsub, rank=rank, nranks=world, stream=stream, nccl_id=nccl_id)
+    fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fe0.record(stream)
     ctx.factor()
+    fe1.record(stream)
     if args.orth == "cgs2":
         from paper_2602_00735_b200.helm import ORTH_CGS2
         ctx.set_orthogonalisation(ORTH_CGS2)
     torch.cuda.synchronize()
     setup_s = max_over_ranks(time.time() - t0)
+    factor_s = max_over_ranks(fe0.elapsed_time(fe1) / 1e3)
     lay = ctx.layout.as_dict()
     comm = ctx.comm_info()
     xy, amp, sig = sources(cfg)
@@ -343,6 +347,7 @@ def run_ours(args):
                       "algorithmic_bytes": tts_b, "roofline_s": tts_b / (hbm * 1e9),
                       "roofline_frac": tts_b / (hbm * 1e9) / tts_s},
         "setup_factor_s": setup_s,
+        "factor": factor_roofline(lay, factor_s, gather),
         "comm": comm,
         "clocks": clk.summary(),
     }
@@ -358,6 +363,19 @@ def run_ours(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def factor_roofline(lay, factor_s, gather):
+    """Setup factorisation (s3) against the FP64 tensor-core peak MEASURED on this GPU (helm_probe_fp64_tflops: DMMA
+    issue rate; MEASURED_PEAKS.json has no FP64 figure): flops = sum over blocks of 8 m^3 (Gauss-Jordan inversions)."""
+    from paper_2602_00735_b200.helm import probe_fp64_tflops
+    dmma = probe_fp64_tflops(0)
+    dfma = probe_fp64_tflops(1)
+    flop = sum(gather(float(lay["factor_flop"])))
+    ach = flop / factor_s / 1e12
+    return {"seconds": factor_s, "tflop": flop / 1e12, "achieved_tflops": ach, "bound": "tensor",
+            "peak_dmma_tflops_measured": dmma, "peak_dfma_tflops_measured": dfma, "frac": ach / dmma,
+            "kernel": "k_factor_chains + k_factor_twist (8-wide blocked Gauss-Jordan, DMMA)"}
 
 
 # The paper's timed runs (Table 4, P:317-323: RAS-PML-Imp Richardson to rtol 1e-10, one processor per subdomain;

@@ -92,6 +92,8 @@ typedef struct {
     long long spmv_bytes;     /* algorithmic bytes of one helm_matvec on this rank */
     int stencil_slots;        /* coefficients per row of A (helm_export_stencil): 7 (P1) or 9 (Q1) */
     int overlap_interior;     /* multi-rank: subdomains applied while the halo is in flight (0: no overlap) */
+    long long factor_flop;    /* real FP64 flops of helm_factor's block inversions: sum over blocks of 8 m^3 (one
+                                 complex multiply-add per entry and pivot of Gauss-Jordan) */
 } helm_layout;
 
 typedef struct {

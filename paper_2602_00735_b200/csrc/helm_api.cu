@@ -2038,6 +2038,8 @@ int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
     out->spmv_bytes = 16LL * 2 * ctx->n_local + 16LL * G.ns * (ctx->n_local - ncst);
     out->stencil_slots = G.ns;
     out->overlap_interior = ctx->overlap ? ctx->n_int : 0;
+    out->factor_flop = 0;
+    for (const SubDesc& sd : ctx->subs) out->factor_flop += 8LL * sd.nb * sd.m * sd.m * sd.m;
     return HELM_OK;
 }
 

@@ -37,7 +37,7 @@ class Layout(C.Structure):
                 ("n_local", C.c_longlong), ("n_sub", C.c_int), ("n_sub_local", C.c_int), ("m_max", C.c_int),
                 ("local_unknowns", C.c_longlong), ("factor_bytes", C.c_longlong), ("apply_bytes", C.c_longlong),
                 ("band_bytes", C.c_longlong), ("spmv_bytes", C.c_longlong), ("stencil_slots", C.c_int),
-                ("overlap_interior", C.c_int)]
+                ("overlap_interior", C.c_int), ("factor_flop", C.c_longlong)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
