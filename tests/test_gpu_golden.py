@@ -1,5 +1,6 @@
 """The headline config c3 (k = 1600, 6.58 M unknowns, 64 x 64 subdomains; BASELINE.json configs[3]) at FULL size,
-against the oracle: the whole assembled stencil and right-hand side element by element (oracle run live), and the
+against the oracle: the whole assembled stencil, right-hand side, one apply and one matvec element by element (oracle
+run live, its apply in dedup mode), and the
 GMRES(50) solve against the oracle-only golden record tests/golden/c3_gmres.json (scripts/make_golden.py: MGS GMRES
 on the dedup-mode oracle, written without libhelm) -- iterations +-1, the residual-estimate history to 1e-6 relative,
 ||x|| and a seeded 64-row sketch S x to 1e-6 (north_star: "GPU solutions matching the oracle ... on all five
@@ -42,6 +43,24 @@ def test_c3_stencil_full_vector():
     R = o.stencil().T
     assert A.shape == R.shape
     assert np.max(np.abs(A - R)) <= 1e-13 * np.max(np.abs(R))
+
+
+def test_c3_apply_and_matvec_full_vector():
+    """One RAS-PML apply and one matvec at c3, in the bench's launch configuration, against the oracle on EVERY node
+    (the oracle's apply in dedup mode, D24 -- exact): apply <= 1e-10, matvec <= 1e-13 (north_star)."""
+    ctx, o = c3()
+    cfg = CONFIGS["c3"]
+    from paper_2602_00735_b200.workloads import probe_vector
+    v = probe_vector(ctx.n, int(cfg.k) + 1)
+    vt = torch.from_numpy(v).cuda()
+    z = ctx.precond_apply(vt).cpu().numpy()
+    y = ctx.matvec(vt).cpu().numpy()
+    assert o.factor_dedup() == 16
+    zo = o.apply(v)
+    o.release()
+    yo = o.matvec(v)
+    assert np.linalg.norm(z - zo) / np.linalg.norm(zo) <= 1e-10
+    assert np.linalg.norm(y - yo) / np.linalg.norm(yo) <= 1e-13
 
 
 def test_c3_rhs_full_vector():

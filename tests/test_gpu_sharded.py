@@ -55,22 +55,22 @@ def test_sharded_apply_and_matvec_bitwise(name, nranks, gg):
     ref.close()
 
 
-def test_c4_full_size_shards_sampled():
+def test_c4_full_size_shards_full_vector():
     """k = 3200 (BASELINE.json configs[4], 128 x 128 subdomains, ~197 GB of factors: it needs >= 2 GPUs).
-    Each half of the 2 x 1 rank grid is set up on this one GPU in turn as a communication-free shard
-    (~99 GB of factors), fed its ghost-framed input, and the oracle solves a sample of subdomains one by one
-    -- corners, edges, interior, and the columns on both sides of the rank cut, whose full boxes read the
-    ghost frame.  Matvec on sampled rows of each shard."""
+    Each half of the 2 x 1 rank grid is set up on this one GPU in turn as a communication-free shard (~99 GB of
+    factors) and fed its ghost-framed input; its apply and matvec are compared ELEMENT BY ELEMENT on every owned node
+    with the oracle's full apply (dedup mode, D24: one band LU per bitwise-distinct A_j, exact) and full matvec."""
     from oracle.oracle import Oracle
     cfg = CONFIGS["c4"]
     P = cfg.nsub
     o = Oracle.from_config(k=cfg.k, nsub_x=P, nsub_y=P)
+    assert o.factor_dedup() <= 16
     v = probe_vector(o.nfree, int(cfg.k) + 1)
     nfx = o.nf[0]
-    picks = {0: [(0, 0), (63, 0), (0, 127), (63, 127), (63, 64), (31, 77), (62, 5)],
-             1: [(64, 0), (127, 127), (64, 64), (100, 30), (127, 1)]}
+    zo = o.apply(v).reshape(o.nf[1], nfx)
+    yo = o.matvec(v).reshape(o.nf[1], nfx)
+    o.release()
     V = grid(torch.from_numpy(v).cuda(), nfx)
-    rng = np.random.default_rng(7)
     for r in (0, 1):
         c = Context(cfg.k, P, P, rank=r, nranks=2, gpu_grid=(2, 1))
         c.factor()
@@ -78,30 +78,14 @@ def test_c4_full_size_shards_sampled():
         ext = V[pl["ext_j0"] - 1:pl["ext_j1"] - 1, pl["ext_i0"] - 1:pl["ext_i1"] - 1].contiguous().view(-1)
         i0, i1, j0, j1 = pl["owned_i0"], pl["owned_i1"], pl["owned_j0"], pl["owned_j1"]
         z = c.precond_apply_ext(ext).view(j1 - j0, i1 - i0).cpu().numpy()
-        subs = [bx + P * by for bx, by in picks[r]]
-        o.factor(subs)
-        zo = o.apply(v, subs=subs).reshape(o.nf[1], nfx)
-        o.release()
-        got, want = [], []
-        for j in subs:
-            s = o.subdomain(j)
-            a0, a1 = max(s["own_lo"][0], 1), min(s["own_hi"][0], o.N[0])
-            b0, b1 = max(s["own_lo"][1], 1), min(s["own_hi"][1], o.N[1])
-            assert i0 <= a0 and a1 <= i1 and j0 <= b0 and b1 <= j1
-            got.append(z[b0 - j0:b1 - j0, a0 - i0:a1 - i0].ravel())
-            want.append(zo[b0 - 1:b1 - 1, a0 - 1:a1 - 1].ravel())
-        got, want = np.concatenate(got), np.concatenate(want)
-        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-10
+        want = zo[j0 - 1:j1 - 1, i0 - 1:i1 - 1]
+        assert np.linalg.norm(z - want) / np.linalg.norm(want) <= 1e-10
         nb = pl["nbr"]
         li, ri, dj, uj = int(nb[0] >= 0), int(nb[1] >= 0), int(nb[2] >= 0), int(nb[3] >= 0)
         ext1 = V[j0 - 1 - dj:j1 - 1 + uj, i0 - 1 - li:i1 - 1 + ri].contiguous().view(-1)
         y = c.matvec_ext(ext1).view(j1 - j0, i1 - i0).cpu().numpy()
-        li_ = rng.integers(i0, i1, 20000)
-        lj_ = rng.integers(j0, j1, 20000)
-        rows = (li_ - 1) + nfx * (lj_ - 1)
-        yo = o.matvec_rows(v, rows)
-        yg = y[lj_ - j0, li_ - i0]
-        assert np.linalg.norm(yg - yo) / np.linalg.norm(yo) <= 1e-13
+        ywant = yo[j0 - 1:j1 - 1, i0 - 1:i1 - 1]
+        assert np.linalg.norm(y - ywant) / np.linalg.norm(ywant) <= 1e-13
         c.close()
         del ext, ext1
         torch.cuda.empty_cache()
