@@ -296,17 +296,27 @@ struct LoopGroup {
     std::condition_variable cv;
     int arrived = 0;
     long gen = 0;
-    void barrier()
+    bool aborted = false;   // a rank failed inside a collective call: the others leave their barriers with an error
+    // false if the group was aborted (a failed rank would otherwise leave its peers waiting forever)
+    bool barrier()
     {
         std::unique_lock<std::mutex> lk(mu);
+        if (aborted) return false;
         const long g = gen;
         if (++arrived == nranks) {
             arrived = 0;
             gen++;
             cv.notify_all();
         } else {
-            cv.wait(lk, [&] { return gen != g; });
+            cv.wait(lk, [&] { return gen != g || aborted; });
         }
+        return !aborted;
+    }
+    void abort()
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = true;
+        cv.notify_all();
     }
 };
 std::mutex g_loop_mu;
@@ -693,7 +703,7 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
 {
     LoopGroup* L = ctx->loop;
     CK(cudaStreamSynchronize(st));
-    L->barrier();   // every rank has packed this phase
+    if (!L->barrier()) return set_err(ctx, HELM_ENCCL, "loopback group aborted by another rank");   // all packed
     for (int a = 0; a < k; a++) {
         const helm_msg& m = msgs[idx[a]];
         const helm_ctx* peer = L->ctx[m.peer];
@@ -724,7 +734,7 @@ int loop_sendrecv(helm_ctx* ctx, int W, int phase, const helm_msg* msgs, const i
                            st));
     }
     CK(cudaStreamSynchronize(st));
-    L->barrier();   // peers may refill their send buffers
+    if (!L->barrier()) return set_err(ctx, HELM_ENCCL, "loopback group aborted by another rank");   // may refill
     return HELM_OK;
 }
 
@@ -829,11 +839,11 @@ int allreduce(helm_ctx* ctx, double* buf, size_t count)
         if (count > 4 * NVMAX) return set_err(ctx, HELM_EINVAL, "loopback allreduce of %zu doubles", count);
         CK(cudaStreamSynchronize(ctx->stream));
         L->slot[ctx->rank] = buf;
-        L->barrier();
+        if (!L->barrier()) return set_err(ctx, HELM_ENCCL, "loopback group aborted by another rank");
         launch_sum_ranks(L->slot.data(), L->nranks, (int)count, ctx->d_loop_tmp, ctx->stream);
         ctx->launches++;
         CK(cudaStreamSynchronize(ctx->stream));
-        L->barrier();   // everyone has read everyone's contribution
+        if (!L->barrier()) return set_err(ctx, HELM_ENCCL, "loopback group aborted by another rank");   // all read
         CK(cudaMemcpyAsync(buf, ctx->d_loop_tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
         return HELM_OK;
     }
@@ -1522,12 +1532,21 @@ int helm_set_orthogonalisation(helm_ctx* ctx, int mode)
     return HELM_OK;
 }
 
+// A collective entry point that fails on one rank of a loopback group aborts the group, so that its peers leave their
+// barriers with an error instead of waiting forever (with NCCL the peers would hang in the collective; with the
+// loopback transport they can be told).
+static int coll(helm_ctx* ctx, int rc)
+{
+    if (rc < 0 && ctx && ctx->loop) ctx->loop->abort();
+    return rc;
+}
+
 int helm_richardson(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, double rtol, int maxit,
                     helm_richardson_info* info)
 {
     if (!ctx || !b_dev || !x_dev || (const void*)b_dev == (void*)x_dev)
-        return set_err(ctx, HELM_EINVAL, "helm_richardson: bad arguments");
-    return richardson_impl(ctx, (const z2*)b_dev, (z2*)x_dev, rtol, maxit, info);
+        return coll(ctx, set_err(ctx, HELM_EINVAL, "helm_richardson: bad arguments"));
+    return coll(ctx, richardson_impl(ctx, (const z2*)b_dev, (z2*)x_dev, rtol, maxit, info));
 }
 extern "C" {
 
@@ -2125,7 +2144,7 @@ int helm_matvec(helm_ctx* ctx, const helm_z* x_dev, helm_z* y_dev)
     if (!ctx || !x_dev || !y_dev || (const void*)x_dev == (void*)y_dev)
         return set_err(ctx, HELM_EINVAL, "helm_matvec: bad arguments");
     int rc = spmv_impl(ctx, (const z2*)x_dev, (z2*)y_dev);
-    if (rc) return rc;
+    if (rc) return coll(ctx, rc);
     CK(cudaGetLastError());
     return HELM_OK;
 }
@@ -2146,7 +2165,7 @@ int helm_precond_apply(helm_ctx* ctx, const helm_z* r_dev, helm_z* z_dev)
 {
     if (!ctx || !r_dev || !z_dev || (const void*)r_dev == (void*)z_dev)
         return set_err(ctx, HELM_EINVAL, "helm_precond_apply: bad arguments");
-    return apply_impl(ctx, (const z2*)r_dev, (z2*)z_dev);
+    return coll(ctx, apply_impl(ctx, (const z2*)r_dev, (z2*)z_dev));
 }
 
 int helm_precond_apply_ext(helm_ctx* ctx, const helm_z* ext_dev, helm_z* z_dev)
@@ -2160,10 +2179,10 @@ int helm_precond_apply_host(helm_ctx* ctx, const helm_z* r_host, helm_z* z_host)
 {
     if (!ctx || !r_host || !z_host) return set_err(ctx, HELM_EINVAL, "helm_precond_apply_host: bad arguments");
     int rc;
-    if ((rc = ensure_krylov(ctx, 0))) return rc;
+    if ((rc = ensure_krylov(ctx, 0))) return coll(ctx, rc);
     const size_t bytes = sizeof(z2) * ctx->n_local;
     CK(cudaMemcpyAsync(ctx->d_t, r_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return rc;
+    if ((rc = apply_impl(ctx, ctx->d_t, ctx->d_z))) return coll(ctx, rc);
     CK(cudaMemcpyAsync(z_host, ctx->d_z, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return HELM_OK;
@@ -2174,7 +2193,7 @@ int helm_gmres(helm_ctx* ctx, const helm_z* b_dev, helm_z* x_dev, int restart, d
 {
     if (!ctx || !b_dev || !x_dev || (const void*)b_dev == (void*)x_dev)
         return set_err(ctx, HELM_EINVAL, "helm_gmres: bad arguments");
-    return gmres_impl(ctx, (const z2*)b_dev, (z2*)x_dev, restart, rtol, maxit, info);
+    return coll(ctx, gmres_impl(ctx, (const z2*)b_dev, (z2*)x_dev, restart, rtol, maxit, info));
 }
 
 int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int restart, double rtol, int maxit,
@@ -2183,12 +2202,12 @@ int helm_gmres_host(helm_ctx* ctx, const helm_z* b_host, helm_z* x_host, int res
     if (!ctx || !b_host || !x_host) return set_err(ctx, HELM_EINVAL, "helm_gmres_host: bad arguments");
     int rc;
     if (!ctx->d_bb && ((rc = dalloc(ctx, &ctx->d_bb, ctx->n_local)) || (rc = dalloc(ctx, &ctx->d_xb, ctx->n_local))))
-        return rc;
+        return coll(ctx, rc);
     const size_t bytes = sizeof(z2) * ctx->n_local;
     CK(cudaMemcpyAsync(ctx->d_bb, b_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_xb, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     rc = gmres_impl(ctx, ctx->d_bb, ctx->d_xb, restart, rtol, maxit, info);
-    if (rc < 0) return rc;
+    if (rc < 0) return coll(ctx, rc);
     CK(cudaMemcpyAsync(x_host, ctx->d_xb, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return rc;

@@ -26,6 +26,18 @@ from paper_2602_00735_b200 import Context  # noqa: E402
 _C = {}
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _release_c3():
+    """The c3 context holds ~58 GB of device memory: free it when this module is done."""
+    yield
+    ctx = _C.pop("ctx", None)
+    if ctx is not None:
+        ctx.close()
+    _C.clear()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
 def c3():
     if "ctx" not in _C:
         cfg = CONFIGS["c3"]

@@ -445,3 +445,30 @@ def test_loopback_gmres_collectives_per_step(fold, monkeypatch):
     per_step = 1 if fold == "1" else 2
     ar = outs[0]["cnt"]["allreduces"]
     assert steps * per_step <= ar <= steps * per_step + 3 * cycles + 2, (ar, steps, cycles)
+
+
+def test_loopback_failed_rank_aborts_the_group():
+    """A collective entry point that fails on one rank (here: invalid restart) aborts the loopback group: its peer
+    leaves the collective with HELM_ENCCL at once instead of waiting for a rank that never arrives."""
+    from paper_2602_00735_b200 import HelmError
+    cfg = CONFIGS["c1"]
+    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    gid = next(_gid)
+
+    def rank(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c = Context(**kw, gpu_grid=(2, 1), rank=r, nranks=2, stream=s, loopback_group=gid)
+            c.factor()
+            b = torch.ones(c.n, dtype=torch.complex128, device="cuda")
+            try:
+                c.gmres(b, restart=0 if r == 0 else 50, rtol=1e-6)
+                return None
+            except HelmError as e:
+                return e.code
+            finally:
+                s.synchronize()
+                c.close()
+
+    codes = run_ranks(2, rank, timeout=120)
+    assert codes[0] == -1 and codes[1] == -4, codes
