@@ -384,10 +384,7 @@ int apply_configure(int m_max, int nslots, int* block_threads, int* smem_bytes, 
     *slot_bytes = slot_bytes_for(m_max);
     *smem_bytes = nslots * *slot_bytes + 2 * nslots * 8 + 3 * (32 * ncw + 1) * (int)sizeof(z2);
     const void* fn = apply_fn(*block_threads);
-    int cur = 0;
-    cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) cur = fa.maxDynamicSharedSizeBytes;
-    if (*smem_bytes > cur) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem_bytes);
+    raise_smem_attr(fn, *smem_bytes);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, *block_threads, *smem_bytes);
     *ctas_per_sm = occ;
@@ -408,18 +405,8 @@ void launch_pou_gather(const SubDesc* desc, const int* candx, const int* candy, 
 
 void launch_apply(const ApplyArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, cudaStream_t s)
 {
-    // the dynamic-smem limit is a per-function attribute shared by every context in the process: raise it
-    // whenever a context needs more than any earlier one
-    static std::mutex mu;
-    static int smem_set[4] = {0, 0, 0, 0};
+    raise_smem_attr(apply_fn(block), smem);
     const int cls = block <= 128 ? 3 : (block <= 256 ? 0 : (block <= 512 ? 1 : 2));
-    {
-        std::lock_guard<std::mutex> lk(mu);   // contexts may launch from concurrent threads (loopback ranks)
-        if (smem > smem_set[cls]) {
-            cudaFuncSetAttribute(apply_fn(block), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            smem_set[cls] = smem;
-        }
-    }
     const int ncw = block / 32 - 1;
     if (cls == 3) k_apply<128, 4><<<grid, block, smem, s>>>(a, ncw, slot_bytes, nslots);
     else if (cls == 0) k_apply<256, 1><<<grid, block, smem, s>>>(a, ncw, slot_bytes, nslots);
@@ -498,7 +485,7 @@ extern "C" int helm_probe_read_bandwidth_mode(long long bytes, int reps, int mod
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int smem = NS * chunk + 2 * NS * 8;
-    cudaFuncSetAttribute(k_read_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    raise_smem_attr((const void*)k_read_probe, smem);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);

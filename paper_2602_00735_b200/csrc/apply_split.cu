@@ -382,18 +382,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_apply_split(ApplyArgs a, int G, 
 const void* split_fn(int block) { return block <= 288 ? (const void*)k_apply_split<288, 2> : (const void*)k_apply_split<512, 1>; }
 
 // the dynamic-smem limit is a per-function attribute shared by every context in the process: only ever raise it
-void ensure_split_smem(int block, int smem)
-{
-    static std::mutex mu;
-    static int smem_set[2] = {0, 0};
-    const int cls = block <= 288 ? 0 : 1;
-    std::lock_guard<std::mutex> lk(mu);   // contexts may launch from concurrent threads (loopback ranks)
-    if (smem > smem_set[cls]) {
-        cudaFuncSetAttribute(split_fn(block), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(split_fn(block), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        smem_set[cls] = smem;
-    }
-}
+void ensure_split_smem(int block, int smem) { raise_smem_attr(split_fn(block), smem, true); }
 
 // slab-major relayout of every inverse block (column-major m x m -> G contiguous column-major R_g x m panels)
 __global__ void k_relayout(const SubDesc* __restrict__ desc, const int2* __restrict__ blocks, int nblocks, z2* dinv,

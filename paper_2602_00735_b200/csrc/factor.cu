@@ -878,7 +878,7 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
             double best = 1e300;
             for (int cand : {8, 6}) {
                 const int sm = big_smem_bytes(m_max, cand);
-                cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+                raise_smem_attr((const void*)k_factor_big, sm);
                 int occ = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_big, BT, sm);
                 if (occ < 1) continue;
@@ -893,8 +893,7 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
         }
         if (const char* e = getenv("HELM_FACTOR_BC")) bc = atoi(e);
         const int smem = big_smem_bytes(m_max, bc);
-        cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (bc > 8) cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        raise_smem_attr((const void*)k_factor_big, smem, bc > 8);
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -914,8 +913,8 @@ void launch_factor(const SubDesc* d_desc, const SubDesc* /*h_desc*/, int nsub, i
     }
     const int smem = factor_smem_bytes(m_max);
     auto go = [&](auto kc, auto kt) {
-        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        raise_smem_attr((const void*)kc, smem);
+        raise_smem_attr((const void*)kt, smem);
         kc<<<2 * nsub, FT, smem, s>>>(d_desc, stencil, dinv, d_err);
         kt<<<nsub, FT, smem, s>>>(d_desc, stencil, dinv, d_err);
     };

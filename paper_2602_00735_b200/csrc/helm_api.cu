@@ -18,6 +18,19 @@
 
 #include "internal.cuh"
 
+void raise_smem_attr(const void* fn, int smem, bool nonportable)
+{
+    static std::mutex mu;
+    static std::map<const void*, int> cur;
+    std::lock_guard<std::mutex> lk(mu);
+    int& c = cur[fn];
+    if (smem > c) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        c = smem;
+    }
+    if (nonportable) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
 // NVTX ranges (host-side, zero cost without a tool attached): setup, factor, apply, spmv, gmres, orth, comm
 struct NvtxRange {
     explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
@@ -2092,7 +2105,7 @@ int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_h
     return rc;
 }
 
-int helm_factor(helm_ctx* ctx)
+static int factor_impl(helm_ctx* ctx)
 {
     NvtxRange nv_("helm.factor");
     if (!ctx) return HELM_EINVAL;
@@ -2137,6 +2150,13 @@ int helm_factor(helm_ctx* ctx)
     if ((rc = ensure_krylov(ctx, 0))) return rc;   // the solvers' work buffers belong to setup, not to a solve
     ctx->factored = true;
     return HELM_OK;
+}
+
+int helm_factor(helm_ctx* ctx)
+{
+    const int rc = factor_impl(ctx);
+    if (rc < 0 && ctx && ctx->loop) ctx->loop->abort();   // (peers would wait for this rank in their next collective)
+    return rc;
 }
 
 int helm_matvec(helm_ctx* ctx, const helm_z* x_dev, helm_z* y_dev)
@@ -2257,7 +2277,19 @@ int helm_setup(const helm_params* params, int rank, int nranks, const void* nccl
 int helm_setup_loopback(const helm_params* params, int rank, int nranks, int group, void* cuda_stream, helm_ctx** out)
 {
     if (group < 0 || nranks < 2 || nranks > 16) return HELM_EINVAL;
-    return setup_impl(params, rank, nranks, nullptr, group, cuda_stream, out);
+    const int rc = setup_impl(params, rank, nranks, nullptr, group, cuda_stream, out);
+    if (rc < 0) {   // the peers must not wait for this rank in their first collective: abort the group
+        std::lock_guard<std::mutex> lk(g_loop_mu);
+        LoopGroup*& L = g_loops[group];
+        if (!L) {
+            L = new LoopGroup();
+            L->nranks = nranks;
+            L->ctx.assign(nranks, nullptr);
+            L->slot.assign(nranks, nullptr);
+        }
+        L->abort();
+    }
+    return rc;
 }
 
 const char* helm_last_error(const helm_ctx* ctx) { return ctx ? ctx->err : "null context"; }

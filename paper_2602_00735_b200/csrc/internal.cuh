@@ -7,6 +7,12 @@
 
 #include "helm.h"
 
+// The dynamic shared-memory limit of a kernel is a per-function attribute shared by every context of the process, and
+// contexts may configure / launch from concurrent host threads (loopback ranks): raise it monotonically under one lock
+// (a context lowering it between another context's set and launch would make that launch fail).  Also sets
+// NonPortableClusterSizeAllowed when `nonportable`.  Defined in helm_api.cu.
+void raise_smem_attr(const void* fn, int smem, bool nonportable = false);
+
 // ---------------------------------------------------------------------------------------------------
 // complex128 helpers (double2 = (re, im))
 // ---------------------------------------------------------------------------------------------------

@@ -45,7 +45,8 @@ def run_ranks(nranks, fn, timeout=300):
     for t in th:
         t.join(timeout)
     if any(t.is_alive() for t in th):
-        pytest.fail("loopback ranks did not finish (deadlock?)")
+        errs = [f"rank {r}: {e!r}" for r, e in enumerate(err) if e is not None]
+        pytest.fail("loopback ranks did not finish (deadlock?); errors on the others: " + "; ".join(errs))
     for e in err:
         if e is not None:
             raise e
