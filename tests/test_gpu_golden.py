@@ -106,3 +106,20 @@ def test_c3_gmres_matches_the_oracle_golden():
     xn = x.cpu().numpy()
     assert abs(np.linalg.norm(xn) - g["norm_x"]) <= 1e-6 * g["norm_x"]
     assert sketch_rel(xn, g) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+def test_small_configs_gmres_match_the_oracle_golden(name):
+    """The same golden comparison at c0-c2 (BASELINE.json configs[0..2]): iterations +-1, history 1e-6, x sketch 1e-6."""
+    g = load_golden(name)
+    cfg = CONFIGS[name]
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub)
+    ctx.factor()
+    b = ctx.rhs(*sources(cfg))
+    x, info, hist = ctx.gmres(b, restart=cfg.restart, rtol=cfg.rtol, maxit=g["maxit"], history=True)
+    assert info.status == g["status"] == 0 and abs(info.iterations - g["iterations"]) <= 1
+    h_orc = np.asarray(g["history"])
+    n = min(len(hist), len(h_orc))
+    assert np.max(np.abs(hist[:n] - h_orc[:n]) / h_orc[:n]) <= 1e-6
+    assert sketch_rel(x.cpu().numpy(), g) <= 1e-6
+    ctx.close()

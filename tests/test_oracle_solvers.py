@@ -244,3 +244,26 @@ def test_impedance_face_on_the_boundary_is_refused():
     Oracle(problem_from_config(k, nsub_x=10, nsub_y=2, n_ovlp=2, n_pml=3, local_bc=0))
     with pytest.raises(OracleError):
         Oracle(problem_from_config(k, nsub_x=10, nsub_y=2, n_ovlp=2, n_pml=3, local_bc=1))
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_committed_golden_records_are_the_oracles(name):
+    """tests/golden/<cfg>_gmres.json was written by scripts/make_golden.py from the oracle alone: re-running the oracle
+    reproduces its iterations, history and solution sketch (no expected value comes from the CUDA path)."""
+    import json
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from make_golden import sketch
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{name}_gmres.json")) as f:
+        g = json.load(f)
+    cfg = CONFIGS[name]
+    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    o.factor_dedup()
+    b = o.rhs(*sources(cfg))
+    res = gmres(o.matvec, o.apply, b, restart=cfg.restart, rtol=cfg.rtol, maxit=g["maxit"])
+    assert res.iterations == g["iterations"] and res.status == g["status"]
+    assert np.allclose(res.history, g["history"], rtol=1e-12, atol=0)
+    s = sketch(res.x, g["sketch_rows"])
+    ref = np.array([complex(a, c) for a, c in g["sketch_x"]])
+    assert np.allclose(s, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
