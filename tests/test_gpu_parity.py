@@ -258,3 +258,32 @@ def test_gmres_initial_guess_and_restart_bounds():
     with pytest.raises(HelmError) as e:
         ctx.gmres(to_dev(b), restart=64, rtol=1e-6)
     assert e.value.code == -1
+
+
+def test_degenerate_inputs():
+    """Edge cases of the boundary: no sources (b = 0 -> x = 0 after 0 iterations; Richardson likewise), maxit = 0 (x0
+    returned unchanged, HELM_NOT_CONVERGED, no apply issued), an impedance layout whose face would sit on dOmega
+    (refused on the GPU as by the oracle, tests/test_oracle_solvers.py), and the apply of a unit vector (one nonzero
+    node: the response is confined to the blocks of the subdomains that cover it) against the oracle."""
+    import math
+    ctx, o = pair("c1")
+    b0 = ctx.rhs(np.zeros((0, 2)), np.zeros(0, np.complex128), 0.01)
+    assert torch.count_nonzero(b0).item() == 0
+    x, info, _ = ctx.gmres(b0)
+    assert info.iterations == 0 and torch.count_nonzero(x).item() == 0
+    xr, rinfo, _ = ctx.richardson(b0)
+    assert rinfo.iterations == 0 and torch.count_nonzero(xr).item() == 0
+    b = ctx.rhs(*sources(CONFIGS["c1"]))
+    x0 = to_dev(probe_vector(ctx.n, 4))
+    x = x0.clone()
+    _, info, _ = ctx.gmres(b, x, maxit=0)
+    assert info.status == 2 and info.iterations == 0 and info.applies == 0 and torch.equal(x, x0)
+    with pytest.raises(HelmError) as e:
+        Context(6 * math.pi, 10, 2, n_ovlp=2, n_pml=3, local_bc=1)
+    assert e.value.code == -6
+    e1 = np.zeros(ctx.n, np.complex128)
+    e1[ctx.n // 2 + 17] = 1.0 - 2.0j
+    z = to_np(ctx.precond_apply(to_dev(e1)))
+    zo = o.apply(e1)
+    assert np.linalg.norm(z - zo) <= 1e-10 * np.linalg.norm(zo)
+    assert np.count_nonzero(zo) < ctx.n // 2
