@@ -4,15 +4,21 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_00735_b200 import build  # noqa: E402
+
+if os.environ.get("HELM_LIB_PATH"):      # time another build of libhelm (A/B of compile-time variants)
+    build.LIB = os.environ["HELM_LIB_PATH"]
 import torch  # noqa: E402
 
+from paper_2602_00735_b200 import helm  # noqa: E402
 from paper_2602_00735_b200 import Context  # noqa: E402
+
+helm.load(build_if_missing=False)
 from paper_2602_00735_b200.workloads import CONFIGS  # noqa: E402
 
 for name in sys.argv[1:] or ["c3"]:
     c = CONFIGS[name]
-    for look, panel in (("1", "8"), ("0", "32")):
-        os.environ["HELM_FACTOR_LOOKAHEAD"] = look
+    for look, panel in (("1", "8"),):
         os.environ["HELM_FACTOR_PANEL"] = panel
         best = None
         for _ in range(3):
