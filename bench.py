@@ -351,6 +351,8 @@ def run_ours(args):
         "comm": comm,
         "clocks": clk.summary(),
     }
+    if world == 1:
+        out["tts_vs_k"] = tts_vs_k(stream, cfg, tts_s, tinfo, factor_s)
     if world == 1 and not args.no_paper:
         out["paper_table4"] = paper_table4(stream)
         out["gmres_tts_ramp_pou"] = ramp_pou_tts(cfg, stream, xy, amp, sig)
@@ -363,6 +365,50 @@ def run_ours(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main):
+    """BASELINE.json's 'GMRES time-to-solve vs k': every single-GPU config c0..c3 solved to 1e-6 on this GPU (setup,
+    factorisation and solve timed with CUDA events; the bench config's own solve reused), beside the oracle's solve of
+    the same system from the golden records (another host: context)."""
+    import torch
+
+    from paper_2602_00735_b200 import Context
+    from paper_2602_00735_b200.workloads import CONFIGS, sources
+    rows = []
+    for name in ("c0", "c1", "c2", "c3"):
+        c = CONFIGS[name]
+        gold = os.path.join(ROOT, "tests", "golden", f"{name}_gmres.json")
+        orc = None
+        if os.path.exists(gold):
+            with open(gold) as f:
+                g = json.load(f)
+            orc = {"iterations": g["iterations"], "gmres_s": g["oracle_timing"]["gmres_s"],
+                   "cores": g["oracle_timing"]["host"]["cores"]}
+        if name == cfg_main.name:
+            rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": factor_main,
+                         "solve_s": tts_main, "iterations": tinfo_main.iterations, "relres_true": tinfo_main.relres_true,
+                         "oracle": orc})
+            continue
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ctx = Context(c.k, c.nsub, c.nsub, stream=stream)
+        ev[0].record(stream)
+        ctx.factor()
+        ev[1].record(stream)
+        b = ctx.rhs(*sources(c))
+        ctx.gmres(b, restart=c.restart, rtol=c.rtol)            # warm-up (first launches of this shape)
+        ev[2].record(stream)
+        _, info, _ = ctx.gmres(b, restart=c.restart, rtol=c.rtol)
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": ev[0].elapsed_time(ev[1]) / 1e3,
+                     "solve_s": ev[2].elapsed_time(ev[3]) / 1e3, "iterations": info.iterations,
+                     "relres_true": info.relres_true, "oracle": orc})
+        ctx.close()
+        del ctx, b
+        torch.cuda.empty_cache()
+    return rows
 
 
 def factor_roofline(lay, factor_s, gather):
