@@ -126,7 +126,8 @@ enum { HELM_TRANSPORT_NONE = 0, HELM_TRANSPORT_NCCL = 1, HELM_TRANSPORT_LOOPBACK
 int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* comm_rank);
 
 /* Test aid: the NCCL transport of the halo exchange (the grouped ncclSend / ncclRecv every exchange phase posts) run on
- * this context's communicator with every rank sending nmsg (1..4) messages of nelem - q complex elements to ITSELF --
+ * this context's communicator with every rank sending nmsg (1..4) messages of nelem - q complex elements (nelem >= nmsg)
+ * to ITSELF --
  * the same function exchange phases call, executable on a single GPU.  *mismatches = received elements that differ
  * from what was sent (0 on success).  HELM_ENCCL without a communicator. */
 int helm_nccl_selftest(helm_ctx* ctx, long long nelem, int nmsg, long long* mismatches);

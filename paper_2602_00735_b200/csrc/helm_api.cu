@@ -1938,7 +1938,7 @@ int helm_comm_info(const helm_ctx* ctx, int* transport, int* comm_nranks, int* c
 
 int helm_nccl_selftest(helm_ctx* ctx, long long nelem, int nmsg, long long* mismatches)
 {
-    if (!ctx || nelem < 1 || nmsg < 1 || nmsg > 4 || !mismatches) return HELM_EINVAL;
+    if (!ctx || nmsg < 1 || nmsg > 4 || nelem < nmsg || !mismatches) return HELM_EINVAL;   // counts nelem - q >= 1
     z2 *sb[4] = {}, *rb[4] = {};
     size_t cnt[4];
     int peers[4];
