@@ -48,18 +48,26 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // Complex 8 x 8 tile update C -= A B over k in [0, kw) on the tensor cores, with A(r, q) = la(r, q), B(q, c) = lb(q, c)
 // supplied as accessors returning complex values (zero outside the matrix): Cr += (-Ar) Br + Ai Bi,
 // Ci += (-Ar) Bi + (-Ai) Br -- four real DMMAs per k-step of 4.
+// The four real products accumulate into four independent fragments (C_r += -A_r B_r, R2 += A_i B_i, C_i += -A_r B_i,
+// I2 += -A_i B_r), summed at the end: the dependent DMMA chain per tile is half as long (the factorisation's trailing
+// tiles are latency-bound on it: ncu "wait" stalls on the NOPs between dependent DMMAs).
 template <class LA, class LB>
 __device__ __forceinline__ void ztile_fms(z2& c0, z2& c1, int kw, LA la, LB lb)
 {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    double r20 = 0.0, r21 = 0.0, i20 = 0.0, i21 = 0.0;
     for (int k = 0; k < kw; k += 4) {
         const z2 a = k + t < kw ? la(g, k + t) : zmk(0, 0);
         const z2 b = k + t < kw ? lb(k + t, g) : zmk(0, 0);
         dmma(c0.x, c1.x, -a.x, b.x);
-        dmma(c0.x, c1.x, a.y, b.y);
+        dmma(r20, r21, a.y, b.y);
         dmma(c0.y, c1.y, -a.x, b.y);
-        dmma(c0.y, c1.y, -a.y, b.x);
+        dmma(i20, i21, -a.y, b.x);
     }
+    c0.x += r20;
+    c1.x += r21;
+    c0.y += i20;
+    c1.y += i21;
 }
 
 // D (kw x kw, row-major, stride DLD, kw <= 32) <- D^-1 by unpivoted in-place Gauss-Jordan, executed by the first
@@ -493,11 +501,18 @@ __device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
         }
         {
             const int w0 = nk < m ? 1 : 0;   // warp 0 is busy with the next pivot
-            for (int tile = w - w0; tile < mt * mt; tile += nw - w0) {
-                if (tile < 0) break;
-                const int i0 = (tile / mt) * 8, j0 = (tile % mt) * 8;
-                if (i0 == kb || j0 == kb || (i0 == nk && j0 == nk)) continue;
-                trail_tile(S, ld, m, kb, kw, i0, j0);
+            const int stp = nw - w0, sq = stp / mt, sr = stp - sq * mt;
+            int it = (w - w0) / mt, jt = (w - w0) - it * mt;   // tile (it, jt) = the warp's linear index, stepped
+            for (int tile = w - w0; tile < mt * mt; tile += stp) {   // without a division per tile
+                if (tile < 0) break;                                  // (warp 0 when it forms the next pivot)
+                const int i0 = it * 8, j0 = jt * 8;
+                if (!(i0 == kb || j0 == kb || (i0 == nk && j0 == nk))) trail_tile(S, ld, m, kb, kw, i0, j0);
+                it += sq;
+                jt += sr;
+                if (jt >= mt) {
+                    jt -= mt;
+                    it++;
+                }
             }
         }
         __syncthreads();
@@ -580,9 +595,10 @@ __global__ void __launch_bounds__(FT) k_factor_chains(const SubDesc* __restrict_
         report(err, bad, sub, i);
     }
 #ifdef HELM_FACTOR_PROF
-    if (threadIdx.x == 0 && blockIdx.x == 0)
-        printf("CPROF m %d blocks %d build %lld pinv %lld row %lld nextpiv %lld trail %lld col %lld store %lld\n", d.m,
-               d.tw, prl[0], prl[1], prl[2], prl[3], prl[4], prl[5], prl[6]);
+    // CTA 0 (a corner subdomain) and the bottom chain of the middle subdomain (an interior one)
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 2 * (gridDim.x / 4 + 32)))
+        printf("CPROF cta %d m %d blocks %d build %lld pinv %lld row %lld nextpiv %lld trail %lld col %lld store %lld\n",
+               blockIdx.x, d.m, d.tw, prl[0], prl[1], prl[2], prl[3], prl[4], prl[5], prl[6]);
 #endif
 }
 
