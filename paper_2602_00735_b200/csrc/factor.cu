@@ -458,6 +458,86 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
 // barrier per pivot), and warp 0 forms the NEXT panel's pivot tile (its trailing update, in the accumulator layout
 // inv8_regs takes) and inverts it while warps 1.. finish the trailing update: three CTA barriers per 8 pivots instead
 // of one 256-thread barrier per pivot.  The DMMA work (row panel, trailing update, column panel) is the same m^3.
+// Full 8-wide panels (kw = 8) with S zero-padded to a multiple of 8 rows (padded rows / columns stay 0 through the
+// elimination): no bounds tests, swizzle bits hoisted -- ncu at c3 counted 31 integer / control instructions per DMMA in
+// the generic tile code (IMAD 26 %, ISETP 11 %, DMMA 3 % of the warp instructions), which left the kernel issue-bound.
+// Row r's swizzle is c ^ (r & 2); rows kb + t and kb + 4 + t (kb a multiple of 8) share the bit t & 2.
+template <bool STORE>
+__device__ __forceinline__ void trail8(z2* S, int ld, int kb, int i0, int j0, z2& c0, z2& c1)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int r = i0 + g, sw = r & 2, tb = t & 2;
+    z2* Sr = S + r * ld;
+    const int cc = j0 + ((2 * t) ^ sw);
+    if (STORE) {
+        c0 = Sr[cc];
+        c1 = Sr[cc + 1];
+    }
+    const z2 a0 = Sr[kb + (t ^ sw)], a1 = Sr[kb + ((4 + t) ^ sw)];
+    const z2 b0 = S[(kb + t) * ld + ((j0 + g) ^ tb)], b1 = S[(kb + 4 + t) * ld + ((j0 + g) ^ tb)];
+    double r20 = 0.0, r21 = 0.0, i20 = 0.0, i21 = 0.0;
+    dmma(c0.x, c1.x, -a0.x, b0.x);
+    dmma(r20, r21, a0.y, b0.y);
+    dmma(c0.y, c1.y, -a0.x, b0.y);
+    dmma(i20, i21, -a0.y, b0.x);
+    dmma(c0.x, c1.x, -a1.x, b1.x);
+    dmma(r20, r21, a1.y, b1.y);
+    dmma(c0.y, c1.y, -a1.x, b1.y);
+    dmma(i20, i21, -a1.y, b1.x);
+    c0.x += r20;
+    c1.x += r21;
+    c0.y += i20;
+    c1.y += i21;
+    if (STORE) {
+        Sr[cc] = c0;
+        Sr[cc + 1] = c1;
+    }
+}
+
+// S[K, j0..j0+7] = Dk S[K, j0..j0+7] (kw = 8): B fragments loaded before the tile is written
+__device__ __forceinline__ void row8(z2* S, int ld, int kb, const z2* Dk, int j0)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tb = t & 2;
+    const z2 b0 = S[(kb + t) * ld + ((j0 + g) ^ tb)], b1 = S[(kb + 4 + t) * ld + ((j0 + g) ^ tb)];
+    const z2 a0 = Dk[g * DLD + t], a1 = Dk[g * DLD + 4 + t];
+    double cr0 = 0.0, cr1 = 0.0, r20 = 0.0, r21 = 0.0, ci0 = 0.0, ci1 = 0.0, i20 = 0.0, i21 = 0.0;
+    dmma(cr0, cr1, a0.x, b0.x);
+    dmma(r20, r21, -a0.y, b0.y);
+    dmma(ci0, ci1, a0.x, b0.y);
+    dmma(i20, i21, a0.y, b0.x);
+    dmma(cr0, cr1, a1.x, b1.x);
+    dmma(r20, r21, -a1.y, b1.y);
+    dmma(ci0, ci1, a1.x, b1.y);
+    dmma(i20, i21, a1.y, b1.x);
+    const int r = kb + g;
+    z2* Sr = S + r * ld;
+    const int cc = j0 + ((2 * t) ^ (r & 2));
+    Sr[cc] = zmk(cr0 + r20, ci0 + i20);
+    Sr[cc + 1] = zmk(cr1 + r21, ci1 + i21);
+}
+
+// S[i0..i0+7, K] = -S[i0..i0+7, K] Dk (kw = 8): A fragments loaded before the tile is written
+__device__ __forceinline__ void col8(z2* S, int ld, int kb, const z2* Dk, int i0)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int r = i0 + g, sw = r & 2;
+    z2* Sr = S + r * ld;
+    const z2 a0 = Sr[kb + (t ^ sw)], a1 = Sr[kb + ((4 + t) ^ sw)];
+    const z2 b0 = Dk[t * DLD + g], b1 = Dk[(4 + t) * DLD + g];
+    double cr0 = 0.0, cr1 = 0.0, r20 = 0.0, r21 = 0.0, ci0 = 0.0, ci1 = 0.0, i20 = 0.0, i21 = 0.0;
+    dmma(cr0, cr1, -a0.x, b0.x);
+    dmma(r20, r21, a0.y, b0.y);
+    dmma(ci0, ci1, -a0.x, b0.y);
+    dmma(i20, i21, -a0.y, b0.x);
+    dmma(cr0, cr1, -a1.x, b1.x);
+    dmma(r20, r21, a1.y, b1.y);
+    dmma(ci0, ci1, -a1.x, b1.y);
+    dmma(i20, i21, -a1.y, b1.x);
+    const int cc = kb + ((2 * t) ^ sw);
+    Sr[cc] = zmk(cr0 + r20, ci0 + i20);
+    Sr[cc + 1] = zmk(cr1 + r21, ci1 + i21);
+}
+
 __device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
 {
     const int ld = lds_of(m);
@@ -479,19 +559,21 @@ __device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
         const int kw = min(8, m - kb);
         const z2* Dk = cur ? sm.Dk[1] : sm.Dk[0];
         // ---- row panel: S[K, j] = Dk S[K, j] (j not in K), one 8 x 8 tile per warp
+        const bool full = kw == 8;
         for (int strip = w; strip < mt; strip += nw)
-            if (strip * 8 != kb) row_strip(S, ld, m, kb, kw, Dk, strip * 8);
+            if (strip * 8 != kb) {
+                if (full) row8(S, ld, kb, Dk, strip * 8);
+                else row_strip(S, ld, m, kb, kw, Dk, strip * 8);
+            }
         __syncthreads();
         CPROF(2);
         // ---- trailing update; warp 0 first forms and inverts the next pivot tile
         const int nk = kb + 8;
         if (w == 0 && nk < m) {
             const int w8 = min(8, m - nk);
-            z2 c0 = (g < w8 && 2 * t < w8) ? S[sx(nk + g, nk + 2 * t, ld)] : zmk(0, 0);
-            z2 c1 = (g < w8 && 2 * t + 1 < w8) ? S[sx(nk + g, nk + 2 * t + 1, ld)] : zmk(0, 0);
-            ztile_fms(
-                c0, c1, kw, [&](int rr, int q) { return nk + rr < m ? S[sx(nk + rr, kb + q, ld)] : zmk(0, 0); },
-                [&](int q, int cc) { return nk + cc < m ? S[sx(kb + q, nk + cc, ld)] : zmk(0, 0); });
+            // (a next panel exists, so this one is full: kw = 8)
+            z2 c0 = S[sx(nk + g, nk + 2 * t, ld)], c1 = S[sx(nk + g, nk + 2 * t + 1, ld)];
+            trail8<false>(S, ld, kb, nk, nk, c0, c1);
             if (!(g < w8 && 2 * t < w8)) c0 = zmk(g == 2 * t ? 1.0 : 0.0, 0.0);          // identity padding
             if (!(g < w8 && 2 * t + 1 < w8)) c1 = zmk(g == 2 * t + 1 ? 1.0 : 0.0, 0.0);
             inv8_regs(c0, c1, w8, nk, bad_row);
@@ -506,7 +588,14 @@ __device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
             for (int tile = w - w0; tile < mt * mt; tile += stp) {   // without a division per tile
                 if (tile < 0) break;                                  // (warp 0 when it forms the next pivot)
                 const int i0 = it * 8, j0 = jt * 8;
-                if (!(i0 == kb || j0 == kb || (i0 == nk && j0 == nk))) trail_tile(S, ld, m, kb, kw, i0, j0);
+                if (!(i0 == kb || j0 == kb || (i0 == nk && j0 == nk))) {
+                    if (full) {
+                        z2 c0, c1;
+                        trail8<true>(S, ld, kb, i0, j0, c0, c1);
+                    } else {
+                        trail_tile(S, ld, m, kb, kw, i0, j0);
+                    }
+                }
                 it += sq;
                 jt += sr;
                 if (jt >= mt) {
@@ -519,7 +608,10 @@ __device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
         CPROF(4);
         // ---- column panel: S[i, K] = -S[i, K] Dk (i not in K); S[K, K] = Dk
         for (int strip = w; strip < mt; strip += nw)
-            if (strip * 8 != kb) col_strip(S, ld, m, kb, kw, Dk, strip * 8);
+            if (strip * 8 != kb) {
+                if (full) col8(S, ld, kb, Dk, strip * 8);
+                else col_strip(S, ld, m, kb, kw, Dk, strip * 8);
+            }
         if (tid < 64) {
             const int r = tid >> 3, c = tid & 7;
             if (r < kw && c < kw) S[sx(kb + r, kb + c, ld)] = Dk[r * DLD + c];
@@ -547,7 +639,7 @@ __device__ FactorSmem carve(unsigned char* base, int m)
 {
     FactorSmem sm;
     sm.S = reinterpret_cast<z2*>(base);
-    sm.Dk[0] = sm.S + (size_t)m * lds_of(m);
+    sm.Dk[0] = sm.S + (size_t)((m + 7) / 8 * 8) * lds_of(m);   // S has m rounded up to a multiple of 8 rows
     sm.Dk[1] = sm.Dk[0] + GB * DLD;
     sm.rowbuf = sm.Dk[1] + 8 * DLD;
     return sm;
@@ -573,6 +665,8 @@ __global__ void __launch_bounds__(FT) k_factor_chains(const SubDesc* __restrict_
     FactorSmem sm = carve(smem, d.m);
     __shared__ int bad;
     if (threadIdx.x == 0) bad = -1;
+    // zero S once: the rows / columns padding m up to a multiple of 8 stay zero through every elimination
+    for (int e = threadIdx.x; e < (d.m + 7) / 8 * 8 * lds_of(d.m); e += blockDim.x) sm.S[e] = zmk(0, 0);
     __syncthreads();
 #ifdef HELM_FACTOR_PROF
     // development aid (-DHELM_FACTOR_PROF): clock64 cycles per phase as thread 0 sees them (waits included), printed
@@ -612,6 +706,8 @@ __global__ void __launch_bounds__(FT) k_factor_twist(const SubDesc* __restrict__
     FactorSmem sm = carve(smem, d.m);
     __shared__ int bad;
     if (threadIdx.x == 0) bad = -1;
+    // zero S once: the rows / columns padding m up to a multiple of 8 stay zero through every elimination
+    for (int e = threadIdx.x; e < (d.m + 7) / 8 * 8 * lds_of(d.m); e += blockDim.x) sm.S[e] = zmk(0, 0);
     __syncthreads();
     build_block(d, d.tw, 2, stc, dinv, sm);
 #ifdef HELM_FACTOR_PROF
@@ -868,7 +964,7 @@ int big_smem_bytes(int m_max, int bc) { return (int)sizeof(z2) * (GB * DLD + GB 
 
 int factor_smem_bytes(int m_max)
 {
-    return (int)(sizeof(z2) * ((size_t)m_max * lds_of(m_max) + GB * DLD + 8 * DLD + 2 * GB));
+    return (int)(sizeof(z2) * ((size_t)((m_max + 7) / 8 * 8) * lds_of(m_max) + GB * DLD + 8 * DLD + 2 * GB));
 }
 
 // 8-wide panels with the register-resident pivot inverse (gj_panels8) unless HELM_FACTOR_PANEL=32
