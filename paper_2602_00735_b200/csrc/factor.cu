@@ -462,6 +462,10 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
 // elimination): no bounds tests, swizzle bits hoisted -- ncu at c3 counted 31 integer / control instructions per DMMA in
 // the generic tile code (IMAD 26 %, ISETP 11 %, DMMA 3 % of the warp instructions), which left the kernel issue-bound.
 // Row r's swizzle is c ^ (r & 2); rows kb + t and kb + 4 + t (kb a multiple of 8) share the bit t & 2.
+#ifndef HELM_TRAIL_SPLIT
+#define HELM_TRAIL_SPLIT 0
+#endif
+constexpr bool TRAIL_SPLIT = HELM_TRAIL_SPLIT;   // split real / imaginary accumulators in the trailing tiles
 template <bool STORE>
 __device__ __forceinline__ void trail8(z2* S, int ld, int kb, int i0, int j0, z2& c0, z2& c1)
 {
@@ -475,19 +479,30 @@ __device__ __forceinline__ void trail8(z2* S, int ld, int kb, int i0, int j0, z2
     }
     const z2 a0 = Sr[kb + (t ^ sw)], a1 = Sr[kb + ((4 + t) ^ sw)];
     const z2 b0 = S[(kb + t) * ld + ((j0 + g) ^ tb)], b1 = S[(kb + 4 + t) * ld + ((j0 + g) ^ tb)];
-    double r20 = 0.0, r21 = 0.0, i20 = 0.0, i21 = 0.0;
-    dmma(c0.x, c1.x, -a0.x, b0.x);
-    dmma(r20, r21, a0.y, b0.y);
-    dmma(c0.y, c1.y, -a0.x, b0.y);
-    dmma(i20, i21, -a0.y, b0.x);
-    dmma(c0.x, c1.x, -a1.x, b1.x);
-    dmma(r20, r21, a1.y, b1.y);
-    dmma(c0.y, c1.y, -a1.x, b1.y);
-    dmma(i20, i21, -a1.y, b1.x);
-    c0.x += r20;
-    c1.x += r21;
-    c0.y += i20;
-    c1.y += i21;
+    if (TRAIL_SPLIT) {
+        double r20 = 0.0, r21 = 0.0, i20 = 0.0, i21 = 0.0;
+        dmma(c0.x, c1.x, -a0.x, b0.x);
+        dmma(r20, r21, a0.y, b0.y);
+        dmma(c0.y, c1.y, -a0.x, b0.y);
+        dmma(i20, i21, -a0.y, b0.x);
+        dmma(c0.x, c1.x, -a1.x, b1.x);
+        dmma(r20, r21, a1.y, b1.y);
+        dmma(c0.y, c1.y, -a1.x, b1.y);
+        dmma(i20, i21, -a1.y, b1.x);
+        c0.x += r20;
+        c1.x += r21;
+        c0.y += i20;
+        c1.y += i21;
+    } else {
+        dmma(c0.x, c1.x, -a0.x, b0.x);
+        dmma(c0.y, c1.y, -a0.x, b0.y);
+        dmma(c0.x, c1.x, a0.y, b0.y);
+        dmma(c0.y, c1.y, -a0.y, b0.x);
+        dmma(c0.x, c1.x, -a1.x, b1.x);
+        dmma(c0.y, c1.y, -a1.x, b1.y);
+        dmma(c0.x, c1.x, a1.y, b1.y);
+        dmma(c0.y, c1.y, -a1.y, b1.x);
+    }
     if (STORE) {
         Sr[cc] = c0;
         Sr[cc + 1] = c1;
