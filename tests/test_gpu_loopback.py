@@ -325,8 +325,8 @@ def test_loopback_c3_full_size(gg):
         assert sketch_rel(X.view(-1).cpu().numpy(), g) <= 1e-6
 
 
-@pytest.mark.parametrize("name,nranks,gg", [("c1", 4, (2, 2)), ("c2", 8, (4, 2))])
-def test_loopback_richardson_residual_band(name, nranks, gg):
+@pytest.mark.parametrize("name,nranks,gg,bc", [("c1", 4, (2, 2), 0), ("c2", 8, (4, 2), 0), ("c1", 4, (2, 2), 1)])
+def test_loopback_richardson_residual_band(name, nranks, gg, bc):
     """Section 3(i): Richardson restricting its residual to the interface band and exchanging only the band
     part of the apply's ghost frame.  Exact counts: every apply after the first receives exactly the band area of the
     ghost frame (helm_halo_band_counts), the first one the full frame, each residual the width-1 frame.  The solution
@@ -335,7 +335,7 @@ def test_loopback_richardson_residual_band(name, nranks, gg):
     from oracle.oracle import richardson as orc_rich
     from paper_2602_00735_b200.helm import halo_band_counts, halo_schedule, make_params
     cfg = CONFIGS[name]
-    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    kw = dict(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, local_bc=bc)
     ref = Context(**kw)
     ref.factor()
     nf = ref.layout.N_cells - 1
@@ -345,7 +345,7 @@ def test_loopback_richardson_residual_band(name, nranks, gg):
     x1f, i1f, _ = ref.richardson(b, rtol=cfg.rtol, maxit=300)
     ref.close()
     B = b.view(nf, nf)
-    p = make_params(cfg.k, cfg.nsub, gpu_grid=gg)
+    p = make_params(cfg.k, cfg.nsub, gpu_grid=gg, local_bc=bc)
     gid = next(_gid)
     torch.cuda.synchronize()
 
