@@ -15,7 +15,7 @@ from paper_2602_00735_b200.workloads import CONFIGS  # noqa: E402
 helm.load(build_if_missing=False)
 for name in sys.argv[1:] or ["c3"]:
     c = CONFIGS[name]
-    for look, panel in (("1", "8"), ("0", "32")):
+    for look, panel in (("1", "8"),):
         os.environ["HELM_FACTOR_LOOKAHEAD"] = look
         os.environ["HELM_FACTOR_PANEL"] = panel
         ctx = helm.Context(c.k, c.nsub, c.nsub)

@@ -5,6 +5,7 @@
 #include <cstdio>
 typedef double2 z2;
 __device__ __forceinline__ z2 zmk(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ z2 zadd(z2 a, z2 b) { return zmk(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ z2 zmul(z2 a, z2 b) { return zmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
 __device__ __forceinline__ void zfms(z2& acc, z2 a, z2 b)
 {
@@ -30,9 +31,9 @@ __device__ __forceinline__ void inv8(z2& x0, z2& x1)
         const z2 pv = shfl_z(mine, 4 * p + (p >> 1));
         const z2 f = shfl_z(mine, (lane & ~3) + (p >> 1));
         const double n2 = pv.x * pv.x + pv.y * pv.y;
-        const double rd = V == 2 ? rcp_fast(n2) : 1.0 / n2;
+        const double rd = (V == 2 || V == 3) ? rcp_fast(n2) : 1.0 / n2;
         const z2 inv = zmk(pv.x * rd, -pv.y * rd);
-        if (V == 0) {
+        if (V == 0 || V == 3) {
             const z2 s0 = c0 == p ? inv : zmul(x0, inv), s1 = c1 == p ? inv : zmul(x1, inv);
             const z2 y0 = shfl_z(s0, 4 * p + t), y1 = shfl_z(s1, 4 * p + t);
             if (r == p) { x0 = s0; x1 = s1; }
@@ -55,6 +56,47 @@ __device__ __forceinline__ void inv8(z2& x0, z2& x1)
         }
     }
 }
+// 2x2 block pivots: 4 steps; pivot block Pq = D[2q..2q+1][2q..2q+1] inverted in closed form
+__device__ __forceinline__ void inv8_2x2(z2& x0, z2& x1)
+{
+    const int lane = threadIdx.x & 31, r = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int ra = 2 * q, rb = 2 * q + 1;
+        // a b / c d: a,b in lane 4 ra + q (slots 0,1), c,d in lane 4 rb + q
+        const z2 a = shfl_z(x0, 4 * ra + q), b = shfl_z(x1, 4 * ra + q);
+        const z2 c = shfl_z(x0, 4 * rb + q), d = shfl_z(x1, 4 * rb + q);
+        // my row's entries in the pivot columns (2q, 2q+1): lane (l & ~3) + q
+        const z2 f0 = shfl_z(x0, (lane & ~3) + q), f1 = shfl_z(x1, (lane & ~3) + q);
+        const z2 det = zmk(a.x * d.x - a.y * d.y - (b.x * c.x - b.y * c.y), a.x * d.y + a.y * d.x - (b.x * c.y + b.y * c.x));
+        const double n2 = det.x * det.x + det.y * det.y;
+        const double rd = 1.0 / n2;
+        const z2 idet = zmk(det.x * rd, -det.y * rd);
+        const z2 i00 = zmul(d, idet), i11 = zmul(a, idet);
+        const z2 i01 = zmul(zmk(-b.x, -b.y), idet), i10 = zmul(zmk(-c.x, -c.y), idet);
+        // pivot rows scaled: Y = Pinv * D[K][c] for my columns (rows ra, rb of my column pair)
+        const z2 ya0 = shfl_z(x0, 4 * ra + t), ya1 = shfl_z(x1, 4 * ra + t);
+        const z2 yb0 = shfl_z(x0, 4 * rb + t), yb1 = shfl_z(x1, 4 * rb + t);
+        const z2 s00 = zadd(zmul(i00, ya0), zmul(i01, yb0)), s01 = zadd(zmul(i00, ya1), zmul(i01, yb1));   // row ra
+        const z2 s10 = zadd(zmul(i10, ya0), zmul(i11, yb0)), s11 = zadd(zmul(i10, ya1), zmul(i11, yb1));   // row rb
+        const bool pc = t == q;   // my column pair is the pivot pair
+        if (r == ra) {
+            x0 = pc ? i00 : s00;
+            x1 = pc ? i01 : s01;
+        } else if (r == rb) {
+            x0 = pc ? i10 : s10;
+            x1 = pc ? i11 : s11;
+        } else if (pc) {   // -F Pinv
+            x0 = zmk(0, 0); x1 = zmk(0, 0);
+            zfms(x0, f0, i00); zfms(x0, f1, i10);
+            zfms(x1, f0, i01); zfms(x1, f1, i11);
+        } else {           // D - F Y
+            zfms(x0, f0, s00); zfms(x0, f1, s10);
+            zfms(x1, f0, s01); zfms(x1, f1, s11);
+        }
+    }
+}
+
 template <int V>
 __global__ void k(z2* io, long long* cyc, int reps)
 {
@@ -65,7 +107,7 @@ __global__ void k(z2* io, long long* cyc, int reps)
     for (int i = 0; i < reps; i++) {
         x0 = a0; x1 = a1;
         x0.x += 1e-300 * i;
-        inv8<V>(x0, x1);
+        if (V == 4) inv8_2x2(x0, x1); else inv8<V>(x0, x1);
         a0.y += 1e-300 * x0.x;   // keep a dependency between reps
     }
     long long t1 = clock64();
@@ -77,18 +119,19 @@ int main()
 {
     z2* io;
     long long* c;
-    cudaMallocManaged(&io, 64 * 4 * sizeof(z2));
-    cudaMallocManaged(&c, 4 * 8);
+    cudaMallocManaged(&io, 64 * 6 * sizeof(z2));
+    cudaMallocManaged(&c, 6 * 8);
     for (int i = 0; i < 64; i++) io[i] = make_double2((i % 9 == 0 ? 4.0 : 0.0) + 0.1 * ((i * 37) % 11) / 11.0, 0.05 * ((i * 13) % 7));
     for (int it = 0; it < 2; it++) {
         k<0><<<1, 32>>>(io, c, 1000); k<1><<<1, 32>>>(io, c, 1000); k<2><<<1, 32>>>(io, c, 1000);
+        k<3><<<1, 32>>>(io, c, 1000); k<4><<<1, 32>>>(io, c, 1000);
         cudaDeviceSynchronize();
     }
-    double d1 = 0, d2 = 0;
-    for (int i = 0; i < 64; i++) {
-        d1 = fmax(d1, fabs(io[128 + i].x - io[64 + i].x) + fabs(io[128 + i].y - io[64 + i].y));
-        d2 = fmax(d2, fabs(io[192 + i].x - io[64 + i].x) + fabs(io[192 + i].y - io[64 + i].y));
-    }
-    printf("inv8 cycles: v0 %lld v1 %lld v2 %lld | max diff v1 %.2e v2 %.2e\n", c[0], c[1], c[2], d1, d2);
+    double d[5] = {0, 0, 0, 0, 0};
+    for (int v = 1; v < 5; v++)
+        for (int i = 0; i < 64; i++)
+            d[v] = fmax(d[v], fabs(io[64 * (v + 1) + i].x - io[64 + i].x) + fabs(io[64 * (v + 1) + i].y - io[64 + i].y));
+    printf("inv8 cycles: v0 %lld v1 %lld v2 %lld v3(fast rcp) %lld v4(2x2 pivots) %lld | max diff vs v0: %.2e %.2e %.2e %.2e\n",
+           c[0], c[1], c[2], c[3], c[4], d[1], d[2], d[3], d[4]);
     return 0;
 }
