@@ -185,6 +185,11 @@ def run_ours(args):
         dist.all_reduce(t)
         return t.cpu().tolist()
 
+    # untimed warm-up of the setup kernels on a small problem (lazy module loading, clocks ramping up from idle)
+    wctx = Context(100.0, 4, 4, stream=stream)
+    wctx.factor()
+    wctx.close()
+    del wctx
     barrier()
     t0 = time.time()
     ctx = Context(cfg.k, cfg.nsub, cfg.nsub, rank=rank, nranks=world, stream=stream, nccl_id=nccl_id)
@@ -352,7 +357,8 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if world == 1:
-        out["tts_vs_k"] = tts_vs_k(stream, cfg, tts_s, tinfo, factor_s)
+        out["tts_vs_k"] = tts_vs_k(stream, cfg, tts_s, tinfo, factor_s, apply_only_ms,
+                                   lay["apply_bytes"] / apply_only_ms / 1e6)
     if world == 1 and not args.no_paper:
         out["paper_table4"] = paper_table4(stream)
         out["gmres_tts_ramp_pou"] = ramp_pou_tts(cfg, stream, xy, amp, sig)
@@ -367,10 +373,10 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main):
-    """BASELINE.json's 'GMRES time-to-solve vs k': every single-GPU config c0..c3 solved to 1e-6 on this GPU (setup,
-    factorisation and solve timed with CUDA events; the bench config's own solve reused), beside the oracle's solve of
-    the same system from the golden records (another host: context)."""
+def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main, apply_main_ms, apply_main_GBps):
+    """BASELINE.json's 'GMRES time-to-solve vs k; local-solve HBM GB/s': every single-GPU config c0..c3 solved to 1e-6
+    on this GPU (factorisation, solve and the apply alone timed with CUDA events; the bench config's own numbers
+    reused), beside the oracle's solve of the same system from the golden records (another host: context)."""
     import torch
 
     from paper_2602_00735_b200 import Context
@@ -388,7 +394,7 @@ def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main):
         if name == cfg_main.name:
             rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": factor_main,
                          "solve_s": tts_main, "iterations": tinfo_main.iterations, "relres_true": tinfo_main.relres_true,
-                         "oracle": orc})
+                         "apply_ms": apply_main_ms, "apply_GBps": apply_main_GBps, "oracle": orc})
             continue
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -402,9 +408,22 @@ def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main):
         _, info, _ = ctx.gmres(b, restart=c.restart, rtol=c.rtol)
         ev[3].record(stream)
         torch.cuda.synchronize()
-        rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": ev[0].elapsed_time(ev[1]) / 1e3,
-                     "solve_s": ev[2].elapsed_time(ev[3]) / 1e3, "iterations": info.iterations,
-                     "relres_true": info.relres_true, "oracle": orc})
+        factor_s_row, solve_s_row = ev[0].elapsed_time(ev[1]) / 1e3, ev[2].elapsed_time(ev[3]) / 1e3
+        v = torch.randn(ctx.n, dtype=torch.complex128, device="cuda")
+        z = torch.empty_like(v)
+        for _ in range(3):
+            ctx.precond_apply(v, z)
+        ev[0].record(stream)
+        for _ in range(20):
+            ctx.precond_apply(v, z)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        apply_ms = ev[0].elapsed_time(ev[1]) / 20
+        lay = ctx.layout
+        rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": factor_s_row,
+                     "solve_s": solve_s_row, "iterations": info.iterations,
+                     "relres_true": info.relres_true, "apply_ms": apply_ms,
+                     "apply_GBps": lay.apply_bytes / apply_ms / 1e6, "oracle": orc})
         ctx.close()
         del ctx, b
         torch.cuda.empty_cache()
