@@ -79,11 +79,14 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--maxit", type=int, default=5000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--pou", default="owner", choices=["owner", "ramp"],
+                    help="partition of unity: the owner write (D10, the hot path) or the paper's linear ramps (P:225)")
     args = ap.parse_args()
     os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
     cfg = CONFIGS[args.config]
     ohash = oracle_hash()          # before the (long) run: the source the numbers come from
-    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub)
+    pou = 1 if args.pou == "ramp" else 0
+    o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, pou=pou)
     t = time.perf_counter()
     ncls = o.factor_dedup()
     factor_s = time.perf_counter() - t
@@ -115,7 +118,7 @@ def main():
     tts = time.perf_counter() - t
     out = {
         "config": cfg.name, "k": cfg.k, "nsub": cfg.nsub, "seed": cfg.seed, "nsrc": cfg.nsrc, "n_free": o.nfree,
-        "restart": cfg.restart, "rtol": cfg.rtol, "maxit": args.maxit, "x0": "zero",
+        "restart": cfg.restart, "rtol": cfg.rtol, "maxit": args.maxit, "x0": "zero", "pou": args.pou,
         "solver": "oracle.gmres: right-preconditioned GMRES(50), MGS, Hermitian inner products (O9, P:240-242)",
         "iterations": res.iterations, "restarts": res.restarts, "status": res.status,
         "relres_est": res.relres_est, "relres_true": res.relres_true, "history": [float(h) for h in res.history],
@@ -128,7 +131,8 @@ def main():
                           "host": host_info(), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())},
         "written_by": "scripts/make_golden.py (imports oracle/ and workloads only)",
     }
-    path = args.out or os.path.join(ROOT, "tests", "golden", f"{cfg.name}_gmres.json")
+    suffix = "" if args.pou == "owner" else "_ramp"
+    path = args.out or os.path.join(ROOT, "tests", "golden", f"{cfg.name}{suffix}_gmres.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps({k: out[k] for k in ("config", "iterations", "restarts", "status", "relres_true", "norm_x")}))
