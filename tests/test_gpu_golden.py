@@ -123,3 +123,23 @@ def test_small_configs_gmres_match_the_oracle_golden(name):
     assert np.max(np.abs(hist[:n] - h_orc[:n]) / h_orc[:n]) <= 1e-6
     assert sketch_rel(x.cpu().numpy(), g) <= 1e-6
     ctx.close()
+
+
+@pytest.mark.skipif(not os.path.exists(golden_path("c3_ramp")), reason="no c3 ramp-PoU golden record")
+def test_c3_ramp_pou_gmres_matches_the_oracle_golden():
+    """NEXT-3 at full size: GMRES(50) with the paper's linear-ramp partition of unity at c3 against the
+    oracle-only golden record (scripts/make_golden.py c3 --pou ramp)."""
+    from paper_2602_00735_b200.helm import POU_RAMP
+    g = load_golden("c3_ramp")
+    cfg = CONFIGS["c3"]
+    ctx = Context(cfg.k, cfg.nsub, cfg.nsub, pou=POU_RAMP)
+    ctx.factor()
+    b = ctx.rhs(*sources(cfg))
+    x, info, hist = ctx.gmres(b, restart=cfg.restart, rtol=cfg.rtol, maxit=g["maxit"], history=True)
+    assert info.status == g["status"] == 0 and abs(info.iterations - g["iterations"]) <= 1
+    h_orc = np.asarray(g["history"])
+    n = min(len(hist), len(h_orc))
+    assert np.max(np.abs(hist[:n] - h_orc[:n]) / h_orc[:n]) <= 1e-6
+    assert sketch_rel(x.cpu().numpy(), g) <= 1e-6
+    ctx.close()
+    torch.cuda.empty_cache()
