@@ -32,3 +32,20 @@ def test_depths_spread_over_a_cycle():
     ds = bench.depths(20, 50)
     assert len(ds) == 20 and min(ds) >= 0 and max(ds) <= 49
     assert abs(sum(ds) / len(ds) - 24.5) <= 1.0          # the cycle-average depth
+
+
+def test_relaunch_command_for_several_gpus(monkeypatch):
+    """--gpus N without torchrun's environment re-launches bench.py under torch.distributed.run: one process per GPU,
+    rendezvous on 127.0.0.1, the same arguments."""
+    sys.path.insert(0, ROOT)
+    import argparse
+
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "7"])
+    bench.relaunch_distributed(argparse.Namespace(gpus=4))
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "7"] and cmd[-5].endswith("bench.py")
