@@ -1,5 +1,5 @@
-"""Factorisation time (CUDA events around helm_factor, best of 3 contexts) per config; HELM_FACTOR_LOOKAHEAD=0/1
-selects the pivot-inverse lookahead.  python scripts/factor_time.py c2 c3"""
+"""Factorisation time (CUDA events around helm_factor, best of 3 contexts) per config, with the default 8-wide panels;
+HELM_LIB_PATH times another build of libhelm (A/B of compile-time variants).  python scripts/factor_time.py c2 c3"""
 import os
 import sys
 
