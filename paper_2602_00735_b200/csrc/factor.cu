@@ -74,11 +74,13 @@ __device__ __forceinline__ void ztile_fms(z2& c0, z2& c1, int kw, LA la, LB lb)
 // GJW warps of the CTA (lane c owns column c, warp w the rows r = w, w + GJW, ...; named barrier 2 over those warps
 // only).  A zero pivot is recorded as row kb + p.
 // Shared-memory layout of the block S being inverted: row stride ld = round_up(m, 8) + 4 16-B words (== 4 mod 8) and
-// the column swizzle c ^ (r & 2).  An LDS.128 is served 8 lanes at a time; with this layout the DMMA fragment loads of
-// both operands -- A (lanes: rows g in {2h, 2h+1}, columns t in 0..3) and B (rows t, columns g) -- hit 8 distinct 16-B
-// bank groups per quarter warp (with ld == 1 mod 8 both were 2-way conflicted: 5.3e9 excess wavefronts at c3, ncu).
+// the column swizzle c ^ (r & 3).  An LDS.128 is served 8 lanes at a time; with this layout the DMMA fragment loads of
+// both operands -- A (lanes: rows g in {2h, 2h+1}, columns t in 0..3) and B (rows t, columns g) -- AND the loads and
+// stores of the accumulator tile C (rows g in {2h, 2h+1}, columns 2t or 2t + 1) hit 8 distinct 16-B bank groups per
+// quarter warp.  (ld == 1 mod 8 left A and B 2-way conflicted: 5.3e9 excess wavefronts at c3; the swizzle c ^ (r & 2)
+// fixed those but left C 2-way conflicted: 3.9e9 excess shared-load wavefronts, ncu.)
 __host__ __device__ __forceinline__ int lds_of(int m) { return ((m + 7) / 8) * 8 + 4; }
-__device__ __forceinline__ int sx(int r, int c, int ld) { return r * ld + (c ^ (r & 2)); }
+__device__ __forceinline__ int sx(int r, int c, int ld) { return r * ld + (c ^ (r & 3)); }
 
 constexpr int GJW = 8;
 // |pivot| < 1e-12 is reported as singular: the stencil entries of A_j are O(1e-3 .. 10) (P1/Q1 stiffness is
@@ -461,7 +463,7 @@ __device__ void gj_blocked(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
 // Full 8-wide panels (kw = 8) with S zero-padded to a multiple of 8 rows (padded rows / columns stay 0 through the
 // elimination): no bounds tests, swizzle bits hoisted -- ncu at c3 counted 31 integer / control instructions per DMMA in
 // the generic tile code (IMAD 26 %, ISETP 11 %, DMMA 3 % of the warp instructions), which left the kernel issue-bound.
-// Row r's swizzle is c ^ (r & 2); rows kb + t and kb + 4 + t (kb a multiple of 8) share the bit t & 2.
+// Row r's swizzle is c ^ (r & 3); rows kb + t and kb + 4 + t (kb a multiple of 8) both swizzle by t.
 #ifndef HELM_TRAIL_SPLIT
 #define HELM_TRAIL_SPLIT 0
 #endif
@@ -470,12 +472,12 @@ template <bool STORE>
 __device__ __forceinline__ void trail8(z2* S, int ld, int kb, int i0, int j0, z2& c0, z2& c1)
 {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int r = i0 + g, sw = r & 2, tb = t & 2;
+    const int r = i0 + g, sw = r & 3, tb = t;      // rows kb + t and kb + 4 + t swizzle by t
     z2* Sr = S + r * ld;
-    const int cc = j0 + ((2 * t) ^ sw);
+    const int cA = j0 + ((2 * t) ^ sw), cB = j0 + ((2 * t + 1) ^ sw);
     if (STORE) {
-        c0 = Sr[cc];
-        c1 = Sr[cc + 1];
+        c0 = Sr[cA];
+        c1 = Sr[cB];
     }
     const z2 a0 = Sr[kb + (t ^ sw)], a1 = Sr[kb + ((4 + t) ^ sw)];
     const z2 b0 = S[(kb + t) * ld + ((j0 + g) ^ tb)], b1 = S[(kb + 4 + t) * ld + ((j0 + g) ^ tb)];
@@ -504,15 +506,15 @@ __device__ __forceinline__ void trail8(z2* S, int ld, int kb, int i0, int j0, z2
         dmma(c0.y, c1.y, -a1.y, b1.x);
     }
     if (STORE) {
-        Sr[cc] = c0;
-        Sr[cc + 1] = c1;
+        Sr[cA] = c0;
+        Sr[cB] = c1;
     }
 }
 
 // S[K, j0..j0+7] = Dk S[K, j0..j0+7] (kw = 8): B fragments loaded before the tile is written
 __device__ __forceinline__ void row8(z2* S, int ld, int kb, const z2* Dk, int j0)
 {
-    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tb = t & 2;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tb = t;
     const z2 b0 = S[(kb + t) * ld + ((j0 + g) ^ tb)], b1 = S[(kb + 4 + t) * ld + ((j0 + g) ^ tb)];
     const z2 a0 = Dk[g * DLD + t], a1 = Dk[g * DLD + 4 + t];
     double cr0 = 0.0, cr1 = 0.0, r20 = 0.0, r21 = 0.0, ci0 = 0.0, ci1 = 0.0, i20 = 0.0, i21 = 0.0;
@@ -526,16 +528,15 @@ __device__ __forceinline__ void row8(z2* S, int ld, int kb, const z2* Dk, int j0
     dmma(i20, i21, a1.y, b1.x);
     const int r = kb + g;
     z2* Sr = S + r * ld;
-    const int cc = j0 + ((2 * t) ^ (r & 2));
-    Sr[cc] = zmk(cr0 + r20, ci0 + i20);
-    Sr[cc + 1] = zmk(cr1 + r21, ci1 + i21);
+    Sr[j0 + ((2 * t) ^ (r & 3))] = zmk(cr0 + r20, ci0 + i20);
+    Sr[j0 + ((2 * t + 1) ^ (r & 3))] = zmk(cr1 + r21, ci1 + i21);
 }
 
 // S[i0..i0+7, K] = -S[i0..i0+7, K] Dk (kw = 8): A fragments loaded before the tile is written
 __device__ __forceinline__ void col8(z2* S, int ld, int kb, const z2* Dk, int i0)
 {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int r = i0 + g, sw = r & 2;
+    const int r = i0 + g, sw = r & 3;
     z2* Sr = S + r * ld;
     const z2 a0 = Sr[kb + (t ^ sw)], a1 = Sr[kb + ((4 + t) ^ sw)];
     const z2 b0 = Dk[t * DLD + g], b1 = Dk[(4 + t) * DLD + g];
@@ -548,9 +549,8 @@ __device__ __forceinline__ void col8(z2* S, int ld, int kb, const z2* Dk, int i0
     dmma(r20, r21, a1.y, b1.y);
     dmma(ci0, ci1, -a1.x, b1.y);
     dmma(i20, i21, -a1.y, b1.x);
-    const int cc = kb + ((2 * t) ^ sw);
-    Sr[cc] = zmk(cr0 + r20, ci0 + i20);
-    Sr[cc + 1] = zmk(cr1 + r21, ci1 + i21);
+    Sr[kb + ((2 * t) ^ sw)] = zmk(cr0 + r20, ci0 + i20);
+    Sr[kb + ((2 * t + 1) ^ sw)] = zmk(cr1 + r21, ci1 + i21);
 }
 
 __device__ void gj_panels8(int m, FactorSmem sm, int* bad_row CPROF_ARGS)
