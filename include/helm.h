@@ -206,6 +206,17 @@ int helm_set_residual_band(helm_ctx* ctx, int on);
  * exchanges, halo messages posted, allreduces issued}; reset != 0 zeroes them after reading.  Host only. */
 int helm_comm_counters(helm_ctx* ctx, int reset, long long* out4);
 
+/* Shared factors (D28; P:85-94 defines A_j, P:143-147 its use).  Subdomains whose assembled local operators
+ * are bitwise equal (with c = 1, the interior subdomains are translates of one another) form a class; helm_factor
+ * factors one representative per class and every member uses its inverses, and when the classes are large the apply
+ * runs class tiles of 16 subdomains as complex GEMMs on the FP64 tensor cores (k_apply_batch).  Filled after
+ * helm_factor (HELM_ESTATE before): out4 = {classes, shared-factor apply on (1) / off (0), tiles of that apply,
+ * factor bytes held on the device}; class_of (may be NULL) receives n_sub_local class indices, cap entries at most.
+ * Environment (read at helm_setup): HELM_SHARE_FACTORS=0 factors every subdomain (one class each);
+ * HELM_APPLY_BATCH=1 / 0 forces the tensor-core apply on / off (default: on when the whole problem has at least
+ * 4 x SMs subdomains and m_max <= 128).  Host only. */
+int helm_factor_classes(const helm_ctx* ctx, long long* out4, int* class_of, int cap);
+
 /* Host logic, no GPU: this rank's apply-frame halo volume in complex elements -- out4 = {sent full, sent band, received
  * full, received band} (band = the section 3(i) restriction) -- and the band sub-rectangles (i0, i1, j0, j1 per
  * rectangle, node indices, canonical packing order) of message `msg` of helm_halo_schedule(width 0), side 0 = its

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <complex>
 #include <condition_variable>
 #include <map>
@@ -439,6 +440,25 @@ struct helm_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
     int launches = 0;
 
+    // shared factors (D28): classes of subdomains whose local operators are bitwise equal; one representative per
+    // class is factored and every member's fac_off points at its factors.  HELM_SHARE_FACTORS=0 factors every
+    // subdomain (the general path, e.g. for a variable wave speed where no two local operators agree).
+    bool share = true;
+    std::vector<int> cls_rep, cls_of;
+    long long n_dinv_all = 0;   // factor complex entries without sharing (layout reporting)
+    // shared-factor apply on the tensor cores (batch.cu): HELM_APPLY_BATCH = 0 / 1 forces it off / on; by default on
+    // when the factors are shared, m_max <= 128 and the whole problem has >= 4 x SMs subdomains (decided on global
+    // quantities so that every rank of a decomposition takes the same path)
+    bool batched = false;
+    z2* d_dinvB = nullptr;
+    BatchTile* d_tiles = nullptr;
+    BatchClass* d_bcls = nullptr;
+    int* d_members = nullptr;
+    z2* d_bscr = nullptr;
+    int bt_ntiles = 0, bt_nint = 0, bt_grid = 0, bt_grid_int = 0, bt_grid_bnd = 0;
+    int bt_block = 0, bt_smem = 0, bt_slot = 0, bt_nslots = 0, bt_mpmax = 0, bt_occ = 0;
+    long long bt_scr_per_cta = 0, dinvB_len = 0;
+
     // constant interior stencil (rows with gamma = 1 on all six triangles) and its node range
     int cst[4] = {0, 0, 0, 0};
     z2 c7[9] = {};
@@ -650,7 +670,7 @@ int build_layout(helm_ctx* ctx)
             ctx->band_bytes += 16 * (n * (2LL * (d.m + 1) + 1) + n + owned);
             ctx->subs.push_back(d);
         }
-    ctx->n_dinv = fac;
+    ctx->n_dinv = ctx->n_dinv_all = fac;
     ctx->n_stc = stc;
     // ramp PoU: the gather re-reads every weighted value once and writes z once
     if (ctx->p.pou == HELM_POU_RAMP) ctx->apply_bytes += 16 * (ctx->pou_len + ctx->n_local);
@@ -939,6 +959,39 @@ ApplyArgs apply_args(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long lon
     return a;
 }
 
+// shared-factor apply (batch.cu) over tiles [t0, t0 + nt) with `grid` CTAs whose scratch starts at CTA slot `slot0`
+BatchArgs batch_args(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z, int t0, int nt,
+                     int slot0)
+{
+    BatchArgs b{};
+    b.desc = ctx->d_desc;
+    b.tiles = ctx->d_tiles + t0;
+    b.ntiles = nt;
+    b.members = ctx->d_members;
+    b.cls = ctx->d_bcls;
+    b.dinvB = ctx->d_dinvB;
+    b.stencil = ctx->d_stc;
+    b.in = in;
+    b.in_i0 = in_i0;
+    b.in_j0 = in_j0;
+    b.in_stride = in_stride;
+    b.out = z;
+    b.out_i0 = ctx->G.i0;
+    b.out_j0 = ctx->G.j0;
+    b.out_stride = ctx->G.i1 - ctx->G.i0;
+    b.scratch = ctx->d_bscr + (long long)slot0 * ctx->bt_scr_per_cta;
+    b.scratch_per_cta = ctx->bt_scr_per_cta;
+    b.cc = CplConst{ctx->lcS, ctx->lcSW, ctx->lcN, ctx->lcNE, ctx->lcSE, ctx->lcNW, ctx->G.ns};
+    b.pou_buf = ctx->d_pou;
+    b.delta = ctx->G.wo;
+    return b;
+}
+
+void launch_batch(helm_ctx* ctx, const BatchArgs& b, int grid, cudaStream_t st)
+{
+    launch_apply_batch(b, grid, ctx->bt_block, ctx->bt_smem, ctx->bt_slot, ctx->bt_nslots, ctx->bt_mpmax, st);
+}
+
 int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z)
 {
     if (!ctx->factored) return set_err(ctx, HELM_ESTATE, "preconditioner applied before helm_factor");
@@ -946,7 +999,10 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int rc;
     if ((rc = prof_begin(ctx, &e0, &e1))) return rc;
-    if (ctx->sp_G > 0) {
+    if (ctx->batched) {
+        const int grid = std::min(ctx->bt_ntiles, ctx->bt_grid_int + ctx->bt_grid_bnd);
+        launch_batch(ctx, batch_args(ctx, in, in_i0, in_j0, in_stride, z, 0, ctx->bt_ntiles, 0), grid, ctx->stream);
+    } else if (ctx->sp_G > 0) {
         const int e = launch_apply_split(a, (int)ctx->subs.size(), ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
                                          ctx->sp_ncw, ctx->m_max, ctx->sp_nss, ctx->stream);
         if (e != 0) {
@@ -986,7 +1042,13 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
         if ((rc = prof_begin(ctx, &e0, &e1))) return rc;
         ApplyArgs a = apply_args(ctx, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, z);
         auto part = [&](int grid, cudaStream_t st) -> int {
-            if (ctx->sp_G > 0) {
+            if (ctx->batched) {
+                const bool inner = st == ctx->stream;   // interior tiles on the library stream, the rest after the halo
+                const int t0 = inner ? 0 : ctx->bt_nint, nt = inner ? ctx->bt_nint : ctx->bt_ntiles - ctx->bt_nint;
+                launch_batch(ctx, batch_args(ctx, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, z, t0, nt,
+                                             inner ? 0 : ctx->bt_grid_int),
+                             inner ? ctx->bt_grid_int : ctx->bt_grid_bnd, st);
+            } else if (ctx->sp_G > 0) {
                 const int e = launch_apply_split(a, a.nsub, ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
                                                  ctx->sp_ncw, ctx->m_max, ctx->sp_nss, st);
                 if (e != 0) {
@@ -1805,9 +1867,17 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     // Among the G <= 8 whose clusters are all resident at once, take the smallest that keeps >= 80 % of the SMs
     // streaming (more G only adds exchange partners), else the largest; each CTA's ring takes the shared memory its
     // share of an SM leaves.  HELM_SPLIT_G overrides (0 = off).
+    // D28: factor sharing, and the shared-factor apply on the tensor cores when the classes are large
+    if (const char* e = getenv("HELM_SHARE_FACTORS")) ctx->share = e[0] != '0';
+    {
+        const long long nsub_global = (long long)ctx->G.P[0] * ctx->G.P[1];
+        bool b = nsub_global >= 4LL * nsm;
+        if (const char* e = getenv("HELM_APPLY_BATCH")) b = e[0] == '1';
+        ctx->batched = b && ctx->share && ctx->m_max <= 128;
+    }
     const char* env_g = getenv("HELM_SPLIT_G");
     const int gforce = env_g ? atoi(env_g) : -1;
-    if (nsub < nsm || gforce > 0) {
+    if (!ctx->batched && (nsub < nsm || gforce > 0)) {
         int gbest = 0, cbest = 1;
         for (int G = 1; G <= 8; G++) {
             if (gforce >= 0 && G != gforce) continue;
@@ -1907,6 +1977,19 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
         }
     }
     CK(cudaStreamSynchronize(ctx->stream));
+    return HELM_OK;
+}
+
+int helm_factor_classes(const helm_ctx* ctx, long long* out4, int* class_of, int cap)
+{
+    if (!ctx || !out4) return HELM_EINVAL;
+    if (!ctx->factored) return HELM_ESTATE;
+    out4[0] = (long long)ctx->cls_rep.size();
+    out4[1] = ctx->batched ? 1 : 0;
+    out4[2] = ctx->bt_ntiles;
+    out4[3] = 16LL * (ctx->n_dinv + ctx->dinvB_len);
+    if (class_of)
+        for (int j = 0; j < (int)ctx->cls_of.size() && j < cap; j++) class_of[j] = ctx->cls_of[j];
     return HELM_OK;
 }
 
@@ -2105,22 +2188,229 @@ int helm_rhs(helm_ctx* ctx, int nsrc, const double* xy_host, const helm_z* amp_h
     return rc;
 }
 
+// D28: group the subdomains into classes whose assembled local operators are bitwise equal.  Candidates share every
+// shape field of the descriptor (block sizes, twist, owned ranges, constant-coupling range, stencil width, impedance
+// faces); k_stencil_eq then compares each candidate's whole local stencil with its class representative, bit for bit,
+// and a candidate that differs anywhere starts a class of its own.  Fills cls_rep / cls_of (HELM_SHARE_FACTORS=0: one
+// class per subdomain).
+static int build_classes(helm_ctx* ctx)
+{
+    const int n = (int)ctx->subs.size();
+    ctx->cls_rep.clear();
+    ctx->cls_of.assign(n, -1);
+    if (!ctx->share) {
+        for (int j = 0; j < n; j++) {
+            ctx->cls_of[j] = j;
+            ctx->cls_rep.push_back(j);
+        }
+        return HELM_OK;
+    }
+    auto key = [](const SubDesc& d) {
+        return std::array<int, 16>{d.m, d.nb, d.tw, d.lo, d.hi, d.olo, d.ohi, d.cx0, d.cx1, d.cy0, d.cy1, d.ns, d.imp,
+                                   d.flags, d.fx1 - d.fx0, d.fy1 - d.fy0};
+    };
+    std::map<std::array<int, 16>, std::vector<int>> groups;
+    for (int j = 0; j < n; j++) groups[key(ctx->subs[j])].push_back(j);
+    std::vector<std::vector<int>> pending;
+    for (auto& kv : groups) pending.push_back(kv.second);
+    int2* d_pairs = nullptr;
+    int* d_diff = nullptr;
+    int rc = HELM_OK;
+    if ((rc = dalloc(ctx, &d_pairs, n)) || (rc = dalloc(ctx, &d_diff, n))) {
+        cudaFree(d_pairs);
+        return rc;
+    }
+    std::vector<int2> pairs;
+    std::vector<int> diff;
+    while (!pending.empty() && rc == HELM_OK) {
+        // one comparison pass over every pending group: member vs the group's first subdomain
+        pairs.clear();
+        for (auto& grp : pending)
+            for (size_t q = 1; q < grp.size(); q++) pairs.push_back(make_int2(grp[q], grp[0]));
+        diff.assign(pairs.size(), 0);
+        if (!pairs.empty()) {
+            if (cudaMemcpyAsync(d_pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice,
+                                ctx->stream) != cudaSuccess) {
+                rc = set_err(ctx, HELM_ECUDA, "class detection: copy failed");
+                break;
+            }
+            launch_stencil_eq(ctx->d_desc, ctx->d_stc, d_pairs, (int)pairs.size(), d_diff, ctx->stream);
+            if (cudaMemcpyAsync(diff.data(), d_diff, sizeof(int) * diff.size(), cudaMemcpyDeviceToHost, ctx->stream) !=
+                    cudaSuccess ||
+                cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+                rc = set_err(ctx, HELM_ECUDA, "class detection: %s", cudaGetErrorString(cudaGetLastError()));
+                break;
+            }
+        }
+        std::vector<std::vector<int>> next;
+        size_t p = 0;
+        for (auto& grp : pending) {
+            const int c = (int)ctx->cls_rep.size();
+            ctx->cls_rep.push_back(grp[0]);
+            ctx->cls_of[grp[0]] = c;
+            std::vector<int> rest;
+            for (size_t q = 1; q < grp.size(); q++, p++) {
+                if (diff[p]) rest.push_back(grp[q]);
+                else ctx->cls_of[grp[q]] = c;
+            }
+            if (!rest.empty()) next.push_back(rest);
+        }
+        pending.swap(next);
+    }
+    cudaFree(d_pairs);
+    cudaFree(d_diff);
+    return rc;
+}
+
+// The shared-factor apply (batch.cu): class factors in the batch layout, tiles of BATCH_NT members of one class
+// (cost-sorted; on several ranks with the overlapped apply the interior subdomains' tiles first), launch
+// configuration and per-CTA scratch.
+static int setup_batch(helm_ctx* ctx)
+{
+    int rc;
+    const int ncls = (int)ctx->cls_rep.size();
+    std::vector<BatchClass> bc(ncls);
+    long long off = 0;
+    int mpmax = 0;
+    for (int c = 0; c < ncls; c++) {
+        const SubDesc& r = ctx->subs[ctx->cls_rep[c]];
+        bc[c].rep = ctx->cls_rep[c];
+        bc[c].mp = (r.m + 7) / 8 * 8;
+        bc[c].S = bc[c].mp + 2;
+        bc[c].off = off;
+        off += (long long)r.nb * bc[c].mp * bc[c].S;
+        mpmax = std::max(mpmax, bc[c].mp);
+    }
+    ctx->dinvB_len = off;
+    ctx->bt_mpmax = mpmax;
+    if ((rc = dalloc(ctx, &ctx->d_dinvB, off)) || (rc = dalloc(ctx, &ctx->d_bcls, ncls))) return rc;
+    for (int c = 0; c < ncls; c++) {
+        const SubDesc& r = ctx->subs[bc[c].rep];
+        launch_relayout_batch(ctx->d_dinv, r.fac_off, r.m, r.nb, ctx->d_dinvB + bc[c].off, bc[c].mp, bc[c].S,
+                              ctx->stream);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->d_bcls, bc.data(), sizeof(BatchClass) * ncls, cudaMemcpyHostToDevice, ctx->stream));
+    // tiles: the members of each class in subdomain order, BATCH_NT at a time; sorted by cost, most expensive first
+    std::vector<BatchTile> tiles;
+    std::vector<int> members;
+    auto make_tiles = [&](const std::vector<int>& set) {
+        std::vector<std::vector<int>> per(ncls);
+        for (int j : set) per[ctx->cls_of[j]].push_back(j);
+        std::vector<BatchTile> t;
+        for (int c = 0; c < ncls; c++)
+            for (size_t q = 0; q < per[c].size(); q += BATCH_NT) {
+                BatchTile bt{};
+                bt.cls = c;
+                bt.first = (int)members.size();
+                bt.cnt = (int)std::min<size_t>(BATCH_NT, per[c].size() - q);
+                members.insert(members.end(), per[c].begin() + q, per[c].begin() + q + bt.cnt);
+                t.push_back(bt);
+            }
+        auto cost = [&](const BatchTile& x) {
+            const SubDesc& d = ctx->subs[bc[x.cls].rep];
+            return (long long)(d.nb + d.hi - d.lo) * bc[x.cls].mp * bc[x.cls].mp;
+        };
+        std::stable_sort(t.begin(), t.end(), [&](const BatchTile& x, const BatchTile& y) { return cost(x) > cost(y); });
+        tiles.insert(tiles.end(), t.begin(), t.end());
+        return (int)t.size();
+    };
+    const int nsub = (int)ctx->subs.size();
+    if (ctx->overlap) {
+        const GridInfo& G = ctx->G;
+        std::vector<int> si, sb;
+        for (int j = 0; j < nsub; j++) {
+            const SubDesc& sd = ctx->subs[j];
+            const bool inside = sd.gx0 >= G.i0 && sd.gx0 + sd.m <= G.i1 && sd.gy0 >= G.j0 && sd.gy0 + sd.nb <= G.j1;
+            (inside ? si : sb).push_back(j);
+        }
+        ctx->bt_nint = make_tiles(si);
+        make_tiles(sb);
+    } else {
+        std::vector<int> all(nsub);
+        for (int j = 0; j < nsub; j++) all[j] = j;
+        ctx->bt_nint = make_tiles(all);
+    }
+    ctx->bt_ntiles = (int)tiles.size();
+    if ((rc = dalloc(ctx, &ctx->d_tiles, tiles.size())) || (rc = dalloc(ctx, &ctx->d_members, members.size())))
+        return rc;
+    CK(cudaMemcpyAsync(ctx->d_tiles, tiles.data(), sizeof(BatchTile) * tiles.size(), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_members, members.data(), sizeof(int) * members.size(), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    batch_configure(mpmax, &ctx->bt_block, &ctx->bt_smem, &ctx->bt_slot, &ctx->bt_nslots, &ctx->bt_occ);
+    if (ctx->bt_occ < 1) return set_err(ctx, HELM_ECUDA, "shared-factor apply kernel does not fit (m_max %d)", mpmax);
+    int nsm = 148, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int slots = nsm * ctx->bt_occ;
+    auto trim = [](int n, int s) {
+        s = std::max(1, std::min(s, n));
+        const int per = (n + s - 1) / s;
+        return (n + per - 1) / per;
+    };
+    const int nbnd = ctx->bt_ntiles - ctx->bt_nint;
+    if (ctx->overlap && ctx->bt_nint > 0 && nbnd > 0) {
+        int sb = (int)std::lround((double)slots * nbnd / ctx->bt_ntiles);
+        sb = std::max(1, std::min(slots - 1, sb));
+        ctx->bt_grid_int = trim(ctx->bt_nint, slots - sb);
+        ctx->bt_grid_bnd = trim(nbnd, sb);
+    } else {
+        ctx->bt_grid_int = trim(ctx->bt_ntiles, slots);
+        ctx->bt_grid_bnd = 0;
+    }
+    ctx->bt_grid = ctx->bt_grid_int;
+    long long per = 0;
+    for (int c = 0; c < ncls; c++) {
+        const SubDesc& d = ctx->subs[bc[c].rep];
+        per = std::max(per, (long long)(d.hi - d.lo + 1) * BATCH_NT * bc[c].mp);
+    }
+    ctx->bt_scr_per_cta = per;
+    if ((rc = dalloc(ctx, &ctx->d_bscr, (size_t)per * (ctx->bt_grid_int + ctx->bt_grid_bnd)))) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HELM_OK;
+}
+
 static int factor_impl(helm_ctx* ctx)
 {
     NvtxRange nv_("helm.factor");
     if (!ctx) return HELM_EINVAL;
     if (ctx->factored) return HELM_OK;
     int rc;
-    if (!ctx->d_dinv && (rc = dalloc(ctx, &ctx->d_dinv, ctx->n_dinv))) return rc;
+    // D28: factor one representative per class of bitwise-equal local operators; members alias its factors
+    if (ctx->cls_rep.empty() && (rc = build_classes(ctx))) return rc;
+    const int ncls = (int)ctx->cls_rep.size();
+    std::vector<SubDesc> reps(ncls);
+    long long fac = 0;
+    for (int c = 0; c < ncls; c++) {
+        reps[c] = ctx->subs[ctx->cls_rep[c]];
+        reps[c].fac_off = fac;
+        fac += (long long)reps[c].nb * reps[c].m * reps[c].m;
+    }
+    for (size_t j = 0; j < ctx->subs.size(); j++) ctx->subs[j].fac_off = reps[ctx->cls_of[j]].fac_off;
+    ctx->n_dinv = fac;
+    SubDesc* d_reps = nullptr;
+    if ((rc = dalloc(ctx, &d_reps, ncls))) return rc;
+    if (!ctx->d_dinv && (rc = dalloc(ctx, &ctx->d_dinv, ctx->n_dinv))) {
+        cudaFree(d_reps);
+        return rc;
+    }
+    CK(cudaMemcpyAsync(d_reps, reps.data(), sizeof(SubDesc) * ncls, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_desc, ctx->subs.data(), sizeof(SubDesc) * ctx->subs.size(), cudaMemcpyHostToDevice,
+                       ctx->stream));
     CK(cudaMemsetAsync(ctx->d_err, 0, 4 * sizeof(int), ctx->stream));
-    launch_factor(ctx->d_desc, ctx->subs.data(), (int)ctx->subs.size(), ctx->m_max, ctx->d_stc, ctx->d_dinv,
-                  ctx->d_err, ctx->stream);
+    launch_factor(d_reps, reps.data(), ncls, ctx->m_max, ctx->d_stc, ctx->d_dinv, ctx->d_err, ctx->stream);
     CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_reps);
     if (ctx->sp_G > 1) {
-        // cluster-split apply: relay every inverse block slab-major (one contiguous panel per CTA of a chain)
+        // cluster-split apply: relay every inverse block slab-major (one contiguous panel per CTA of a chain) --
+        // once per class (members alias the representative's blocks)
         std::vector<int2> blocks;
-        for (int j = 0; j < (int)ctx->subs.size(); j++)
+        for (int c = 0; c < ncls; c++) {
+            const int j = ctx->cls_rep[c];
             for (int i = 0; i < ctx->subs[j].nb; i++) blocks.push_back(make_int2(j, i));
+        }
         int2* d_blocks = nullptr;
         z2* d_tmp = nullptr;
         const int grid = 148;
@@ -2146,7 +2436,8 @@ static int factor_impl(helm_ctx* ctx)
     CK(cudaStreamSynchronize(ctx->stream));
     if (herr[0])
         return set_err(ctx, HELM_EZEROPIVOT, "zero pivot (|pivot| < 1e-12 or not finite): subdomain %d, block %d, row %d",
-                       herr[1], herr[2], herr[3]);
+                       herr[1] >= 0 && herr[1] < ncls ? ctx->cls_rep[herr[1]] : herr[1], herr[2], herr[3]);
+    if (ctx->batched && !ctx->d_dinvB && (rc = setup_batch(ctx))) return rc;
     if ((rc = ensure_krylov(ctx, 0))) return rc;   // the solvers' work buffers belong to setup, not to a solve
     ctx->factored = true;
     return HELM_OK;
@@ -2312,6 +2603,9 @@ void helm_destroy(helm_ctx* ctx)
         ctx->loop = nullptr;
     }
     if (ctx->d_loop_tmp) cudaFree(ctx->d_loop_tmp);
+    for (void* b : {(void*)ctx->d_dinvB, (void*)ctx->d_tiles, (void*)ctx->d_bcls, (void*)ctx->d_members,
+                    (void*)ctx->d_bscr})
+        if (b) cudaFree(b);
     void* bufs[] = {ctx->d_desc, ctx->d_order, ctx->d_A7, ctx->d_stc, ctx->d_dinv, ctx->d_scratch, ctx->d_err,
                     ctx->d_V, ctx->d_w, ctx->d_z, ctx->d_t, ctx->d_r, ctx->d_xb, ctx->d_bb, ctx->d_h1, ctx->d_h2,
                     ctx->d_Hcol, ctx->d_y, ctx->d_norm, ctx->d_zpart, ctx->d_dpart, ctx->d_ext, ctx->d_sq,

@@ -201,3 +201,37 @@ void launch_axpy(z2* x, const z2* z, long long n, cudaStream_t s);
 void launch_copy(z2* dst, const z2* src, long long n, cudaStream_t s);
 void launch_sum_ranks(const double* const* ptrs, int nranks, int count, double* out, cudaStream_t s);
 void launch_norm_partial(const z2* x, long long n, double* partial, int nblk, cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------------------------------------
+// Shared-factor apply (batch.cu, D28): subdomains with bitwise-equal local operators form a class; one
+// representative is factored and the class's inverses are applied to BATCH_NT subdomains at a time on DMMA.
+// ---------------------------------------------------------------------------------------------------------------------
+#define BATCH_NT 16
+struct CplConst { z2 cS, cSW, cN, cNE, cSE, cNW; int ns; };   // constant interior couplings (apply fast path)
+struct BatchTile { int cls, first, cnt, pad; };                // members[first .. first + cnt) of class cls
+struct BatchClass { long long off; int rep, mp, S, pad; };     // batch-layout factor offset, representative, padded m, stride
+struct BatchArgs {
+    const SubDesc* desc;
+    const BatchTile* tiles;
+    int ntiles;
+    const int* members;     // subdomain indices, grouped per tile
+    const BatchClass* cls;
+    const z2* dinvB;        // class factors, batch layout
+    const z2* stencil;
+    const z2* in;
+    int in_i0, in_j0;
+    long long in_stride;
+    z2* out;
+    int out_i0, out_j0;
+    long long out_stride;
+    z2* scratch;            // per CTA [max(hi - lo + 1)][BATCH_NT][mp_max]
+    long long scratch_per_cta;
+    CplConst cc;
+    z2* pou_buf;
+    int delta;
+};
+int batch_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslots, int* ctas_per_sm);
+void launch_apply_batch(const BatchArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, int mpmax,
+                        cudaStream_t s);
+void launch_relayout_batch(const z2* dinv, long long fac_off, int m, int nb, z2* dst, int mp, int S, cudaStream_t s);
+void launch_stencil_eq(const SubDesc* desc, const z2* stc, const int2* pairs, int npairs, int* diff, cudaStream_t s);

@@ -82,7 +82,8 @@ EXPORTS = ["helm_setup", "helm_get_layout", "helm_rhs", "helm_factor", "helm_mat
            "helm_matvec_ext", "helm_richardson", "helm_probe_read_bandwidth", "helm_setup_loopback",
            "helm_probe_read_bandwidth_mode", "helm_set_orthogonalisation",
            "helm_get_krylov_basis", "helm_comm_info", "helm_probe_fp64_tflops", "helm_set_residual_band",
-           "helm_comm_counters", "helm_halo_band_counts", "helm_halo_band_rects", "helm_nccl_selftest"]
+           "helm_comm_counters", "helm_halo_band_counts", "helm_halo_band_rects", "helm_nccl_selftest",
+           "helm_factor_classes"]
 
 
 def lib_path() -> str:
@@ -130,6 +131,7 @@ def load(build_if_missing: bool = True):
     L.helm_halo_band_counts.argtypes = [C.POINTER(Params), i, i, C.POINTER(C.c_longlong)]
     L.helm_halo_band_rects.argtypes = [C.POINTER(Params), i, i, i, i, C.POINTER(i), i]
     L.helm_comm_info.argtypes = [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]
+    L.helm_factor_classes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(i), i]
     L.helm_last_error.argtypes = [vp]
     L.helm_last_error.restype = C.c_char_p
     L.helm_destroy.argtypes = [vp]
@@ -410,6 +412,18 @@ class Context:
         out = (C.c_longlong * 4)()
         self._check(self.L.helm_comm_counters(self._h, int(bool(reset)), out))
         return {"sent": out[0], "recv": out[1], "msgs": out[2], "allreduces": out[3]}
+
+    def factor_classes(self, with_members: bool = False) -> dict:
+        """After factor(): {'classes', 'batched', 'tiles', 'factor_bytes'} (D28), plus 'class_of' (one class index per
+        local subdomain) when with_members."""
+        out = (C.c_longlong * 4)()
+        n = self._layout().n_sub_local if with_members else 0
+        cls = (C.c_int * max(n, 1))()
+        self._check(self.L.helm_factor_classes(self._h, out, cls if with_members else None, n))
+        r = {"classes": out[0], "batched": bool(out[1]), "tiles": out[2], "factor_bytes": out[3]}
+        if with_members:
+            r["class_of"] = list(cls[:n])
+        return r
 
     TRANSPORTS = {0: "none", 1: "nccl", 2: "loopback", 3: "shard"}
 
