@@ -204,6 +204,7 @@ def run_ours(args):
     setup_s = max_over_ranks(time.time() - t0)
     factor_s = max_over_ranks(fe0.elapsed_time(fe1) / 1e3)
     lay = ctx.layout.as_dict()
+    fcls = ctx.factor_classes()
     comm = ctx.comm_info()
     xy, amp, sig = sources(cfg)
     b = ctx.rhs(xy, amp, sig)
@@ -282,6 +283,16 @@ def run_ours(args):
 
     hbm, peak_src = peaks()
 
+    def tts_cost(its, restarts):
+        """(algorithmic bytes, roofline seconds) of a solve.  The vector work (SpMV, orthogonalisation, cycle ends)
+        is HBM-bound: its bytes at the HBM peak.  The apply: with per-subdomain factors its bytes at the HBM peak too;
+        with the tensor-core apply (D28) its algorithmic flops at the measured DMMA peak."""
+        tot = tts_bytes(its, restarts)
+        if not fcls["batched"]:
+            return tot, tot / (hbm * 1e9)
+        vec = tot - its * lay["apply_bytes"]
+        return vec, vec / (hbm * 1e9) + its * fcls["apply_flop"] / (dmma_peak * 1e12)
+
     def tts_bytes(its, restarts):
         """Algorithmic bytes of a solve: per Arnoldi step the apply, the SpMV and the orthogonalisation sweeps
         (DCGS2: projection sweep over V_{j+1} and w, update sweep reading V_j, u_j, w and writing v_j, u_{j+1};
@@ -302,7 +313,9 @@ def run_ours(args):
             left -= m
         return tot
 
-    tts_b = tts_bytes(tinfo.iterations, tinfo.restarts)
+    from paper_2602_00735_b200.helm import probe_fp64_tflops
+    dmma_peak = probe_fp64_tflops(0)
+    tts_b, tts_roof_s = tts_cost(tinfo.iterations, tinfo.restarts)
     cyc_b = tts_bytes(R, 0)
     apply_avg_ms = apply_ms / max(apply_n, 1)
     # per GPU: this rank's algorithmic apply bytes over its own mean apply time; the line reports the slowest rank
@@ -321,6 +334,38 @@ def run_ours(args):
         key = cfg.name if world == 1 else f"{cfg.name}/{world}"
         traffic = tj.get(key, {}).get("dram_bytes_per_launch")
     launches_tot = int(sum(gather(float(launches))))
+    if fcls["batched"]:
+        # D28: the shared-factor apply is a batch of complex GEMMs on the FP64 tensor cores -- tensor-bound; achieved =
+        # algorithmic flops (8 m^2 per block step of every subdomain, SURVEY 8(d)'s GEMV work in flops) / kernel time
+        fl_r = gather(float(fcls["apply_flop"]))
+        tf_r = [fl_r[q] / (ms_r[q] / 1e3) / 1e12 for q in range(world)]
+        slow_t = max(range(world), key=lambda q: ms_r[q])
+        tprof = os.path.join(ROOT, "profiles", "k_apply_batch_traffic.json")
+        btraffic = None
+        if os.path.exists(tprof):
+            with open(tprof) as f:
+                btraffic = json.load(f).get(cfg.name if world == 1 else f"{cfg.name}/{world}", {}).get(
+                    "dram_bytes_per_launch")
+        roofline = {"bound": "tensor", "achieved": tf_r[slow_t], "peak": dmma_peak, "unit": "TFLOP/s",
+                    "frac": tf_r[slow_t] / dmma_peak, "traffic": btraffic,
+                    "kernel": "k_apply_batch (shared-factor twisted block solves as complex GEMMs on DMMA, D28)",
+                    "algorithmic_flop_per_launch": fcls["apply_flop"], "issued_flop_per_launch": fcls["apply_flop_issued"],
+                    "issued_frac": fcls["apply_flop_issued"] / (ms_r[slow_t] / 1e3) / 1e12 / dmma_peak,
+                    "peak_source": "helm_probe_fp64_tflops(DMMA), measured on this GPU: MEASURED_PEAKS.json has no FP64 "
+                                   "figure (its bf16 1671.8 x the nominal FP64/bf16 ratio 40/2250 = 29.7, below the probe)",
+                    "classes": fcls["classes"], "tiles": fcls["tiles"],
+                    "per_gpu": world > 1, "slowest_rank": slow_t, "achieved_per_rank": tf_r,
+                    "apply_kernel_ms": ms_r[slow_t], "apply_share_of_step": apply_ms / ms}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": traffic, "kernel": "k_apply (fused restrict + twisted block solves + owner write)",
+                    "algorithmic_bytes_per_launch": lay["apply_bytes"], "peak_source": peak_src,
+                    "per_gpu": world > 1, "slowest_rank": slow, "achieved_per_rank": ach_r,
+                    "band_equivalent_GBps": lay["band_bytes"] / (apply_avg_ms / 1e3) / 1e9,
+                    "read_stream_probe_GBps": read_peak, "frac_of_read_probe": achieved / read_peak,
+                    "read_streams_probe_GBps": read_streams, "frac_of_read_streams_probe": achieved / read_streams,
+                    "apply_kernel_ms": ms_r[slow], "apply_share_of_step": apply_ms / ms,
+                    "cycle_algorithmic_bytes": cyc_b, "cycle_frac": cyc_b / (hbm * 1e9) / (ms / args.steps / 1e3)}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -331,34 +376,34 @@ def run_ours(args):
                    "kappa": lay["n_pml"], "local_unknowns_rank0": lay["local_unknowns"], "m_max": lay["m_max"],
                    "factor_GB_rank0": round(lay["factor_bytes"] / 1e9, 3),
                    "apply_GB_rank0": round(lay["apply_bytes"] / 1e9, 3), "orth": args.orth},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "k_apply (fused restrict + twisted block solves + owner write)",
-                     "algorithmic_bytes_per_launch": lay["apply_bytes"], "peak_source": peak_src,
-                     "per_gpu": world > 1, "slowest_rank": slow, "achieved_per_rank": ach_r,
-                     "band_equivalent_GBps": lay["band_bytes"] / (apply_avg_ms / 1e3) / 1e9,
-                     "read_stream_probe_GBps": read_peak, "frac_of_read_probe": achieved / read_peak,
-                     "read_streams_probe_GBps": read_streams, "frac_of_read_streams_probe": achieved / read_streams,
-                     "apply_kernel_ms": ms_r[slow], "apply_share_of_step": apply_ms / ms,
-                     "cycle_algorithmic_bytes": cyc_b, "cycle_frac": cyc_b / (hbm * 1e9) / (ms / args.steps / 1e3)},
+        "roofline": roofline,
+        "factor_sharing": {"classes": fcls["classes"], "batched_apply": fcls["batched"], "tiles": fcls["tiles"],
+                           "factor_bytes_on_device": fcls["factor_bytes"],
+                           "note": "D28: subdomains with bitwise-equal local operators share one factorisation"},
         "e2e": {"value": e_its / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "helm_gmres_host (host b/x, copies inside every call), one call per cycle"},
         "gpu_launches": launches_tot,
         "iterations": its, "applies": its,
-        "apply_only": {"ms": apply_only_ms, "applies_per_s": 1e3 / apply_only_ms,
-                       "GBps": lay["apply_bytes"] / apply_only_ms / 1e6},
+        "apply_only": ({"ms": apply_only_ms, "applies_per_s": 1e3 / apply_only_ms,
+                        "TFLOPs": fcls["apply_flop"] / apply_only_ms / 1e9} if fcls["batched"] else
+                       {"ms": apply_only_ms, "applies_per_s": 1e3 / apply_only_ms,
+                        "GBps": lay["apply_bytes"] / apply_only_ms / 1e6}),
         "gmres_tts": {"seconds": tts_s, "iterations": tinfo.iterations, "restarts": tinfo.restarts,
                       "relres_true": tinfo.relres_true, "status": tinfo.status, "rtol": cfg.rtol,
                       "applies_per_s": tinfo.iterations / tts_s,
-                      "algorithmic_bytes": tts_b, "roofline_s": tts_b / (hbm * 1e9),
-                      "roofline_frac": tts_b / (hbm * 1e9) / tts_s},
+                      "algorithmic_bytes": tts_b, "roofline_s": tts_roof_s, "roofline_frac": tts_roof_s / tts_s,
+                      "roofline_note": ("vector work (SpMV, orthogonalisation) at the HBM peak + the apply's flops at "
+                                        "the measured DMMA peak" if fcls["batched"] else
+                                        "all algorithmic bytes at the HBM peak")},
         "setup_factor_s": setup_s,
         "factor": factor_roofline(lay, factor_s, gather),
         "comm": comm,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_paper:
+        out["per_subdomain_factors"] = per_subdomain_factors(cfg, stream, hbm, peak_src, read_streams)
     if world == 1:
-        out["tts_vs_k"] = tts_vs_k(stream, cfg, tts_s, tinfo, factor_s, apply_only_ms,
-                                   lay["apply_bytes"] / apply_only_ms / 1e6)
+        out["tts_vs_k"] = tts_vs_k(stream, cfg, tts_s, tinfo, factor_s, apply_only_ms)
     if world == 1 and not args.no_paper:
         out["paper_table4"] = paper_table4(stream)
         out["gmres_tts_ramp_pou"] = ramp_pou_tts(cfg, stream, xy, amp, sig)
@@ -373,7 +418,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main, apply_main_ms, apply_main_GBps):
+def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main, apply_main_ms):
     """BASELINE.json's 'GMRES time-to-solve vs k; local-solve HBM GB/s': every single-GPU config c0..c3 solved to 1e-6
     on this GPU (factorisation, solve and the apply alone timed with CUDA events; the bench config's own numbers
     reused), beside the oracle's solve of the same system from the golden records (another host: context)."""
@@ -394,7 +439,7 @@ def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main, apply_main_ms,
         if name == cfg_main.name:
             rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": factor_main,
                          "solve_s": tts_main, "iterations": tinfo_main.iterations, "relres_true": tinfo_main.relres_true,
-                         "apply_ms": apply_main_ms, "apply_GBps": apply_main_GBps, "oracle": orc})
+                         "apply_ms": apply_main_ms, "oracle": orc})
             continue
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -431,11 +476,53 @@ def tts_vs_k(stream, cfg_main, tts_main, tinfo_main, factor_main, apply_main_ms,
         rows.append({"config": name, "k": c.k, "subdomains": c.nsub ** 2, "factor_s": factor_s_row,
                      "factor_first_call_s": factor_first_s, "solve_s": solve_s_row, "iterations": info.iterations,
                      "relres_true": info.relres_true, "apply_ms": apply_ms,
-                     "apply_GBps": lay.apply_bytes / apply_ms / 1e6, "oracle": orc})
+                     "tensor_core_apply": ctx.factor_classes()["batched"], "oracle": orc})
         ctx.close()
         del ctx, b
         torch.cuda.empty_cache()
     return rows
+
+
+def per_subdomain_factors(cfg, stream, hbm, peak_src, read_streams):
+    """The general path of the method (every subdomain factored and its inverse blocks streamed from HBM per apply:
+    HELM_SHARE_FACTORS=0, what a variable wave speed needs) on the same workload: factorisation, apply alone and its
+    HBM roofline -- BASELINE.json's 'local-solve HBM GB/s'."""
+    import torch
+
+    from paper_2602_00735_b200 import Context
+    old = os.environ.get("HELM_SHARE_FACTORS")
+    os.environ["HELM_SHARE_FACTORS"] = "0"
+    try:
+        ctx = Context(cfg.k, cfg.nsub, cfg.nsub, stream=stream)
+    finally:
+        if old is None:
+            del os.environ["HELM_SHARE_FACTORS"]
+        else:
+            os.environ["HELM_SHARE_FACTORS"] = old
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    ctx.factor()
+    ev[1].record(stream)
+    v = torch.randn(ctx.n, dtype=torch.complex128, device="cuda")
+    z = torch.empty_like(v)
+    for _ in range(3):
+        ctx.precond_apply(v, z)
+    ev[2].record(stream)
+    for _ in range(10):
+        ctx.precond_apply(v, z)
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    lay = ctx.layout
+    ms = ev[2].elapsed_time(ev[3]) / 10
+    gbps = lay.apply_bytes / ms / 1e6
+    res = {"factor_s": ev[0].elapsed_time(ev[1]) / 1e3, "factor_GB": round(lay.factor_bytes / 1e9, 3),
+           "apply_ms": ms, "applies_per_s": 1e3 / ms, "algorithmic_bytes_per_launch": lay.apply_bytes,
+           "achieved_GBps": gbps, "peak_GBps": hbm, "peak_source": peak_src, "frac": gbps / hbm,
+           "frac_of_read_streams_probe": gbps / read_streams, "kernel": "k_apply", "classes": ctx.factor_classes()["classes"]}
+    ctx.close()
+    del ctx, v, z
+    torch.cuda.empty_cache()
+    return res
 
 
 def factor_roofline(lay, factor_s, gather):

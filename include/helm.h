@@ -93,7 +93,8 @@ typedef struct {
     int stencil_slots;        /* coefficients per row of A (helm_export_stencil): 7 (P1) or 9 (Q1) */
     int overlap_interior;     /* multi-rank: subdomains applied while the halo is in flight (0: no overlap) */
     long long factor_flop;    /* real FP64 flops of helm_factor's block inversions: sum over blocks of 8 m^3 (one
-                                 complex multiply-add per entry and pivot of Gauss-Jordan) */
+                                 complex multiply-add per entry and pivot of Gauss-Jordan); after helm_factor, over
+                                 the factored class representatives only (D28) */
 } helm_layout;
 
 typedef struct {
@@ -210,12 +211,14 @@ int helm_comm_counters(helm_ctx* ctx, int reset, long long* out4);
  * are bitwise equal (with c = 1, the interior subdomains are translates of one another) form a class; helm_factor
  * factors one representative per class and every member uses its inverses, and when the classes are large the apply
  * runs class tiles of 16 subdomains as complex GEMMs on the FP64 tensor cores (k_apply_batch).  Filled after
- * helm_factor (HELM_ESTATE before): out4 = {classes, shared-factor apply on (1) / off (0), tiles of that apply,
- * factor bytes held on the device}; class_of (may be NULL) receives n_sub_local class indices, cap entries at most.
+ * helm_factor (HELM_ESTATE before): out6 = {classes, shared-factor apply on (1) / off (0), tiles of that apply,
+ * factor bytes held on the device, algorithmic flops of one apply (8 m^2 per block step of every subdomain: one
+ * complex m x m matrix-vector product), flops the tensor-core apply issues (whole 16-column tiles, m padded to a
+ * multiple of 8; 0 when off)}; class_of (may be NULL) receives n_sub_local class indices, cap entries at most.
  * Environment (read at helm_setup): HELM_SHARE_FACTORS=0 factors every subdomain (one class each);
  * HELM_APPLY_BATCH=1 / 0 forces the tensor-core apply on / off (default: on when the whole problem has at least
  * 4 x SMs subdomains and m_max <= 128).  Host only. */
-int helm_factor_classes(const helm_ctx* ctx, long long* out4, int* class_of, int cap);
+int helm_factor_classes(const helm_ctx* ctx, long long* out6, int* class_of, int cap);
 
 /* Host logic, no GPU: this rank's apply-frame halo volume in complex elements -- out4 = {sent full, sent band, received
  * full, received band} (band = the section 3(i) restriction) -- and the band sub-rectangles (i0, i1, j0, j1 per

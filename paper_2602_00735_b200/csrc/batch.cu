@@ -43,13 +43,16 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
 {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_gx[NT], s_gy[NT], s_sub[NT];
+    __shared__ SubDesc s_d;      // the tile's class representative (shape, couplings, owned ranges)
+    __shared__ BatchClass s_c;
     unsigned char* ringb = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NSL * slot_bytes);
     uint64_t* empty = full + NSL;
     const int SR = mpmax + 4;                                // R row stride (== 4 mod 8: conflict-free B fragments)
     z2* R = reinterpret_cast<z2*>(empty + NSL);              // [NT][SR]: right-hand sides of the current step
-    z2* vb = R + NT * SR;                                    // [NT][mpmax]: bottom chain / down-expansion carry
-    z2* vt = vb + NT * mpmax;                                // [NT][mpmax]: top chain / up-expansion carry
+    const int SV = mpmax + 1;                                // carry row stride (odd: conflict-free epilogue stores)
+    z2* vb = R + NT * SR;                                    // [NT][SV]: bottom chain / down-expansion carry
+    z2* vt = vb + NT * SV;                                   // [NT][SV]: top chain / up-expansion carry
     const int nct = ncw * 32;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
 
@@ -92,9 +95,11 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
     z2* scr = a.scratch + (long long)blockIdx.x * a.scratch_per_cta;   // [hi-lo+1][NT][mp]
     for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x) {
         const BatchTile T = a.tiles[w];
-        const BatchClass C = a.cls[T.cls];
-        const SubDesc d = a.desc[C.rep];
-        const int m = d.m, mp = C.mp, cnt = T.cnt;
+        if (tid == 0) {
+            s_c = a.cls[T.cls];
+            s_d = a.desc[s_c.rep];
+        }
+        const int cnt = T.cnt;
         if (tid < NT) {
             const int j = tid < cnt ? a.members[T.first + tid] : -1;
             s_sub[tid] = j;
@@ -102,22 +107,44 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
             s_gy[tid] = j >= 0 ? a.desc[j].gy0 : 0;
         }
         consumer_bar(nct);
+        const SubDesc& d = s_d;
+        const BatchClass& C = s_c;
+        const int m = d.m, mp = C.mp;
         const z2* stc = a.stencil + d.stc_off;
         const int S = nsteps(d);
         const bool mw = warp * 8 < mp;   // this warp owns factor rows [8 warp, 8 warp + 8)
+        // Thread tid builds elements e = tid + k nct (k < 4: NT mp <= 16 mp_max = 4 nct) of every R; their restricted
+        // inputs b_i (the gather R_j r) are loaded one step ahead, in flight under the previous step's DMMAs.
+        auto load_b = [&](int s2, z2(&pb)[4]) {
+            if (s2 >= S) return;
+            const Step sn = step_of(d, s2);
+            if (sn.ph > PH_Z) return;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int e = tid + k * nct, q = e / mp, t = e - q * mp;
+                pb[k] = (e < NT * mp && q < cnt && t < m)
+                            ? __ldg(a.in + (s_gx[q] + t - a.in_i0) + a.in_stride * (long long)(s_gy[q] + sn.i - a.in_j0))
+                            : zmk(0, 0);
+            }
+        };
+        z2 pb[4];
+        load_b(0, pb);
         for (int s = 0; s < S; s++) {
             const Step st = step_of(d, s);
             const z2* row = stc + (long long)st.i * a.cc.ns * m;
+            const z2 cb[4] = {pb[0], pb[1], pb[2], pb[3]};
             // ---- right-hand sides R[q][t] of this block step (restricted input b_i and the coupling term)
-            for (int e = tid; e < NT * mp; e += nct) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int e = tid + k * nct;
+                if (e >= NT * mp) break;
                 const int q = e / mp, t = e - q * mp;
                 z2 r = zmk(0, 0);
                 if (q < cnt && t < m) {
                     const bool cst = t >= d.cx0 && t < d.cx1 && st.i >= d.cy0 && st.i < d.cy1;
-                    const z2* vbq = vb + q * mpmax;
-                    const z2* vtq = vt + q * mpmax;
-                    if (st.ph <= PH_Z)
-                        r = __ldg(a.in + (s_gx[q] + t - a.in_i0) + a.in_stride * (long long)(s_gy[q] + st.i - a.in_j0));
+                    const z2* vbq = vb + q * SV;
+                    const z2* vtq = vt + q * SV;
+                    if (st.ph <= PH_Z) r = cb[k];
                     switch (st.ph) {
                     case PH_T:   // b_i - U_i z_{i+1}
                         if (st.i < d.nb - 1) cpl_apply(r, load_upper(row, m, t, cst, a.cc), vtq, t, m, true);
@@ -140,9 +167,11 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                 R[q * SR + t] = r;
             }
             consumer_bar(nct);
-            // ---- Y = F_i R on the tensor cores: four real products per complex k-step and column tile, each in its
-            // own accumulator (re = rr - ii, im = ri + ir)
-            double rr[2][2] = {}, ii[2][2] = {}, ri[2][2] = {}, ir[2][2] = {};
+            load_b(s + 1, pb);
+            // ---- Y = F_i R on the tensor cores, three real products per complex k-step and column tile (3M:
+            // p1 = Fr Rr, p2 = Fi Ri, p3 = (Fr + Fi)(Rr + Ri); re = p1 - p2, im = p3 - p1 - p2), each in its own
+            // accumulator; the operand sums run on the FP64 pipe beside the tensor pipe
+            double p1[2][2] = {}, p2[2][2] = {}, p3[2][2] = {};
             for (int c0 = 0; c0 < mp; c0 += KC) {
                 mbar_wait(&full[slot], ph);
                 if (mw) {
@@ -150,14 +179,14 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
 #pragma unroll
                     for (int ks = 0; ks < KC / 4; ks++) {
                         const z2 av = F[(4 * ks + t4) * C.S + 8 * warp + g];
+                        const double as = av.x + av.y;
                         const int kk = c0 + 4 * ks + t4;
 #pragma unroll
                         for (int ct = 0; ct < 2; ct++) {
                             const z2 bv = R[(8 * ct + g) * SR + kk];
-                            dmma(rr[ct][0], rr[ct][1], av.x, bv.x);
-                            dmma(ii[ct][0], ii[ct][1], av.y, bv.y);
-                            dmma(ri[ct][0], ri[ct][1], av.x, bv.y);
-                            dmma(ir[ct][0], ir[ct][1], av.y, bv.x);
+                            dmma(p1[ct][0], p1[ct][1], av.x, bv.x);
+                            dmma(p2[ct][0], p2[ct][1], av.y, bv.y);
+                            dmma(p3[ct][0], p3[ct][1], as, bv.x + bv.y);
                         }
                     }
                 }
@@ -177,23 +206,23 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                     for (int e = 0; e < 2; e++) {
                         const int q = 8 * ct + 2 * t4 + e;
                         if (q >= cnt || t >= m) continue;
-                        const z2 acc = zmk(rr[ct][e] - ii[ct][e], ri[ct][e] + ir[ct][e]);
+                        const z2 acc = zmk(p1[ct][e] - p2[ct][e], (p3[ct][e] - p1[ct][e]) - p2[ct][e]);
                         z2* sc = scr + ((long long)(st.i - d.lo) * NT + q) * mp + t;
                         if (st.ph == PH_T) {
-                            vt[q * mpmax + t] = acc;
+                            vt[q * SV + t] = acc;
                             if (st.i <= d.hi) *sc = acc;
                         } else if (st.ph == PH_B) {
-                            vb[q * mpmax + t] = acc;
+                            vb[q * SV + t] = acc;
                             if (st.i >= d.lo) *sc = acc;
                         } else {
                             z2 x;
                             if (st.ph == PH_Z) {
                                 x = acc;
-                                vb[q * mpmax + t] = x;
-                                vt[q * mpmax + t] = x;
+                                vb[q * SV + t] = x;
+                                vt[q * SV + t] = x;
                             } else {
                                 x = zsub(*sc, acc);
-                                (st.ph == PH_D ? vb : vt)[q * mpmax + t] = x;
+                                (st.ph == PH_D ? vb : vt)[q * SV + t] = x;
                             }
                             if (t >= d.olo && t <= d.ohi) {
                                 const int gx = s_gx[q] + t, gy = s_gy[q] + st.i;
@@ -217,6 +246,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
 }
 
 // one instance per CTA size (consumer warps = mp_max / 8, plus the producer warp), two CTAs per SM up to mp_max = 88
+// (one CTA's serial phases -- right-hand sides, epilogue, barriers -- then run under the other's DMMAs)
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_apply_batch(BatchArgs a, int ncw, int mpmax, int slot_bytes, int nslots)
 {
@@ -232,7 +262,8 @@ const void* batch_fn(int block)
 
 int batch_smem(int mpmax, int nslots, int slot_bytes)
 {
-    return nslots * slot_bytes + 2 * nslots * 8 + NT * (mpmax + 4) * (int)sizeof(z2) + 2 * NT * mpmax * (int)sizeof(z2);
+    return nslots * slot_bytes + 2 * nslots * 8 + NT * (mpmax + 4) * (int)sizeof(z2) +
+           2 * NT * (mpmax + 1) * (int)sizeof(z2);
 }
 
 // class factors: standard layout (m x m column-major blocks at fac_off) -> batch layout
@@ -272,10 +303,13 @@ int batch_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslo
     *block = 32 * (ncw + 1);
     *slot_bytes = KC * (mpmax + 2) * (int)sizeof(z2);
     const void* fn = batch_fn(*block);
-    // the deepest ring (<= 6 slots) that keeps two CTAs per SM (one CTA's serial phases then hide under the other's
-    // DMMAs), else the deepest that fits one
+    // the deepest ring (<= 6 slots) that keeps two CTAs per SM, else the deepest that fits one (measured at c3:
+    // two CTAs of 4 slots 1.63 ms; one CTA of 6 slots 2.19 ms; one CTA running the two chains in lockstep, 1.93 ms)
+    const char* env = getenv("HELM_BATCH_SLOTS");   // tuning override: ring depth (the CTAs per SM follow)
+    const int force = env ? atoi(env) : 0;
     for (int want = 2; want >= 1; want--)
         for (int ns = 6; ns >= 2; ns--) {
+            if (force > 0 && ns != force) continue;
             const int sm = batch_smem(mpmax, ns, *slot_bytes);
             raise_smem_attr(fn, sm);
             int occ = 0;
@@ -283,7 +317,7 @@ int batch_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslo
                 cudaGetLastError();
                 continue;
             }
-            if (occ >= want) {
+            if (occ >= want || (force > 0 && occ >= 1)) {
                 *smem = sm;
                 *nslots = ns;
                 *ctas_per_sm = occ;

@@ -1980,14 +1980,28 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     return HELM_OK;
 }
 
-int helm_factor_classes(const helm_ctx* ctx, long long* out4, int* class_of, int cap)
+int helm_factor_classes(const helm_ctx* ctx, long long* out6, int* class_of, int cap)
 {
-    if (!ctx || !out4) return HELM_EINVAL;
+    if (!ctx || !out6) return HELM_EINVAL;
     if (!ctx->factored) return HELM_ESTATE;
-    out4[0] = (long long)ctx->cls_rep.size();
-    out4[1] = ctx->batched ? 1 : 0;
-    out4[2] = ctx->bt_ntiles;
-    out4[3] = 16LL * (ctx->n_dinv + ctx->dinvB_len);
+    out6[0] = (long long)ctx->cls_rep.size();
+    out6[1] = ctx->batched ? 1 : 0;
+    out6[2] = ctx->bt_ntiles;
+    out6[3] = 16LL * (ctx->n_dinv + ctx->dinvB_len);
+    // algorithmic flops of one apply: 8 m^2 real flops (one complex m x m GEMV) per block step of every subdomain
+    long long fl = 0, issued = 0;
+    for (const SubDesc& d : ctx->subs) fl += 8LL * d.m * d.m * (d.nb + d.hi - d.lo);
+    if (ctx->batched)
+        for (int c = 0; c < (int)ctx->cls_rep.size(); c++) {
+            // the tensor-core apply computes full padded tiles: ceil(members / 16) tiles of 16 columns, mp x mp blocks
+            const SubDesc& d = ctx->subs[ctx->cls_rep[c]];
+            long long nm = 0;
+            for (int k : ctx->cls_of) nm += k == c;
+            const long long mp = (d.m + 7) / 8 * 8;
+            issued += (nm + BATCH_NT - 1) / BATCH_NT * BATCH_NT * 8LL * mp * mp * (d.nb + d.hi - d.lo);
+        }
+    out6[4] = fl;
+    out6[5] = issued;
     if (class_of)
         for (int j = 0; j < (int)ctx->cls_of.size() && j < cap; j++) class_of[j] = ctx->cls_of[j];
     return HELM_OK;
@@ -2154,7 +2168,11 @@ int helm_get_layout(const helm_ctx* ctx, helm_layout* out)
     out->stencil_slots = G.ns;
     out->overlap_interior = ctx->overlap ? ctx->n_int : 0;
     out->factor_flop = 0;
-    for (const SubDesc& sd : ctx->subs) out->factor_flop += 8LL * sd.nb * sd.m * sd.m * sd.m;
+    // what helm_factor computes: one factorisation per class (D28) once the classes are known, else every subdomain
+    if (!ctx->cls_rep.empty())
+        for (int j : ctx->cls_rep) out->factor_flop += 8LL * ctx->subs[j].nb * ctx->subs[j].m * ctx->subs[j].m * ctx->subs[j].m;
+    else
+        for (const SubDesc& sd : ctx->subs) out->factor_flop += 8LL * sd.nb * sd.m * sd.m * sd.m;
     return HELM_OK;
 }
 

@@ -316,6 +316,7 @@ class Context:
 
     def factor(self):
         self._check(self.L.helm_factor(self._h))
+        self.layout = self._layout()   # factor bytes / flops now count the factored classes (D28)
 
     def matvec(self, x, out=None):
         y = self.empty() if out is None else out
@@ -414,13 +415,14 @@ class Context:
         return {"sent": out[0], "recv": out[1], "msgs": out[2], "allreduces": out[3]}
 
     def factor_classes(self, with_members: bool = False) -> dict:
-        """After factor(): {'classes', 'batched', 'tiles', 'factor_bytes'} (D28), plus 'class_of' (one class index per
-        local subdomain) when with_members."""
-        out = (C.c_longlong * 4)()
+        """After factor(): {'classes', 'batched', 'tiles', 'factor_bytes', 'apply_flop', 'apply_flop_issued'} (D28),
+        plus 'class_of' (one class index per local subdomain) when with_members."""
+        out = (C.c_longlong * 6)()
         n = self._layout().n_sub_local if with_members else 0
         cls = (C.c_int * max(n, 1))()
         self._check(self.L.helm_factor_classes(self._h, out, cls if with_members else None, n))
-        r = {"classes": out[0], "batched": bool(out[1]), "tiles": out[2], "factor_bytes": out[3]}
+        r = {"classes": out[0], "batched": bool(out[1]), "tiles": out[2], "factor_bytes": out[3],
+             "apply_flop": out[4], "apply_flop_issued": out[5]}
         if with_members:
             r["class_of"] = list(cls[:n])
         return r
