@@ -18,6 +18,7 @@
 // Layout of the class factors ("batch layout"): block i of class c at off_c + i * mp * S, column k (mp of them, m
 // padded to a multiple of 8, zero beyond m) at k * S, rows contiguous with S = mp + 2 (== 2 mod 8 z2: the A-fragment
 // loads of a quarter warp -- rows g, g+1, columns t..t+3 -- hit eight distinct 16-byte bank groups).
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "internal.cuh"
@@ -39,8 +40,19 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+#ifdef HELM_BATCH_PROF
+// development aid (-DHELM_BATCH_PROF): clock64 cycles per phase of every block step as thread 0 of CTA 0 sees them
+// (waits included), printed at the end: right-hand sides, barrier after them, ring waits, DMMA loop, epilogue, barrier
+#define BPROF(k) do { if (tid == 0 && blockIdx.x == 0) { const long long t_ = clock64(); bpr[k] += t_ - bt0; bt0 = t_; } } while (0)
+#else
+#define BPROF(k) do { } while (0)
+#endif
+
 __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpmax, int slot_bytes, int NSL)
 {
+#ifdef HELM_BATCH_PROF
+    long long bpr[6] = {0, 0, 0, 0, 0, 0}, bt0 = clock64();
+#endif
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_gx[NT], s_gy[NT], s_sub[NT];
     __shared__ SubDesc s_d;      // the tile's class representative (shape, couplings, owned ranges)
@@ -130,6 +142,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
         z2 pb[4];
         load_b(0, pb);
         for (int s = 0; s < S; s++) {
+            BPROF(5);
             const Step st = step_of(d, s);
             const z2* row = stc + (long long)st.i * a.cc.ns * m;
             const z2 cb[4] = {pb[0], pb[1], pb[2], pb[3]};
@@ -166,14 +179,18 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                 }
                 R[q * SR + t] = r;
             }
+            BPROF(0);
             consumer_bar(nct);
+            BPROF(1);
             load_b(s + 1, pb);
             // ---- Y = F_i R on the tensor cores, three real products per complex k-step and column tile (3M:
             // p1 = Fr Rr, p2 = Fi Ri, p3 = (Fr + Fi)(Rr + Ri); re = p1 - p2, im = p3 - p1 - p2), each in its own
             // accumulator; the operand sums run on the FP64 pipe beside the tensor pipe
             double p1[2][2] = {}, p2[2][2] = {}, p3[2][2] = {};
             for (int c0 = 0; c0 < mp; c0 += KC) {
+                BPROF(3);
                 mbar_wait(&full[slot], ph);
+                BPROF(2);
                 if (mw) {
                     const z2* F = reinterpret_cast<const z2*>(ringb + (size_t)slot * slot_bytes);
 #pragma unroll
@@ -197,6 +214,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                     ph ^= 1;
                 }
             }
+            BPROF(3);
             // ---- finish the step: carries, y / z scratch, owner write
             if (mw) {
                 const int t = 8 * warp + g;
@@ -240,9 +258,15 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                         }
                     }
             }
+            BPROF(4);
             consumer_bar(nct);
         }
     }
+#ifdef HELM_BATCH_PROF
+    if (tid == 0 && blockIdx.x == 0)
+        printf("BPROF rhs %lld bar_rhs %lld ring_wait %lld dmma %lld epilogue %lld bar_end %lld\n", bpr[0], bpr[1], bpr[2],
+               bpr[3], bpr[4], bpr[5]);
+#endif
 }
 
 // one instance per CTA size (consumer warps = mp_max / 8, plus the producer warp), two CTAs per SM up to mp_max = 88

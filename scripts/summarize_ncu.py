@@ -63,5 +63,9 @@ if __name__ == "__main__":
                 "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
                 "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
                 "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
-                "lts__t_sector_hit_rate.pct"]
+                "lts__t_sector_hit_rate.pct",
+                "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+                "smsp__pipe_tensor_subpipe_dmma_cycles_active.avg", "sm__cycles_active.avg", "sm__cycles_elapsed.avg",
+                "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
         print(json.dumps(full(sys.argv[2], sys.argv[3], sys.argv[4], keep), indent=1))
