@@ -51,7 +51,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpmax, int slot_bytes, int NSL)
 {
 #ifdef HELM_BATCH_PROF
-    long long bpr[6] = {0, 0, 0, 0, 0, 0}, bt0 = clock64();
+    long long bpr[7] = {0, 0, 0, 0, 0, 0, 0}, bt0 = clock64();
 #endif
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_gx[NT], s_gy[NT], s_sub[NT];
@@ -61,10 +61,14 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NSL * slot_bytes);
     uint64_t* empty = full + NSL;
     const int SR = mpmax + 4;                                // R row stride (== 4 mod 8: conflict-free B fragments)
-    z2* R = reinterpret_cast<z2*>(empty + NSL);              // [NT][SR]: right-hand sides of the current step
+    z2* R = reinterpret_cast<z2*>(empty + NSL + 2);          // [NT][SR]: right-hand sides of the current step
     const int SV = mpmax + 1;                                // carry row stride (odd: conflict-free epilogue stores)
     z2* vb = R + NT * SR;                                    // [NT][SV]: bottom chain / down-expansion carry
     z2* vt = vb + NT * SV;                                   // [NT][SV]: top chain / up-expansion carry
+    // the coupling rows of the current block step, bulk-copied by the producer: U_i (N, NE, NW) then L_i (S, SW, SE)
+    z2* cpb = vt + NT * SV;                                  // [6][mpmax]
+    uint64_t* cfull = empty + NSL;                           // coupling rows landed
+    uint64_t* cempty = cfull + 1;                            // every consumer warp has built its right-hand sides
     const int nct = ncw * 32;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
 
@@ -73,21 +77,37 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], ncw);
         }
+        mbar_init(cfull, 1);
+        mbar_init(cempty, ncw);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int e = tid; e < 6 * mpmax; e += blockDim.x) cpb[e] = zmk(0, 0);   // NW / SE stay 0 for P1
     __syncthreads();
 
     if (warp == ncw) {
         // ---------------------------------------------------------------- producer: stream the class factors
         if (lane != 0) return;
-        uint32_t slot = 0, ph = 0;
+        uint32_t slot = 0, ph = 0, cph = 0;
+        const int ns = a.cc.ns, nv = ns == 9 ? 3 : 2;
+        const int sl_u[3] = {SL_N, SL_NE, SL_NW}, sl_l[3] = {SL_S, SL_SW, SL_SE};
         for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x) {
             const BatchClass C = a.cls[a.tiles[w].cls];
             const SubDesc d = a.desc[C.rep];
             const int S = nsteps(d);
             const uint32_t bytes = (uint32_t)(KC * C.S * sizeof(z2));
+            const uint32_t vbytes = (uint32_t)(d.m * sizeof(z2));
             for (int s = 0; s < S; s++) {
-                const z2* blk = a.dinvB + C.off + (long long)step_of(d, s).i * C.mp * C.S;
+                const int i = step_of(d, s).i;
+                // coupling rows of step s (once the previous step's right-hand sides are built), then its factor block
+                mbar_wait(cempty, cph ^ 1);
+                mbar_arrive_expect_tx(cfull, 2 * nv * vbytes);
+                const z2* row = a.stencil + d.stc_off + (long long)i * ns * d.m;
+                for (int q = 0; q < nv; q++) {
+                    bulk_g2s(cpb + q * mpmax, row + sl_u[q] * d.m, vbytes, cfull);
+                    bulk_g2s(cpb + (3 + q) * mpmax, row + sl_l[q] * d.m, vbytes, cfull);
+                }
+                cph ^= 1;
+                const z2* blk = a.dinvB + C.off + (long long)i * C.mp * C.S;
                 for (int c0 = 0; c0 < C.mp; c0 += KC) {
                     mbar_wait(&empty[slot], ph ^ 1);
                     mbar_arrive_expect_tx(&full[slot], bytes);
@@ -103,7 +123,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
     }
 
     // ------------------------------------------------------------------------ consumers
-    uint32_t slot = 0, ph = 0;
+    uint32_t slot = 0, ph = 0, cph = 0;
     z2* scr = a.scratch + (long long)blockIdx.x * a.scratch_per_cta;   // [hi-lo+1][NT][mp]
     for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x) {
         const BatchTile T = a.tiles[w];
@@ -122,20 +142,22 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
         const SubDesc& d = s_d;
         const BatchClass& C = s_c;
         const int m = d.m, mp = C.mp;
-        const z2* stc = a.stencil + d.stc_off;
         const int S = nsteps(d);
         const bool mw = warp * 8 < mp;   // this warp owns factor rows [8 warp, 8 warp + 8)
-        // Thread tid builds elements e = tid + k nct (k < 4: NT mp <= 16 mp_max = 4 nct) of every R; their restricted
-        // inputs b_i (the gather R_j r) are loaded one step ahead, in flight under the previous step's DMMAs.
+        // Phase-A mapping: thread tid owns row tr of the subdomain columns q = tq + k P (P = nct / mp >= 4 rows of mp
+        // threads per pass, k < 4), so its coupling coefficients are read once per step for all its columns.  The
+        // restricted inputs b_i (the gather R_j r) are loaded one step ahead, in flight under the DMMAs.
+        const int P = nct / mp, tq = tid / mp, tr = tid - tq * mp;
+        const bool ract = tq < P;
         auto load_b = [&](int s2, z2(&pb)[4]) {
-            if (s2 >= S) return;
+            if (s2 >= S || !ract) return;
             const Step sn = step_of(d, s2);
             if (sn.ph > PH_Z) return;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                const int e = tid + k * nct, q = e / mp, t = e - q * mp;
-                pb[k] = (e < NT * mp && q < cnt && t < m)
-                            ? __ldg(a.in + (s_gx[q] + t - a.in_i0) + a.in_stride * (long long)(s_gy[q] + sn.i - a.in_j0))
+                const int q = tq + k * P;
+                pb[k] = (q < cnt && tr < m)
+                            ? __ldg(a.in + (s_gx[q] + tr - a.in_i0) + a.in_stride * (long long)(s_gy[q] + sn.i - a.in_j0))
                             : zmk(0, 0);
             }
         };
@@ -144,41 +166,52 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
         for (int s = 0; s < S; s++) {
             BPROF(5);
             const Step st = step_of(d, s);
-            const z2* row = stc + (long long)st.i * a.cc.ns * m;
             const z2 cb[4] = {pb[0], pb[1], pb[2], pb[3]};
-            // ---- right-hand sides R[q][t] of this block step (restricted input b_i and the coupling term)
+            mbar_wait(cfull, cph);
+            BPROF(6);
+            // ---- right-hand sides R[q][tr] of this block step: r = [b_i] - C1 v1 [- C2 v2] (T: U_i z_{i+1}; B: L_i
+            // y_{i-1}; Z: both) or r = C1 v1 (D: U_i x_{i+1}; U: L_i x_{i-1}); the step's form is uniform, so it is
+            // resolved once and the thread's four columns run as independent chains
+            if (ract) {
+                const Cp up = {cpb[tr], cpb[2 * mpmax + tr], cpb[mpmax + tr]};                  // d = N, lo = NW, hi = NE
+                const Cp dn = {cpb[3 * mpmax + tr], cpb[4 * mpmax + tr], cpb[5 * mpmax + tr]};  // S, SW, SE
+                const bool hb = st.ph <= PH_Z;                                   // restricted input present
+                const bool lower = st.ph == PH_B || st.ph == PH_U || st.ph == PH_Z;
+                const bool use1 = st.ph == PH_T ? st.i < d.nb - 1 : (st.ph == PH_B || st.ph == PH_Z) ? st.i > 0 : true;
+                const bool use2 = st.ph == PH_Z && st.i < d.nb - 1;              // the twist's U_tw z_{tw+1}
+                const double sg = hb ? -1.0 : 1.0;
+                const Cp c0 = lower ? dn : up;
+                const Cp c1 = {zscale(c0.d, sg), zscale(c0.lo, sg), zscale(c0.hi, sg)};
+                const Cp c2 = {zscale(up.d, -1.0), zscale(up.lo, -1.0), zscale(up.hi, -1.0)};
+                const z2* v1 = (st.ph == PH_B || st.ph == PH_Z || st.ph == PH_D) ? vb : vt;
+                const bool lo_ok = tr > 0, hi_ok = tr + 1 < m;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int e = tid + k * nct;
-                if (e >= NT * mp) break;
-                const int q = e / mp, t = e - q * mp;
-                z2 r = zmk(0, 0);
-                if (q < cnt && t < m) {
-                    const bool cst = t >= d.cx0 && t < d.cx1 && st.i >= d.cy0 && st.i < d.cy1;
-                    const z2* vbq = vb + q * SV;
-                    const z2* vtq = vt + q * SV;
-                    if (st.ph <= PH_Z) r = cb[k];
-                    switch (st.ph) {
-                    case PH_T:   // b_i - U_i z_{i+1}
-                        if (st.i < d.nb - 1) cpl_apply(r, load_upper(row, m, t, cst, a.cc), vtq, t, m, true);
-                        break;
-                    case PH_B:   // b_i - L_i y_{i-1}
-                        if (st.i > 0) cpl_apply(r, load_lower(row, m, t, cst, a.cc), vbq, t, m, true);
-                        break;
-                    case PH_Z:
-                        if (st.i > 0) cpl_apply(r, load_lower(row, m, t, cst, a.cc), vbq, t, m, true);
-                        if (st.i < d.nb - 1) cpl_apply(r, load_upper(row, m, t, cst, a.cc), vtq, t, m, true);
-                        break;
-                    case PH_D:   // U_i x_{i+1}
-                        cpl_apply(r, load_upper(row, m, t, cst, a.cc), vbq, t, m, false);
-                        break;
-                    default:     // PH_U: L_i x_{i-1}
-                        cpl_apply(r, load_lower(row, m, t, cst, a.cc), vtq, t, m, false);
-                        break;
+                for (int k = 0; k < 4; k++) {
+                    const int q = tq + k * P;
+                    if (q < NT) {
+                        z2 r = zmk(0, 0);
+                        if (q < cnt && tr < m) {
+                            if (hb) r = cb[k];
+                            if (use1) {
+                                const z2* v = v1 + q * SV + tr;
+                                zfma(r, c1.d, v[0]);
+                                if (lo_ok) zfma(r, c1.lo, v[-1]);
+                                if (hi_ok) zfma(r, c1.hi, v[1]);
+                            }
+                            if (use2) {
+                                const z2* v = vt + q * SV + tr;
+                                zfma(r, c2.d, v[0]);
+                                if (lo_ok) zfma(r, c2.lo, v[-1]);
+                                if (hi_ok) zfma(r, c2.hi, v[1]);
+                            }
+                        }
+                        R[q * SR + tr] = r;
                     }
                 }
-                R[q * SR + t] = r;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(cempty);
+            cph ^= 1;
             BPROF(0);
             consumer_bar(nct);
             BPROF(1);
@@ -264,8 +297,8 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
     }
 #ifdef HELM_BATCH_PROF
     if (tid == 0 && blockIdx.x == 0)
-        printf("BPROF rhs %lld bar_rhs %lld ring_wait %lld dmma %lld epilogue %lld bar_end %lld\n", bpr[0], bpr[1], bpr[2],
-               bpr[3], bpr[4], bpr[5]);
+        printf("BPROF cpl_wait %lld rhs %lld bar_rhs %lld ring_wait %lld dmma %lld epilogue %lld bar_end %lld\n", bpr[6],
+               bpr[0], bpr[1], bpr[2], bpr[3], bpr[4], bpr[5]);
 #endif
 }
 
@@ -286,8 +319,8 @@ const void* batch_fn(int block)
 
 int batch_smem(int mpmax, int nslots, int slot_bytes)
 {
-    return nslots * slot_bytes + 2 * nslots * 8 + NT * (mpmax + 4) * (int)sizeof(z2) +
-           2 * NT * (mpmax + 1) * (int)sizeof(z2);
+    return nslots * slot_bytes + 2 * nslots * 8 + 16 + NT * (mpmax + 4) * (int)sizeof(z2) +
+           2 * NT * (mpmax + 1) * (int)sizeof(z2) + 6 * mpmax * (int)sizeof(z2);
 }
 
 // class factors: standard layout (m x m column-major blocks at fac_off) -> batch layout
