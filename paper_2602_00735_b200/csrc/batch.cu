@@ -167,6 +167,13 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
             BPROF(5);
             const Step st = step_of(d, s);
             const z2 cb[4] = {pb[0], pb[1], pb[2], pb[3]};
+            if (mw && st.ph >= PH_D)   // the epilogue's y_i / z_i entries: on their way to L1 under phase A and the DMMAs
+#pragma unroll
+                for (int ct = 0; ct < 2; ct++) {
+                    const int q = 8 * ct + 2 * t4;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(scr + ((long long)(st.i - d.lo) * NT + q) * mp + 8 * warp + g));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(scr + ((long long)(st.i - d.lo) * NT + q + 1) * mp + 8 * warp + g));
+                }
             mbar_wait(cfull, cph);
             BPROF(6);
             // ---- right-hand sides R[q][tr] of this block step: r = [b_i] - C1 v1 [- C2 v2] (T: U_i z_{i+1}; B: L_i
