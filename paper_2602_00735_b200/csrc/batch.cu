@@ -309,348 +309,6 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
 #endif
 }
 
-// ---------------------------------------------------------------------------------------------------------------------
-// Warp-specialised form (HELM_BATCH_WS=1): the same arithmetic, one CTA per SM.  Builder warps form the right-hand
-// sides of the next block step while the DMMA warps run the current one.  The block steps of a tile are issued with
-// the two twisted chains interleaved -- T0 B0 T1 B1 ... Z D0 U0 D1 U1 ... -- so the step after the current one
-// belongs to the other chain and its inputs are ready one GEMM early.  Hand-offs use named barriers (the builder
-// arrives on FULL[b] when R[b] is written, the DMMA warps arrive on EMPTY[b] once they have read it and on DONE[b]
-// once the step's epilogue has written its carry); the producer warp streams factor chunks and coupling rows through
-// mbarrier rings in the same order.
-struct SubStep { int ph, i, pred; };   // pred: index in the tile of the step whose carry this one reads (-1: none)
-
-__device__ __forceinline__ int nsub_steps(const SubDesc& d) { return d.nb + d.hi - d.lo; }
-
-__device__ __forceinline__ SubStep sub_of(const SubDesc& d, int n)
-{
-    const int nT = d.nb - 1 - d.tw, nB = d.tw, m1 = min(nT, nB), P1 = nT + nB;
-    if (n < P1) {
-        if (n < 2 * m1) {
-            const int k = n >> 1;
-            return (n & 1) ? SubStep{PH_B, k, k > 0 ? n - 2 : -1} : SubStep{PH_T, d.nb - 1 - k, k > 0 ? n - 2 : -1};
-        }
-        const int k = m1 + (n - 2 * m1);
-        const bool isT = nT > nB;
-        const int pred = k == 0 ? -1 : (k - 1 < m1 ? 2 * (k - 1) + (isT ? 0 : 1) : n - 1);
-        return isT ? SubStep{PH_T, d.nb - 1 - k, pred} : SubStep{PH_B, k, pred};
-    }
-    if (n == P1) return SubStep{PH_Z, d.tw, P1 - 1};
-    const int nD = d.tw - d.lo, nU = d.hi - d.tw, m2 = min(nD, nU), base = P1 + 1, r = n - base;
-    if (r < 2 * m2) {
-        const int k = r >> 1;
-        return (r & 1) ? SubStep{PH_U, d.tw + 1 + k, k > 0 ? n - 2 : P1} : SubStep{PH_D, d.tw - 1 - k, k > 0 ? n - 2 : P1};
-    }
-    const int k = m2 + (r - 2 * m2);
-    const bool isD = nD > nU;
-    const int pred = k == 0 ? P1 : (k - 1 < m2 ? base + 2 * (k - 1) + (isD ? 0 : 1) : n - 1);
-    return isD ? SubStep{PH_D, d.tw - 1 - k, pred} : SubStep{PH_U, d.tw + 1 + k, pred};
-}
-
-struct TileMeta {
-    SubDesc d;
-    BatchClass c;
-    int cnt;
-    int gx[NT], gy[NT], sub[NT];
-};
-
-__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-constexpr int WS_NB = 8;   // builder warps (NT mp_max <= 8 elements per builder thread)
-enum { BAR_BUILD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_DONE = 6 };   // FULL / EMPTY / DONE: ids + buffer parity
-
-#ifdef HELM_BATCH_PROF
-#define WPROF(k) do { if (prof_on) { const long long t_ = clock64(); wpr[k] += t_ - wt0; wt0 = t_; } } while (0)
-#else
-#define WPROF(k) do { } while (0)
-#endif
-
-__device__ __forceinline__ void batch_ws_body(const BatchArgs& a, int ncw, int mpmax, int slot_bytes, int NSL)
-{
-#ifdef HELM_BATCH_PROF
-    long long wpr[6] = {0, 0, 0, 0, 0, 0}, wt0 = clock64();
-    const bool prof_on = blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == ncw * 32);
-#endif
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ TileMeta s_meta[2];
-    unsigned char* ringb = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NSL * slot_bytes);
-    uint64_t* empty = full + NSL;
-    uint64_t* cfull = empty + NSL;   // [2] coupling rows landed (per step parity)
-    uint64_t* cempty = cfull + 2;    // [2] the builders have read them
-    const int SR = mpmax + 4, SV = mpmax + 1;
-    z2* R = reinterpret_cast<z2*>(cempty + 2);   // [2][NT][SR]
-    z2* vb = R + 2 * NT * SR;                     // [NT][SV]
-    z2* vt = vb + NT * SV;                        // [NT][SV]
-    z2* cpb = vt + NT * SV;                       // [2][6][mpmax]: U_i (N, NE, NW), L_i (S, SW, SE)
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-    const int GB = (ncw + WS_NB) * 32;            // DMMA + builder threads (the cross-role barriers)
-    const int NBT = WS_NB * 32;
-
-    if (tid == 0) {
-        for (int s = 0; s < NSL; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], ncw);
-        }
-        for (int b = 0; b < 2; b++) {
-            mbar_init(&cfull[b], 1);
-            mbar_init(&cempty[b], WS_NB);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int e = tid; e < 12 * mpmax; e += blockDim.x) cpb[e] = zmk(0, 0);   // NW / SE stay 0 for P1
-    __syncthreads();
-
-    if (warp == ncw + WS_NB) {
-        // ------------------------------------------------ producer: coupling rows and factor chunks, in step order
-        if (lane != 0) return;
-        uint32_t slot = 0, ph = 0, cph[2] = {0, 0};
-        const int ns = a.cc.ns, nv = ns == 9 ? 3 : 2;
-        const int sl_u[3] = {SL_N, SL_NE, SL_NW}, sl_l[3] = {SL_S, SL_SW, SL_SE};
-        uint32_t n = 0;
-        for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x) {
-            const BatchClass C = a.cls[a.tiles[w].cls];
-            const SubDesc d = a.desc[C.rep];
-            const int N = nsub_steps(d);
-            const uint32_t bytes = (uint32_t)(KC * C.S * sizeof(z2));
-            const uint32_t vbytes = (uint32_t)(d.m * sizeof(z2));
-            for (int j = 0; j < N; j++, n++) {
-                const int i = sub_of(d, j).i, b = n & 1;
-                mbar_wait(&cempty[b], cph[b] ^ 1);
-                mbar_arrive_expect_tx(&cfull[b], 2 * nv * vbytes);
-                const z2* row = a.stencil + d.stc_off + (long long)i * ns * d.m;
-                z2* dst = cpb + b * 6 * mpmax;
-                for (int q = 0; q < nv; q++) {
-                    bulk_g2s(dst + q * mpmax, row + sl_u[q] * d.m, vbytes, &cfull[b]);
-                    bulk_g2s(dst + (3 + q) * mpmax, row + sl_l[q] * d.m, vbytes, &cfull[b]);
-                }
-                cph[b] ^= 1;
-                const z2* blk = a.dinvB + C.off + (long long)i * C.mp * C.S;
-                for (int c0 = 0; c0 < C.mp; c0 += KC) {
-                    mbar_wait(&empty[slot], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[slot], bytes);
-                    bulk_g2s(ringb + (size_t)slot * slot_bytes, blk + (long long)c0 * C.S, bytes, &full[slot]);
-                    if (++slot == (uint32_t)NSL) {
-                        slot = 0;
-                        ph ^= 1;
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    if (warp >= ncw) {
-        // ------------------------------------------------ builders: right-hand sides R[n & 1] of step n
-        const int tb = tid - ncw * 32;
-        uint32_t n = 0, done_seen = 0, cph[2] = {0, 0};
-        int local = 0;
-        for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x, local++) {
-            TileMeta& M = s_meta[local & 1];
-            const BatchTile T = a.tiles[w];
-            if (tb == 0) {
-                M.c = a.cls[T.cls];
-                M.d = a.desc[M.c.rep];
-                M.cnt = T.cnt;
-            }
-            if (tb < NT) {
-                const int j = tb < T.cnt ? a.members[T.first + tb] : -1;
-                M.sub[tb] = j;
-                M.gx[tb] = j >= 0 ? a.desc[j].gx0 : 0;
-                M.gy[tb] = j >= 0 ? a.desc[j].gy0 : 0;
-            }
-            nbar_sync(BAR_BUILD, NBT);
-            const SubDesc& d = M.d;
-            const int m = d.m, mp = M.c.mp, cnt = M.cnt, N = nsub_steps(d);
-            for (int j = 0; j < N; j++, n++) {
-                const SubStep st = sub_of(d, j);
-                const int b = n & 1;
-                const bool hb = st.ph <= PH_Z;
-                // restricted inputs b_i of this thread's elements, issued before the waits below
-                z2 bin[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const int e = tb + k * NBT, q = e / mp, tr = e - q * mp;
-                    bin[k] = (hb && e < NT * mp && q < cnt && tr < m)
-                                 ? __ldg(a.in + (M.gx[q] + tr - a.in_i0) + a.in_stride * (long long)(M.gy[q] + st.i - a.in_j0))
-                                 : zmk(0, 0);
-                }
-                WPROF(0);
-                if (n >= 2) nbar_sync(BAR_EMPTY + b, GB);   // the DMMA warps have read R[b] (step n - 2)
-                WPROF(1);
-                // carries: every epilogue up to this step's predecessor (and at least up to step n - 2, so that no
-                // DONE barrier is more than one round ahead)
-                const uint32_t need = max(st.pred >= 0 ? n - j + st.pred + 1 : 0u, n >= 1 ? n - 1 : 0u);
-                while (done_seen < need) {
-                    nbar_sync(BAR_DONE + (done_seen & 1), GB);
-                    done_seen++;
-                }
-                WPROF(2);
-                mbar_wait(&cfull[b], cph[b]);
-                WPROF(3);
-                const z2* cp = cpb + b * 6 * mpmax;
-                z2* Rb = R + b * NT * SR;
-                const bool lower = st.ph == PH_B || st.ph == PH_U || st.ph == PH_Z;
-                const bool use1 = st.ph == PH_T ? st.i < d.nb - 1 : (st.ph == PH_B || st.ph == PH_Z) ? st.i > 0 : true;
-                const bool use2 = st.ph == PH_Z && st.i < d.nb - 1;
-                const z2* v1 = (st.ph == PH_B || st.ph == PH_Z || st.ph == PH_D) ? vb : vt;
-                const double sg = hb ? -1.0 : 1.0;
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const int e = tb + k * NBT;
-                    if (e >= NT * mp) break;
-                    const int q = e / mp, tr = e - q * mp;
-                    z2 r = bin[k];
-                    if (q < cnt && tr < m) {
-                        // d / lo / hi rows: U_i = (N, NW, NE) at slots 0, 2, 1; L_i = (S, SW, SE) at slots 3, 4, 5
-                        const int od = lower ? 3 : 0, olo = lower ? 4 : 2, ohi = lower ? 5 : 1;
-                        if (use1) {
-                            const z2* v = v1 + q * SV + tr;
-                            zfma(r, zscale(cp[od * mpmax + tr], sg), v[0]);
-                            if (tr > 0) zfma(r, zscale(cp[olo * mpmax + tr], sg), v[-1]);
-                            if (tr + 1 < m) zfma(r, zscale(cp[ohi * mpmax + tr], sg), v[1]);
-                        }
-                        if (use2) {
-                            const z2* v = vt + q * SV + tr;
-                            zfma(r, zscale(cp[tr], -1.0), v[0]);
-                            if (tr > 0) zfma(r, zscale(cp[2 * mpmax + tr], -1.0), v[-1]);
-                            if (tr + 1 < m) zfma(r, zscale(cp[mpmax + tr], -1.0), v[1]);
-                        }
-                    }
-                    Rb[q * SR + tr] = r;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&cempty[b]);
-                cph[b] ^= 1;
-                nbar_arrive(BAR_FULL + b, GB);
-                WPROF(4);
-            }
-        }
-#ifdef HELM_BATCH_PROF
-        if (prof_on)
-            printf("WPROF builder loads %lld empty %lld done %lld cpl %lld build %lld\n", wpr[0], wpr[1], wpr[2], wpr[3],
-                   wpr[4]);
-#endif
-        // consume the last rounds of the DMMA warps' EMPTY / DONE arrivals
-        for (uint32_t k = n >= 2 ? n - 2 : 0; k < n; k++) nbar_sync(BAR_EMPTY + (k & 1), GB);
-        for (; done_seen < n; done_seen++) nbar_sync(BAR_DONE + (done_seen & 1), GB);
-        return;
-    }
-
-    // ---------------------------------------------------- DMMA warps: Y = F_i R (3M), then the step's epilogue
-    uint32_t slot = 0, ph = 0, n = 0;
-    z2* scr = a.scratch + (long long)blockIdx.x * a.scratch_per_cta;   // [hi-lo+1][NT][mp]
-    int local = 0;
-    for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x, local++) {
-        const TileMeta& M = s_meta[local & 1];
-        int N = 0;
-        for (int j = 0; j == 0 || j < N; j++, n++) {
-            const int b = n & 1;
-            WPROF(5);
-            nbar_sync(BAR_FULL + b, GB);   // R[b] written (and, for j = 0, the tile metadata)
-            WPROF(0);
-            const SubDesc& d = M.d;
-            const int m = d.m, mp = M.c.mp, cnt = M.cnt, S = M.c.S;
-            N = nsub_steps(d);
-            const SubStep st = sub_of(d, j);
-            const bool mw = warp * 8 < mp;
-            if (mw && st.ph >= PH_D)   // the epilogue's y_i / z_i entries: on their way to L1 under the DMMAs
-#pragma unroll
-                for (int ct = 0; ct < 2; ct++) {
-                    const int q = 8 * ct + 2 * t4;
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(scr + ((long long)(st.i - d.lo) * NT + q) * mp + 8 * warp + g));
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(scr + ((long long)(st.i - d.lo) * NT + q + 1) * mp + 8 * warp + g));
-                }
-            const z2* Rb = R + b * NT * SR;
-            double p1[2][2] = {}, p2[2][2] = {}, p3[2][2] = {};
-            for (int c0 = 0; c0 < mp; c0 += KC) {
-                mbar_wait(&full[slot], ph);
-                if (mw) {
-                    const z2* F = reinterpret_cast<const z2*>(ringb + (size_t)slot * slot_bytes);
-#pragma unroll
-                    for (int ks = 0; ks < KC / 4; ks++) {
-                        const z2 av = F[(4 * ks + t4) * S + 8 * warp + g];
-                        const double as = av.x + av.y;
-                        const int kk = c0 + 4 * ks + t4;
-#pragma unroll
-                        for (int ct = 0; ct < 2; ct++) {
-                            const z2 bv = Rb[(8 * ct + g) * SR + kk];
-                            dmma(p1[ct][0], p1[ct][1], av.x, bv.x);
-                            dmma(p2[ct][0], p2[ct][1], av.y, bv.y);
-                            dmma(p3[ct][0], p3[ct][1], as, bv.x + bv.y);
-                        }
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-                if (++slot == (uint32_t)NSL) {
-                    slot = 0;
-                    ph ^= 1;
-                }
-            }
-            nbar_arrive(BAR_EMPTY + b, GB);
-            WPROF(1);
-            if (mw) {
-                const int t = 8 * warp + g;
-#pragma unroll
-                for (int ct = 0; ct < 2; ct++)
-#pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const int q = 8 * ct + 2 * t4 + e;
-                        if (q >= cnt || t >= m) continue;
-                        const z2 acc = zmk(p1[ct][e] - p2[ct][e], (p3[ct][e] - p1[ct][e]) - p2[ct][e]);
-                        z2* sc = scr + ((long long)(st.i - d.lo) * NT + q) * mp + t;
-                        if (st.ph == PH_T) {
-                            vt[q * SV + t] = acc;
-                            if (st.i <= d.hi) *sc = acc;
-                        } else if (st.ph == PH_B) {
-                            vb[q * SV + t] = acc;
-                            if (st.i >= d.lo) *sc = acc;
-                        } else {
-                            z2 x;
-                            if (st.ph == PH_Z) {
-                                x = acc;
-                                vb[q * SV + t] = x;
-                                vt[q * SV + t] = x;
-                            } else {
-                                x = zsub(*sc, acc);
-                                (st.ph == PH_D ? vb : vt)[q * SV + t] = x;
-                            }
-                            if (t >= d.olo && t <= d.ohi) {
-                                const int gx = M.gx[q] + t, gy = M.gy[q] + st.i;
-                                if (a.pou_buf) {
-                                    const SubDesc& dj = a.desc[M.sub[q]];
-                                    const double wgt = chi_ramp(gx, dj.s0x, dj.s1x, a.delta, dj.flags & 1, dj.flags & 2) *
-                                                       chi_ramp(gy, dj.s0y, dj.s1y, a.delta, dj.flags & 4, dj.flags & 8);
-                                    a.pou_buf[dj.pou_off + (t - d.olo) + (long long)(d.ohi - d.olo + 1) * (st.i - d.lo)] =
-                                        zscale(x, wgt);
-                                } else {
-                                    a.out[(gx - a.out_i0) + a.out_stride * (long long)(gy - a.out_j0)] = x;
-                                }
-                            }
-                        }
-                    }
-            }
-            nbar_arrive(BAR_DONE + b, GB);
-            WPROF(2);
-        }
-    }
-#ifdef HELM_BATCH_PROF
-    if (prof_on) printf("WPROF dmma-warp full_wait %lld dmma %lld epilogue %lld\n", wpr[0], wpr[1], wpr[2]);
-#endif
-}
-
-__global__ void __launch_bounds__(672, 1) k_apply_batch_ws(BatchArgs a, int ncw, int mpmax, int slot_bytes, int nslots)
-{
-    batch_ws_body(a, ncw, mpmax, slot_bytes, nslots);
-}
-
-int batch_ws_smem(int mpmax, int nslots, int slot_bytes)
-{
-    return nslots * slot_bytes + 2 * nslots * 8 + 32 + 2 * NT * (mpmax + 4) * (int)sizeof(z2) +
-           2 * NT * (mpmax + 1) * (int)sizeof(z2) + 12 * mpmax * (int)sizeof(z2);
-}
-
 // one instance per CTA size (consumer warps = mp_max / 8, plus the producer warp), two CTAs per SM up to mp_max = 88
 // (one CTA's serial phases -- right-hand sides, epilogue, barriers -- then run under the other's DMMAs)
 template <int MAXT, int MINB>
@@ -734,42 +392,9 @@ int batch_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslo
     return ncw;
 }
 
-int batch_ws_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslots, int* ctas_per_sm)
-{
-    const int ncw = mpmax / 8;
-    *block = 32 * (ncw + WS_NB + 1);
-    *slot_bytes = KC * (mpmax + 2) * (int)sizeof(z2);
-    const void* fn = (const void*)k_apply_batch_ws;
-    const char* env = getenv("HELM_BATCH_SLOTS");
-    const int force = env ? atoi(env) : 0;
-    for (int ns = 8; ns >= 2; ns--) {   // one CTA per SM, the deepest ring that fits
-        if (force > 0 && ns != force) continue;
-        const int sm = batch_ws_smem(mpmax, ns, *slot_bytes);
-        raise_smem_attr(fn, sm);
-        int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, *block, sm) != cudaSuccess) {
-            cudaGetLastError();
-            continue;
-        }
-        if (occ >= 1) {
-            *smem = sm;
-            *nslots = ns;
-            *ctas_per_sm = occ;
-            return ncw;
-        }
-    }
-    *ctas_per_sm = 0;
-    return ncw;
-}
-
 void launch_apply_batch(const BatchArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, int mpmax,
                         cudaStream_t s)
 {
-    if (block == 32 * (mpmax / 8 + WS_NB + 1)) {   // the warp-specialised configuration
-        raise_smem_attr((const void*)k_apply_batch_ws, smem);
-        k_apply_batch_ws<<<grid, block, smem, s>>>(a, mpmax / 8, mpmax, slot_bytes, nslots);
-        return;
-    }
     raise_smem_attr(batch_fn(block), smem);
     const int ncw = block / 32 - 1;
     if (block <= 288) k_apply_batch<288, 2><<<grid, block, smem, s>>>(a, ncw, mpmax, slot_bytes, nslots);

@@ -2356,11 +2356,7 @@ static int setup_batch(helm_ctx* ctx)
                        ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_members, members.data(), sizeof(int) * members.size(), cudaMemcpyHostToDevice,
                        ctx->stream));
-    const char* ws = getenv("HELM_BATCH_WS");   // warp-specialised form (batch.cu); same results
-    if (ws && ws[0] == '1')
-        batch_ws_configure(mpmax, &ctx->bt_block, &ctx->bt_smem, &ctx->bt_slot, &ctx->bt_nslots, &ctx->bt_occ);
-    else
-        batch_configure(mpmax, &ctx->bt_block, &ctx->bt_smem, &ctx->bt_slot, &ctx->bt_nslots, &ctx->bt_occ);
+    batch_configure(mpmax, &ctx->bt_block, &ctx->bt_smem, &ctx->bt_slot, &ctx->bt_nslots, &ctx->bt_occ);
     if (ctx->bt_occ < 1) return set_err(ctx, HELM_ECUDA, "shared-factor apply kernel does not fit (m_max %d)", mpmax);
     int nsm = 148, dev = 0;
     CK(cudaGetDevice(&dev));
