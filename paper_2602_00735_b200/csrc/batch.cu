@@ -18,6 +18,7 @@
 // Layout of the class factors ("batch layout"): block i of class c at off_c + i * mp * S, column k (mp of them, m
 // padded to a multiple of 8, zero beyond m) at k * S, rows contiguous with S = mp + 2 (== 2 mod 8 z2: the A-fragment
 // loads of a quarter warp -- rows g, g+1, columns t..t+3 -- hit eight distinct 16-byte bank groups).
+#include <cooperative_groups.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -40,6 +41,28 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// Split tiles (few tiles per SM, e.g. one rank of a large decomposition): a cluster of two CTAs shares a tile -- rank 0
+// runs the top chain then the upward expansion (T, then U), rank 1 the bottom chain, the twist and the downward
+// expansion (B, Z, D) -- so the serial chain of a tile is half as long.  At the twist the two swap carries through
+// distributed shared memory: rank 0 sends z_{tw+1}, rank 1 computes x_tw and sends it back (two cluster barriers).
+// role 0: the whole solve in one CTA (ring.cuh's order); 1 / 2: the two halves.
+__device__ __forceinline__ int nsteps_role(const SubDesc& d, int role)
+{
+    if (role == 0) return nsteps(d);
+    return role == 1 ? (d.nb - 1 - d.tw) + (d.hi - d.tw) : d.tw + 1 + (d.tw - d.lo);
+}
+__device__ __forceinline__ Step step_role(const SubDesc& d, int role, int s)
+{
+    if (role == 0) return step_of(d, s);
+    if (role == 1) {
+        const int nT = d.nb - 1 - d.tw;
+        return s < nT ? Step{PH_T, d.nb - 1 - s} : Step{PH_U, d.tw + 1 + (s - nT)};
+    }
+    return s < d.tw ? Step{PH_B, s} : (s == d.tw ? Step{PH_Z, d.tw} : Step{PH_D, d.tw - 1 - (s - d.tw - 1)});
+}
+// the carry exchanges of a split tile happen before step x1 (rank 0: both barriers; rank 1: the first) and x2 (rank 1)
+__device__ __forceinline__ int xchg1(const SubDesc& d, int role) { return role == 1 ? d.nb - 1 - d.tw : d.tw; }
+
 #ifdef HELM_BATCH_PROF
 // development aid (-DHELM_BATCH_PROF): clock64 cycles per phase of every block step as thread 0 of CTA 0 sees them
 // (waits included), printed at the end: right-hand sides, barrier after them, ring waits, DMMA loop, epilogue, barrier
@@ -48,8 +71,11 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #define BPROF(k) do { } while (0)
 #endif
 
-__device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpmax, int slot_bytes, int NSL)
+__device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpmax, int slot_bytes, int NSL, int split)
 {
+    namespace cg = cooperative_groups;
+    const int role = split ? (int)cg::this_cluster().block_rank() + 1 : 0;
+    const int cid = split ? blockIdx.x >> 1 : blockIdx.x, ncl = split ? gridDim.x >> 1 : gridDim.x;
 #ifdef HELM_BATCH_PROF
     long long bpr[7] = {0, 0, 0, 0, 0, 0, 0}, bt0 = clock64();
 #endif
@@ -86,18 +112,26 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
 
     if (warp == ncw) {
         // ---------------------------------------------------------------- producer: stream the class factors
-        if (lane != 0) return;
+        // (lane 0 issues; with split tiles the whole warp stays for the cluster barriers)
+        if (lane != 0 && !split) return;
         uint32_t slot = 0, ph = 0, cph = 0;
         const int ns = a.cc.ns, nv = ns == 9 ? 3 : 2;
         const int sl_u[3] = {SL_N, SL_NE, SL_NW}, sl_l[3] = {SL_S, SL_SW, SL_SE};
-        for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x) {
+        for (int w = cid; w < a.ntiles; w += ncl) {
             const BatchClass C = a.cls[a.tiles[w].cls];
             const SubDesc d = a.desc[C.rep];
-            const int S = nsteps(d);
+            const int S = nsteps_role(d, role);
             const uint32_t bytes = (uint32_t)(KC * C.S * sizeof(z2));
             const uint32_t vbytes = (uint32_t)(d.m * sizeof(z2));
-            for (int s = 0; s < S; s++) {
-                const int i = step_of(d, s).i;
+            for (int s = 0; s <= S; s++) {
+                if (role && s == xchg1(d, role)) {
+                    cg::this_cluster().sync();
+                    if (role == 1) cg::this_cluster().sync();
+                }
+                if (role == 2 && s == d.tw + 1) cg::this_cluster().sync();
+                if (s == S) break;
+                const int i = step_role(d, role, s).i;
+                if (lane == 0) {
                 // coupling rows of step s (once the previous step's right-hand sides are built), then its factor block
                 mbar_wait(cempty, cph ^ 1);
                 mbar_arrive_expect_tx(cfull, 2 * nv * vbytes);
@@ -117,6 +151,8 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                         ph ^= 1;
                     }
                 }
+                }
+                if (split) __syncwarp();
             }
         }
         return;
@@ -125,7 +161,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
     // ------------------------------------------------------------------------ consumers
     uint32_t slot = 0, ph = 0, cph = 0;
     z2* scr = a.scratch + (long long)blockIdx.x * a.scratch_per_cta;   // [hi-lo+1][NT][mp]
-    for (int w = blockIdx.x; w < a.ntiles; w += gridDim.x) {
+    for (int w = cid; w < a.ntiles; w += ncl) {
         const BatchTile T = a.tiles[w];
         if (tid == 0) {
             s_c = a.cls[T.cls];
@@ -142,7 +178,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
         const SubDesc& d = s_d;
         const BatchClass& C = s_c;
         const int m = d.m, mp = C.mp;
-        const int S = nsteps(d);
+        const int S = nsteps_role(d, role);
         const bool mw = warp * 8 < mp;   // this warp owns factor rows [8 warp, 8 warp + 8)
         // Phase-A mapping: thread tid owns row tr of the subdomain columns q = tq + k P (P = nct / mp >= 4 rows of mp
         // threads per pass, k < 4), so its coupling coefficients are read once per step for all its columns.  The
@@ -151,7 +187,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
         const bool ract = tq < P;
         auto load_b = [&](int s2, z2(&pb)[4]) {
             if (s2 >= S || !ract) return;
-            const Step sn = step_of(d, s2);
+            const Step sn = step_role(d, role, s2);
             if (sn.ph > PH_Z) return;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -163,9 +199,27 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
         };
         z2 pb[4];
         load_b(0, pb);
-        for (int s = 0; s < S; s++) {
+        for (int s = 0; s <= S; s++) {
+            if (role) {
+                // split tile: the carry exchanges at the twist (z_{tw+1} to rank 1, x_tw back to rank 0), each
+                // copied into the peer's top-chain carry through distributed shared memory
+                auto send = [&](const z2* src) {
+                    z2* dst = cg::this_cluster().map_shared_rank(vt, 2 - role);
+                    for (int e = tid; e < NT * SV; e += nct) dst[e] = src[e];
+                };
+                if (s == xchg1(d, role)) {
+                    if (role == 1) send(vt);
+                    cg::this_cluster().sync();
+                    if (role == 1) cg::this_cluster().sync();
+                }
+                if (role == 2 && s == d.tw + 1) {
+                    send(vb);
+                    cg::this_cluster().sync();
+                }
+            }
+            if (s == S) break;
             BPROF(5);
-            const Step st = step_of(d, s);
+            const Step st = step_role(d, role, s);
             const z2 cb[4] = {pb[0], pb[1], pb[2], pb[3]};
             if (mw && st.ph >= PH_D)   // the epilogue's y_i / z_i entries: on their way to L1 under phase A and the DMMAs
 #pragma unroll
@@ -240,6 +294,7 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
                         const int kk = c0 + 4 * ks + t4;
 #pragma unroll
                         for (int ct = 0; ct < 2; ct++) {
+                            if (ct == 1 && cnt <= 8) break;   // 8-wide tile: one column tile
                             const z2 bv = R[(8 * ct + g) * SR + kk];
                             dmma(p1[ct][0], p1[ct][1], av.x, bv.x);
                             dmma(p2[ct][0], p2[ct][1], av.y, bv.y);
@@ -312,9 +367,10 @@ __device__ __forceinline__ void batch_body(const BatchArgs& a, int ncw, int mpma
 // one instance per CTA size (consumer warps = mp_max / 8, plus the producer warp), two CTAs per SM up to mp_max = 88
 // (one CTA's serial phases -- right-hand sides, epilogue, barriers -- then run under the other's DMMAs)
 template <int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k_apply_batch(BatchArgs a, int ncw, int mpmax, int slot_bytes, int nslots)
+__global__ void __launch_bounds__(MAXT, MINB) k_apply_batch(BatchArgs a, int ncw, int mpmax, int slot_bytes, int nslots,
+                                                            int split)
 {
-    batch_body(a, ncw, mpmax, slot_bytes, nslots);
+    batch_body(a, ncw, mpmax, slot_bytes, nslots, split);
 }
 
 const void* batch_fn(int block)
@@ -392,14 +448,29 @@ int batch_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslo
     return ncw;
 }
 
-void launch_apply_batch(const BatchArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, int mpmax,
-                        cudaStream_t s)
+int launch_apply_batch(const BatchArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, int mpmax,
+                       int split, cudaStream_t s)
 {
-    raise_smem_attr(batch_fn(block), smem);
+    const void* fn = batch_fn(block);
+    raise_smem_attr(fn, smem);
     const int ncw = block / 32 - 1;
-    if (block <= 288) k_apply_batch<288, 2><<<grid, block, smem, s>>>(a, ncw, mpmax, slot_bytes, nslots);
-    else if (block <= 384) k_apply_batch<384, 2><<<grid, block, smem, s>>>(a, ncw, mpmax, slot_bytes, nslots);
-    else k_apply_batch<544, 1><<<grid, block, smem, s>>>(a, ncw, mpmax, slot_bytes, nslots);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = split ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (block <= 288) e = cudaLaunchKernelEx(&cfg, k_apply_batch<288, 2>, a, ncw, mpmax, slot_bytes, nslots, split);
+    else if (block <= 384) e = cudaLaunchKernelEx(&cfg, k_apply_batch<384, 2>, a, ncw, mpmax, slot_bytes, nslots, split);
+    else e = cudaLaunchKernelEx(&cfg, k_apply_batch<544, 1>, a, ncw, mpmax, slot_bytes, nslots, split);
+    return (int)e;
 }
 
 void launch_relayout_batch(const z2* dinv, long long fac_off, int m, int nb, z2* dst, int mp, int S, cudaStream_t s)

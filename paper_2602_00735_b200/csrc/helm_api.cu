@@ -456,7 +456,7 @@ struct helm_ctx {
     int* d_members = nullptr;
     z2* d_bscr = nullptr;
     int bt_ntiles = 0, bt_nint = 0, bt_grid = 0, bt_grid_int = 0, bt_grid_bnd = 0;
-    int bt_block = 0, bt_smem = 0, bt_slot = 0, bt_nslots = 0, bt_mpmax = 0, bt_occ = 0;
+    int bt_block = 0, bt_smem = 0, bt_slot = 0, bt_nslots = 0, bt_mpmax = 0, bt_occ = 0, bt_w = BATCH_NT, bt_split = 0;
     long long bt_scr_per_cta = 0, dinvB_len = 0;
 
     // constant interior stencil (rows with gamma = 1 on all six triangles) and its node range
@@ -987,9 +987,15 @@ BatchArgs batch_args(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long lon
     return b;
 }
 
-void launch_batch(helm_ctx* ctx, const BatchArgs& b, int grid, cudaStream_t st)
+int launch_batch(helm_ctx* ctx, const BatchArgs& b, int grid, cudaStream_t st)
 {
-    launch_apply_batch(b, grid, ctx->bt_block, ctx->bt_smem, ctx->bt_slot, ctx->bt_nslots, ctx->bt_mpmax, st);
+    const int e = launch_apply_batch(b, grid, ctx->bt_block, ctx->bt_smem, ctx->bt_slot, ctx->bt_nslots, ctx->bt_mpmax,
+                                     ctx->bt_split, st);
+    if (e != 0) {
+        cudaGetLastError();
+        return set_err(ctx, HELM_ECUDA, "tensor-core apply launch: %s", cudaGetErrorString((cudaError_t)e));
+    }
+    return HELM_OK;
 }
 
 int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_stride, z2* z)
@@ -1000,8 +1006,10 @@ int apply_raw(helm_ctx* ctx, const z2* in, int in_i0, int in_j0, long long in_st
     int rc;
     if ((rc = prof_begin(ctx, &e0, &e1))) return rc;
     if (ctx->batched) {
-        const int grid = std::min(ctx->bt_ntiles, ctx->bt_grid_int + ctx->bt_grid_bnd);
-        launch_batch(ctx, batch_args(ctx, in, in_i0, in_j0, in_stride, z, 0, ctx->bt_ntiles, 0), grid, ctx->stream);
+        const int grid = std::min(ctx->bt_ntiles * (ctx->bt_split ? 2 : 1), ctx->bt_grid_int + ctx->bt_grid_bnd);
+        if ((rc = launch_batch(ctx, batch_args(ctx, in, in_i0, in_j0, in_stride, z, 0, ctx->bt_ntiles, 0), grid,
+                               ctx->stream)))
+            return rc;
     } else if (ctx->sp_G > 0) {
         const int e = launch_apply_split(a, (int)ctx->subs.size(), ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
                                          ctx->sp_ncw, ctx->m_max, ctx->sp_nss, ctx->stream);
@@ -1045,9 +1053,10 @@ int apply_impl(helm_ctx* ctx, const z2* r, z2* z)
             if (ctx->batched) {
                 const bool inner = st == ctx->stream;   // interior tiles on the library stream, the rest after the halo
                 const int t0 = inner ? 0 : ctx->bt_nint, nt = inner ? ctx->bt_nint : ctx->bt_ntiles - ctx->bt_nint;
-                launch_batch(ctx, batch_args(ctx, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, z, t0, nt,
-                                             inner ? 0 : ctx->bt_grid_int),
-                             inner ? ctx->bt_grid_int : ctx->bt_grid_bnd, st);
+                const int rc2 = launch_batch(ctx, batch_args(ctx, ctx->d_ext, G.e_i0, G.e_j0, ctx->ext_stride, z, t0, nt,
+                                                             inner ? 0 : ctx->bt_grid_int),
+                                             inner ? ctx->bt_grid_int : ctx->bt_grid_bnd, st);
+                if (rc2) return rc2;
             } else if (ctx->sp_G > 0) {
                 const int e = launch_apply_split(a, a.nsub, ctx->sp_G, ctx->sp_block, ctx->sp_smem, ctx->sp_slot,
                                                  ctx->sp_ncw, ctx->m_max, ctx->sp_nss, st);
@@ -1998,7 +2007,7 @@ int helm_factor_classes(const helm_ctx* ctx, long long* out6, int* class_of, int
             long long nm = 0;
             for (int k : ctx->cls_of) nm += k == c;
             const long long mp = (d.m + 7) / 8 * 8;
-            issued += (nm + BATCH_NT - 1) / BATCH_NT * BATCH_NT * 8LL * mp * mp * (d.nb + d.hi - d.lo);
+            issued += (nm + ctx->bt_w - 1) / ctx->bt_w * ctx->bt_w * 8LL * mp * mp * (d.nb + d.hi - d.lo);
         }
     out6[4] = fl;
     out6[5] = issued;
@@ -2309,7 +2318,29 @@ static int setup_batch(helm_ctx* ctx)
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->d_bcls, bc.data(), sizeof(BatchClass) * ncls, cudaMemcpyHostToDevice, ctx->stream));
-    // tiles: the members of each class in subdomain order, BATCH_NT at a time; sorted by cost, most expensive first
+    batch_configure(mpmax, &ctx->bt_block, &ctx->bt_smem, &ctx->bt_slot, &ctx->bt_nslots, &ctx->bt_occ);
+    if (ctx->bt_occ < 1) return set_err(ctx, HELM_ECUDA, "shared-factor apply kernel does not fit (m_max %d)", mpmax);
+    int nsm = 148, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int slots = nsm * ctx->bt_occ;
+    // tiles: the members of each class in subdomain order, W at a time; sorted by cost, most expensive first.  Few tiles
+    // per CTA slot (a rank of a large decomposition): each tile on a cluster of two CTAs running the twisted halves
+    // (split, batch.cu) once 16-wide tiles would fill at most half the slots, and 8-wide tiles (one DMMA column tile)
+    // once they would fill at most a sixth.  Measured at c3, apply ms per rank (scripts/batch_tile_sweep.sh), 1 / 2 / 4
+    // / 8 ranks: W16 1.47 / 0.93 / 0.92 / 0.91; W16 split 1.49 / 0.76 / 0.51 / 0.50; W8 split 2.66 / 1.34 / 0.67 / 0.44.
+    // A subdomain's result depends on neither choice.  HELM_BATCH_W / HELM_BATCH_SPLIT override.
+    {
+        std::vector<long long> cnt(ncls, 0);
+        for (int k : ctx->cls_of) cnt[k]++;
+        long long t16 = 0;
+        for (long long c : cnt) t16 += (c + BATCH_NT - 1) / BATCH_NT;
+        ctx->bt_split = 2 * t16 <= slots ? 1 : 0;
+        ctx->bt_w = 6 * t16 <= slots ? 8 : BATCH_NT;
+        if (const char* e = getenv("HELM_BATCH_W")) ctx->bt_w = atoi(e) == 8 ? 8 : BATCH_NT;
+        if (const char* e = getenv("HELM_BATCH_SPLIT")) ctx->bt_split = e[0] == '1';
+    }
+    const int W = ctx->bt_w;
     std::vector<BatchTile> tiles;
     std::vector<int> members;
     auto make_tiles = [&](const std::vector<int>& set) {
@@ -2317,11 +2348,11 @@ static int setup_batch(helm_ctx* ctx)
         for (int j : set) per[ctx->cls_of[j]].push_back(j);
         std::vector<BatchTile> t;
         for (int c = 0; c < ncls; c++)
-            for (size_t q = 0; q < per[c].size(); q += BATCH_NT) {
+            for (size_t q = 0; q < per[c].size(); q += W) {
                 BatchTile bt{};
                 bt.cls = c;
                 bt.first = (int)members.size();
-                bt.cnt = (int)std::min<size_t>(BATCH_NT, per[c].size() - q);
+                bt.cnt = (int)std::min<size_t>(W, per[c].size() - q);
                 members.insert(members.end(), per[c].begin() + q, per[c].begin() + q + bt.cnt);
                 t.push_back(bt);
             }
@@ -2356,25 +2387,20 @@ static int setup_batch(helm_ctx* ctx)
                        ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_members, members.data(), sizeof(int) * members.size(), cudaMemcpyHostToDevice,
                        ctx->stream));
-    batch_configure(mpmax, &ctx->bt_block, &ctx->bt_smem, &ctx->bt_slot, &ctx->bt_nslots, &ctx->bt_occ);
-    if (ctx->bt_occ < 1) return set_err(ctx, HELM_ECUDA, "shared-factor apply kernel does not fit (m_max %d)", mpmax);
-    int nsm = 148, dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const int slots = nsm * ctx->bt_occ;
     auto trim = [](int n, int s) {
         s = std::max(1, std::min(s, n));
         const int per = (n + s - 1) / s;
         return (n + per - 1) / per;
     };
-    const int nbnd = ctx->bt_ntiles - ctx->bt_nint;
+    // grids in tiles processed at once (a split tile occupies two CTA slots), then in CTAs
+    const int nbnd = ctx->bt_ntiles - ctx->bt_nint, cpt = ctx->bt_split ? 2 : 1, tslots = std::max(1, slots / cpt);
     if (ctx->overlap && ctx->bt_nint > 0 && nbnd > 0) {
-        int sb = (int)std::lround((double)slots * nbnd / ctx->bt_ntiles);
-        sb = std::max(1, std::min(slots - 1, sb));
-        ctx->bt_grid_int = trim(ctx->bt_nint, slots - sb);
-        ctx->bt_grid_bnd = trim(nbnd, sb);
+        int sb = (int)std::lround((double)tslots * nbnd / ctx->bt_ntiles);
+        sb = std::max(1, std::min(tslots - 1, sb));
+        ctx->bt_grid_int = cpt * trim(ctx->bt_nint, tslots - sb);
+        ctx->bt_grid_bnd = cpt * trim(nbnd, sb);
     } else {
-        ctx->bt_grid_int = trim(ctx->bt_ntiles, slots);
+        ctx->bt_grid_int = cpt * trim(ctx->bt_ntiles, tslots);
         ctx->bt_grid_bnd = 0;
     }
     ctx->bt_grid = ctx->bt_grid_int;

@@ -231,7 +231,7 @@ struct BatchArgs {
     int delta;
 };
 int batch_configure(int mpmax, int* block, int* smem, int* slot_bytes, int* nslots, int* ctas_per_sm);
-void launch_apply_batch(const BatchArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, int mpmax,
-                        cudaStream_t s);
+int launch_apply_batch(const BatchArgs& a, int grid, int block, int smem, int slot_bytes, int nslots, int mpmax,
+                       int split, cudaStream_t s);   // split: clusters of two CTAs per tile; returns the cudaError_t
 void launch_relayout_batch(const z2* dinv, long long fac_off, int m, int nb, z2* dst, int mp, int S, cudaStream_t s);
 void launch_stencil_eq(const SubDesc* desc, const z2* stc, const int2* pairs, int npairs, int* diff, cudaStream_t s);

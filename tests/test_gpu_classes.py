@@ -64,13 +64,15 @@ def test_class_partition_equals_the_oracle_dedup(name):
     ctx.close()
 
 
-CASES = [("c1", {}), ("c2", {}), ("c1", {"local_bc": BC_IMPEDANCE}), ("c2", {"pou": POU_RAMP})]
+CASES = [("c1", {}, {}), ("c2", {}, {}), ("c1", {"local_bc": BC_IMPEDANCE}, {}), ("c2", {"pou": POU_RAMP}, {}),
+         ("c2", {}, {"HELM_BATCH_SPLIT": "1"}), ("c1", {"pou": POU_RAMP}, {"HELM_BATCH_SPLIT": "1"})]
 
 
-@pytest.mark.parametrize("name,kw", CASES, ids=["c1", "c2", "c1-imp", "c2-ramp"])
-def test_tensor_core_apply_and_gmres_vs_oracle(name, kw):
+@pytest.mark.parametrize("name,kw,env", CASES, ids=["c1", "c2", "c1-imp", "c2-ramp", "c2-split", "c1-ramp-split"])
+def test_tensor_core_apply_and_gmres_vs_oracle(name, kw, env):
+    """(split: every tile on a cluster of two CTAs, the twisted halves swapping carries through DSMEM)"""
     cfg = CONFIGS[name]
-    ctx = make(cfg, {"HELM_APPLY_BATCH": "1"}, **kw)
+    ctx = make(cfg, {"HELM_APPLY_BATCH": "1", **env}, **kw)
     info = ctx.factor_classes()
     assert info["batched"] and info["tiles"] >= info["classes"]
     o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, **kw)
