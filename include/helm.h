@@ -217,7 +217,7 @@ int helm_comm_counters(helm_ctx* ctx, int reset, long long* out4);
  * multiple of 8; 0 when off)}; class_of (may be NULL) receives n_sub_local class indices, cap entries at most.
  * Environment (read at helm_setup): HELM_SHARE_FACTORS=0 factors every subdomain (one class each);
  * HELM_APPLY_BATCH=1 / 0 forces the tensor-core apply on / off (default: on when the whole problem has at least
- * 4 x SMs subdomains and m_max <= 128).  Host only. */
+ * as many subdomains as the GPU has SMs and m_max <= 128).  Host only. */
 int helm_factor_classes(const helm_ctx* ctx, long long* out6, int* class_of, int cap);
 
 /* Host logic, no GPU: this rank's apply-frame halo volume in complex elements -- out4 = {sent full, sent band, received

@@ -447,8 +447,8 @@ struct helm_ctx {
     std::vector<int> cls_rep, cls_of;
     long long n_dinv_all = 0;   // factor complex entries without sharing (layout reporting)
     // shared-factor apply on the tensor cores (batch.cu): HELM_APPLY_BATCH = 0 / 1 forces it off / on; by default on
-    // when the factors are shared, m_max <= 128 and the whole problem has >= 4 x SMs subdomains (decided on global
-    // quantities so that every rank of a decomposition takes the same path)
+    // when the factors are shared, m_max <= 128 and the whole problem has at least one subdomain per SM (decided on
+    // global quantities so that every rank of a decomposition takes the same path)
     bool batched = false;
     z2* d_dinvB = nullptr;
     BatchTile* d_tiles = nullptr;
@@ -1880,7 +1880,7 @@ static int setup_impl(const helm_params* params, int rank, int nranks, const voi
     if (const char* e = getenv("HELM_SHARE_FACTORS")) ctx->share = e[0] != '0';
     {
         const long long nsub_global = (long long)ctx->G.P[0] * ctx->G.P[1];
-        bool b = nsub_global >= 4LL * nsm;
+        bool b = nsub_global >= nsm;   // c2 (256 subdomains): 0.365 vs 0.455 ms streaming; c1 (16): 0.31 vs 0.10
         if (const char* e = getenv("HELM_APPLY_BATCH")) b = e[0] == '1';
         ctx->batched = b && ctx->share && ctx->m_max <= 128;
     }

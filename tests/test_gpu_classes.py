@@ -64,17 +64,25 @@ def test_class_partition_equals_the_oracle_dedup(name):
     ctx.close()
 
 
-CASES = [("c1", {}, {}), ("c2", {}, {}), ("c1", {"local_bc": BC_IMPEDANCE}, {}), ("c2", {"pou": POU_RAMP}, {}),
-         ("c2", {}, {"HELM_BATCH_SPLIT": "1"}), ("c1", {"pou": POU_RAMP}, {"HELM_BATCH_SPLIT": "1"})]
+CASES = [("c1", {}, {}), ("c2", {}, {"HELM_BATCH_SPLIT": "0", "HELM_BATCH_W": "16"}),
+         ("c1", {"local_bc": BC_IMPEDANCE}, {}), ("c2", {"pou": POU_RAMP}, {}),
+         ("c2", {}, {"HELM_BATCH_SPLIT": "1"}), ("c1", {"pou": POU_RAMP}, {"HELM_BATCH_SPLIT": "1"}),
+         ("c2", {}, {"HELM_APPLY_BATCH": "0"}), ("c2", {"local_bc": BC_IMPEDANCE}, {"HELM_SHARE_FACTORS": "0"})]
 
 
-@pytest.mark.parametrize("name,kw,env", CASES, ids=["c1", "c2", "c1-imp", "c2-ramp", "c2-split", "c1-ramp-split"])
+@pytest.mark.parametrize("name,kw,env", CASES, ids=["c1", "c2-w16", "c1-imp", "c2-ramp", "c2-split", "c1-ramp-split",
+                                                    "c2-streaming", "c2-imp-per-subdomain"])
 def test_tensor_core_apply_and_gmres_vs_oracle(name, kw, env):
-    """(split: every tile on a cluster of two CTAs, the twisted halves swapping carries through DSMEM)"""
+    """The tensor-core apply forced on (split: every tile on a cluster of two CTAs, the twisted halves swapping carries
+    through DSMEM; w16: one CTA per 16-wide tile), and the streaming apply on shared / per-subdomain factors, against
+    the oracle."""
     cfg = CONFIGS[name]
-    ctx = make(cfg, {"HELM_APPLY_BATCH": "1", **env}, **kw)
+    env = {"HELM_APPLY_BATCH": "1", **env}
+    ctx = make(cfg, env, **kw)
     info = ctx.factor_classes()
-    assert info["batched"] and info["tiles"] >= info["classes"]
+    batched = env["HELM_APPLY_BATCH"] == "1" and env.get("HELM_SHARE_FACTORS") != "0"
+    assert info["batched"] == batched
+    assert not batched or info["tiles"] >= info["classes"]
     o = Oracle.from_config(k=cfg.k, nsub_x=cfg.nsub, nsub_y=cfg.nsub, **kw)
     o.factor()
     v = probe_vector(o.nfree, int(cfg.k) + 1)
