@@ -1360,7 +1360,8 @@ int gmres_impl(helm_ctx* ctx, const z2* b, z2* x, int restart, double rtol, int 
         auto mark = [&](int k) { if (ctx->phases) cudaEventRecord(ctx->ev_ph[k], s); };
         // Several ranks: step j + 1 (it needs only device data) is queued before the host's update of step j, so the
         // devices never wait for the host's turnaround.  One rank: the turnaround is 0.3 % of a c3 step (93.59 vs
-        // 93.56 applies/s with and without), not worth a discarded apply at convergence.
+        // 93.56 applies/s with and without; with the tensor-core apply 386.5 vs 385.2), not worth a discarded apply at
+        // convergence.
         const bool lookahead = ctx->multi && !ctx->phases;
         // folded norm (several ranks, HELM_GMRES_FOLD=0 disables): one collective per Arnoldi step -- the convergence
         // test uses column j - 1 once step j's record has made it final, one step later than the tentative test; the
