@@ -402,7 +402,7 @@ def run_ours(args):
     }
     if world == 1 and not args.no_paper:
         out["per_subdomain_factors"] = per_subdomain_factors(cfg, stream, hbm, peak_src, read_streams)
-    if world == 1:
+    if world == 1 and not args.no_tts:
         out["tts_vs_k"] = tts_vs_k(stream, cfg, tts_s, tinfo, factor_s, apply_only_ms)
     if world == 1 and not args.no_paper:
         out["paper_table4"] = paper_table4(stream)
@@ -782,6 +782,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper Table 4 comparison rows")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solve-vs-k rows (c0..c4)")
     ap.add_argument("--seed", type=int, default=None, help="source draw seed (default: the config's, = k)")
     ap.add_argument("--orth", default="dcgs2", choices=["dcgs2", "cgs2"],
                     help="GMRES orthogonalisation (DESIGN.md 5.6); cgs2 = the undelayed form, for A/B")
