@@ -115,3 +115,28 @@ def test_shared_and_per_subdomain_factors_agree(name):
     assert rel(z2, z0) <= 1e-13
     for c in (per, shared, batch):
         c.close()
+
+
+@pytest.mark.parametrize("bc", [0, 1], ids=["drch", "imp"])
+def test_tensor_core_apply_q1_paper_frame_vs_oracle(bc):
+    """The paper's own discretisation (Q1, 9-point couplings with the NW / SE terms, D18; RAS-PML-Imp and the ramp PoU
+    by default) through the tensor-core apply, forced on, against the oracle."""
+    from paper_2602_00735_b200.helm import paper_params
+    kw = paper_params(100.0, 3, 4, 2, local_bc=bc)
+    old = os.environ.get("HELM_APPLY_BATCH")
+    os.environ["HELM_APPLY_BATCH"] = "1"
+    try:
+        ctx = Context(**kw)
+    finally:
+        if old is None:
+            del os.environ["HELM_APPLY_BATCH"]
+        else:
+            os.environ["HELM_APPLY_BATCH"] = old
+    ctx.factor()
+    assert ctx.layout.stencil_slots == 9 and ctx.factor_classes()["batched"]
+    o = Oracle.from_paper(k=100.0, nsub=3, pml=4, ovlp=2, local_bc=bc, pou=kw["pou"])
+    o.factor()
+    v = probe_vector(o.nfree, 11)
+    z = ctx.precond_apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    assert rel(z, o.apply(v)) <= 1e-10
+    ctx.close()
