@@ -9,11 +9,13 @@
 // class's explicit Schur-complement inverses to NT = 16 subdomains at a time: every block step of the twisted
 // substitution (ring.cuh) becomes one complex GEMM
 //     Y_i (m x 16) = F_i (m x m) R_i (m x 16),     R_i = b_i - L_i Y_{i-1}  (or the U / D / Z forms)
-// on mma.sync.m8n8k4.f64 (DMMA), with F_i streamed by TMA bulk copies into a shared-memory ring (read once per 16
-// subdomains instead of once per subdomain) and R_i, the two chain carries and the accumulator epilogue in shared
-// memory.  The result of every subdomain is computed exactly as in the per-subdomain solve, up to the order of the
+// on mma.sync.m8n8k4.f64 (DMMA; three real products per complex k-step, the 3M form), with F_i streamed by TMA bulk
+// copies into a shared-memory ring (read once per 16 subdomains instead of once per subdomain), the step's coupling
+// rows bulk-copied beside it, and R_i, the two chain carries and the accumulator epilogue in shared memory.  Two CTAs
+// per SM; on ranks with few tiles per SM, 8-wide tiles and a cluster of two CTAs per tile (one per twisted half).
+// The result of every subdomain is computed exactly as in the per-subdomain solve, up to the order of the
 // floating-point additions of the GEMV (column n of a DMMA product depends on column n of R only, so a subdomain's
-// result does not depend on which other subdomains share its tile or rank).
+// result does not depend on which other subdomains share its tile, on the tile width, on the split, or on the rank).
 //
 // Layout of the class factors ("batch layout"): block i of class c at off_c + i * mp * S, column k (mp of them, m
 // padded to a multiple of 8, zero beyond m) at k * S, rows contiguous with S = mp + 2 (== 2 mod 8 z2: the A-fragment
