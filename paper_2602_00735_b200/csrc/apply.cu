@@ -22,6 +22,7 @@
 #include <mutex>
 
 #include "internal.cuh"
+#include "ring.cuh"
 
 namespace {
 
@@ -31,65 +32,21 @@ constexpr int NS = 8;              // ring slots of the read probe; k_apply take
 // 163-register CTAs per SM) 9.35 -- a short ring of large chunks over more CTAs wins.  HELM_APPLY_SLOTB overrides.
 constexpr int SLOT_TARGET = 20000;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
-{
-    uint32_t ok = 0;
-    const uint32_t a = smem_u32(bar);
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void consumer_bar(int nthreads)
-{
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
-enum { PH_T = 0, PH_B = 1, PH_Z = 2, PH_D = 3, PH_U = 4 };
-
-struct Step { int ph, i; };
-
-__device__ __forceinline__ int nsteps(const SubDesc& d) { return d.nb + d.hi - d.lo; }
-
-__device__ __forceinline__ Step step_of(const SubDesc& d, int s)
-{
-    const int nT = d.nb - 1 - d.tw, nB = d.tw, nD = d.tw - d.lo;
-    if (s < nT) return {PH_T, d.nb - 1 - s};
-    s -= nT;
-    if (s < nB) return {PH_B, s};
-    s -= nB;
-    if (s == 0) return {PH_Z, d.tw};
-    s -= 1;
-    if (s < nD) return {PH_D, d.tw - 1 - s};
-    s -= nD;
-    return {PH_U, d.tw + 1 + s};
-}
+// the bulk-copy ring and the twisted step order are shared with the tensor-core apply (ring.cuh)
+using ring::bulk_g2s;
+using ring::consumer_bar;
+using ring::mbar_arrive;
+using ring::mbar_arrive_expect_tx;
+using ring::mbar_init;
+using ring::mbar_wait;
+using ring::nsteps;
+using ring::PH_B;
+using ring::PH_D;
+using ring::PH_T;
+using ring::PH_U;
+using ring::PH_Z;
+using ring::Step;
+using ring::step_of;
 
 // A coupling row (L_i or U_i) at node t: r += d v[t] + lo v[t-1] + hi v[t+1].  U_i: d = N, lo = NW, hi = NE;
 // L_i: d = S, lo = SW, hi = SE (NW / SE exist for the 9-point Q1 stencil only, D18; zero for P1).
